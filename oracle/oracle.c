@@ -1,0 +1,333 @@
+/*
+ * oracle.c -- plain single-threaded CPU oracle (TEST INFRASTRUCTURE ONLY; see
+ * oracle.h).  Every function is the plain definition written out as a loop
+ * over edges in ascending edge id, with double accumulation and a single
+ * rounding to float at the end.  No blocking, fusion or reordering.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (see
+ * oracle/__init__.py).  -ffp-contract=off keeps "w * x" a single float
+ * multiply for the MAX path (reading Q4/Q10): the argmax decision is taken on
+ * the float message the GPU also computes.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+static int check_index(const int64_t* idx, int64_t E, int64_t n) {
+    for (int64_t k = 0; k < E; ++k)
+        if (idx[k] < 0 || idx[k] >= n) return ORC_ERR_OOB;
+    return ORC_OK;
+}
+
+int orc_degree(const int64_t* index, int64_t E, int64_t n, int64_t* deg) {
+    if (E < 0 || n < 0 || (E > 0 && !index) || (n > 0 && !deg)) return ORC_ERR_INVALID;
+    if (check_index(index, E, n)) return ORC_ERR_OOB;
+    for (int64_t i = 0; i < n; ++i) deg[i] = 0;
+    for (int64_t k = 0; k < E; ++k) deg[index[k]] += 1; /* count of incident edges */
+    return ORC_OK;
+}
+
+int orc_csr(const int64_t* dst, int64_t E, int64_t n, int64_t* rowptr, int64_t* perm) {
+    if (E < 0 || n < 0 || !rowptr || (E > 0 && (!dst || !perm))) return ORC_ERR_INVALID;
+    if (check_index(dst, E, n)) return ORC_ERR_OOB;
+    /* counting sort: rowptr = exclusive prefix sum of in-degrees */
+    for (int64_t i = 0; i <= n; ++i) rowptr[i] = 0;
+    for (int64_t k = 0; k < E; ++k) rowptr[dst[k] + 1] += 1;
+    for (int64_t i = 0; i < n; ++i) rowptr[i + 1] += rowptr[i];
+    int64_t* next = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    if (!next) return ORC_ERR_INVALID;
+    for (int64_t i = 0; i < n; ++i) next[i] = rowptr[i];
+    for (int64_t k = 0; k < E; ++k) perm[next[dst[k]]++] = k; /* ascending k => stable */
+    free(next);
+    return ORC_OK;
+}
+
+/* ---- the reduction core shared by scatter / propagate / pooling --------- */
+/* The caller supplies, for edge k and output column c, the message value as
+ * a float (what MAX compares, reading Q4) and as a double (what SUM/MEAN
+ * accumulate: the exact product for weighted messages). */
+typedef struct {
+    /* propagate inputs */
+    const float* x_src; int64_t ldx;
+    const float* x_dst; int64_t ldxd;
+    const float* edge_attr; int64_t D;
+    const float* w;
+    int64_t F; int concat_xi;
+    /* scatter input */
+    const float* src; int64_t lds;
+    const int64_t* src_idx; /* NULL for scatter */
+    const int64_t* dst_idx;
+} msg_ctx;
+
+/* Column layout of the propagate message: [x_i (F, if concat) | w x_j (F) | e (D)] */
+static void message(const msg_ctx* m, int64_t k, int64_t c, float* mf, double* md) {
+    if (!m->src_idx) { /* scatter: the message is the edge-space row itself */
+        float v = m->src[k * m->lds + c];
+        *mf = v; *md = (double)v;
+        return;
+    }
+    int64_t j = m->src_idx[k], i = m->dst_idx[k];
+    int64_t off = 0;
+    if (m->concat_xi) {
+        if (c < m->F) {
+            const float* xd = m->x_dst ? m->x_dst : m->x_src;
+            int64_t ld = m->x_dst ? m->ldxd : m->ldx;
+            float v = xd[i * ld + c];
+            *mf = v; *md = (double)v;
+            return;
+        }
+        off = m->F;
+    }
+    if (c < off + m->F) {
+        float x = m->x_src[j * m->ldx + (c - off)];
+        if (m->w) {
+            float wk = m->w[k];
+            *mf = wk * x;                     /* one float multiply (MAX decision) */
+            *md = (double)wk * (double)x;      /* exact product (SUM / MEAN) */
+        } else {
+            *mf = x; *md = (double)x;
+        }
+        return;
+    }
+    float e = m->edge_attr[k * m->D + (c - off - m->F)];
+    *mf = e; *md = (double)e;
+}
+
+static int reduce_core(const msg_ctx* m, int64_t E, int64_t n_out, int64_t F_out, int reduce,
+                       float* out, int64_t* arg, double* abs_sum) {
+    size_t cells = (size_t)n_out * (size_t)F_out;
+    int64_t* deg = (int64_t*)calloc((size_t)(n_out > 0 ? n_out : 1), sizeof(int64_t));
+    if (!deg) return ORC_ERR_INVALID;
+    for (int64_t k = 0; k < E; ++k) deg[m->dst_idx[k]] += 1;
+    if (abs_sum)
+        for (size_t t = 0; t < cells; ++t) abs_sum[t] = 0.0;
+
+    if (reduce == ORC_SUM || reduce == ORC_MEAN) {
+        double* acc = (double*)calloc(cells ? cells : 1, sizeof(double));
+        if (!acc) { free(deg); return ORC_ERR_INVALID; }
+        for (int64_t k = 0; k < E; ++k) {
+            int64_t i = m->dst_idx[k];
+            for (int64_t c = 0; c < F_out; ++c) {
+                float mf; double md;
+                message(m, k, c, &mf, &md);
+                acc[i * F_out + c] += md;
+                if (abs_sum) abs_sum[i * F_out + c] += fabs(md);
+            }
+        }
+        for (int64_t i = 0; i < n_out; ++i)
+            for (int64_t c = 0; c < F_out; ++c) {
+                double a = acc[i * F_out + c];
+                if (reduce == ORC_MEAN) /* mean = sum / integer in-degree; deg 0 -> 0 (Q6) */
+                    out[i * F_out + c] = deg[i] > 0 ? (float)(a / (double)deg[i]) : 0.0f;
+                else
+                    out[i * F_out + c] = (float)a;
+                if (abs_sum && reduce == ORC_MEAN && deg[i] > 0)
+                    abs_sum[i * F_out + c] /= (double)deg[i];
+            }
+        free(acc);
+    } else if (reduce == ORC_MAX) {
+        /* scan k ascending; take m if the segment is empty so far or m > best
+         * (strict IEEE) => arg = lowest edge id among equal maxima (Q4);
+         * empty segment -> out 0, arg E (Q2, Q3). */
+        float* best = (float*)malloc((cells ? cells : 1) * sizeof(float));
+        if (!best) { free(deg); return ORC_ERR_INVALID; }
+        for (size_t t = 0; t < cells; ++t) { best[t] = 0.0f; arg[t] = E; }
+        for (int64_t k = 0; k < E; ++k) {
+            int64_t i = m->dst_idx[k];
+            for (int64_t c = 0; c < F_out; ++c) {
+                float mf; double md;
+                message(m, k, c, &mf, &md);
+                size_t t = (size_t)(i * F_out + c);
+                if (arg[t] == E || mf > best[t]) { best[t] = mf; arg[t] = k; }
+            }
+        }
+        for (size_t t = 0; t < cells; ++t) out[t] = (arg[t] == E) ? 0.0f : best[t];
+        free(best);
+    } else {
+        free(deg);
+        return ORC_ERR_INVALID;
+    }
+    free(deg);
+    return ORC_OK;
+}
+
+int orc_scatter(const float* src, int64_t E, int64_t F, int64_t lds, const int64_t* index,
+                int64_t dim_size, int reduce, float* out, int64_t* arg, double* abs_sum) {
+    if (E < 0 || F < 0 || dim_size < 0 || lds < F) return ORC_ERR_DIMENSION;
+    if (reduce < ORC_SUM || reduce > ORC_MAX) return ORC_ERR_INVALID;
+    if ((E > 0 && (!index || (F > 0 && !src))) || (dim_size * F > 0 && !out)) return ORC_ERR_INVALID;
+    if (reduce == ORC_MAX && dim_size * F > 0 && !arg) return ORC_ERR_INVALID;
+    if (check_index(index, E, dim_size)) return ORC_ERR_OOB;
+    msg_ctx m;
+    memset(&m, 0, sizeof m);
+    m.src = src; m.lds = lds; m.dst_idx = index; m.F = F;
+    return reduce_core(&m, E, dim_size, F, reduce, out, arg, abs_sum);
+}
+
+int orc_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t ldx, const float* x_dst,
+                  int64_t ldxd, int64_t n_dst, const int64_t* edge_index, int64_t E,
+                  const float* edge_attr, int64_t D, const float* edge_weight, int reduce,
+                  int concat_xi, float* out, int64_t* arg, double* abs_sum) {
+    if (E < 0 || F < 0 || D < 0 || n_src < 0 || n_dst < 0 || ldx < F) return ORC_ERR_DIMENSION;
+    if (x_dst && ldxd < F) return ORC_ERR_DIMENSION;
+    if (concat_xi && !x_dst && n_dst > n_src) return ORC_ERR_DIMENSION;
+    if (reduce < ORC_SUM || reduce > ORC_MAX) return ORC_ERR_INVALID;
+    if (D > 0 && E > 0 && !edge_attr) return ORC_ERR_INVALID;
+    int64_t F_out = (concat_xi ? F : 0) + F + D;
+    if (n_dst * F_out > 0 && !out) return ORC_ERR_INVALID;
+    if (reduce == ORC_MAX && n_dst * F_out > 0 && !arg) return ORC_ERR_INVALID;
+    if (E > 0 && !edge_index) return ORC_ERR_INVALID;
+    const int64_t* src_idx = edge_index;
+    const int64_t* dst_idx = edge_index + E;
+    if (check_index(src_idx, E, n_src) || check_index(dst_idx, E, n_dst)) return ORC_ERR_OOB;
+    msg_ctx m;
+    memset(&m, 0, sizeof m);
+    m.x_src = x_src; m.ldx = ldx; m.x_dst = x_dst; m.ldxd = ldxd;
+    m.edge_attr = edge_attr; m.D = D; m.w = edge_weight; m.F = F; m.concat_xi = concat_xi;
+    m.src_idx = src_idx; m.dst_idx = dst_idx;
+    return reduce_core(&m, E, n_dst, F_out, reduce, out, arg, abs_sum);
+}
+
+int orc_scatter_backward(const float* grad_out, int64_t F, const int64_t* index, int64_t E,
+                         int64_t dim_size, int reduce, const int64_t* arg, float* grad_src) {
+    if (E < 0 || F < 0 || dim_size < 0) return ORC_ERR_DIMENSION;
+    if (reduce < ORC_SUM || reduce > ORC_MAX) return ORC_ERR_INVALID;
+    if (reduce == ORC_MAX && dim_size * F > 0 && !arg) return ORC_ERR_INVALID;
+    if (check_index(index, E, dim_size)) return ORC_ERR_OOB;
+    int64_t* deg = (int64_t*)calloc((size_t)(dim_size > 0 ? dim_size : 1), sizeof(int64_t));
+    if (!deg) return ORC_ERR_INVALID;
+    for (int64_t k = 0; k < E; ++k) deg[index[k]] += 1;
+    for (int64_t k = 0; k < E; ++k) {
+        int64_t i = index[k];
+        for (int64_t c = 0; c < F; ++c) {
+            float g = grad_out[i * F + c];
+            float r;
+            if (reduce == ORC_SUM) r = g;                         /* gather of grad */
+            else if (reduce == ORC_MEAN) r = g / (float)deg[i];   /* scaled by 1/count */
+            else r = (arg[i * F + c] == k) ? g : 0.0f;             /* routed to argmax */
+            grad_src[k * F + c] = r;
+        }
+    }
+    free(deg);
+    return ORC_OK;
+}
+
+int orc_propagate_backward(const float* x_src, int64_t n_src, int64_t F, int64_t ldx,
+                           int64_t n_dst, const int64_t* edge_index, int64_t E, int64_t D,
+                           const float* edge_weight, int reduce, int concat_xi,
+                           const float* grad_out, const int64_t* arg, float* grad_x_src,
+                           float* grad_x_dst, float* grad_edge_attr, float* grad_edge_weight,
+                           double* abs_sum_x_src) {
+    if (E < 0 || F < 0 || D < 0 || n_src < 0 || n_dst < 0 || ldx < F) return ORC_ERR_DIMENSION;
+    if (reduce < ORC_SUM || reduce > ORC_MAX) return ORC_ERR_INVALID;
+    int64_t F_out = (concat_xi ? F : 0) + F + D;
+    if (reduce == ORC_MAX && n_dst * F_out > 0 && !arg) return ORC_ERR_INVALID;
+    if (grad_edge_weight && !x_src && E * F > 0) return ORC_ERR_INVALID;
+    const int64_t* src_idx = edge_index;
+    const int64_t* dst_idx = edge_index + E;
+    if (check_index(src_idx, E, n_src) || check_index(dst_idx, E, n_dst)) return ORC_ERR_OOB;
+    int64_t off1 = concat_xi ? F : 0, off2 = off1 + F;
+
+    int64_t* deg = (int64_t*)calloc((size_t)(n_dst > 0 ? n_dst : 1), sizeof(int64_t));
+    double* gxs = (double*)calloc((size_t)(n_src * F > 0 ? n_src * F : 1), sizeof(double));
+    double* gxd = (double*)calloc((size_t)(n_dst * F > 0 ? n_dst * F : 1), sizeof(double));
+    if (!deg || !gxs || !gxd) { free(deg); free(gxs); free(gxd); return ORC_ERR_INVALID; }
+    for (int64_t k = 0; k < E; ++k) deg[dst_idx[k]] += 1;
+    if (abs_sum_x_src)
+        for (int64_t t = 0; t < n_src * F; ++t) abs_sum_x_src[t] = 0.0;
+
+    for (int64_t k = 0; k < E; ++k) {
+        int64_t j = src_idx[k], i = dst_idx[k];
+        double wk = edge_weight ? (double)edge_weight[k] : 1.0;
+        double gw = 0.0;
+        for (int64_t c = 0; c < F_out; ++c) {
+            /* dL/dm_k[c]: the adjoint of the reduction */
+            double g = (double)grad_out[i * F_out + c];
+            double gm;
+            if (reduce == ORC_SUM) gm = g;
+            else if (reduce == ORC_MEAN) gm = g / (double)deg[i];
+            else gm = (arg[i * F_out + c] == k) ? g : 0.0;
+            if (c < off1) {
+                gxd[i * F + c] += gm;                       /* x_i block */
+            } else if (c < off2) {
+                double t = wk * gm;                         /* w_k x_j block */
+                gxs[j * F + (c - off1)] += t;
+                if (abs_sum_x_src) abs_sum_x_src[j * F + (c - off1)] += fabs(t);
+                if (grad_edge_weight) gw += (double)x_src[j * ldx + (c - off1)] * gm;
+            } else if (grad_edge_attr) {
+                grad_edge_attr[k * D + (c - off2)] = (float)gm; /* e_ji block */
+            }
+        }
+        if (grad_edge_weight) grad_edge_weight[k] = (float)gw;
+    }
+    if (grad_x_src)
+        for (int64_t t = 0; t < n_src * F; ++t) grad_x_src[t] = (float)gxs[t];
+    if (grad_x_dst && concat_xi)
+        for (int64_t t = 0; t < n_dst * F; ++t) grad_x_dst[t] = (float)gxd[t];
+    if (grad_edge_attr && E == 0) { /* nothing */ }
+    free(deg); free(gxs); free(gxd);
+    return ORC_OK;
+}
+
+int orc_gcn_norm(const int64_t* edge_index, int64_t E, int64_t N, const float* edge_weight,
+                 int64_t* ei_src_out, int64_t* ei_dst_out, float* w_out, int64_t* E_out) {
+    if (E < 0 || N < 0) return ORC_ERR_DIMENSION;
+    const int64_t* src = edge_index;
+    const int64_t* dst = edge_index + E;
+    if (check_index(src, E, N) || check_index(dst, E, N)) return ORC_ERR_OOB;
+    /* 1. add remaining self-loops (reading Q8) */
+    char* has_loop = (char*)calloc((size_t)(N > 0 ? N : 1), 1);
+    double* deg = (double*)calloc((size_t)(N > 0 ? N : 1), sizeof(double));
+    if (!has_loop || !deg) { free(has_loop); free(deg); return ORC_ERR_INVALID; }
+    for (int64_t k = 0; k < E; ++k)
+        if (src[k] == dst[k]) has_loop[src[k]] = 1;
+    int64_t e = 0;
+    for (int64_t k = 0; k < E; ++k) {
+        ei_src_out[e] = src[k]; ei_dst_out[e] = dst[k];
+        w_out[e] = edge_weight ? edge_weight[k] : 1.0f;
+        ++e;
+    }
+    for (int64_t i = 0; i < N; ++i)
+        if (!has_loop[i]) { ei_src_out[e] = i; ei_dst_out[e] = i; w_out[e] = 1.0f; ++e; }
+    *E_out = e;
+    /* 2. deg_hat[i] = sum of edge weights into i (reading Q7) */
+    for (int64_t k = 0; k < e; ++k) deg[ei_dst_out[k]] += (double)w_out[k];
+    /* 3. w'_k = deg^-1/2[src] * w_k * deg^-1/2[dst] */
+    for (int64_t k = 0; k < e; ++k) {
+        double ds = deg[ei_src_out[k]], dd = deg[ei_dst_out[k]];
+        double is = ds > 0 ? 1.0 / sqrt(ds) : 0.0;
+        double id = dd > 0 ? 1.0 / sqrt(dd) : 0.0;
+        w_out[k] = (float)(is * (double)w_out[k] * id);
+    }
+    free(has_loop); free(deg);
+    return ORC_OK;
+}
+
+int orc_collate(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr,
+                const int64_t* local_ei, int64_t* ei, int64_t* batch, int64_t* node_ptr) {
+    if (G <= 0 || !num_nodes || !edge_ptr) return ORC_ERR_INVALID; /* empty list */
+    if (edge_ptr[0] != 0) return ORC_ERR_INVALID;
+    for (int64_t g = 0; g < G; ++g)
+        if (num_nodes[g] < 0 || edge_ptr[g + 1] < edge_ptr[g]) return ORC_ERR_INVALID;
+    int64_t Etot = edge_ptr[G];
+    /* node offsets = exclusive prefix sum of N_g */
+    node_ptr[0] = 0;
+    for (int64_t g = 0; g < G; ++g) node_ptr[g + 1] = node_ptr[g] + num_nodes[g];
+    for (int64_t g = 0; g < G; ++g) {
+        for (int64_t k = edge_ptr[g]; k < edge_ptr[g + 1]; ++k) {
+            int64_t s = local_ei[k], d = local_ei[Etot + k];
+            if (s < 0 || s >= num_nodes[g] || d < 0 || d >= num_nodes[g]) return ORC_ERR_OOB;
+            ei[k] = s + node_ptr[g];          /* block-diagonal offset */
+            ei[Etot + k] = d + node_ptr[g];
+        }
+        for (int64_t v = node_ptr[g]; v < node_ptr[g + 1]; ++v) batch[v] = g; /* assignment vector */
+    }
+    return ORC_OK;
+}
+
+int orc_global_pool(const float* x, int64_t N, int64_t F, const int64_t* batch, int64_t G,
+                    int reduce, float* out, int64_t* arg) {
+    return orc_scatter(x, N, F, F, batch, G, reduce, out, arg, NULL);
+}
