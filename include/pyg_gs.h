@@ -1,0 +1,252 @@
+/*
+ * pyg_gs.h -- C ABI of libpygs.so: B200 (sm_100a) gather / phi / scatter-reduce
+ * neighbourhood aggregation, the data-parallel hot path of Fey & Lenssen,
+ * "Fast Graph Representation Learning with PyTorch Geometric" (arXiv 1903.02428).
+ *
+ * Citations: P:n = PAPER.md line n (section / equation named beside it),
+ *            S:n = SPEC.md line n (interface shapes and edge-case conventions only).
+ * Readings of ambiguous passages (Q1..Q20) are listed in DESIGN.md.
+ *
+ * The method (Eq. 1, without gamma):
+ *     x'_i = BOX_{j in N(i)} phi(x_i, x_j, e_{j,i}),   BOX in {sum, mean, max}
+ * computed as gather (node -> edge space) + phi + scatter (edge -> node space)
+ * (Fig. 1), with the E x F edge space never materialised.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions shared by every entry point
+ *  - Memory: every tensor argument is a DEVICE pointer owned by the caller
+ *    (allocated e.g. by torch).  The library never allocates, frees or retains
+ *    caller memory.  Exceptions are marked (host) explicitly.  Plans
+ *    (pyg_plan_t) are small host objects created by pyg_plan_build and released
+ *    by pyg_plan_destroy; their device arrays live in caller-provided workspace.
+ *  - Layout: row-major.  A matrix argument M[n x F] has a leading dimension
+ *    ldM >= F in elements (floats); row r starts at M + r * ldM.  When
+ *    ldM >= round_up(F, 4), ldM % 4 == 0 and M is 16-byte aligned, the kernels
+ *    may READ (never use, never write) the padding columns [F, round_up(F,4))
+ *    of each row, so such buffers must span n * ldM elements.
+ *  - Indices: int64 (PyG's torch.long; P:25 I in N^{2 x E}).  edge_index is
+ *    [2 x E] row-major: row 0 = source j, row 1 = target i; messages flow
+ *    j -> i (reading Q1).  Arg outputs are int64 original edge ids.
+ *    Internally E < 2^31 and node counts < 2^31 are required
+ *    (PYG_ERR_UNSUPPORTED otherwise).
+ *  - Precision: fp32 values, fp32 accumulation (hub rows are split into chunks
+ *    and combined in fp64; reading Q12), IEEE division (no fast-math).
+ *  - Outputs are OVERWRITTEN, never accumulated into (reading Q14).
+ *  - Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Every call is asynchronous on `stream` unless documented as
+ *    synchronous.  Return codes cover host-side validation; with the
+ *    PYG_VALIDATE flag a device pre-pass checks index ranges and the call
+ *    synchronises `stream` to report PYG_ERR_INDEX_OUT_OF_BOUNDS.
+ *  - Aliasing: outputs must not alias inputs.
+ *  - Errors: a non-OK status leaves outputs unspecified; pyg_last_error()
+ *    returns a thread-local message for the last failing call.
+ */
+#ifndef PYG_GS_H
+#define PYG_GS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Aggregation BOX of Eq. (1) ("sum, mean or max"). */
+typedef enum { PYG_SUM = 0, PYG_MEAN = 1, PYG_MAX = 2 } pyg_reduce_t;
+
+typedef enum {
+    PYG_OK = 0,
+    PYG_ERR_INVALID_ARGUMENT = 1,   /* null pointer, negative size, bad flag */
+    PYG_ERR_DIMENSION = 2,          /* inconsistent shapes / leading dims */
+    PYG_ERR_INDEX_OUT_OF_BOUNDS = 3,/* an index outside its range */
+    PYG_ERR_ALIGNMENT = 4,          /* a forced vector path on unaligned data */
+    PYG_ERR_UNSUPPORTED = 5,        /* sizes beyond the int32-internal limits */
+    PYG_ERR_CUDA = 6,               /* a CUDA runtime error (message in pyg_last_error) */
+    PYG_ERR_NCCL = 7,               /* reserved for the multi-GPU layer */
+    PYG_ERR_NO_MEMORY = 8           /* workspace smaller than the size query returned */
+} pyg_status_t;
+
+/* flags */
+#define PYG_PHI_CONCAT_XI  (1u << 0)  /* message = [x_i || w x_j || e_ji] */
+#define PYG_VALIDATE       (1u << 8)  /* device index-range pre-pass; synchronous */
+#define PYG_FORCE_ATOMIC   (1u << 9)  /* ignore `plan`, use the atomic COO strategy */
+#define PYG_FORCE_SEGMENT  (1u << 10) /* require a plan (error if NULL) */
+
+typedef struct pyg_plan pyg_plan_t;   /* opaque host handle */
+
+/* Read-only view of a plan's device arrays (for tests and the Python layer). */
+typedef struct {
+    int64_t n_rows;          /* segments (targets for a forward plan) */
+    int64_t n_cols;          /* range of the gathered index (sources), 0 if none */
+    int64_t E;               /* edges in the plan (all rows, before slicing) */
+    int64_t row_offset;      /* first global row of this (possibly sliced) plan */
+    const int64_t* rowptr;   /* [n_rows + 1] absolute positions; row r = [rowptr[r], rowptr[r+1]) */
+    const int32_t* col;      /* [E] gathered index at each sorted position, or NULL */
+    const int32_t* perm;     /* [E] original edge id at each sorted position */
+    int32_t perm_is_identity;/* 1 if the input was already target-sorted */
+    int64_t n_heavy_rows;    /* rows longer than heavy_threshold (split into chunks) */
+    int64_t n_heavy_chunks;  /* chunks of at most chunk_size positions */
+    int32_t heavy_threshold;
+    int32_t chunk_size;
+} pyg_plan_view_t;
+
+/* ---- library ------------------------------------------------------------ */
+const char* pyg_version(void);
+const char* pyg_last_error(void);           /* thread-local, never NULL */
+/* Number of kernels this library has launched since it was loaded (monotonic,
+ * process-wide).  Used by bench.py to report gpu_launches. */
+uint64_t pyg_launch_count(void);
+
+/* ---- degree ------------------------------------------------- */
+/* deg[i] = #{k : index[k] == i}, i in [0, n); multi-edges and self-loops count
+ * (reading Q6).  deg: int32 [n], overwritten.  Asynchronous. */
+pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t flags, int32_t* deg,
+                        void* stream);
+
+/* ---- plan: CSR / target-sorted segments (App. A) --------------- */
+/* A plan is the stable sort of edges by `row_index` (the target for a forward
+ * plan; the source for the transposed plan the backward uses), i.e. CSR with
+ * row = target.  P:276: coalescing is "expensive to compute on
+ * GPUs and should be hence performed as part of the pre-processing" -- a plan
+ * is built once per graph and reused by every call.
+ *   row_index [E] int64 in [0, n_rows);  col_index [E] int64 in [0, n_cols)
+ *   or NULL (scatter plans: the gathered row is the edge id itself).
+ * Workspace: `bytes` from pyg_plan_workspace_size; it holds the plan's device
+ * arrays and must outlive the plan.  SYNCHRONOUS (reads back counts); returns
+ * PYG_ERR_INDEX_OUT_OF_BOUNDS if an index is out of range. */
+pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, size_t* bytes);
+pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, int64_t E,
+                            int64_t n_rows, int64_t n_cols, uint32_t flags, void* workspace,
+                            size_t bytes, pyg_plan_t** plan, void* stream);
+/* Sub-plan of rows [row_lo, row_hi) sharing the parent's arrays (dst-range
+ * partitioning for the multi-GPU layer).  Output row r of a call using the
+ * slice is global row row_lo + r; arg outputs stay GLOBAL edge ids. */
+pyg_status_t pyg_plan_slice(const pyg_plan_t* plan, int64_t row_lo, int64_t row_hi,
+                            pyg_plan_t** slice);
+pyg_status_t pyg_plan_view(const pyg_plan_t* plan, pyg_plan_view_t* view);
+/* Copy a plan's CSR arrays into caller device buffers (any may be NULL):
+ * rowptr [n_rows + 1] int64 (positions relative to the plan's first row),
+ * col [E_p] int64 and perm [E_p] int64 for the E_p positions of the plan's
+ * rows.  Asynchronous. */
+pyg_status_t pyg_plan_export(const pyg_plan_t* plan, int64_t* rowptr, int64_t* col, int64_t* perm,
+                             void* stream);
+void pyg_plan_destroy(pyg_plan_t* plan);
+
+/* Scratch needed by pyg_scatter / pyg_propagate / pyg_propagate_backward for
+ * an output of F_out columns: fp64-combined partials of split hub rows (plan
+ * path) or the in-degree array (atomic path).  bytes may be 0. */
+pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t n_out, int64_t F_out,
+                                pyg_reduce_t reduce, uint32_t flags, size_t* bytes);
+
+/* ---- scatter: edge space -> node space -------------- */
+/* out[i] = BOX_{k : index[k] = i} src[k]; empty segment -> 0 (Q2).
+ *   src [E x F] stride lds; index [E] int64 in [0, dim_size)
+ *   out [dim_size x F] stride ldo, overwritten
+ *   arg_out [dim_size x F] int64 stride ldo, REQUIRED iff reduce == PYG_MAX:
+ *     the lowest edge id attaining the max (north_star tie rule, Q4); E for
+ *     empty segments (Q3).  (On the atomic path it doubles as the 64-bit key
+ *     buffer before being decoded in place.)
+ *   plan: built with row_index = index, col_index = NULL -> deterministic
+ *     CSR segment-reduce; NULL -> atomic COO (red.global.add.v4.f32 /
+ *     64-bit atomicMax keys), non-deterministic for sum/mean. */
+pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, const int64_t* index,
+                         int64_t dim_size, pyg_reduce_t reduce, uint32_t flags, float* out,
+                         int64_t ldo, int64_t* arg_out, const pyg_plan_t* plan, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
+/* scatter backward w.r.t. src: grad_src[k] = g[index[k]] (sum),
+ * g[index[k]] / deg[index[k]] (mean, IEEE float divide), g[i] where
+ * arg_out[i] == k else 0 (max).  deg (int32 [dim_size], from pyg_degree)
+ * required for MEAN; arg_out (stride ldg) required for MAX.  Pure gather,
+ * deterministic. */
+pyg_status_t pyg_scatter_backward(const float* grad_out, int64_t ldg, const int64_t* index, int64_t E,
+                                  int64_t F, int64_t dim_size, pyg_reduce_t reduce,
+                                  const int64_t* arg_out, const int32_t* deg, float* grad_src,
+                                  int64_t lds, void* stream);
+
+/* ---- propagate: fused gather + phi + reduce (Eq. 1; Fig. 1) ----------------- */
+/* For every edge k = (j -> i) the message is
+ *     m_k = [ x_dst[i] (only if PYG_PHI_CONCAT_XI) || w_k * x_src[j] || edge_attr[k] (if D > 0) ]
+ * (phi in {identity, edge-weight scale, concatenation})
+ * and out[i] = BOX_k m_k, F_out = (CONCAT_XI ? F : 0) + F + D, computed
+ * without materialising the messages.
+ *   x_src [n_src x F] stride ldx; x_dst [n_dst x F] stride ldxd (NULL -> x_src,
+ *     requires n_dst <= n_src); edge_index [2 x E] int64 (row-major, see top);
+ *   edge_attr [E x D] stride lde or NULL (D = 0); edge_weight [E] or NULL (w=1);
+ *   out [n_dst x F_out] stride ldo; arg_out [n_dst x F_out] int64 stride ldo
+ *   (MAX only).  mean divides by the integer in-degree (Q6).
+ *   plan: forward plan (row_index = edge_index[1], col_index = edge_index[0]),
+ *   possibly a slice; NULL -> atomic COO.  workspace: pyg_workspace_size. */
+pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t ldx,
+                           const float* x_dst, int64_t ldxd, int64_t n_dst,
+                           const int64_t* edge_index, int64_t E, const float* edge_attr,
+                           int64_t D, int64_t lde, const float* edge_weight,
+                           pyg_reduce_t reduce, uint32_t flags, float* out, int64_t ldo,
+                           int64_t* arg_out, const pyg_plan_t* plan, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* propagate backward ("both for forward and backward passes", P:277;
+ * S:142).  grad_out [n_dst x F_out] stride ldg.  Outputs, each
+ * optional (NULL to skip), overwritten:
+ *   grad_x_src [n_src x F] stride ldgx:  sum_k w_k * dL/dm_k  over k with src_k = j
+ *       (mean: dL/dm_k = g[dst_k] / deg[dst_k]; max: g routed to arg_out).
+ *       With plan_T (row_index = edge_index[0], col_index = edge_index[1]) this
+ *       is a deterministic segment-reduce over sources; else atomic COO.
+ *   grad_x_dst [n_dst x F] stride ldgxd (CONCAT_XI block): deg*g (sum),
+ *       g if deg > 0 (mean, max).
+ *   grad_edge_attr [E x D] stride ldge: the e block of dL/dm_k.
+ *   grad_edge_weight [E]: sum_c x_src[j][c] * dL/dm_k[c] over the x_j block.
+ * deg_dst (int32 [n_dst], pyg_degree of edge_index[1]) is required for MEAN
+ * and for the CONCAT_XI block with SUM; arg_out (stride ldg) for MAX. */
+pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F, int64_t ldx,
+                                    int64_t n_dst, const int64_t* edge_index, int64_t E, int64_t D,
+                                    const float* edge_weight, pyg_reduce_t reduce, uint32_t flags,
+                                    const float* grad_out, int64_t ldg, const int64_t* arg_out,
+                                    const int32_t* deg_dst, float* grad_x_src, int64_t ldgx,
+                                    float* grad_x_dst, int64_t ldgxd, float* grad_edge_attr,
+                                    int64_t ldge, float* grad_edge_weight,
+                                    const pyg_plan_t* plan_T, void* workspace,
+                                    size_t workspace_bytes, void* stream);
+
+/* ---- GCN normalisation ------------------------- */
+/* Appends (i,i) with weight 1 after the E original edges, in ascending i, for
+ * every node lacking a self-loop (existing loops kept; Q8); d[i] = sum of
+ * weights into i (Q7); w'_k = d[src]^-1/2 * w_k * d[dst]^-1/2.
+ *   edge_index_out: capacity 2 x (E + N) int64; written as a packed row-major
+ *   [2 x E_out] array (targets start at edge_index_out + E_out).
+ *   weight_out: capacity E + N floats.  E_out: (host) receives E'.
+ * SYNCHRONOUS (E_out is read back).  Workspace: pyg_gcn_norm_workspace_size. */
+pyg_status_t pyg_gcn_norm_workspace_size(int64_t E, int64_t N, size_t* bytes);
+pyg_status_t pyg_gcn_norm(const int64_t* edge_index, int64_t E, int64_t N,
+                          const float* edge_weight, uint32_t flags, int64_t* edge_index_out,
+                          float* weight_out, int64_t* E_out, void* workspace, size_t bytes,
+                          void* stream);
+
+/* ---- mini-batch collate ------------------------------- */
+/* Block-diagonal batching: node_ptr = exclusive prefix sum of num_nodes
+ * (G+1 entries); edge_index[:, e] = local_edge_index[:, e] + node_ptr[g(e)]
+ * where g(e) is the graph owning column e (edge_ptr[g] <= e < edge_ptr[g+1]);
+ * batch[v] = g for node_ptr[g] <= v < node_ptr[g+1].
+ *   num_nodes [G], edge_ptr [G+1] (device, int64); local_edge_index and
+ *   edge_index [2 x E_total]; batch [N_total]; node_ptr [G+1].
+ *   E_total = edge_ptr[G] and N_total = sum num_nodes are passed by the host
+ *   (it sized the outputs).  G <= 0 -> PYG_ERR_INVALID_ARGUMENT.
+ *   With PYG_VALIDATE the call synchronises and returns
+ *   PYG_ERR_INDEX_OUT_OF_BOUNDS if a local id is outside [0, N_g) or
+ *   PYG_ERR_DIMENSION if E_total / N_total disagree with the arrays. */
+pyg_status_t pyg_collate(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr,
+                         const int64_t* local_edge_index, int64_t E_total, int64_t N_total,
+                         uint32_t flags, int64_t* edge_index, int64_t* batch, int64_t* node_ptr,
+                         void* stream);
+
+/* ---- global pooling readout ------------------------ */
+/* out[g] = BOX over nodes v in [node_ptr[g], node_ptr[g+1]) of x[v]
+ * (contiguous segments of the collated batch).  arg_out = node id (MAX). */
+pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx,
+                             const int64_t* node_ptr, int64_t G, pyg_reduce_t reduce, float* out,
+                             int64_t ldo, int64_t* arg_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PYG_GS_H */

@@ -1,0 +1,315 @@
+"""paper_1903_02428_b200 -- B200-native gather / phi / scatter-reduce aggregation
+(Fey & Lenssen, arXiv 1903.02428, Eq. 1 without gamma).
+
+Thin Python binding over the C ABI of libpygs.so (include/pyg_gs.h): each
+function has the C name, marshals torch CUDA tensors into pointers, leading
+dimensions and the current stream, allocates outputs/workspace with torch, and
+calls the library.  Every step of the path runs in the library's sm_100a
+kernels; there is no CPU or PyTorch fallback (importing fails loudly if the
+library is missing).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import torch
+
+from . import _abi
+from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, PHI_CONCAT_XI, SUM, VALIDATE, PygError, check,
+                   launch_count, lib)
+
+__all__ = [
+    "Plan", "pyg_degree", "pyg_plan_build", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
+    "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
+    "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "FORCE_SEGMENT", "version",
+]
+
+
+def version() -> str:
+    return lib.pyg_version().decode()
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device=None):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _red(reduce) -> int:
+    return _abi.REDUCE[reduce] if isinstance(reduce, str) else int(reduce)
+
+
+def _rows(x: torch.Tensor, name: str):
+    """(n, F, ld) of a 2-D float32 CUDA tensor whose rows may be strided."""
+    if x.dim() != 2:
+        raise ValueError(f"{name}: expected 2-D, got {tuple(x.shape)}")
+    if x.dtype != torch.float32 or not x.is_cuda:
+        raise ValueError(f"{name}: expected a float32 CUDA tensor")
+    if x.shape[1] > 1 and x.stride(1) != 1:
+        raise ValueError(f"{name}: columns must be contiguous")
+    ld = x.stride(0) if x.shape[0] > 1 else x.shape[1]
+    return x.shape[0], x.shape[1], max(ld, x.shape[1])
+
+
+def _i64(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.dtype != torch.int64 or not t.is_cuda:
+        raise ValueError(f"{name}: expected an int64 CUDA tensor")
+    return t.contiguous()
+
+
+def _workspace(nbytes: int, device) -> Optional[torch.Tensor]:
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+class Plan:
+    """CSR plan (stable sort of edges by `row_index`).  Owns its workspace."""
+
+    def __init__(self, handle, workspace, parent=None):
+        self._h = handle
+        self._ws = workspace
+        self._parent = parent  # keep the root's workspace alive for slices
+
+    @property
+    def handle(self):
+        return self._h
+
+    def view(self) -> dict:
+        v = _abi.PlanView()
+        check(lib.pyg_plan_view(self._h, ctypes.byref(v)), "pyg_plan_view")
+        return {f: getattr(v, f) for f, _ in _abi.PlanView._fields_}
+
+    def slice(self, lo: int, hi: int) -> "Plan":
+        h = ctypes.c_void_p()
+        check(lib.pyg_plan_slice(self._h, lo, hi, ctypes.byref(h)), "pyg_plan_slice")
+        return Plan(h, None, parent=self)
+
+    def export(self):
+        """(rowptr, col or None, perm) as int64 CUDA tensors (test helper)."""
+        v = self.view()
+        dev = self._device()
+        rowptr = torch.empty(v["n_rows"] + 1, dtype=torch.int64, device=dev)
+        check(lib.pyg_plan_export(self._h, _ptr(rowptr), None, None, _stream()), "pyg_plan_export")
+        E_p = int(rowptr[-1].item())
+        col = torch.empty(E_p, dtype=torch.int64, device=dev) if v["col"] else None
+        perm = torch.empty(E_p, dtype=torch.int64, device=dev)
+        check(lib.pyg_plan_export(self._h, None, _ptr(col), _ptr(perm), _stream()), "pyg_plan_export")
+        return rowptr, col, perm
+
+    def _device(self):
+        p = self
+        while p._ws is None:
+            p = p._parent
+        return p._ws.device
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.pyg_plan_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def pyg_plan_build(row_index: torch.Tensor, col_index: Optional[torch.Tensor], n_rows: int,
+                   n_cols: int = 0) -> Plan:
+    """Build a plan: forward plan = (edge_index[1], edge_index[0]); transposed plan for the
+    backward = (edge_index[0], edge_index[1]); scatter plan = (index, None).  Synchronous."""
+    row_index = _i64(row_index, "row_index")
+    E = row_index.numel()
+    if col_index is not None:
+        col_index = _i64(col_index, "col_index")
+        assert col_index.numel() == E
+    nb = ctypes.c_size_t()
+    check(lib.pyg_plan_workspace_size(E, n_rows, n_cols, ctypes.byref(nb)), "pyg_plan_workspace_size")
+    ws = _workspace(nb.value, row_index.device)
+    h = ctypes.c_void_p()
+    check(lib.pyg_plan_build(_ptr(row_index), _ptr(col_index), E, n_rows, n_cols, 0, _ptr(ws), nb.value,
+                             ctypes.byref(h), _stream(row_index.device)), "pyg_plan_build")
+    return Plan(h, ws)
+
+
+def pyg_workspace_size(plan: Optional[Plan], n_out: int, F_out: int, reduce, flags: int = 0) -> int:
+    nb = ctypes.c_size_t()
+    check(lib.pyg_workspace_size(plan.handle if plan else None, n_out, F_out, _red(reduce), flags,
+                                 ctypes.byref(nb)), "pyg_workspace_size")
+    return nb.value
+
+
+def pyg_degree(index: torch.Tensor, n: int, flags: int = 0) -> torch.Tensor:
+    index = _i64(index, "index")
+    deg = torch.empty(n, dtype=torch.int32, device=index.device)
+    check(lib.pyg_degree(_ptr(index), index.numel(), n, flags, _ptr(deg), _stream(index.device)), "pyg_degree")
+    return deg
+
+
+def pyg_scatter(src: torch.Tensor, index: torch.Tensor, dim_size: int, reduce="sum", plan: Optional[Plan] = None,
+                out: Optional[torch.Tensor] = None, arg_out: Optional[torch.Tensor] = None, flags: int = 0,
+                workspace: Optional[torch.Tensor] = None):
+    """scatter(src, index, reduce).  Returns out, or (out, arg) for max."""
+    E, F, lds = _rows(src, "src")
+    index = _i64(index, "index")
+    r = _red(reduce)
+    dev = src.device
+    if out is None:
+        out = torch.empty((dim_size, F), dtype=torch.float32, device=dev)
+    if r == MAX and arg_out is None:
+        arg_out = torch.empty((dim_size, F), dtype=torch.int64, device=dev)
+    _, _, ldo = _rows(out, "out")
+    if workspace is None:
+        workspace = _workspace(pyg_workspace_size(plan, dim_size, F, r, flags), dev)
+    check(lib.pyg_scatter(_ptr(src), E, F, lds, _ptr(index), dim_size, r, flags, _ptr(out), ldo, _ptr(arg_out),
+                          plan.handle if plan else None, _ptr(workspace), workspace.numel(), _stream(dev)),
+          "pyg_scatter")
+    return (out, arg_out) if r == MAX else out
+
+
+def pyg_scatter_backward(grad_out: torch.Tensor, index: torch.Tensor, reduce="sum",
+                         arg_out: Optional[torch.Tensor] = None, deg: Optional[torch.Tensor] = None,
+                         grad_src: Optional[torch.Tensor] = None):
+    dim_size, F, ldg = _rows(grad_out, "grad_out")
+    index = _i64(index, "index")
+    E = index.numel()
+    r = _red(reduce)
+    if r == MEAN and deg is None:
+        deg = pyg_degree(index, dim_size)
+    if grad_src is None:
+        grad_src = torch.empty((E, F), dtype=torch.float32, device=grad_out.device)
+    _, _, lds = _rows(grad_src, "grad_src")
+    check(lib.pyg_scatter_backward(_ptr(grad_out), ldg, _ptr(index), E, F, dim_size, r, _ptr(arg_out), _ptr(deg),
+                                   _ptr(grad_src), lds, _stream(grad_out.device)), "pyg_scatter_backward")
+    return grad_src
+
+
+def pyg_propagate(x_src: torch.Tensor, edge_index: Optional[torch.Tensor], n_dst: Optional[int] = None,
+                  reduce="sum", edge_weight: Optional[torch.Tensor] = None,
+                  edge_attr: Optional[torch.Tensor] = None, x_dst: Optional[torch.Tensor] = None,
+                  concat_xi: bool = False, plan: Optional[Plan] = None, out: Optional[torch.Tensor] = None,
+                  arg_out: Optional[torch.Tensor] = None, flags: int = 0, E: Optional[int] = None,
+                  workspace: Optional[torch.Tensor] = None):
+    """Fused gather + phi + reduce of Eq. (1).  Returns out, or (out, arg) for max."""
+    n_src, F, ldx = _rows(x_src, "x_src")
+    if n_dst is None:
+        n_dst = n_src
+    if edge_index is not None:
+        edge_index = _i64(edge_index, "edge_index")
+        assert edge_index.dim() == 2 and edge_index.shape[0] == 2
+        E = edge_index.shape[1]
+    elif E is None:
+        E = plan.view()["E"] if plan is not None else 0
+    r = _red(reduce)
+    if concat_xi:
+        flags |= PHI_CONCAT_XI
+    ldxd = 0
+    if x_dst is not None:
+        _, Fd, ldxd = _rows(x_dst, "x_dst")
+        assert Fd == F
+    D, lde = 0, 0
+    if edge_attr is not None:
+        _, D, lde = _rows(edge_attr, "edge_attr")
+    F_out = (F if concat_xi else 0) + F + D
+    dev = x_src.device
+    if out is None:
+        out = torch.empty((n_dst, F_out), dtype=torch.float32, device=dev)
+    if r == MAX and arg_out is None:
+        arg_out = torch.empty((n_dst, F_out), dtype=torch.int64, device=dev)
+    _, _, ldo = _rows(out, "out")
+    if workspace is None:
+        workspace = _workspace(pyg_workspace_size(plan, n_dst, F_out, r, flags), dev)
+    check(lib.pyg_propagate(_ptr(x_src), n_src, F, ldx, _ptr(x_dst), ldxd, n_dst, _ptr(edge_index), E,
+                            _ptr(edge_attr), D, lde, _ptr(edge_weight), r, flags, _ptr(out), ldo, _ptr(arg_out),
+                            plan.handle if plan else None, _ptr(workspace), workspace.numel(), _stream(dev)),
+          "pyg_propagate")
+    return (out, arg_out) if r == MAX else out
+
+
+def pyg_propagate_backward(x_src: Optional[torch.Tensor], edge_index: torch.Tensor, grad_out: torch.Tensor,
+                           n_src: Optional[int] = None, F: Optional[int] = None, reduce="sum",
+                           edge_weight: Optional[torch.Tensor] = None, D: int = 0, concat_xi: bool = False,
+                           arg_out: Optional[torch.Tensor] = None, deg_dst: Optional[torch.Tensor] = None,
+                           plan_T: Optional[Plan] = None, need_x_src: bool = True, need_x_dst: bool = False,
+                           need_edge_attr: bool = False, need_edge_weight: bool = False, flags: int = 0,
+                           grad_x_src: Optional[torch.Tensor] = None):
+    """Gradients of pyg_propagate.  Returns a dict."""
+    edge_index = _i64(edge_index, "edge_index")
+    E = edge_index.shape[1]
+    n_dst, F_out, ldg = _rows(grad_out, "grad_out")
+    ldx = 0
+    if x_src is not None:
+        n_src, F, ldx = _rows(x_src, "x_src")
+    assert n_src is not None and F is not None
+    r = _red(reduce)
+    if concat_xi:
+        flags |= PHI_CONCAT_XI
+    assert F_out == (F if concat_xi else 0) + F + D
+    dev = grad_out.device
+    if deg_dst is None and (r == MEAN or (concat_xi and need_x_dst)):
+        deg_dst = pyg_degree(edge_index[1], n_dst)
+    res = {}
+    gxs = grad_x_src if grad_x_src is not None else (
+        torch.empty((n_src, F), dtype=torch.float32, device=dev) if need_x_src else None)
+    gxd = torch.empty((n_dst, F), dtype=torch.float32, device=dev) if (need_x_dst and concat_xi) else None
+    gea = torch.empty((E, D), dtype=torch.float32, device=dev) if (need_edge_attr and D > 0) else None
+    gew = torch.empty(E, dtype=torch.float32, device=dev) if need_edge_weight else None
+    ws = _workspace(pyg_workspace_size(plan_T, n_src, F, SUM, flags), dev)
+    check(lib.pyg_propagate_backward(_ptr(x_src), n_src, F, ldx, n_dst, _ptr(edge_index), E, D, _ptr(edge_weight), r,
+                                     flags, _ptr(grad_out), ldg, _ptr(arg_out), _ptr(deg_dst), _ptr(gxs),
+                                     gxs.stride(0) if gxs is not None else 0, _ptr(gxd), F, _ptr(gea), D, _ptr(gew),
+                                     plan_T.handle if plan_T else None, _ptr(ws), ws.numel(), _stream(dev)),
+          "pyg_propagate_backward")
+    for k, v in (("x_src", gxs), ("x_dst", gxd), ("edge_attr", gea), ("edge_weight", gew)):
+        if v is not None:
+            res[k] = v
+    return res
+
+
+def pyg_gcn_norm(edge_index: torch.Tensor, N: int, edge_weight: Optional[torch.Tensor] = None, flags: int = 0):
+    """(edge_index' [2 x E'], w' [E']) = GCN normalisation with remaining self-loops. Synchronous."""
+    edge_index = _i64(edge_index, "edge_index")
+    E = edge_index.shape[1]
+    dev = edge_index.device
+    nb = ctypes.c_size_t()
+    check(lib.pyg_gcn_norm_workspace_size(E, N, ctypes.byref(nb)), "pyg_gcn_norm_workspace_size")
+    ws = _workspace(nb.value, dev)
+    eo = torch.empty(2 * (E + N), dtype=torch.int64, device=dev)
+    wo = torch.empty(E + N, dtype=torch.float32, device=dev)
+    e_out = ctypes.c_int64()
+    check(lib.pyg_gcn_norm(_ptr(edge_index), E, N, _ptr(edge_weight), flags, _ptr(eo), _ptr(wo),
+                           ctypes.byref(e_out), _ptr(ws), nb.value, _stream(dev)), "pyg_gcn_norm")
+    e = e_out.value
+    return eo[:2 * e].view(2, e), wo[:e]
+
+
+def pyg_collate(num_nodes: torch.Tensor, edge_ptr: torch.Tensor, local_edge_index: torch.Tensor,
+                N_total: Optional[int] = None, flags: int = 0):
+    """Block-diagonal mini-batch: (edge_index, batch, node_ptr)."""
+    num_nodes = _i64(num_nodes, "num_nodes")
+    edge_ptr = _i64(edge_ptr, "edge_ptr")
+    local_edge_index = _i64(local_edge_index, "local_edge_index")
+    G = num_nodes.numel()
+    E_total = local_edge_index.shape[1] if local_edge_index.dim() == 2 else 0
+    if N_total is None:
+        N_total = int(num_nodes.sum().item()) if G > 0 else 0
+    dev = num_nodes.device
+    ei = torch.empty((2, E_total), dtype=torch.int64, device=dev)
+    batch = torch.empty(N_total, dtype=torch.int64, device=dev)
+    node_ptr = torch.empty(G + 1, dtype=torch.int64, device=dev)
+    check(lib.pyg_collate(G, _ptr(num_nodes), _ptr(edge_ptr), _ptr(local_edge_index), E_total, N_total, flags,
+                          _ptr(ei), _ptr(batch), _ptr(node_ptr), _stream(dev)), "pyg_collate")
+    return ei, batch, node_ptr
+
+
+def pyg_global_pool(x: torch.Tensor, node_ptr: torch.Tensor, reduce="sum"):
+    """Global add/mean/max pooling over contiguous graphs."""
+    N, F, ldx = _rows(x, "x")
+    node_ptr = _i64(node_ptr, "node_ptr")
+    G = node_ptr.numel() - 1
+    r = _red(reduce)
+    out = torch.empty((G, F), dtype=torch.float32, device=x.device)
+    arg = torch.empty((G, F), dtype=torch.int64, device=x.device) if r == MAX else None
+    check(lib.pyg_global_pool(_ptr(x), N, F, ldx, _ptr(node_ptr), G, r, _ptr(out), F, _ptr(arg), _stream(x.device)),
+          "pyg_global_pool")
+    return (out, arg) if r == MAX else out

@@ -1,0 +1,441 @@
+// api.cu -- the extern "C" boundary of libpygs.so (include/pyg_gs.h): host-side
+// validation, strategy selection (plan => CSR segment-reduce, no plan => atomic
+// COO) and the launch sequence of each call.  No compute happens here.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include <mutex>
+#include <string>
+
+#include "kernels.cuh"
+
+namespace pyg {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_err;
+
+void set_error(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+}
+
+pyg_status_t fail(pyg_status_t st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return st;
+}
+
+pyg_status_t cuda_check(cudaError_t e, const char* what) {
+    return fail(PYG_ERR_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+}
+
+static std::mutex g_flag_mu;
+static int* g_flag = nullptr;
+
+int* validate_flag_dev() {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    if (!g_flag) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&g_flag), sizeof(int),
+                          cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+            g_flag = nullptr;
+            return nullptr;
+        }
+        *g_flag = 0;
+    }
+    return g_flag;  // UVA: the host pointer is valid on the device
+}
+
+pyg_status_t validate_flag_check(cudaStream_t s, const char* what) {
+    PYG_CUDA(cudaStreamSynchronize(s));
+    int* f = validate_flag_dev();
+    const int v = f ? *f : 0;
+    if (f) *f = 0;
+    if (v == 1) return fail(PYG_ERR_INDEX_OUT_OF_BOUNDS, "%s", what);
+    if (v == 2) return fail(PYG_ERR_DIMENSION, "%s", what);
+    return PYG_OK;
+}
+
+// defined in plan.cu / misc.cu
+pyg_status_t plan_workspace(int64_t E, int64_t n_rows, size_t* bytes);
+pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, int64_t n_rows, int64_t n_cols,
+                             void* ws, size_t bytes, pyg_plan** out, cudaStream_t s);
+pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out);
+pyg_status_t plan_export_impl(const pyg_plan* p, int64_t* rowptr, int64_t* col, int64_t* perm, cudaStream_t s);
+pyg_status_t gcn_norm_impl(const int64_t* ei, int64_t E, int64_t N, const float* w, int64_t* eo, float* wo,
+                           int64_t* E_out, void* ws, size_t bytes, cudaStream_t s, size_t* need);
+pyg_status_t collate_impl(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr, const int64_t* local,
+                          int64_t Et, int64_t Nt, uint32_t flags, int64_t* ei, int64_t* batch, int64_t* node_ptr,
+                          cudaStream_t s);
+
+constexpr int64_t kMaxI32 = 0x7fffffffLL - 1;
+
+static size_t coo_ws_bytes(int64_t n_out) { return 2 * align_up((size_t)std::max<int64_t>(n_out, 1) * 4, 256); }
+
+static bool use_plan(const pyg_plan* plan, uint32_t flags) { return plan && !(flags & PYG_FORCE_ATOMIC); }
+
+}  // namespace pyg
+
+using namespace pyg;
+
+#define REQUIRE(cond, st, ...)                   \
+    do {                                         \
+        if (!(cond)) return fail(st, __VA_ARGS__); \
+    } while (0)
+
+extern "C" {
+
+const char* pyg_version(void) { return "pygs 0.1.0 (sm_100a)"; }
+const char* pyg_last_error(void) { return t_err.c_str(); }
+uint64_t pyg_launch_count(void) { return g_launches.load(); }
+
+pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t flags, int32_t* deg, void* stream) {
+    REQUIRE(E >= 0 && n >= 0, PYG_ERR_INVALID_ARGUMENT, "degree: negative size");
+    REQUIRE((E == 0 || index) && (n == 0 || deg), PYG_ERR_INVALID_ARGUMENT, "degree: null pointer");
+    REQUIRE(E <= kMaxI32 && n <= kMaxI32, PYG_ERR_UNSUPPORTED, "degree: sizes must be < 2^31");
+    cudaStream_t s = as_stream(stream);
+    if (flags & PYG_VALIDATE) {
+        PYG_TRY(validate_index(index, E, 0, n, s));
+        PYG_TRY(validate_flag_check(s, "degree: index out of range"));
+    }
+    return coo_degree(index, E, n, deg, nullptr, s);
+}
+
+pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, size_t* bytes) {
+    REQUIRE(bytes && E >= 0 && n_rows >= 0 && n_cols >= 0, PYG_ERR_INVALID_ARGUMENT, "plan_workspace_size: bad args");
+    REQUIRE(E <= kMaxI32 && n_rows <= kMaxI32 && n_cols <= kMaxI32, PYG_ERR_UNSUPPORTED, "plan: sizes must be < 2^31");
+    return plan_workspace(E, n_rows, bytes);
+}
+
+pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, int64_t E, int64_t n_rows,
+                            int64_t n_cols, uint32_t flags, void* workspace, size_t bytes, pyg_plan_t** plan,
+                            void* stream) {
+    (void)flags;
+    REQUIRE(plan && E >= 0 && n_rows >= 0 && n_cols >= 0, PYG_ERR_INVALID_ARGUMENT, "plan_build: bad args");
+    REQUIRE(E == 0 || row_index, PYG_ERR_INVALID_ARGUMENT, "plan_build: null row_index");
+    REQUIRE(E <= kMaxI32 && n_rows <= kMaxI32 && n_cols <= kMaxI32, PYG_ERR_UNSUPPORTED, "plan: sizes must be < 2^31");
+    *plan = nullptr;
+    return plan_build_impl(row_index, col_index, E, n_rows, n_cols, workspace, bytes, plan, as_stream(stream));
+}
+
+pyg_status_t pyg_plan_slice(const pyg_plan_t* plan, int64_t lo, int64_t hi, pyg_plan_t** slice) {
+    REQUIRE(plan && slice, PYG_ERR_INVALID_ARGUMENT, "plan_slice: null");
+    REQUIRE(0 <= lo && lo <= hi && hi <= plan->n_rows, PYG_ERR_DIMENSION, "plan_slice: rows [%lld, %lld) outside [0, %lld)",
+            (long long)lo, (long long)hi, (long long)plan->n_rows);
+    return plan_slice_impl(plan, lo, hi, slice);
+}
+
+pyg_status_t pyg_plan_view(const pyg_plan_t* p, pyg_plan_view_t* v) {
+    REQUIRE(p && v, PYG_ERR_INVALID_ARGUMENT, "plan_view: null");
+    v->n_rows = p->n_rows;
+    v->n_cols = p->n_cols;
+    v->E = p->E;
+    v->row_offset = p->row_offset;
+    v->rowptr = p->rowptr;
+    v->col = p->col;
+    v->perm = p->perm;
+    v->perm_is_identity = p->perm_identity;
+    v->n_heavy_rows = p->h_hi - p->h_lo;
+    v->n_heavy_chunks = p->item_hi - p->item_lo;
+    v->heavy_threshold = p->heavy_threshold;
+    v->chunk_size = p->chunk;
+    return PYG_OK;
+}
+
+void pyg_plan_destroy(pyg_plan_t* p) { delete p; }
+
+pyg_status_t pyg_plan_export(const pyg_plan_t* p, int64_t* rowptr, int64_t* col, int64_t* perm, void* stream) {
+    REQUIRE(p, PYG_ERR_INVALID_ARGUMENT, "plan_export: null plan");
+    REQUIRE(!col || p->col, PYG_ERR_INVALID_ARGUMENT, "plan_export: plan has no col array");
+    return plan_export_impl(p, rowptr, col, perm, as_stream(stream));
+}
+
+pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t n_out, int64_t F_out, pyg_reduce_t reduce,
+                                uint32_t flags, size_t* bytes) {
+    REQUIRE(bytes && n_out >= 0 && F_out >= 0, PYG_ERR_INVALID_ARGUMENT, "workspace_size: bad args");
+    size_t b = coo_ws_bytes(n_out);
+    if (use_plan(plan, flags)) b = std::max(b, segment_ws_bytes(plan, F_out, (int)reduce));
+    *bytes = b + 256;
+    return PYG_OK;
+}
+
+pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, const int64_t* index, int64_t dim_size,
+                         pyg_reduce_t reduce, uint32_t flags, float* out, int64_t ldo, int64_t* arg_out,
+                         const pyg_plan_t* plan, void* ws, size_t ws_bytes, void* stream) {
+    REQUIRE(E >= 0 && F >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "scatter: negative size");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "scatter: bad reduce");
+    REQUIRE(lds >= F && ldo >= F, PYG_ERR_DIMENSION, "scatter: leading dimension < F");
+    REQUIRE(E <= kMaxI32 && dim_size <= kMaxI32 && F <= kMaxI32, PYG_ERR_UNSUPPORTED, "scatter: sizes must be < 2^31");
+    REQUIRE((E == 0 || F == 0 || src) && (E == 0 || index) && (dim_size * F == 0 || out), PYG_ERR_INVALID_ARGUMENT,
+            "scatter: null pointer");
+    REQUIRE(reduce != PYG_MAX || dim_size * F == 0 || arg_out, PYG_ERR_INVALID_ARGUMENT, "scatter: max needs arg_out");
+    REQUIRE(!(flags & PYG_FORCE_SEGMENT) || plan, PYG_ERR_INVALID_ARGUMENT, "scatter: FORCE_SEGMENT without plan");
+    cudaStream_t s = as_stream(stream);
+    if (flags & PYG_VALIDATE) {
+        PYG_TRY(validate_index(index, E, 0, dim_size, s));
+        PYG_TRY(validate_flag_check(s, "scatter: index out of range"));
+    }
+    if (dim_size == 0 || F == 0) return PYG_OK;
+    if (use_plan(plan, flags)) {
+        REQUIRE(plan->n_rows == dim_size && plan->col == nullptr, PYG_ERR_DIMENSION,
+                "scatter: plan is not a scatter plan over dim_size rows");
+        SegArgs a;
+        a.X = src; a.ldx = lds; a.ncols = (int)F;
+        a.rowptr = plan->rowptr;
+        a.eid = plan->perm_identity ? nullptr : plan->perm;
+        a.out = out; a.ldo = ldo; a.arg = arg_out; a.lda = ldo;
+        a.n_rows = dim_size; a.E_sentinel = E;
+        a.heavy_threshold = plan->heavy_threshold;
+        return segment_reduce(a, reduce, plan, ws, ws_bytes, s);
+    }
+    CooArgs c;
+    c.X = src; c.ldx = lds; c.ncols = (int)F;
+    c.sidx = index;
+    c.out = out; c.ldo = ldo;
+    c.keys = reinterpret_cast<unsigned long long*>(arg_out); c.ldk = ldo;
+    c.E = E; c.n_out = dim_size;
+    PYG_TRY(coo_reduce(c, reduce, s));
+    if (reduce == PYG_MEAN) {
+        Carver cv(ws, ws_bytes);
+        int32_t* deg = cv.take<int32_t>((size_t)dim_size);
+        REQUIRE(ws && cv.ok(), PYG_ERR_NO_MEMORY, "scatter: workspace too small for mean");
+        PYG_TRY(coo_degree(index, E, dim_size, deg, nullptr, s));
+        PYG_TRY(mean_divide(out, ldo, (int)F, dim_size, deg, s));
+    } else if (reduce == PYG_MAX) {
+        PYG_TRY(max_decode(c.keys, ldo, out, ldo, (int)F, dim_size, E, s));
+    }
+    return PYG_OK;
+}
+
+pyg_status_t pyg_scatter_backward(const float* grad_out, int64_t ldg, const int64_t* index, int64_t E, int64_t F,
+                                  int64_t dim_size, pyg_reduce_t reduce, const int64_t* arg_out, const int32_t* deg,
+                                  float* grad_src, int64_t lds, void* stream) {
+    REQUIRE(E >= 0 && F >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "scatter_backward: negative size");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "scatter_backward: bad reduce");
+    REQUIRE(ldg >= F && lds >= F, PYG_ERR_DIMENSION, "scatter_backward: leading dimension < F");
+    REQUIRE(E <= kMaxI32 && F <= kMaxI32, PYG_ERR_UNSUPPORTED, "scatter_backward: sizes must be < 2^31");
+    REQUIRE(E * F == 0 || (grad_out && index && grad_src), PYG_ERR_INVALID_ARGUMENT, "scatter_backward: null pointer");
+    REQUIRE(reduce != PYG_MEAN || deg, PYG_ERR_INVALID_ARGUMENT, "scatter_backward: mean needs deg");
+    REQUIRE(reduce != PYG_MAX || arg_out, PYG_ERR_INVALID_ARGUMENT, "scatter_backward: max needs arg_out");
+    return edge_gather_grad(grad_out, ldg, index, E, (int)F, reduce, arg_out, ldg, deg, grad_src, lds,
+                            as_stream(stream));
+}
+
+pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t ldx, const float* x_dst, int64_t ldxd,
+                           int64_t n_dst, const int64_t* edge_index, int64_t E, const float* edge_attr, int64_t D,
+                           int64_t lde, const float* edge_weight, pyg_reduce_t reduce, uint32_t flags, float* out,
+                           int64_t ldo, int64_t* arg_out, const pyg_plan_t* plan, void* ws, size_t ws_bytes,
+                           void* stream) {
+    const bool cat = flags & PYG_PHI_CONCAT_XI;
+    REQUIRE(n_src >= 0 && F >= 0 && n_dst >= 0 && E >= 0 && D >= 0, PYG_ERR_INVALID_ARGUMENT, "propagate: negative size");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "propagate: bad reduce");
+    const int64_t F_out = (cat ? F : 0) + F + D;
+    REQUIRE(ldx >= F && ldo >= F_out && (D == 0 || lde >= D), PYG_ERR_DIMENSION, "propagate: leading dimension too small");
+    REQUIRE(!cat || x_dst || n_dst <= n_src, PYG_ERR_DIMENSION, "propagate: concat x_i with x_dst=NULL needs n_dst <= n_src");
+    if (cat && x_dst) REQUIRE(ldxd >= F, PYG_ERR_DIMENSION, "propagate: ldxd < F");
+    REQUIRE(E <= kMaxI32 && n_src <= kMaxI32 && n_dst <= kMaxI32 && F_out <= kMaxI32, PYG_ERR_UNSUPPORTED,
+            "propagate: sizes must be < 2^31");
+    REQUIRE(n_dst * F_out == 0 || out, PYG_ERR_INVALID_ARGUMENT, "propagate: null out");
+    REQUIRE(reduce != PYG_MAX || n_dst * F_out == 0 || arg_out, PYG_ERR_INVALID_ARGUMENT, "propagate: max needs arg_out");
+    REQUIRE(E == 0 || F == 0 || x_src, PYG_ERR_INVALID_ARGUMENT, "propagate: null x_src");
+    REQUIRE(E == 0 || D == 0 || edge_attr, PYG_ERR_INVALID_ARGUMENT, "propagate: null edge_attr");
+    REQUIRE(!(flags & PYG_FORCE_SEGMENT) || plan, PYG_ERR_INVALID_ARGUMENT, "propagate: FORCE_SEGMENT without plan");
+    const bool seg = use_plan(plan, flags);
+    REQUIRE(seg || E == 0 || edge_index, PYG_ERR_INVALID_ARGUMENT, "propagate: null edge_index without plan");
+    cudaStream_t s = as_stream(stream);
+    if ((flags & PYG_VALIDATE) && edge_index) {
+        PYG_TRY(validate_index(edge_index, E, 0, n_src, s));
+        PYG_TRY(validate_index(edge_index + E, E, 0, n_dst, s));
+        PYG_TRY(validate_flag_check(s, "propagate: edge_index out of range"));
+    }
+    if (n_dst == 0 || F_out == 0) return PYG_OK;
+    const float* xd = x_dst ? x_dst : x_src;
+    const int64_t ldd = x_dst ? ldxd : ldx;
+    const int64_t off1 = cat ? F : 0, off2 = off1 + F;
+
+    if (seg) {
+        REQUIRE(plan->n_rows == n_dst && plan->col != nullptr && plan->n_cols <= n_src, PYG_ERR_DIMENSION,
+                "propagate: plan does not match (n_rows %lld vs n_dst %lld)", (long long)plan->n_rows, (long long)n_dst);
+        const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
+        if (cat) PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, plan->rowptr, eid, nullptr, nullptr, reduce, out, ldo, arg_out,
+                                  ldo, E, s));
+        if (F > 0) {
+            SegArgs a;
+            a.X = x_src; a.ldx = ldx; a.ncols = (int)F;
+            a.rowptr = plan->rowptr; a.gidx = plan->col; a.eid = eid; a.w = edge_weight;
+            a.out = out + off1; a.ldo = ldo; a.arg = arg_out ? arg_out + off1 : nullptr; a.lda = ldo;
+            a.n_rows = n_dst; a.E_sentinel = E; a.heavy_threshold = plan->heavy_threshold;
+            a.allow_pad_read = 1;
+            PYG_TRY(segment_reduce(a, reduce, plan, ws, ws_bytes, s));
+        }
+        if (D > 0) {
+            SegArgs a;
+            a.X = edge_attr; a.ldx = lde; a.ncols = (int)D;
+            a.rowptr = plan->rowptr; a.gidx = nullptr; a.eid = eid;
+            a.out = out + off2; a.ldo = ldo; a.arg = arg_out ? arg_out + off2 : nullptr; a.lda = ldo;
+            a.n_rows = n_dst; a.E_sentinel = E; a.heavy_threshold = plan->heavy_threshold;
+            PYG_TRY(segment_reduce(a, reduce, plan, ws, ws_bytes, s));
+        }
+        return PYG_OK;
+    }
+
+    // atomic COO
+    Carver cv(ws, ws_bytes);
+    int32_t* deg = cv.take<int32_t>((size_t)n_dst);
+    int32_t* first = cv.take<int32_t>((size_t)n_dst);
+    const bool need_deg = cat || reduce == PYG_MEAN;
+    if (need_deg) {
+        REQUIRE(ws && cv.ok(), PYG_ERR_NO_MEMORY, "propagate: workspace too small (see pyg_workspace_size)");
+        PYG_TRY(coo_degree(edge_index + E, E, n_dst, deg, (cat && reduce == PYG_MAX) ? first : nullptr, s));
+    }
+    if (cat) PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, nullptr, nullptr, deg, first, reduce, out, ldo, arg_out, ldo, E, s));
+    auto block = [&](const float* X, int64_t ld, int64_t nc, const int64_t* gidx, const float* w, int64_t off) -> pyg_status_t {
+        CooArgs c;
+        c.X = X; c.ldx = ld; c.ncols = (int)nc;
+        c.gidx = gidx; c.sidx = edge_index + E; c.w = w;
+        c.out = out + off; c.ldo = ldo;
+        c.keys = arg_out ? reinterpret_cast<unsigned long long*>(arg_out + off) : nullptr; c.ldk = ldo;
+        c.E = E; c.n_out = n_dst;
+        c.allow_pad_read = (X == x_src);
+        PYG_TRY(coo_reduce(c, reduce, s));
+        if (reduce == PYG_MEAN) PYG_TRY(mean_divide(out + off, ldo, (int)nc, n_dst, deg, s));
+        if (reduce == PYG_MAX) PYG_TRY(max_decode(c.keys, ldo, out + off, ldo, (int)nc, n_dst, E, s));
+        return PYG_OK;
+    };
+    if (F > 0) PYG_TRY(block(x_src, ldx, F, edge_index, edge_weight, off1));
+    if (D > 0) PYG_TRY(block(edge_attr, lde, D, nullptr, nullptr, off2));
+    return PYG_OK;
+}
+
+pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F, int64_t ldx, int64_t n_dst,
+                                    const int64_t* edge_index, int64_t E, int64_t D, const float* edge_weight,
+                                    pyg_reduce_t reduce, uint32_t flags, const float* grad_out, int64_t ldg,
+                                    const int64_t* arg_out, const int32_t* deg_dst, float* grad_x_src, int64_t ldgx,
+                                    float* grad_x_dst, int64_t ldgxd, float* grad_edge_attr, int64_t ldge,
+                                    float* grad_edge_weight, const pyg_plan_t* plan_T, void* ws, size_t ws_bytes,
+                                    void* stream) {
+    const bool cat = flags & PYG_PHI_CONCAT_XI;
+    REQUIRE(n_src >= 0 && F >= 0 && n_dst >= 0 && E >= 0 && D >= 0, PYG_ERR_INVALID_ARGUMENT,
+            "propagate_backward: negative size");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "propagate_backward: bad reduce");
+    const int64_t F_out = (cat ? F : 0) + F + D;
+    REQUIRE(ldg >= F_out, PYG_ERR_DIMENSION, "propagate_backward: ldg < F_out");
+    REQUIRE(E <= kMaxI32 && n_src <= kMaxI32 && n_dst <= kMaxI32 && F_out <= kMaxI32, PYG_ERR_UNSUPPORTED,
+            "propagate_backward: sizes must be < 2^31");
+    REQUIRE(n_dst * F_out == 0 || grad_out, PYG_ERR_INVALID_ARGUMENT, "propagate_backward: null grad_out");
+    REQUIRE(E == 0 || edge_index, PYG_ERR_INVALID_ARGUMENT, "propagate_backward: null edge_index");
+    REQUIRE(reduce != PYG_MAX || n_dst * F_out == 0 || arg_out, PYG_ERR_INVALID_ARGUMENT,
+            "propagate_backward: max needs arg_out");
+    REQUIRE(!(reduce == PYG_MEAN || (cat && reduce == PYG_SUM && grad_x_dst)) || deg_dst || n_dst == 0,
+            PYG_ERR_INVALID_ARGUMENT, "propagate_backward: deg_dst required");
+    cudaStream_t s = as_stream(stream);
+    if (flags & PYG_VALIDATE) {
+        PYG_TRY(validate_index(edge_index, E, 0, n_src, s));
+        PYG_TRY(validate_index(edge_index + E, E, 0, n_dst, s));
+        PYG_TRY(validate_flag_check(s, "propagate_backward: edge_index out of range"));
+    }
+    const int64_t off1 = cat ? F : 0, off2 = off1 + F;
+    const int64_t* src = edge_index;
+    const int64_t* dst = edge_index ? edge_index + E : nullptr;
+    const int64_t* argx = arg_out ? arg_out + off1 : nullptr;
+
+    if (cat && grad_x_dst) {
+        REQUIRE(ldgxd >= F, PYG_ERR_DIMENSION, "propagate_backward: ldgxd < F");
+        PYG_TRY(xdst_grad(grad_out, ldg, (int)F, n_dst, deg_dst, arg_out, ldg, E, reduce, grad_x_dst, ldgxd, s));
+    }
+    if (grad_x_src && F > 0 && n_src > 0) {
+        REQUIRE(ldgx >= F, PYG_ERR_DIMENSION, "propagate_backward: ldgx < F");
+        if (reduce == PYG_MAX) {
+            PYG_TRY(fill_rows(grad_x_src, ldgx, (int)F, n_src, s));
+            PYG_TRY(max_route_grad(grad_out + off1, ldg, argx, ldg, (int)F, n_dst, src, edge_weight, E, grad_x_src,
+                                   ldgx, s));
+        } else if (use_plan(plan_T, flags)) {
+            REQUIRE(plan_T->n_rows == n_src && plan_T->col != nullptr && plan_T->n_cols <= n_dst, PYG_ERR_DIMENSION,
+                    "propagate_backward: plan_T must be built with row_index = sources, col_index = targets");
+            SegArgs a;
+            a.X = grad_out + off1; a.ldx = ldg; a.ncols = (int)F;
+            a.rowptr = plan_T->rowptr; a.gidx = plan_T->col;
+            a.eid = plan_T->perm_identity ? nullptr : plan_T->perm;
+            a.w = edge_weight; a.gdeg = reduce == PYG_MEAN ? deg_dst : nullptr;
+            a.out = grad_x_src; a.ldo = ldgx; a.n_rows = n_src; a.E_sentinel = E;
+            a.heavy_threshold = plan_T->heavy_threshold;
+            PYG_TRY(segment_reduce(a, PYG_SUM, plan_T, ws, ws_bytes, s));
+        } else {
+            CooArgs c;
+            c.X = grad_out + off1; c.ldx = ldg; c.ncols = (int)F;
+            c.gidx = dst; c.sidx = src; c.w = edge_weight; c.gdeg = reduce == PYG_MEAN ? deg_dst : nullptr;
+            c.out = grad_x_src; c.ldo = ldgx; c.E = E; c.n_out = n_src;
+            PYG_TRY(coo_reduce(c, PYG_SUM, s));
+        }
+    }
+    if (grad_edge_attr && D > 0) {
+        REQUIRE(ldge >= D, PYG_ERR_DIMENSION, "propagate_backward: ldge < D");
+        PYG_TRY(edge_gather_grad(grad_out + off2, ldg, dst, E, (int)D, reduce, arg_out ? arg_out + off2 : nullptr, ldg,
+                                 deg_dst, grad_edge_attr, ldge, s));
+    }
+    if (grad_edge_weight) {
+        REQUIRE(x_src && ldx >= F, PYG_ERR_INVALID_ARGUMENT, "propagate_backward: grad_edge_weight needs x_src");
+        PYG_TRY(edge_weight_grad(x_src, ldx, grad_out + off1, ldg, argx, ldg, edge_index, E, (int)F, reduce, deg_dst,
+                                 grad_edge_weight, s));
+    }
+    return PYG_OK;
+}
+
+pyg_status_t pyg_gcn_norm_workspace_size(int64_t E, int64_t N, size_t* bytes) {
+    REQUIRE(bytes && E >= 0 && N >= 0, PYG_ERR_INVALID_ARGUMENT, "gcn_norm_workspace_size: bad args");
+    return gcn_norm_impl(nullptr, E, N, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, bytes);
+}
+
+pyg_status_t pyg_gcn_norm(const int64_t* edge_index, int64_t E, int64_t N, const float* edge_weight, uint32_t flags,
+                          int64_t* edge_index_out, float* weight_out, int64_t* E_out, void* ws, size_t bytes,
+                          void* stream) {
+    REQUIRE(E >= 0 && N >= 0 && E_out, PYG_ERR_INVALID_ARGUMENT, "gcn_norm: bad args");
+    REQUIRE(E + N == 0 || (edge_index_out && weight_out), PYG_ERR_INVALID_ARGUMENT, "gcn_norm: null output");
+    REQUIRE(E == 0 || edge_index, PYG_ERR_INVALID_ARGUMENT, "gcn_norm: null edge_index");
+    REQUIRE(E + N <= kMaxI32, PYG_ERR_UNSUPPORTED, "gcn_norm: sizes must be < 2^31");
+    cudaStream_t s = as_stream(stream);
+    if (flags & PYG_VALIDATE) {
+        PYG_TRY(validate_index(edge_index, 2 * E, 0, N, s));
+        PYG_TRY(validate_flag_check(s, "gcn_norm: edge_index out of range"));
+    }
+    return gcn_norm_impl(edge_index, E, N, edge_weight, edge_index_out, weight_out, E_out, ws, bytes, s, nullptr);
+}
+
+pyg_status_t pyg_collate(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr, const int64_t* local_edge_index,
+                         int64_t E_total, int64_t N_total, uint32_t flags, int64_t* edge_index, int64_t* batch,
+                         int64_t* node_ptr, void* stream) {
+    REQUIRE(G > 0, PYG_ERR_INVALID_ARGUMENT, "collate: empty list of graphs (G <= 0)");
+    REQUIRE(E_total >= 0 && N_total >= 0, PYG_ERR_INVALID_ARGUMENT, "collate: negative size");
+    REQUIRE(num_nodes && edge_ptr && node_ptr, PYG_ERR_INVALID_ARGUMENT, "collate: null pointer");
+    REQUIRE(E_total == 0 || (local_edge_index && edge_index), PYG_ERR_INVALID_ARGUMENT, "collate: null edge arrays");
+    REQUIRE(N_total == 0 || batch, PYG_ERR_INVALID_ARGUMENT, "collate: null batch");
+    return collate_impl(G, num_nodes, edge_ptr, local_edge_index, E_total, N_total, flags, edge_index, batch, node_ptr,
+                        as_stream(stream));
+}
+
+pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx, const int64_t* node_ptr, int64_t G,
+                             pyg_reduce_t reduce, float* out, int64_t ldo, int64_t* arg_out, void* stream) {
+    REQUIRE(N >= 0 && F >= 0 && G >= 0, PYG_ERR_INVALID_ARGUMENT, "global_pool: negative size");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "global_pool: bad reduce");
+    REQUIRE(ldx >= F && ldo >= F, PYG_ERR_DIMENSION, "global_pool: leading dimension < F");
+    REQUIRE(N <= kMaxI32 && F <= kMaxI32, PYG_ERR_UNSUPPORTED, "global_pool: sizes must be < 2^31");
+    REQUIRE(G * F == 0 || (out && node_ptr), PYG_ERR_INVALID_ARGUMENT, "global_pool: null pointer");
+    REQUIRE(reduce != PYG_MAX || G * F == 0 || arg_out, PYG_ERR_INVALID_ARGUMENT, "global_pool: max needs arg_out");
+    if (G == 0 || F == 0) return PYG_OK;
+    SegArgs a;
+    a.X = x; a.ldx = ldx; a.ncols = (int)F;
+    a.rowptr = node_ptr;
+    a.out = out; a.ldo = ldo; a.arg = arg_out; a.lda = ldo;
+    a.n_rows = G; a.E_sentinel = N;
+    a.heavy_threshold = INT64_MAX;
+    return segment_reduce(a, reduce, nullptr, nullptr, 0, as_stream(stream));
+}
+
+}  // extern "C"

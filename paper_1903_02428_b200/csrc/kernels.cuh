@@ -1,0 +1,103 @@
+// kernels.cuh -- internal launch interfaces of libpygs (not part of the ABI).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+// Host-side plan object (opaque in the ABI).
+struct pyg_plan {
+    int64_t n_rows = 0, n_cols = 0, E = 0, row_offset = 0;
+    const int64_t* rowptr = nullptr;  // offset by row_offset for slices
+    const int32_t* col = nullptr;     // [E] or null
+    const int32_t* perm = nullptr;    // [E]
+    int perm_identity = 0;
+    // split hub rows ("heavy"): global arrays of the root plan
+    const int32_t* heavy_rows = nullptr;      // [n_heavy_total] global row ids, ascending
+    const int64_t* heavy_item_ptr = nullptr;  // [n_heavy_total + 1]
+    std::vector<int32_t> h_heavy_rows;
+    std::vector<int64_t> h_heavy_item_ptr;
+    int64_t h_lo = 0, h_hi = 0;        // heavy rows of this plan: [h_lo, h_hi)
+    int64_t item_lo = 0, item_hi = 0;  // chunks of this plan
+    int32_t heavy_threshold = 0, chunk = 0;
+};
+
+namespace pyg {
+
+constexpr int kHeavyThreshold = 2048;  // rows longer than this are split (reading Q12)
+constexpr int kChunk = 2048;           // positions per chunk of a split row
+
+// ---- CSR segment-reduce ---------------------------------------------------------
+struct SegArgs {
+    const float* X = nullptr;  // gathered matrix, column offset applied
+    int64_t ldx = 0;
+    int ncols = 0;             // valid columns of this block
+    const int64_t* rowptr = nullptr;
+    const int32_t* gidx = nullptr;  // gathered row per position (null -> edge id)
+    const int32_t* eid = nullptr;   // edge id per position (null -> position)
+    const float* w = nullptr;       // per edge id
+    const int32_t* gdeg = nullptr;  // divisor per gathered row (mean backward)
+    float* out = nullptr;           // column offset applied
+    int64_t ldo = 0;
+    int64_t* arg = nullptr;         // MAX, stride lda, column offset applied
+    int64_t lda = 0;
+    int64_t n_rows = 0;
+    int64_t E_sentinel = 0;
+    int64_t heavy_threshold = 0;    // light pass skips rows longer than this
+    int allow_pad_read = 0;         // X rows may be read up to round_up(ncols, 4)
+};
+// Full segment reduce of a block of columns: light rows, split hub rows (plan
+// may be null for plan-free segment inputs such as pooling), fp64 combine.
+pyg_status_t segment_reduce(const SegArgs& a, int reduce, const pyg_plan* plan, void* ws,
+                            size_t ws_bytes, cudaStream_t s);
+size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce);
+
+// ---- atomic COO --------------------------------------------------------------------
+struct CooArgs {
+    const float* X = nullptr;
+    int64_t ldx = 0;
+    int ncols = 0;
+    const int64_t* gidx = nullptr;  // gathered row per edge (null -> edge id)
+    const int64_t* sidx = nullptr;  // scatter target per edge
+    const float* w = nullptr;
+    const int32_t* gdeg = nullptr;
+    float* out = nullptr;  // SUM / MEAN accumulation target (zeroed by the launcher)
+    int64_t ldo = 0;
+    unsigned long long* keys = nullptr;  // MAX keys (zeroed by the launcher)
+    int64_t ldk = 0;
+    int64_t E = 0;
+    int64_t n_out = 0;
+    int allow_pad_read = 0;
+};
+pyg_status_t coo_reduce(const CooArgs& a, int reduce, cudaStream_t s);
+// counts (and first edge id) per target for the COO path
+pyg_status_t coo_degree(const int64_t* sidx, int64_t E, int64_t n, int32_t* deg, int32_t* first,
+                        cudaStream_t s);
+pyg_status_t mean_divide(float* out, int64_t ldo, int ncols, int64_t n, const int32_t* deg,
+                         cudaStream_t s);
+pyg_status_t max_decode(unsigned long long* keys, int64_t ldk, float* out, int64_t ldo, int ncols,
+                        int64_t n, int64_t E, cudaStream_t s);
+
+// ---- elementwise helpers -----------------------------------------------------------
+// concat x_i block: out[i][c] = f(deg_i) * x[i][c]; arg = first edge of the segment
+// deg from rowptr (plan) or deg array; first from plan perm/rowptr or array.
+pyg_status_t xi_block(const float* x, int64_t ldx, int F, int64_t n, const int64_t* rowptr,
+                      const int32_t* perm, const int32_t* deg, const int32_t* first, int reduce,
+                      float* out, int64_t ldo, int64_t* arg, int64_t lda, int64_t E,
+                      cudaStream_t s);
+// per-edge gather of grad (scatter backward / edge_attr grad)
+pyg_status_t edge_gather_grad(const float* g, int64_t ldg, const int64_t* index, int64_t E, int F,
+                              int reduce, const int64_t* arg, int64_t lda, const int32_t* deg,
+                              float* out, int64_t ldo, cudaStream_t s);
+pyg_status_t xdst_grad(const float* g, int64_t ldg, int F, int64_t n, const int32_t* deg,
+                       const int64_t* arg, int64_t lda, int64_t E, int reduce, float* out,
+                       int64_t ldo, cudaStream_t s);
+pyg_status_t max_route_grad(const float* g, int64_t ldg, const int64_t* arg, int64_t lda, int F,
+                            int64_t n_dst, const int64_t* src, const float* w, int64_t E,
+                            float* gx, int64_t ldgx, cudaStream_t s);
+pyg_status_t edge_weight_grad(const float* x, int64_t ldx, const float* g, int64_t ldg,
+                              const int64_t* arg, int64_t lda, const int64_t* ei, int64_t E, int F,
+                              int reduce, const int32_t* deg, float* gw, cudaStream_t s);
+pyg_status_t fill_rows(float* out, int64_t ldo, int ncols, int64_t n, cudaStream_t s);
+
+}  // namespace pyg

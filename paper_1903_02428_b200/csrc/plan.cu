@@ -1,0 +1,247 @@
+// plan.cu -- one-time preprocessing: the stable sort of edges by target (CSR,
+// "Compressed Row Storage", row = target; App. A).  The paper
+// notes coalescing is "expensive to compute on GPUs and should be hence performed
+// as part of the pre-processing" -- the plan is built once per graph, outside the
+// timed aggregation, and reused by every forward/backward call.
+//
+// Steps (all on `stream`, one synchronisation at the end to read back the sizes the
+// host needs for launch geometry):
+//   1. keys = row_index as int32, vals = 0..E-1 (+ index-range validation);
+//   2. LSD radix sort of (key, edge id) pairs over ceil(log2 n_rows) bits (CUB
+//      onesweep; LSD radix sort is stable => edges of a row keep ascending ids,
+//      which is what the max tie rule needs);
+//   3. rowptr from the sorted keys (boundary scatter), col = col_index[perm];
+//   4. rows longer than kHeavyThreshold (power-law hubs) are listed, in ascending
+//      row order, with the prefix sum of their chunk counts.
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace pyg {
+
+namespace {
+
+int grid_for(int64_t work, int threads = 256) {
+    int64_t b = cdiv(work, threads);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+}
+
+#define GRID_STRIDE(t, total) \
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (total); t += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void keys_init(const int64_t* __restrict__ row, const int64_t* __restrict__ col, int64_t E,
+                          int64_t n_rows, int64_t n_cols, int32_t* keys, int32_t* vals, int* flag) {
+    GRID_STRIDE(k, E) {
+        const int64_t r = row[k];
+        if (r < 0 || r >= n_rows) *flag = 1;
+        if (col) {
+            const int64_t c = col[k];
+            if (c < 0 || c >= n_cols) *flag = 1;
+        }
+        keys[k] = (int32_t)r;
+        vals[k] = (int32_t)k;
+    }
+}
+
+__global__ void rowptr_fill(const int32_t* __restrict__ sk, int64_t E, int64_t n_rows, int64_t* rowptr) {
+    // rowptr[r] = first position p with sk[p] >= r
+    GRID_STRIDE(p, E + 1) {
+        const int64_t prev = p > 0 ? (int64_t)sk[p - 1] : -1;
+        const int64_t cur = p < E ? (int64_t)sk[p] : n_rows;
+        for (int64_t r = prev + 1; r <= cur; ++r) rowptr[r] = p;
+    }
+}
+
+__global__ void col_gather(const int64_t* __restrict__ col, const int32_t* __restrict__ perm, int64_t E,
+                           int32_t* out, int* not_identity) {
+    GRID_STRIDE(p, E) {
+        const int32_t k = perm[p];
+        if (col) out[p] = (int32_t)col[k];
+        if (k != (int32_t)p) *not_identity = 1;
+    }
+}
+
+__global__ void heavy_flags(const int64_t* __restrict__ rowptr, int64_t n_rows, int thr, int32_t* flag_heavy) {
+    GRID_STRIDE(r, n_rows) flag_heavy[r] = (rowptr[r + 1] - rowptr[r]) > thr ? 1 : 0;
+}
+
+__global__ void heavy_compact(const int32_t* __restrict__ flag_heavy, const int32_t* __restrict__ pos,
+                              int64_t n_rows, int32_t* heavy_rows) {
+    GRID_STRIDE(r, n_rows) if (flag_heavy[r]) heavy_rows[pos[r]] = (int32_t)r;
+}
+
+__global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_heavy,
+                             const int64_t* __restrict__ rowptr, int chunk, int64_t* cnt) {
+    GRID_STRIDE(h, n_heavy) {
+        const int64_t r = heavy_rows[h];
+        cnt[h] = cdiv(rowptr[r + 1] - rowptr[r], chunk);
+    }
+}
+
+}  // namespace
+
+struct PlanLayout {
+    int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows;
+    int64_t *rowptr, *cnt, *item_ptr;
+    int* flags2;
+    void* cub_tmp;
+    size_t cub_bytes;
+};
+
+static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, bool has_col, PlanLayout& L) {
+    Carver cv(ws, bytes);
+    const size_t e = (size_t)std::max<int64_t>(E, 1), n = (size_t)std::max<int64_t>(n_rows, 1);
+    // kept arrays first
+    L.rowptr = cv.take<int64_t>(n + 1);
+    L.perm = cv.take<int32_t>(e);
+    L.col = has_col ? cv.take<int32_t>(e) : nullptr;
+    L.heavy_rows = cv.take<int32_t>(n);
+    L.item_ptr = cv.take<int64_t>(n + 1);
+    L.flags2 = cv.take<int>(2);
+    // scratch
+    L.keys = cv.take<int32_t>(e);
+    L.vals = cv.take<int32_t>(e);
+    L.skeys = cv.take<int32_t>(e);
+    L.flag_heavy = cv.take<int32_t>(n);
+    L.pos = cv.take<int32_t>(n);
+    L.cnt = cv.take<int64_t>(n + 1);
+    size_t b1 = 0, b2 = 0, b3 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)e, 0, 32);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+    cub::DeviceScan::ExclusiveSum(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, (int)n + 1);
+    L.cub_bytes = std::max(b1, std::max(b2, b3));
+    L.cub_tmp = cv.take<char>(L.cub_bytes);
+    return cv.off;
+}
+
+#define LAUNCH_CHECK()                  \
+    do {                                \
+        PYG_LAUNCHED();                 \
+        PYG_CUDA(cudaGetLastError());   \
+    } while (0)
+
+pyg_status_t plan_workspace(int64_t E, int64_t n_rows, size_t* bytes) {
+    PlanLayout L;
+    *bytes = plan_layout(nullptr, 0, E, n_rows, true, L) + 1024;
+    return PYG_OK;
+}
+
+pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, int64_t n_rows, int64_t n_cols,
+                             void* ws, size_t bytes, pyg_plan** out, cudaStream_t s) {
+    PlanLayout L;
+    const size_t need = plan_layout(ws, bytes, E, n_rows, col != nullptr, L);
+    if (!ws || need > bytes) return fail(PYG_ERR_NO_MEMORY, "plan workspace too small (%zu < %zu)", bytes, need);
+    int* flag = validate_flag_dev();
+    PYG_CUDA(cudaMemsetAsync(L.flags2, 0, 2 * sizeof(int), s));
+    if (E > 0) {
+        keys_init<<<grid_for(E), 256, 0, s>>>(row, col, E, n_rows, n_cols, L.keys, L.vals, flag);
+        LAUNCH_CHECK();
+        int bits = 1;
+        while (bits < 31 && ((int64_t)1 << bits) < n_rows) ++bits;
+        size_t cb = L.cub_bytes;
+        PYG_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.keys, L.skeys, L.vals, L.perm, (int)E, 0, bits, s));
+        PYG_LAUNCHED();
+    }
+    rowptr_fill<<<grid_for(E + 1), 256, 0, s>>>(L.skeys, E, n_rows, L.rowptr);
+    LAUNCH_CHECK();
+    if (E > 0) {
+        col_gather<<<grid_for(E), 256, 0, s>>>(col, L.perm, E, L.col, L.flags2);
+        LAUNCH_CHECK();
+    }
+    int64_t n_heavy = 0;
+    if (n_rows > 0) {
+        heavy_flags<<<grid_for(n_rows), 256, 0, s>>>(L.rowptr, n_rows, kHeavyThreshold, L.flag_heavy);
+        LAUNCH_CHECK();
+        size_t cb = L.cub_bytes;
+        PYG_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag_heavy, L.pos, (int)n_rows, s));
+        PYG_LAUNCHED();
+        heavy_compact<<<grid_for(n_rows), 256, 0, s>>>(L.flag_heavy, L.pos, n_rows, L.heavy_rows);
+        LAUNCH_CHECK();
+        int32_t last_pos = 0, last_flag = 0;
+        PYG_CUDA(cudaMemcpyAsync(&last_pos, L.pos + n_rows - 1, 4, cudaMemcpyDeviceToHost, s));
+        PYG_CUDA(cudaMemcpyAsync(&last_flag, L.flag_heavy + n_rows - 1, 4, cudaMemcpyDeviceToHost, s));
+        PYG_CUDA(cudaStreamSynchronize(s));
+        n_heavy = (int64_t)last_pos + last_flag;
+    }
+    std::vector<int32_t> h_rows((size_t)n_heavy);
+    std::vector<int64_t> h_ptr((size_t)n_heavy + 1, 0);
+    if (n_heavy > 0) {
+        heavy_counts<<<grid_for(n_heavy), 256, 0, s>>>(L.heavy_rows, n_heavy, L.rowptr, kChunk, L.cnt);
+        LAUNCH_CHECK();
+        PYG_CUDA(cudaMemsetAsync(L.cnt + n_heavy, 0, sizeof(int64_t), s));
+        size_t cb = L.cub_bytes;
+        PYG_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.cnt, L.item_ptr, (int)n_heavy + 1, s));
+        PYG_LAUNCHED();
+        PYG_CUDA(cudaMemcpyAsync(h_rows.data(), L.heavy_rows, 4 * (size_t)n_heavy, cudaMemcpyDeviceToHost, s));
+        PYG_CUDA(cudaMemcpyAsync(h_ptr.data(), L.item_ptr, 8 * ((size_t)n_heavy + 1), cudaMemcpyDeviceToHost, s));
+    } else {
+        PYG_CUDA(cudaMemsetAsync(L.item_ptr, 0, sizeof(int64_t), s));
+    }
+    int flags2[2] = {0, 0};
+    PYG_CUDA(cudaMemcpyAsync(flags2, L.flags2, sizeof(flags2), cudaMemcpyDeviceToHost, s));
+    pyg_status_t st = validate_flag_check(s, "plan_build: index out of range");
+    if (st != PYG_OK) return st;
+
+    pyg_plan* p = new pyg_plan();
+    p->n_rows = n_rows;
+    p->n_cols = n_cols;
+    p->E = E;
+    p->row_offset = 0;
+    p->rowptr = L.rowptr;
+    p->col = col ? L.col : nullptr;
+    p->perm = L.perm;
+    p->perm_identity = flags2[0] == 0;
+    p->heavy_rows = L.heavy_rows;
+    p->heavy_item_ptr = L.item_ptr;
+    p->h_heavy_rows = std::move(h_rows);
+    p->h_heavy_item_ptr = std::move(h_ptr);
+    p->h_lo = 0;
+    p->h_hi = n_heavy;
+    p->item_lo = 0;
+    p->item_hi = p->h_heavy_item_ptr[(size_t)n_heavy];
+    p->heavy_threshold = kHeavyThreshold;
+    p->chunk = kChunk;
+    *out = p;
+    return PYG_OK;
+}
+
+namespace {
+__global__ void export_kernel(const int64_t* __restrict__ rp, int64_t n_rows, const int32_t* __restrict__ col,
+                              const int32_t* __restrict__ perm, int64_t* rowptr, int64_t* col_out, int64_t* perm_out) {
+    const int64_t b = rp[0], e = rp[n_rows];
+    GRID_STRIDE(t, n_rows + 1) if (rowptr) rowptr[t] = rp[t] - b;
+    GRID_STRIDE(p, e - b) {
+        if (col_out) col_out[p] = col[b + p];
+        if (perm_out) perm_out[p] = perm[b + p];
+    }
+}
+}  // namespace
+
+pyg_status_t plan_export_impl(const pyg_plan* p, int64_t* rowptr, int64_t* col, int64_t* perm, cudaStream_t s) {
+    export_kernel<<<grid_for(std::max<int64_t>(p->n_rows + 1, p->E)), 256, 0, s>>>(p->rowptr, p->n_rows, p->col,
+                                                                                  p->perm, rowptr, col, perm);
+    LAUNCH_CHECK();
+    return PYG_OK;
+}
+
+pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out) {
+    pyg_plan* q = new pyg_plan(*p);
+    q->row_offset = p->row_offset + lo;
+    q->rowptr = p->rowptr + lo;
+    q->n_rows = hi - lo;
+    const auto& hr = p->h_heavy_rows;
+    const int64_t glo = q->row_offset, ghi = q->row_offset + (hi - lo);
+    int64_t a = p->h_lo, b = p->h_lo;
+    while (a < p->h_hi && hr[(size_t)a] < glo) ++a;
+    b = a;
+    while (b < p->h_hi && hr[(size_t)b] < ghi) ++b;
+    q->h_lo = a;
+    q->h_hi = b;
+    q->item_lo = p->h_heavy_item_ptr[(size_t)a];
+    q->item_hi = p->h_heavy_item_ptr[(size_t)b];
+    *out = q;
+    return PYG_OK;
+}
+
+}  // namespace pyg

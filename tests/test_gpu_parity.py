@@ -1,0 +1,384 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element,
+on seeded inputs that span several tiles and ragged tails, plus the edge cases
+(empty rows, E = 0, ties, split hub rows, bipartite, strided rows).
+
+Tolerances (tests/tolerance.py): fp32 sum/mean |got-ref| <= 1e-5|ref| + 1e-6
+(north_star) for non-negative data, the conditioned bound 1e-5*S + 1e-6 for signed data;
+max values, argmax, degrees, plans, collate: exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.tolerance import check_close, check_exact
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import paper_1903_02428_b200 as pg
+
+    return pg
+
+
+def T(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    return t if dtype is None else t.to(dtype)
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def rand_graph(rng, n_src, n_dst, E):
+    return np.stack([rng.integers(0, n_src, E), rng.integers(0, n_dst, E)]).astype(np.int64)
+
+
+def strided(x, ld):
+    """Device copy of x with row stride ld (zero padding)."""
+    n, F = x.shape
+    buf = torch.zeros((n, ld), dtype=torch.float32, device=DEV)
+    buf[:, :F] = T(x)
+    return buf[:, :F]
+
+
+def compare(res, ref, red, abs_sum=None, what=""):
+    if red == "max":
+        check_exact(H(res[0]), ref[0], what + " max values")
+        check_exact(H(res[1]), ref[1], what + " argmax")
+    else:
+        check_close(H(res), ref, abs_sum=abs_sum, what=what)
+
+
+# ----------------------------------------------------------------------------- scatter
+
+def test_scatter_printed_examples(pg):
+    import json, os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "scatter_spec_examples.json")))
+    for c in g["cases"]:
+        src = T(np.array(c["src"], np.float32))
+        idx = T(np.array(c["index"], np.int64))
+        plan = pg.pyg_plan_build(idx, None, c["dim_size"])
+        for p in (plan, None):
+            res = pg.pyg_scatter(src, idx, c["dim_size"], c["reduce"], plan=p)
+            out = res[0] if isinstance(res, tuple) else res
+            check_exact(H(out), np.array(c["out"], np.float32))
+
+
+@pytest.mark.parametrize("F", [1, 3, 4, 16, 37, 128, 300])
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+@pytest.mark.parametrize("strategy", ["segment", "atomic"])
+def test_scatter_random(pg, F, red, strategy):
+    rng = np.random.default_rng(F * 7 + len(red))
+    E, n = 3000, 211
+    idx = rng.integers(0, n, E)
+    idx[idx == 5] = 6  # an empty segment
+    src = synth.features(E, F, F, signed=(red == "max"))
+    res_ref = oracle.scatter(src, idx, n, red, with_abs=True)
+    ti = T(idx)
+    plan = pg.pyg_plan_build(ti, None, n) if strategy == "segment" else None
+    res = pg.pyg_scatter(T(src), ti, n, red, plan=plan)
+    if red == "max":
+        compare(res, res_ref[:2], red)
+    else:
+        compare(res, res_ref[0], red, abs_sum=res_ref[1])
+
+
+def test_scatter_ties_and_signed_zero(pg):
+    rng = np.random.default_rng(0)
+    for trial in range(20):
+        E, n, F = int(rng.integers(1, 400)), int(rng.integers(1, 40)), int(rng.integers(1, 9))
+        idx = rng.integers(0, n, E)
+        src = rng.integers(-2, 3, (E, F)).astype(np.float32)
+        src[rng.random((E, F)) < 0.3] = -0.0
+        ref = oracle.scatter(src, idx, n, "max")
+        ti = T(idx)
+        for p in (pg.pyg_plan_build(ti, None, n), None):
+            res = pg.pyg_scatter(T(src), ti, n, "max", plan=p)
+            compare(res, ref, "max", what=f"trial {trial}")
+
+
+def test_scatter_backward(pg):
+    rng = np.random.default_rng(3)
+    E, n, F = 5000, 300, 20
+    idx = rng.integers(0, n, E)
+    src = synth.features(E, F, 1, signed=True)
+    g = synth.features(n, F, 2, signed=True)
+    out, arg = oracle.scatter(src, idx, n, "max")
+    ti = T(idx)
+    for red in ("sum", "mean", "max"):
+        ref = oracle.scatter_backward(g, idx, red, arg=arg if red == "max" else None)
+        got = pg.pyg_scatter_backward(T(g), ti, red, arg_out=T(arg) if red == "max" else None)
+        check_exact(H(got), ref, red)  # pure gather / IEEE divide: bitwise
+
+
+# ----------------------------------------------------------------------------- propagate
+
+CASES = [
+    # (n_src, n_dst, E, F, ld)
+    (50, 40, 0, 8, None),
+    (1, 1, 5, 1, None),
+    (300, 257, 2000, 2, None),
+    (300, 300, 4000, 5, None),
+    (1000, 900, 20000, 16, None),
+    (500, 400, 6000, 33, 36),
+    (400, 400, 5000, 64, None),
+    (200, 150, 3000, 130, 132),
+    (150, 120, 2500, 602, 608),
+    (150, 120, 2500, 602, None),
+    (80, 60, 900, 2100, None),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+@pytest.mark.parametrize("strategy", ["segment", "atomic"])
+def test_propagate_random(pg, case, red, strategy):
+    n_src, n_dst, E, F, ld = case
+    rng = np.random.default_rng(E + F)
+    ei = rand_graph(rng, n_src, n_dst, E)
+    x = synth.features(n_src, F, F, signed=(red == "max"))
+    w = rng.random(E).astype(np.float32) if (E % 2 == 0) else None
+    ref = oracle.propagate(x, ei, n_dst=n_dst, reduce=red, edge_weight=w, with_abs=True)
+    tei = T(ei)
+    xs = strided(x, ld) if ld else T(x)
+    plan = pg.pyg_plan_build(tei[1], tei[0], n_dst, n_src) if strategy == "segment" else None
+    res = pg.pyg_propagate(xs, tei, n_dst=n_dst, reduce=red, edge_weight=T(w) if w is not None else None, plan=plan)
+    if red == "max":
+        compare(res, ref[:2], red)
+    else:
+        compare(res, ref[0], red, abs_sum=ref[1])
+
+
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+@pytest.mark.parametrize("strategy", ["segment", "atomic"])
+def test_propagate_concat_and_edge_attr(pg, red, strategy):
+    rng = np.random.default_rng(11)
+    n_src, n_dst, E, F, D = 400, 300, 7000, 12, 5
+    ei = rand_graph(rng, n_src, n_dst, E)
+    x = synth.features(n_src, F, 1, signed=True)
+    xd = synth.features(n_dst, F, 2, signed=True)
+    ea = synth.features(E, D, 3, signed=True)
+    w = rng.random(E).astype(np.float32)
+    ref = oracle.propagate(x, ei, n_dst=n_dst, reduce=red, edge_weight=w, edge_attr=ea, x_dst=xd, concat_xi=True,
+                           with_abs=True)
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], n_dst, n_src) if strategy == "segment" else None
+    res = pg.pyg_propagate(T(x), tei, n_dst=n_dst, reduce=red, edge_weight=T(w), edge_attr=T(ea), x_dst=T(xd),
+                           concat_xi=True, plan=plan)
+    if red == "max":
+        compare(res, ref[:2], red)
+    else:
+        compare(res, ref[0], red, abs_sum=ref[1])
+
+
+def test_integer_sums_bitwise_across_strategies(pg):
+    """|x| <= 8 integers: every partial sum is exact => atomic == segment == oracle bitwise."""
+    rng = np.random.default_rng(5)
+    ei = rand_graph(rng, 2000, 1500, 40000)
+    x = rng.integers(-8, 9, (2000, 24)).astype(np.float32)
+    ref = oracle.propagate(x, ei, n_dst=1500, reduce="sum")
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], 1500, 2000)
+    for p in (plan, None):
+        check_exact(H(pg.pyg_propagate(T(x), tei, n_dst=1500, reduce="sum", plan=p)), ref)
+
+
+def test_split_hub_rows(pg):
+    """Rows longer than the split threshold (power-law hubs) go through chunk partials + fp64 combine."""
+    rng = np.random.default_rng(9)
+    n, F = 3000, 20
+    E_uni = 30000
+    hubs = np.array([7, 100, 2999])
+    hub_deg = np.array([2049, 9000, 25000])
+    src = np.concatenate([rng.integers(0, n, E_uni)] + [rng.integers(0, n, d) for d in hub_deg])
+    dst = np.concatenate([rng.integers(0, n, E_uni)] + [np.full(d, h) for h, d in zip(hubs, hub_deg)])
+    p = rng.permutation(src.size)
+    ei = np.stack([src[p], dst[p]]).astype(np.int64)
+    x = synth.features(n, F, 4)
+    xs = synth.features(n, F, 5, signed=True)
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], n, n)
+    v = plan.view()
+    assert v["n_heavy_rows"] == 3 and v["n_heavy_chunks"] == 2 + 5 + 13
+    for red in ("sum", "mean"):
+        ref, ab = oracle.propagate(x, ei, reduce=red, with_abs=True)
+        compare(pg.pyg_propagate(T(x), tei, reduce=red, plan=plan), ref, red)
+    ref = oracle.propagate(xs, ei, reduce="max")
+    compare(pg.pyg_propagate(T(xs), tei, reduce="max", plan=plan), ref, "max")
+    # slices that cut through the hub list
+    for lo, hi in ((0, 50), (50, 2999), (2999, 3000), (0, 3000)):
+        sl = plan.slice(lo, hi)
+        res = pg.pyg_propagate(T(xs), tei, n_dst=hi - lo, reduce="max", plan=sl)
+        check_exact(H(res[0]), ref[0][lo:hi])
+        check_exact(H(res[1]), ref[1][lo:hi])
+
+
+def test_segment_is_deterministic(pg):
+    rng = np.random.default_rng(1)
+    ei = rand_graph(rng, 5000, 5000, 200000)
+    x = synth.features(5000, 48, 1, signed=True)
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], 5000, 5000)
+    a = H(pg.pyg_propagate(T(x), tei, reduce="sum", plan=plan))
+    b = H(pg.pyg_propagate(T(x), tei, reduce="sum", plan=plan))
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+# ----------------------------------------------------------------------------- backward
+
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+@pytest.mark.parametrize("strategy", ["segment", "atomic"])
+def test_propagate_backward(pg, red, strategy):
+    rng = np.random.default_rng(21)
+    n_src, n_dst, E, F, D = 700, 500, 12000, 24, 3
+    ei = rand_graph(rng, n_src, n_dst, E)
+    x = synth.features(n_src, F, 1, signed=True)
+    ea = synth.features(E, D, 2, signed=True)
+    w = rng.random(E).astype(np.float32)
+    _, arg = oracle.propagate(x, ei, n_dst=n_dst, reduce="max", edge_weight=w, edge_attr=ea, concat_xi=True) \
+        if red == "max" else (None, None)
+    g = synth.features(n_dst, 2 * F + D, 3, signed=True)
+    ref = oracle.propagate_backward(x, ei, g, n_dst=n_dst, reduce=red, edge_weight=w, D=D, concat_xi=True, arg=arg,
+                                    need_x_dst=True, need_edge_attr=True, need_edge_weight=True, with_abs=True)
+    tei = T(ei)
+    planT = pg.pyg_plan_build(tei[0], tei[1], n_src, n_dst) if strategy == "segment" else None
+    got = pg.pyg_propagate_backward(T(x), tei, T(g), reduce=red, edge_weight=T(w), D=D, concat_xi=True,
+                                    arg_out=T(arg) if arg is not None else None, plan_T=planT, need_x_dst=True,
+                                    need_edge_attr=True, need_edge_weight=True)
+    check_close(H(got["x_src"]), ref["x_src"], abs_sum=ref["abs_x_src"], what="grad x_src")
+    check_close(H(got["x_dst"]), ref["x_dst"], what="grad x_dst")
+    check_close(H(got["edge_attr"]), ref["edge_attr"], what="grad edge_attr")
+    # edge-weight grad: sum over F terms of signed products -> conditioned bound
+    xg = np.abs(x[ei[0]]) @ np.ones(F) * np.abs(g[ei[1], F:2 * F]).max(1)
+    check_close(H(got["edge_weight"]), ref["edge_weight"], abs_sum=xg * (1 if red != "mean" else 1), what="grad w")
+
+
+def test_gcn_backward_symmetric_equals_forward(pg):
+    """Config-2 invariant: symmetric graph => S^T = S => grad_X = S g."""
+    ei, x, g = synth.pubmed_like()
+    N = x.shape[0]
+    tei = T(ei)
+    ei2, w = pg.pyg_gcn_norm(tei, N)
+    plan = pg.pyg_plan_build(ei2[1], ei2[0], N, N)
+    planT = pg.pyg_plan_build(ei2[0], ei2[1], N, N)
+    tg = T(g)
+    fwd = H(pg.pyg_propagate(tg, ei2, reduce="sum", edge_weight=w, plan=plan))
+    bwd = H(pg.pyg_propagate_backward(None, ei2, tg, n_src=N, F=g.shape[1], reduce="sum", edge_weight=w,
+                                      plan_T=planT)["x_src"])
+    rei, rw = oracle.gcn_norm(ei, N)
+    ref, ab = oracle.propagate(g, rei, reduce="sum", edge_weight=rw, with_abs=True)
+    check_close(fwd, ref, abs_sum=ab)
+    check_close(bwd, ref, abs_sum=ab)
+
+
+# ----------------------------------------------------------------------------- structure
+
+def test_plan_matches_oracle_csr(pg):
+    rng = np.random.default_rng(2)
+    for n, E in ((1, 0), (7, 1), (1000, 30000), (70000, 300000)):
+        ei = rand_graph(rng, n, n, E)
+        tei = T(ei)
+        plan = pg.pyg_plan_build(tei[1], tei[0], n, n)
+        rowptr, col, perm = plan.export()
+        rr, rp = oracle.csr(ei[1], n)
+        check_exact(H(rowptr), rr, "rowptr")
+        check_exact(H(perm), rp, "perm")
+        check_exact(H(col), ei[0][rp], "col")
+    # already sorted input => identity perm detected
+    ei = np.stack([np.arange(100) % 7, np.repeat(np.arange(10), 10)]).astype(np.int64)
+    plan = pg.pyg_plan_build(T(ei[1]), T(ei[0]), 10, 7)
+    assert plan.view()["perm_is_identity"] == 1
+
+
+def test_degree(pg):
+    rng = np.random.default_rng(4)
+    idx = rng.integers(0, 999, 50000)
+    check_exact(H(pg.pyg_degree(T(idx), 1000)), oracle.degree(idx, 1000))
+
+
+def test_gcn_norm_matches_oracle(pg):
+    rng = np.random.default_rng(6)
+    for N, E, weighted in ((1, 1, False), (2, 2, False), (300, 2000, False), (300, 2000, True)):
+        ei = rand_graph(rng, N, N, E)
+        if N > 10:
+            ei[:, :4] = [[3, 3, 9, 9], [3, 3, 9, 9]]
+        w = rng.random(E).astype(np.float32) + 0.5 if weighted else None
+        rei, rw = oracle.gcn_norm(ei, N, edge_weight=w)
+        ei2, w2 = pg.pyg_gcn_norm(T(ei), N, edge_weight=T(w) if w is not None else None)
+        check_exact(H(ei2), rei, "gcn edges")
+        check_close(H(w2), rw, rtol=1e-6, atol=0, what="gcn weights")
+
+
+def test_collate_matches_oracle_and_errors(pg):
+    for seed in range(3):
+        nn, eptr, local = synth.random_graph_list(13, seed)
+        ref = oracle.collate(nn, eptr, local)
+        got = pg.pyg_collate(T(nn), T(eptr), T(local), flags=pg.VALIDATE)
+        for a, b, nm in zip(got, ref, ("edge_index", "batch", "node_ptr")):
+            check_exact(H(a), b, nm)
+    nn, eptr, local = synth.random_graph_list(5, 7)
+    bad = local.copy()
+    bad[1, 0] = nn[0]
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_collate(T(nn), T(eptr), T(bad), flags=pg.VALIDATE)
+    assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_collate(T(np.zeros(0, np.int64)), T(np.zeros(1, np.int64)), T(np.zeros((2, 0), np.int64)))
+    assert e.value.status == "PYG_ERR_INVALID_ARGUMENT"
+
+
+def test_validate_flag_reports_out_of_bounds(pg):
+    x = T(np.ones((4, 2), np.float32))
+    bad = T(np.array([[0, 4], [0, 1]], np.int64))
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_propagate(x, bad, reduce="sum", flags=pg.VALIDATE)
+    assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_plan_build(bad[1], bad[0], 4, 4)
+    assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
+    # after an error the library keeps working
+    ok = pg.pyg_propagate(x, T(np.array([[0, 3], [0, 1]], np.int64)), reduce="sum", flags=pg.VALIDATE)
+    assert H(ok)[1].tolist() == [1.0, 1.0]
+
+
+def test_global_pool(pg):
+    nn, eptr, local = synth.random_graph_list(9, 3, n_range=(0, 50))
+    N = int(nn.sum())
+    x = synth.features(N, 19, 1, signed=True)
+    node_ptr = np.concatenate([[0], np.cumsum(nn)])
+    batch = np.repeat(np.arange(9), nn)
+    for red in ("sum", "mean", "max"):
+        ref = oracle.global_pool(x, batch, 9, red)
+        got = pg.pyg_global_pool(T(x), T(node_ptr), red)
+        if red == "max":
+            check_exact(H(got[0]), ref[0])
+            a = ref[1].copy()
+            a[a == N] = N
+            check_exact(H(got[1]), a)
+        else:
+            check_close(H(got), ref, abs_sum=oracle.global_pool(np.abs(x), batch, 9, red))
+
+
+def test_batching_equivalence_on_gpu(pg):
+    """batched propagate restricted to a block equals the per-graph propagate."""
+    nn, eptr, local = synth.random_graph_list(6, 11)
+    ei, batch, node_ptr = pg.pyg_collate(T(nn), T(eptr), T(local))
+    N = int(nn.sum())
+    x = synth.features(N, 10, 2, signed=True)
+    plan = pg.pyg_plan_build(ei[1], ei[0], N, N)
+    full_out, full_arg = pg.pyg_propagate(T(x), ei, reduce="max", plan=plan)
+    full_out, full_arg = H(full_out), H(full_arg)
+    npp = H(node_ptr)
+    for g in range(6):
+        lo, hi = npp[g], npp[g + 1]
+        le = local[:, eptr[g]:eptr[g + 1]]
+        o, a = oracle.propagate(x[lo:hi], le, reduce="max")
+        check_exact(full_out[lo:hi], o)
+        a = np.where(a == le.shape[1], ei.shape[1], a + eptr[g])
+        check_exact(full_arg[lo:hi], a)
