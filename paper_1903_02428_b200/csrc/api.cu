@@ -184,7 +184,7 @@ pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, co
     }
     if (dim_size == 0 || F == 0) return PYG_OK;
     if (use_plan(plan, flags)) {
-        REQUIRE(plan->n_rows == dim_size && plan->col == nullptr, PYG_ERR_DIMENSION,
+        REQUIRE(plan->n_rows == dim_size && (plan->col == nullptr || plan->E == 0), PYG_ERR_DIMENSION,
                 "scatter: plan is not a scatter plan over dim_size rows");
         SegArgs a;
         a.X = src; a.ldx = lds; a.ncols = (int)F;
@@ -261,7 +261,7 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
     const int64_t off1 = cat ? F : 0, off2 = off1 + F;
 
     if (seg) {
-        REQUIRE(plan->n_rows == n_dst && plan->col != nullptr && plan->n_cols <= n_src, PYG_ERR_DIMENSION,
+        REQUIRE(plan->n_rows == n_dst && (plan->col != nullptr || plan->E == 0) && plan->n_cols <= n_src, PYG_ERR_DIMENSION,
                 "propagate: plan does not match (n_rows %lld vs n_dst %lld)", (long long)plan->n_rows, (long long)n_dst);
         const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
         if (cat) PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, plan->rowptr, eid, nullptr, nullptr, reduce, out, ldo, arg_out,
@@ -357,7 +357,7 @@ pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F
             PYG_TRY(max_route_grad(grad_out + off1, ldg, argx, ldg, (int)F, n_dst, src, edge_weight, E, grad_x_src,
                                    ldgx, s));
         } else if (use_plan(plan_T, flags)) {
-            REQUIRE(plan_T->n_rows == n_src && plan_T->col != nullptr && plan_T->n_cols <= n_dst, PYG_ERR_DIMENSION,
+            REQUIRE(plan_T->n_rows == n_src && (plan_T->col != nullptr || plan_T->E == 0) && plan_T->n_cols <= n_dst, PYG_ERR_DIMENSION,
                     "propagate_backward: plan_T must be built with row_index = sources, col_index = targets");
             SegArgs a;
             a.X = grad_out + off1; a.ldx = ldg; a.ncols = (int)F;

@@ -289,7 +289,8 @@ def test_plan_matches_oracle_csr(pg):
         rr, rp = oracle.csr(ei[1], n)
         check_exact(H(rowptr), rr, "rowptr")
         check_exact(H(perm), rp, "perm")
-        check_exact(H(col), ei[0][rp], "col")
+        if E > 0:
+            check_exact(H(col), ei[0][rp], "col")
     # already sorted input => identity perm detected
     ei = np.stack([np.arange(100) % 7, np.repeat(np.arange(10), 10)]).astype(np.int64)
     plan = pg.pyg_plan_build(T(ei[1]), T(ei[0]), 10, 7)
