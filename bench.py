@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--reduce", default=None, choices=["sum", "mean", "max"])
     ap.add_argument("--strategy", default="segment", choices=["segment", "atomic"])
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
+    ap.add_argument("--col-block", default="auto",
+                    help="source rows per L2-resident pass: auto (pyg_plan_suggest_col_block), 0 (off) or N")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -320,8 +322,13 @@ def main():
 
     t0 = time.perf_counter()
     plan_full = None
+    col_block = 0
     if a.strategy == "segment":
-        plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
+        if a.col_block == "auto":
+            col_block = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4)
+        else:
+            col_block = int(a.col_block)
+        plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=col_block)
         torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - t0) * 1e3
     plan = plan_full.slice(lo, hi) if (plan_full is not None and world > 1) else plan_full
@@ -407,7 +414,9 @@ def main():
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": CONFIGS[a.config]["name"], "N": N, "E": E, "F": F, "ldx": ld, "reduce": red,
-                   "strategy": a.strategy, "parallelism": f"dst-range x{world}" if world > 1 else "single",
+                   "strategy": a.strategy, "col_block": col_block,
+                   "col_blocks": plan_full.view()["n_col_blocks"] if plan_full is not None else 0,
+                   "parallelism": f"dst-range x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (no flush)" if a.config in ("reddit", "rmat")
                    else "L2-resident inputs (warm, back-to-back as in Fig. 3's 1000 runs)"},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
@@ -449,7 +458,7 @@ def main():
         def e2e_step():
             dx.copy_(hx, non_blocking=True)
             dei.copy_(hei, non_blocking=True)
-            p = pg.pyg_plan_build(dei[1], dei[0], N, N) if a.strategy == "segment" else None
+            p = pg.pyg_plan_build(dei[1], dei[0], N, N, col_block=col_block) if a.strategy == "segment" else None
             r = pg.pyg_propagate(dx[:, :F], dei if p is None else None, n_dst=N, reduce=red, plan=p, E=E)
             o = r[0] if isinstance(r, tuple) else r
             hout.copy_(o, non_blocking=True)

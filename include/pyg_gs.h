@@ -88,6 +88,8 @@ typedef struct {
     int64_t n_heavy_chunks;  /* chunks of at most chunk_size positions */
     int32_t heavy_threshold;
     int32_t chunk_size;
+    int64_t col_block;       /* source rows per block (0: not source-blocked) */
+    int64_t n_col_blocks;    /* passes per call (1 unless source-blocked) */
 } pyg_plan_view_t;
 
 /* ---- library ------------------------------------------------------------ */
@@ -111,13 +113,25 @@ pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t fla
  * is built once per graph and reused by every call.
  *   row_index [E] int64 in [0, n_rows);  col_index [E] int64 in [0, n_cols)
  *   or NULL (scatter plans: the gathered row is the edge id itself).
+ * col_block > 0 (forward plans only) builds a SOURCE-BLOCKED plan: edges are
+ * sorted by (col_index / col_block, row, id), and calls make one pass per
+ * block of col_block source rows, accumulating into `out` in block order, so
+ * the block of X a pass gathers stays resident in the 126 MB L2 (B200-specific;
+ * see DESIGN.md "source-blocked passes").  Results are deterministic; the sum
+ * order differs from the unblocked plan's.  col_block = 0: one CSR.
  * Workspace: `bytes` from pyg_plan_workspace_size; it holds the plan's device
  * arrays and must outlive the plan.  SYNCHRONOUS (reads back counts); returns
  * PYG_ERR_INDEX_OUT_OF_BOUNDS if an index is out of range. */
-pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, size_t* bytes);
+pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, int64_t col_block,
+                                     size_t* bytes);
 pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, int64_t E,
-                            int64_t n_rows, int64_t n_cols, uint32_t flags, void* workspace,
-                            size_t bytes, pyg_plan_t** plan, void* stream);
+                            int64_t n_rows, int64_t n_cols, int64_t col_block, uint32_t flags,
+                            void* workspace, size_t bytes, pyg_plan_t** plan, void* stream);
+/* Suggest col_block for gathering rows of `row_bytes` bytes (ldx * 4) on the
+ * current device: 0 when X fits in L2 or when the reuse (E / n_cols) does not
+ * repay the extra read+write of `out` per pass (host-only; queries the L2 size). */
+pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_cols,
+                                        int64_t row_bytes, int64_t* col_block);
 /* Sub-plan of rows [row_lo, row_hi) sharing the parent's arrays (dst-range
  * partitioning for the multi-GPU layer).  Output row r of a call using the
  * slice is global row row_lo + r; arg outputs stay GLOBAL edge ids. */

@@ -20,7 +20,7 @@ from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, PHI_CONCAT_XI, SUM, V
                    launch_count, lib)
 
 __all__ = [
-    "Plan", "pyg_degree", "pyg_plan_build", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
+    "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
@@ -114,20 +114,28 @@ class Plan:
             pass
 
 
+def pyg_plan_suggest_col_block(E: int, n_rows: int, n_cols: int, row_bytes: int) -> int:
+    cb = ctypes.c_int64()
+    check(lib.pyg_plan_suggest_col_block(E, n_rows, n_cols, row_bytes, ctypes.byref(cb)),
+          "pyg_plan_suggest_col_block")
+    return cb.value
+
+
 def pyg_plan_build(row_index: torch.Tensor, col_index: Optional[torch.Tensor], n_rows: int,
-                   n_cols: int = 0) -> Plan:
+                   n_cols: int = 0, col_block: int = 0) -> Plan:
     """Build a plan: forward plan = (edge_index[1], edge_index[0]); transposed plan for the
-    backward = (edge_index[0], edge_index[1]); scatter plan = (index, None).  Synchronous."""
+    backward = (edge_index[0], edge_index[1]); scatter plan = (index, None).  col_block > 0 builds a
+    source-blocked plan (see pyg_plan_suggest_col_block).  Synchronous."""
     row_index = _i64(row_index, "row_index")
     E = row_index.numel()
     if col_index is not None:
         col_index = _i64(col_index, "col_index")
         assert col_index.numel() == E
     nb = ctypes.c_size_t()
-    check(lib.pyg_plan_workspace_size(E, n_rows, n_cols, ctypes.byref(nb)), "pyg_plan_workspace_size")
+    check(lib.pyg_plan_workspace_size(E, n_rows, n_cols, col_block, ctypes.byref(nb)), "pyg_plan_workspace_size")
     ws = _workspace(nb.value, row_index.device)
     h = ctypes.c_void_p()
-    check(lib.pyg_plan_build(_ptr(row_index), _ptr(col_index), E, n_rows, n_cols, 0, _ptr(ws), nb.value,
+    check(lib.pyg_plan_build(_ptr(row_index), _ptr(col_index), E, n_rows, n_cols, col_block, 0, _ptr(ws), nb.value,
                              ctypes.byref(h), _stream(row_index.device)), "pyg_plan_build")
     return Plan(h, ws)
 

@@ -39,6 +39,7 @@ class PlanView(ctypes.Structure):
         ("row_offset", ctypes.c_int64), ("rowptr", ctypes.c_void_p), ("col", ctypes.c_void_p),
         ("perm", ctypes.c_void_p), ("perm_is_identity", ctypes.c_int32), ("n_heavy_rows", ctypes.c_int64),
         ("n_heavy_chunks", ctypes.c_int64), ("heavy_threshold", ctypes.c_int32), ("chunk_size", ctypes.c_int32),
+        ("col_block", ctypes.c_int64), ("n_col_blocks", ctypes.c_int64),
     ]
 
 
@@ -54,8 +55,9 @@ SIGNATURES = {
     "pyg_last_error": ([], ctypes.c_char_p),
     "pyg_launch_count": ([], ctypes.c_uint64),
     "pyg_degree": ([P, I64, I64, U32, P, P], C),
-    "pyg_plan_workspace_size": ([I64, I64, I64, ctypes.POINTER(SZ)], C),
-    "pyg_plan_build": ([P, P, I64, I64, I64, U32, P, SZ, PP, P], C),
+    "pyg_plan_workspace_size": ([I64, I64, I64, I64, ctypes.POINTER(SZ)], C),
+    "pyg_plan_build": ([P, P, I64, I64, I64, I64, U32, P, SZ, PP, P], C),
+    "pyg_plan_suggest_col_block": ([I64, I64, I64, I64, ctypes.POINTER(I64)], C),
     "pyg_plan_slice": ([P, I64, I64, PP], C),
     "pyg_plan_view": ([P, ctypes.POINTER(PlanView)], C),
     "pyg_plan_export": ([P, P, P, P, P], C),

@@ -4,6 +4,7 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <cmath>
 #include <mutex>
 #include <string>
 
@@ -64,9 +65,9 @@ pyg_status_t validate_flag_check(cudaStream_t s, const char* what) {
 }
 
 // defined in plan.cu / misc.cu
-pyg_status_t plan_workspace(int64_t E, int64_t n_rows, size_t* bytes);
+pyg_status_t plan_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int64_t col_block, size_t* bytes);
 pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, int64_t n_rows, int64_t n_cols,
-                             void* ws, size_t bytes, pyg_plan** out, cudaStream_t s);
+                             int64_t col_block, void* ws, size_t bytes, pyg_plan** out, cudaStream_t s);
 pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out);
 pyg_status_t plan_export_impl(const pyg_plan* p, int64_t* rowptr, int64_t* col, int64_t* perm, cudaStream_t s);
 pyg_status_t gcn_norm_impl(const int64_t* ei, int64_t E, int64_t N, const float* w, int64_t* eo, float* wo,
@@ -76,6 +77,7 @@ pyg_status_t collate_impl(int64_t G, const int64_t* num_nodes, const int64_t* ed
                           cudaStream_t s);
 
 constexpr int64_t kMaxI32 = 0x7fffffffLL - 1;
+constexpr double kL2BlockFraction = 0.4;  // X block per pass as a fraction of L2
 
 static size_t coo_ws_bytes(int64_t n_out) { return 2 * align_up((size_t)std::max<int64_t>(n_out, 1) * 4, 256); }
 
@@ -108,21 +110,44 @@ pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t fla
     return coo_degree(index, E, n, deg, nullptr, s);
 }
 
-pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, size_t* bytes) {
-    REQUIRE(bytes && E >= 0 && n_rows >= 0 && n_cols >= 0, PYG_ERR_INVALID_ARGUMENT, "plan_workspace_size: bad args");
+pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, int64_t col_block, size_t* bytes) {
+    REQUIRE(bytes && E >= 0 && n_rows >= 0 && n_cols >= 0 && col_block >= 0, PYG_ERR_INVALID_ARGUMENT,
+            "plan_workspace_size: bad args");
     REQUIRE(E <= kMaxI32 && n_rows <= kMaxI32 && n_cols <= kMaxI32, PYG_ERR_UNSUPPORTED, "plan: sizes must be < 2^31");
-    return plan_workspace(E, n_rows, bytes);
+    return plan_workspace(E, n_rows, n_cols, col_block, bytes);
+}
+
+pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_cols, int64_t row_bytes,
+                                        int64_t* col_block) {
+    REQUIRE(col_block && E >= 0 && n_rows >= 0 && n_cols >= 0 && row_bytes > 0, PYG_ERR_INVALID_ARGUMENT,
+            "plan_suggest_col_block: bad args");
+    *col_block = 0;
+    int dev = 0, l2 = 0;
+    PYG_CUDA(cudaGetDevice(&dev));
+    PYG_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev));
+    const double x_bytes = (double)n_cols * (double)row_bytes;
+    const double budget = kL2BlockFraction * (double)l2;
+    if (x_bytes <= (double)l2 || n_rows == 0) return PYG_OK;  // X already fits L2: one pass
+    const int64_t nb = (int64_t)std::ceil(x_bytes / budget);
+    // DRAM saved on the gather vs the extra read+write of `out` per additional pass
+    const double saved = (double)E * (double)row_bytes * (1.0 - (double)l2 / x_bytes);
+    const double cost = 2.0 * (double)(nb - 1) * (double)n_rows * (double)row_bytes;
+    if (saved < 4.0 * cost || nb * n_rows > kMaxI32) return PYG_OK;
+    *col_block = cdiv(n_cols, nb);
+    return PYG_OK;
 }
 
 pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, int64_t E, int64_t n_rows,
-                            int64_t n_cols, uint32_t flags, void* workspace, size_t bytes, pyg_plan_t** plan,
-                            void* stream) {
+                            int64_t n_cols, int64_t col_block, uint32_t flags, void* workspace, size_t bytes,
+                            pyg_plan_t** plan, void* stream) {
     (void)flags;
-    REQUIRE(plan && E >= 0 && n_rows >= 0 && n_cols >= 0, PYG_ERR_INVALID_ARGUMENT, "plan_build: bad args");
+    REQUIRE(plan && E >= 0 && n_rows >= 0 && n_cols >= 0 && col_block >= 0, PYG_ERR_INVALID_ARGUMENT,
+            "plan_build: bad args");
     REQUIRE(E == 0 || row_index, PYG_ERR_INVALID_ARGUMENT, "plan_build: null row_index");
     REQUIRE(E <= kMaxI32 && n_rows <= kMaxI32 && n_cols <= kMaxI32, PYG_ERR_UNSUPPORTED, "plan: sizes must be < 2^31");
     *plan = nullptr;
-    return plan_build_impl(row_index, col_index, E, n_rows, n_cols, workspace, bytes, plan, as_stream(stream));
+    return plan_build_impl(row_index, col_index, E, n_rows, n_cols, col_block, workspace, bytes, plan,
+                           as_stream(stream));
 }
 
 pyg_status_t pyg_plan_slice(const pyg_plan_t* plan, int64_t lo, int64_t hi, pyg_plan_t** slice) {
@@ -146,6 +171,8 @@ pyg_status_t pyg_plan_view(const pyg_plan_t* p, pyg_plan_view_t* v) {
     v->n_heavy_chunks = p->item_hi - p->item_lo;
     v->heavy_threshold = p->heavy_threshold;
     v->chunk_size = p->chunk;
+    v->col_block = p->col_block;
+    v->n_col_blocks = p->parts.empty() ? 1 : (int64_t)p->parts.size();
     return PYG_OK;
 }
 
@@ -154,6 +181,7 @@ void pyg_plan_destroy(pyg_plan_t* p) { delete p; }
 pyg_status_t pyg_plan_export(const pyg_plan_t* p, int64_t* rowptr, int64_t* col, int64_t* perm, void* stream) {
     REQUIRE(p, PYG_ERR_INVALID_ARGUMENT, "plan_export: null plan");
     REQUIRE(!col || p->col, PYG_ERR_INVALID_ARGUMENT, "plan_export: plan has no col array");
+    REQUIRE(p->parts.empty(), PYG_ERR_UNSUPPORTED, "plan_export: source-blocked plans have one CSR per block");
     return plan_export_impl(p, rowptr, col, perm, as_stream(stream));
 }
 
@@ -264,8 +292,14 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         REQUIRE(plan->n_rows == n_dst && (plan->col != nullptr || plan->E == 0) && plan->n_cols <= n_src, PYG_ERR_DIMENSION,
                 "propagate: plan does not match (n_rows %lld vs n_dst %lld)", (long long)plan->n_rows, (long long)n_dst);
         const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
-        if (cat) PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, plan->rowptr, eid, nullptr, nullptr, reduce, out, ldo, arg_out,
-                                  ldo, E, s));
+        if (cat && !plan->parts.empty()) {
+            REQUIRE(reduce != PYG_MAX, PYG_ERR_UNSUPPORTED, "propagate: CONCAT_XI + MAX needs an unblocked plan");
+            PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, nullptr, nullptr, plan->deg, nullptr, reduce, out, ldo, arg_out,
+                             ldo, E, s));
+        } else if (cat) {
+            PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, plan->rowptr, eid, nullptr, nullptr, reduce, out, ldo, arg_out,
+                             ldo, E, s));
+        }
         if (F > 0) {
             SegArgs a;
             a.X = x_src; a.ldx = ldx; a.ncols = (int)F;

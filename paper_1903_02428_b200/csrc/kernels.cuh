@@ -20,6 +20,11 @@ struct pyg_plan {
     int64_t h_lo = 0, h_hi = 0;        // heavy rows of this plan: [h_lo, h_hi)
     int64_t item_lo = 0, item_hi = 0;  // chunks of this plan
     int32_t heavy_threshold = 0, chunk = 0;
+    // Source-blocked plans: edges sorted by (source block, target, id); `parts[b]` is the
+    // slice of virtual rows of source block b restricted to this plan's target rows.
+    int64_t col_block = 0;            // source rows per block (0 = not blocked)
+    const int32_t* deg = nullptr;     // [n_rows] total in-degree (blocked plans), offset like rowptr
+    std::vector<pyg_plan> parts;
 };
 
 namespace pyg {
@@ -45,6 +50,9 @@ struct SegArgs {
     int64_t E_sentinel = 0;
     int64_t heavy_threshold = 0;    // light pass skips rows longer than this
     int allow_pad_read = 0;         // X rows may be read up to round_up(ncols, 4)
+    int accum = 0;                  // add into out/arg (source-blocked passes after the first)
+    int finalize = 1;               // apply the mean division in this pass
+    const int32_t* deg_total = nullptr;  // mean divisor per row when segments are partial
 };
 // Full segment reduce of a block of columns: light rows, split hub rows (plan
 // may be null for plan-free segment inputs such as pooling), fp64 combine.

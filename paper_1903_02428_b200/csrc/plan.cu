@@ -13,6 +13,8 @@
 //   3. rowptr from the sorted keys (boundary scatter), col = col_index[perm];
 //   4. rows longer than kHeavyThreshold (power-law hubs) are listed, in ascending
 //      row order, with the prefix sum of their chunk counts.
+#include <algorithm>
+
 #include <cub/cub.cuh>
 
 #include "kernels.cuh"
@@ -29,16 +31,21 @@ int grid_for(int64_t work, int threads = 256) {
 #define GRID_STRIDE(t, total) \
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (total); t += (int64_t)gridDim.x * blockDim.x)
 
+// key = row, or (source block, row) as block * n_rows + row for source-blocked plans.
+// Out-of-range indices raise the flag and are clamped so the build stays in bounds.
 __global__ void keys_init(const int64_t* __restrict__ row, const int64_t* __restrict__ col, int64_t E,
-                          int64_t n_rows, int64_t n_cols, int32_t* keys, int32_t* vals, int* flag) {
+                          int64_t n_rows, int64_t n_cols, int64_t col_block, int32_t* keys, int32_t* vals,
+                          int* flag) {
     GRID_STRIDE(k, E) {
-        const int64_t r = row[k];
-        if (r < 0 || r >= n_rows) *flag = 1;
+        int64_t r = row[k];
+        if (r < 0 || r >= n_rows) { *flag = 1; r = 0; }
+        int64_t key = r;
         if (col) {
-            const int64_t c = col[k];
-            if (c < 0 || c >= n_cols) *flag = 1;
+            int64_t c = col[k];
+            if (c < 0 || c >= n_cols) { *flag = 1; c = 0; }
+            if (col_block > 0) key = (c / col_block) * n_rows + r;
         }
-        keys[k] = (int32_t)r;
+        keys[k] = (int32_t)key;
         vals[k] = (int32_t)k;
     }
 }
@@ -81,35 +88,39 @@ __global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_h
 }  // namespace
 
 struct PlanLayout {
-    int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows;
+    int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows, *deg;
     int64_t *rowptr, *cnt, *item_ptr;
     int* flags2;
     void* cub_tmp;
     size_t cub_bytes;
 };
 
-static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, bool has_col, PlanLayout& L) {
+// V = n_blocks * n_rows virtual rows (n_blocks = 1 unless source-blocked)
+static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, int64_t n_blocks, bool has_col,
+                          PlanLayout& L) {
     Carver cv(ws, bytes);
-    const size_t e = (size_t)std::max<int64_t>(E, 1), n = (size_t)std::max<int64_t>(n_rows, 1);
+    const size_t e = (size_t)std::max<int64_t>(E, 1);
+    const size_t v = (size_t)std::max<int64_t>(n_rows * n_blocks, 1);
     // kept arrays first
-    L.rowptr = cv.take<int64_t>(n + 1);
+    L.rowptr = cv.take<int64_t>(v + 1);
     L.perm = cv.take<int32_t>(e);
     L.col = has_col ? cv.take<int32_t>(e) : nullptr;
-    L.heavy_rows = cv.take<int32_t>(n);
-    L.item_ptr = cv.take<int64_t>(n + 1);
+    L.heavy_rows = cv.take<int32_t>(v);
+    L.item_ptr = cv.take<int64_t>(v + 1);
+    L.deg = n_blocks > 1 ? cv.take<int32_t>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
     L.flags2 = cv.take<int>(2);
     // scratch
     L.keys = cv.take<int32_t>(e);
     L.vals = cv.take<int32_t>(e);
     L.skeys = cv.take<int32_t>(e);
-    L.flag_heavy = cv.take<int32_t>(n);
-    L.pos = cv.take<int32_t>(n);
-    L.cnt = cv.take<int64_t>(n + 1);
+    L.flag_heavy = cv.take<int32_t>(v);
+    L.pos = cv.take<int32_t>(v);
+    L.cnt = cv.take<int64_t>(v + 1);
     size_t b1 = 0, b2 = 0, b3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)e, 0, 32);
-    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
-    cub::DeviceScan::ExclusiveSum(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, (int)n + 1);
+    cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)v);
+    cub::DeviceScan::ExclusiveSum(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, (int)v + 1);
     L.cub_bytes = std::max(b1, std::max(b2, b3));
     L.cub_tmp = cv.take<char>(L.cub_bytes);
     return cv.off;
@@ -121,46 +132,60 @@ static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, boo
         PYG_CUDA(cudaGetLastError());   \
     } while (0)
 
-pyg_status_t plan_workspace(int64_t E, int64_t n_rows, size_t* bytes) {
+static int64_t n_blocks_for(int64_t n_cols, int64_t col_block) {
+    return col_block > 0 ? std::max<int64_t>(1, cdiv(n_cols, col_block)) : 1;
+}
+
+pyg_status_t plan_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int64_t col_block, size_t* bytes) {
     PlanLayout L;
-    *bytes = plan_layout(nullptr, 0, E, n_rows, true, L) + 1024;
+    const int64_t nb = n_blocks_for(n_cols, col_block);
+    if (nb * n_rows > 0x7ffffffeLL) return fail(PYG_ERR_UNSUPPORTED, "plan: n_blocks * n_rows must be < 2^31");
+    *bytes = plan_layout(nullptr, 0, E, n_rows, nb, true, L) + 1024;
     return PYG_OK;
 }
 
+pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out);
+
 pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, int64_t n_rows, int64_t n_cols,
-                             void* ws, size_t bytes, pyg_plan** out, cudaStream_t s) {
+                             int64_t col_block, void* ws, size_t bytes, pyg_plan** out, cudaStream_t s) {
     PlanLayout L;
-    const size_t need = plan_layout(ws, bytes, E, n_rows, col != nullptr, L);
+    if (!col) col_block = 0;
+    const int64_t nb = n_blocks_for(n_cols, col_block);
+    if (nb * n_rows > 0x7ffffffeLL) return fail(PYG_ERR_UNSUPPORTED, "plan: n_blocks * n_rows must be < 2^31");
+    const int64_t V = nb * n_rows;  // virtual rows
+    const size_t need = plan_layout(ws, bytes, E, n_rows, nb, col != nullptr, L);
     if (!ws || need > bytes) return fail(PYG_ERR_NO_MEMORY, "plan workspace too small (%zu < %zu)", bytes, need);
     int* flag = validate_flag_dev();
     PYG_CUDA(cudaMemsetAsync(L.flags2, 0, 2 * sizeof(int), s));
     if (E > 0) {
-        keys_init<<<grid_for(E), 256, 0, s>>>(row, col, E, n_rows, n_cols, L.keys, L.vals, flag);
+        keys_init<<<grid_for(E), 256, 0, s>>>(row, col, E, n_rows, n_cols, nb > 1 ? col_block : 0, L.keys, L.vals,
+                                              flag);
         LAUNCH_CHECK();
         int bits = 1;
-        while (bits < 31 && ((int64_t)1 << bits) < n_rows) ++bits;
+        while (bits < 31 && ((int64_t)1 << bits) < V) ++bits;
         size_t cb = L.cub_bytes;
         PYG_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.keys, L.skeys, L.vals, L.perm, (int)E, 0, bits, s));
         PYG_LAUNCHED();
     }
-    rowptr_fill<<<grid_for(E + 1), 256, 0, s>>>(L.skeys, E, n_rows, L.rowptr);
+    rowptr_fill<<<grid_for(E + 1), 256, 0, s>>>(L.skeys, E, V, L.rowptr);
     LAUNCH_CHECK();
     if (E > 0) {
         col_gather<<<grid_for(E), 256, 0, s>>>(col, L.perm, E, L.col, L.flags2);
         LAUNCH_CHECK();
     }
+    if (nb > 1) PYG_TRY(coo_degree(row, E, n_rows, L.deg, nullptr, s));
     int64_t n_heavy = 0;
-    if (n_rows > 0) {
-        heavy_flags<<<grid_for(n_rows), 256, 0, s>>>(L.rowptr, n_rows, kHeavyThreshold, L.flag_heavy);
+    if (V > 0) {
+        heavy_flags<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, kHeavyThreshold, L.flag_heavy);
         LAUNCH_CHECK();
         size_t cb = L.cub_bytes;
-        PYG_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag_heavy, L.pos, (int)n_rows, s));
+        PYG_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag_heavy, L.pos, (int)V, s));
         PYG_LAUNCHED();
-        heavy_compact<<<grid_for(n_rows), 256, 0, s>>>(L.flag_heavy, L.pos, n_rows, L.heavy_rows);
+        heavy_compact<<<grid_for(V), 256, 0, s>>>(L.flag_heavy, L.pos, V, L.heavy_rows);
         LAUNCH_CHECK();
         int32_t last_pos = 0, last_flag = 0;
-        PYG_CUDA(cudaMemcpyAsync(&last_pos, L.pos + n_rows - 1, 4, cudaMemcpyDeviceToHost, s));
-        PYG_CUDA(cudaMemcpyAsync(&last_flag, L.flag_heavy + n_rows - 1, 4, cudaMemcpyDeviceToHost, s));
+        PYG_CUDA(cudaMemcpyAsync(&last_pos, L.pos + V - 1, 4, cudaMemcpyDeviceToHost, s));
+        PYG_CUDA(cudaMemcpyAsync(&last_flag, L.flag_heavy + V - 1, 4, cudaMemcpyDeviceToHost, s));
         PYG_CUDA(cudaStreamSynchronize(s));
         n_heavy = (int64_t)last_pos + last_flag;
     }
@@ -183,25 +208,52 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     pyg_status_t st = validate_flag_check(s, "plan_build: index out of range");
     if (st != PYG_OK) return st;
 
+    pyg_plan root;
+    root.n_rows = V;
+    root.n_cols = n_cols;
+    root.E = E;
+    root.row_offset = 0;
+    root.rowptr = L.rowptr;
+    root.col = col ? L.col : nullptr;
+    root.perm = L.perm;
+    root.perm_identity = flags2[0] == 0;
+    root.heavy_rows = L.heavy_rows;
+    root.heavy_item_ptr = L.item_ptr;
+    root.h_heavy_rows = std::move(h_rows);
+    root.h_heavy_item_ptr = std::move(h_ptr);
+    root.h_lo = 0;
+    root.h_hi = n_heavy;
+    root.item_lo = 0;
+    root.item_hi = root.h_heavy_item_ptr[(size_t)n_heavy];
+    root.heavy_threshold = kHeavyThreshold;
+    root.chunk = kChunk;
+    if (nb == 1) {
+        *out = new pyg_plan(std::move(root));
+        return PYG_OK;
+    }
+    // source-blocked: the user-facing plan has n_rows real rows and one part per block
     pyg_plan* p = new pyg_plan();
     p->n_rows = n_rows;
     p->n_cols = n_cols;
     p->E = E;
-    p->row_offset = 0;
-    p->rowptr = L.rowptr;
-    p->col = col ? L.col : nullptr;
-    p->perm = L.perm;
-    p->perm_identity = flags2[0] == 0;
-    p->heavy_rows = L.heavy_rows;
-    p->heavy_item_ptr = L.item_ptr;
-    p->h_heavy_rows = std::move(h_rows);
-    p->h_heavy_item_ptr = std::move(h_ptr);
-    p->h_lo = 0;
-    p->h_hi = n_heavy;
-    p->item_lo = 0;
-    p->item_hi = p->h_heavy_item_ptr[(size_t)n_heavy];
+    p->col = root.col;
+    p->perm = root.perm;
+    p->perm_identity = 0;
     p->heavy_threshold = kHeavyThreshold;
     p->chunk = kChunk;
+    p->col_block = col_block;
+    p->deg = L.deg;
+    for (int64_t b = 0; b < nb; ++b) {
+        pyg_plan* part = nullptr;
+        PYG_TRY(plan_slice_impl(&root, b * n_rows, (b + 1) * n_rows, &part));
+        p->parts.push_back(std::move(*part));
+        delete part;
+    }
+    p->rowptr = p->parts[0].rowptr;
+    for (const auto& q : p->parts) {
+        p->item_hi += q.item_hi - q.item_lo;
+        p->h_hi += q.h_hi - q.h_lo;
+    }
     *out = p;
     return PYG_OK;
 }
@@ -226,20 +278,45 @@ pyg_status_t plan_export_impl(const pyg_plan* p, int64_t* rowptr, int64_t* col, 
 }
 
 pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out) {
+    if (!p->parts.empty()) {
+        pyg_plan* q = new pyg_plan();
+        q->n_rows = hi - lo;
+        q->n_cols = p->n_cols;
+        q->E = p->E;
+        q->row_offset = p->row_offset + lo;
+        q->col = p->col;
+        q->perm = p->perm;
+        q->heavy_threshold = p->heavy_threshold;
+        q->chunk = p->chunk;
+        q->col_block = p->col_block;
+        q->deg = p->deg + lo;
+        for (const auto& part : p->parts) {
+            pyg_plan* sub = nullptr;
+            PYG_TRY(plan_slice_impl(&part, lo, hi, &sub));
+            q->parts.push_back(std::move(*sub));
+            delete sub;
+        }
+        q->rowptr = q->parts[0].rowptr;
+        for (const auto& r : q->parts) {
+            q->item_hi += r.item_hi - r.item_lo;
+            q->h_hi += r.h_hi - r.h_lo;
+        }
+        *out = q;
+        return PYG_OK;
+    }
     pyg_plan* q = new pyg_plan(*p);
     q->row_offset = p->row_offset + lo;
     q->rowptr = p->rowptr + lo;
     q->n_rows = hi - lo;
     const auto& hr = p->h_heavy_rows;
     const int64_t glo = q->row_offset, ghi = q->row_offset + (hi - lo);
-    int64_t a = p->h_lo, b = p->h_lo;
-    while (a < p->h_hi && hr[(size_t)a] < glo) ++a;
-    b = a;
-    while (b < p->h_hi && hr[(size_t)b] < ghi) ++b;
+    const auto first = hr.begin() + p->h_lo, last = hr.begin() + p->h_hi;
+    const int64_t a = std::lower_bound(first, last, (int32_t)glo) - hr.begin();
+    const int64_t b = std::lower_bound(first, last, (int32_t)std::min<int64_t>(ghi, INT32_MAX)) - hr.begin();
     q->h_lo = a;
-    q->h_hi = b;
-    q->item_lo = p->h_heavy_item_ptr[(size_t)a];
-    q->item_hi = p->h_heavy_item_ptr[(size_t)b];
+    q->h_hi = std::max(a, b);
+    q->item_lo = p->h_heavy_item_ptr[(size_t)q->h_lo];
+    q->item_hi = p->h_heavy_item_ptr[(size_t)q->h_hi];
     *out = q;
     return PYG_OK;
 }

@@ -166,30 +166,60 @@ __global__ void __launch_bounds__(256) seg_kernel(SegArgs a, int lpr, int mode,
     seg_accumulate<V, NCH, RED>(a, beg, end, l, lpr, mask, c0, acc, bi);
 
     if (mode == 0) {
-        const int64_t deg = end - beg;
+        const int64_t dseg = end - beg;
+        // accumulate passes (source-blocked plans) have nothing to add for empty segments
+        if (a.accum && dseg == 0 && !(RED == PYG_MEAN && a.finalize)) return;
+        const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
             const int col = c0 + (l + ch * lpr) * V;
             if (col >= a.ncols) continue;
             const int nv = min(V, a.ncols - col);
-            float r[V];
-#pragma unroll
-            for (int q = 0; q < V; ++q) {
-                if (RED == PYG_MAX) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
-                else if (RED == PYG_MEAN) r[q] = deg > 0 ? acc[ch][q] / (float)deg : 0.0f;
-                else r[q] = acc[ch][q];
-            }
             float* o = a.out + row * a.ldo + col;
-            if (out_vec_ok) stv<V>(o, r, nv);
-            else {
+            if (RED != PYG_MAX) {
+                float r[V];
 #pragma unroll
-                for (int q = 0; q < V; ++q) if (q < nv) o[q] = r[q];
-            }
-            if (RED == PYG_MAX) {
+                for (int q = 0; q < V; ++q) r[q] = acc[ch][q];
+                if (a.accum) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) if (q < nv) r[q] += o[q];
+                }
+                if (RED == PYG_MEAN && a.finalize) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
+                }
+                if (out_vec_ok) stv<V>(o, r, nv);
+                else {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) if (q < nv) o[q] = r[q];
+                }
+            } else {
                 int64_t* ap = a.arg + row * a.lda + col;
+                if (!a.accum) {
+                    float r[V];
 #pragma unroll
-                for (int q = 0; q < V; ++q)
-                    if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
+                    for (int q = 0; q < V; ++q) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
+                    if (out_vec_ok) stv<V>(o, r, nv);
+                    else {
+#pragma unroll
+                        for (int q = 0; q < V; ++q) if (q < nv) o[q] = r[q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < V; ++q)
+                        if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
+                } else {
+                    // merge with the previous blocks: larger value wins, IEEE-equal values -> lower edge id (Q4)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        if (q >= nv || bi[ch][q] < 0) continue;
+                        const int64_t oa = ap[q];
+                        const float ov = o[q];
+                        if (oa == a.E_sentinel || acc[ch][q] > ov || (acc[ch][q] == ov && bi[ch][q] < oa)) {
+                            o[q] = acc[ch][q];
+                            ap[q] = bi[ch][q];
+                        }
+                    }
+                }
             }
         }
     } else {
@@ -220,7 +250,7 @@ __global__ void combine_kernel(SegArgs a, const int32_t* __restrict__ heavy_rows
     const int64_t h = h_lo + blockIdx.x;
     const int64_t r = (int64_t)heavy_rows[h] - row_offset;
     const int64_t i0 = item_ptr[h] - item_lo, i1 = item_ptr[h + 1] - item_lo;
-    const int64_t deg = a.rowptr[r + 1] - a.rowptr[r];
+    const int64_t deg = a.deg_total ? (int64_t)a.deg_total[r] : a.rowptr[r + 1] - a.rowptr[r];
     for (int col = blockIdx.y * blockDim.x + threadIdx.x; col < a.ncols; col += gridDim.y * blockDim.x) {
         if (RED == PYG_MAX) {
             float best = 0.0f;
@@ -230,12 +260,20 @@ __global__ void combine_kernel(SegArgs a, const int32_t* __restrict__ heavy_rows
                 const float pv = part[it * ldp + col];
                 if (pb >= 0 && (b < 0 || pv > best)) { best = pv; b = pb; }
             }
-            a.out[r * a.ldo + col] = b >= 0 ? best : 0.0f;
-            a.arg[r * a.lda + col] = b >= 0 ? (int64_t)b : a.E_sentinel;
+            float* o = a.out + r * a.ldo + col;
+            int64_t* ap = a.arg + r * a.lda + col;
+            if (!a.accum) {
+                *o = b >= 0 ? best : 0.0f;
+                *ap = b >= 0 ? (int64_t)b : a.E_sentinel;
+            } else if (b >= 0 && (*ap == a.E_sentinel || best > *o || (best == *o && b < *ap))) {
+                *o = best;
+                *ap = b;
+            }
         } else {
             double s = 0.0;
             for (int64_t it = i0; it < i1; ++it) s += (double)part[it * ldp + col];
-            if (RED == PYG_MEAN) s = deg > 0 ? s / (double)deg : 0.0;
+            if (a.accum) s += (double)a.out[r * a.ldo + col];
+            if (RED == PYG_MEAN && a.finalize) s = deg > 0 ? s / (double)deg : 0.0;
             a.out[r * a.ldo + col] = (float)s;
         }
     }
@@ -289,6 +327,11 @@ bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) 
 
 size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce) {
     if (!plan) return 0;
+    if (!plan->parts.empty()) {
+        size_t b = 0;
+        for (const auto& p : plan->parts) b = std::max(b, segment_ws_bytes(&p, ncols, reduce));
+        return b;
+    }
     const int64_t items = plan->item_hi - plan->item_lo;
     if (items <= 0) return 0;
     const size_t ldp = align_up((size_t)ncols, 4);
@@ -297,8 +340,31 @@ size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce) {
     return b;
 }
 
+static pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* plan, void* ws,
+                                       size_t ws_bytes, cudaStream_t s);
+
+// Source-blocked plans: one pass per block of source rows (sized so the block of X stays
+// L2-resident), accumulating into `out` in block order (deterministic); the last pass applies
+// the mean division with the total in-degree.
 pyg_status_t segment_reduce(const SegArgs& a0, int reduce, const pyg_plan* plan, void* ws,
                             size_t ws_bytes, cudaStream_t s) {
+    if (!plan || plan->parts.empty()) return segment_reduce_one(a0, reduce, plan, ws, ws_bytes, s);
+    const size_t nb = plan->parts.size();
+    for (size_t b = 0; b < nb; ++b) {
+        SegArgs a = a0;
+        const pyg_plan& p = plan->parts[b];
+        a.rowptr = p.rowptr;
+        a.accum = b > 0;
+        a.finalize = (b + 1 == nb);
+        a.deg_total = plan->deg;
+        a.heavy_threshold = p.heavy_threshold;
+        PYG_TRY(segment_reduce_one(a, reduce, &p, ws, ws_bytes, s));
+    }
+    return PYG_OK;
+}
+
+static pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* plan, void* ws,
+                                       size_t ws_bytes, cudaStream_t s) {
     SegArgs a = a0;
     if (a.n_rows <= 0 || a.ncols <= 0) return PYG_OK;
     // vector width: X rows (and optionally padded reads) must be V-aligned

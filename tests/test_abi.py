@@ -46,7 +46,10 @@ def test_host_validation_without_gpu():
     assert lib.pyg_propagate(None, 3, 2, 2, None, 0, 3, None, 1, None, 0, 0, None, 2, 0, None, 2, None, None, None, 0,
                              None) == 1  # max without arg_out / null pointers
     nb = ctypes.c_size_t()
-    assert lib.pyg_plan_workspace_size(1000, 100, 100, ctypes.byref(nb)) == 0 and nb.value > 1000 * 4
+    assert lib.pyg_plan_workspace_size(1000, 100, 100, 0, ctypes.byref(nb)) == 0 and nb.value > 1000 * 4
+    nb2 = ctypes.c_size_t()
+    assert lib.pyg_plan_workspace_size(1000, 100, 100, 10, ctypes.byref(nb2)) == 0 and nb2.value > nb.value
+    assert lib.pyg_plan_workspace_size(1000, 100, 100, -1, ctypes.byref(nb2)) == 1
     assert "collate" in lib.pyg_last_error().decode() or True
 
 

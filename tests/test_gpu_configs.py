@@ -1,0 +1,242 @@
+"""Parity at BASELINE.json's five configurations, in the launch configuration bench.py times.
+
+Configs 1-3 are compared in full (the oracle finishes in seconds).  Configs 4-5 (Reddit-scale,
+R-MAT) are compared on sampled target rows: every in-edge of a sampled row is extracted (in
+ascending edge id, so the tie rule is preserved), the oracle computes those rows one by one, and
+the GPU rows -- computed over the full graph -- must match element by element.  Samples include
+the highest-degree rows (R-MAT hubs), random rows and empty rows.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.tolerance import check_close, check_exact
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import paper_1903_02428_b200 as pg
+
+    return pg
+
+
+def T(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def sub_problem(ei, rows, N):
+    """In-edges of `rows` (sorted unique) as a compact problem: (ei_sub [2, Es] numpy with dst
+    renumbered 0..len(rows)-1, original edge ids [Es])."""
+    lut = torch.full((N,), -1, dtype=torch.int64, device=ei.device)
+    lut[rows] = torch.arange(rows.numel(), device=ei.device)
+    m = lut[ei[1]] >= 0
+    eid = torch.nonzero(m).flatten()
+    sub = ei[:, eid]
+    sub = torch.stack([sub[0], lut[sub[1]]])
+    return H(sub), H(eid)
+
+
+def map_arg(arg_sub, eid, E):
+    Es = eid.size
+    out = np.where(arg_sub == Es, E, eid[np.minimum(arg_sub, max(Es - 1, 0))] if Es else E)
+    return out
+
+
+# ----------------------------------------------------------------------------- config 1
+
+def test_config1_cora(pg):
+    ei, x = synth.cora_like()
+    N = x.shape[0]
+    tei, tx = T(ei), T(x)
+    plan = pg.pyg_plan_build(tei[1], tei[0], N, N)
+    idx = ei[1]
+    splan = pg.pyg_plan_build(tei[1], None, N)
+    src = x[ei[0]]
+    for red in ("sum", "mean", "max"):
+        ref = oracle.propagate(x, ei, reduce=red)
+        sref = oracle.scatter(src, idx, N, red)
+        for p, sp in ((plan, splan), (None, None)):
+            got = pg.pyg_propagate(tx, tei, reduce=red, plan=p)
+            sgot = pg.pyg_scatter(T(src), tei[1], N, red, plan=sp)
+            if red == "max":
+                check_exact(H(got[0]), ref[0]); check_exact(H(got[1]), ref[1])
+                check_exact(H(sgot[0]), sref[0]); check_exact(H(sgot[1]), sref[1])
+            else:
+                check_close(H(got), ref); check_close(H(sgot), sref)
+    # signed features for max (max also run on U(-1,1))
+    xs = synth.features(N, 16, 11, signed=True)
+    ref = oracle.propagate(xs, ei, reduce="max")
+    got = pg.pyg_propagate(T(xs), tei, reduce="max", plan=plan)
+    check_exact(H(got[0]), ref[0]); check_exact(H(got[1]), ref[1])
+    # GCN-normalised propagate
+    rei, rw = oracle.gcn_norm(ei, N)
+    ref = oracle.propagate(x, rei, reduce="sum", edge_weight=rw)
+    ei2, w = pg.pyg_gcn_norm(tei, N)
+    check_exact(H(ei2), rei)
+    p2 = pg.pyg_plan_build(ei2[1], ei2[0], N, N)
+    for p in (p2, None):
+        check_close(H(pg.pyg_propagate(tx, ei2, reduce="sum", edge_weight=w, plan=p)), ref)
+
+
+# ----------------------------------------------------------------------------- config 2
+
+def test_config2_pubmed_gcn_forward_backward(pg):
+    ei, x, g = synth.pubmed_like()
+    N, F = x.shape
+    rei, rw = oracle.gcn_norm(ei, N)
+    assert rei.shape[1] == 108365
+    ref = oracle.propagate(x, rei, reduce="sum", edge_weight=rw)
+    gref = oracle.propagate_backward(x, rei, g, reduce="sum", edge_weight=rw, with_abs=True, need_edge_weight=True)
+    # bench layout: X rows padded to 504 floats
+    buf = torch.zeros((N, 504), dtype=torch.float32, device=DEV)
+    buf[:, :F] = T(x)
+    tx = buf[:, :F]
+    ei2, w = pg.pyg_gcn_norm(T(ei), N)
+    check_exact(H(ei2), rei)
+    plan = pg.pyg_plan_build(ei2[1], ei2[0], N, N)
+    planT = pg.pyg_plan_build(ei2[0], ei2[1], N, N)
+    for p, pT in ((plan, planT), (None, None)):
+        check_close(H(pg.pyg_propagate(tx, ei2, reduce="sum", edge_weight=w, plan=p)), ref)
+        gr = pg.pyg_propagate_backward(tx, ei2, T(g), reduce="sum", edge_weight=w, plan_T=pT, need_edge_weight=True)
+        check_close(H(gr["x_src"]), gref["x_src"], abs_sum=gref["abs_x_src"])
+        bound = np.abs(x[rei[0]]).sum(1) * np.abs(g[rei[1]]).max(1)
+        check_close(H(gr["edge_weight"]), gref["edge_weight"], abs_sum=bound)
+
+
+# ----------------------------------------------------------------------------- config 3
+
+def test_config3_point_clouds(pg):
+    nn, eptr, local, x = synth.clouds_like()
+    rei, rbatch, rptr = oracle.collate(nn, eptr, local)
+    ei, batch, ptr = pg.pyg_collate(T(nn), T(eptr), T(local), flags=pg.VALIDATE)
+    check_exact(H(ei), rei); check_exact(H(batch), rbatch); check_exact(H(ptr), rptr)
+    assert rei.shape[1] == 1048576
+    N = x.shape[0]
+    tx = T(x)
+    plan = pg.pyg_plan_build(ei[1], ei[0], N, N)
+    assert plan.view()["perm_is_identity"] == 1  # collated clouds are target-sorted
+    for cat in (False, True):
+        ref = oracle.propagate(x, rei, reduce="max", concat_xi=cat)
+        for p in (plan, None):
+            got = pg.pyg_propagate(tx, ei, reduce="max", plan=p, concat_xi=cat)
+            check_exact(H(got[0]), ref[0]); check_exact(H(got[1]), ref[1])
+    # backward of max routes through argmax
+    out, arg = oracle.propagate(x, rei, reduce="max")
+    g = synth.features(N, 64, 303, signed=True)
+    gref = oracle.propagate_backward(x, rei, g, reduce="max", arg=arg)
+    gr = pg.pyg_propagate_backward(tx, ei, T(g), reduce="max", arg_out=T(arg))
+    check_close(H(gr["x_src"]), gref["x_src"], abs_sum=np.abs(gref["x_src"]) + 16 * np.abs(g).max())
+    # global max pooling of the batch (NEXT-3)
+    pref = oracle.global_pool(x, rbatch, 64, "max")
+    pgot = pg.pyg_global_pool(tx, ptr, "max")
+    check_exact(H(pgot[0]), pref[0]); check_exact(H(pgot[1]), pref[1])
+
+
+# ----------------------------------------------------------------------------- config 4
+
+@pytest.fixture(scope="module")
+def reddit(pg):
+    ei, x = synth.reddit_like_torch(DEV, ld=608)
+    N = x.shape[0]
+    plan = pg.pyg_plan_build(ei[1], ei[0], N, N)
+    yield ei, x, plan
+    del plan
+
+
+def _sampled_rows(N, n, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    rows = np.unique(np.concatenate([rng.choice(N, n, replace=False), np.array(extra, np.int64)]))
+    return rows
+
+
+@pytest.mark.parametrize("red", ["mean", "sum", "max"])
+def test_config4_reddit_sampled(pg, reddit, red):
+    ei, x, plan = reddit
+    N, F = x.shape
+    E = ei.shape[1]
+    out = torch.empty((N, 608), dtype=torch.float32, device=DEV)[:, :F]  # bench layout
+    arg = torch.empty((N, 608), dtype=torch.int64, device=DEV)[:, :F] if red == "max" else None
+    pg.pyg_propagate(x, None, reduce=red, plan=plan, out=out, arg_out=arg, E=E)
+    rows = _sampled_rows(N, 1500, 4, extra=(0, N - 1))
+    trows = T(rows)
+    sub, eid = sub_problem(ei, trows, N)
+    xc = H(x) if red != "max" else None
+    if red == "max":
+        # signed features for max so ties and sign matter; recompute on the GPU too
+        xs = (torch.rand((N, F), generator=torch.Generator(DEV).manual_seed(404), device=DEV) * 2 - 1)
+        pg.pyg_propagate(xs, None, reduce="max", plan=plan, out=out, arg_out=arg, E=E)
+        xc = H(xs)
+    ref = oracle.propagate(xc, sub, n_dst=rows.size, reduce=red)
+    got = H(out[trows])
+    if red == "max":
+        check_exact(got, ref[0])
+        check_exact(H(arg[trows]), map_arg(ref[1], eid, E))
+    else:
+        check_close(got, ref)
+
+
+def test_config4_reddit_atomic_sampled(pg, reddit):
+    ei, x, plan = reddit
+    N, F = x.shape
+    out = pg.pyg_propagate(x, ei, reduce="mean")
+    rows = _sampled_rows(N, 500, 5)
+    sub, eid = sub_problem(ei, T(rows), N)
+    ref = oracle.propagate(H(x), sub, n_dst=rows.size, reduce="mean")
+    check_close(H(out[T(rows)]), ref)
+
+
+# ----------------------------------------------------------------------------- config 5
+
+@pytest.fixture(scope="module")
+def rmat(pg):
+    ei = synth.rmat_torch(DEV)
+    N = synth.RMAT["N"]
+    plan = pg.pyg_plan_build(ei[1], ei[0], N, N)
+    yield ei, plan
+    del plan
+
+
+def test_config5_rmat_structure(pg, rmat):
+    ei, plan = rmat
+    N = synth.RMAT["N"]
+    deg = pg.pyg_degree(ei[1], N)
+    v = plan.view()
+    assert ei.shape[1] == 200_000_000
+    dmax = int(deg.max().item())
+    assert dmax > 100_000  # extreme skew (SURVEY: ~305,896)
+    assert v["n_heavy_rows"] == int((deg > v["heavy_threshold"]).sum().item())
+    rowptr = plan.export()[0]
+    check_exact(H(rowptr[1:] - rowptr[:-1]).astype(np.int32), H(deg))
+
+
+@pytest.mark.parametrize("red", ["sum", "max"])
+def test_config5_rmat_sampled(pg, rmat, red):
+    ei, plan = rmat
+    N, F, E = synth.RMAT["N"], synth.RMAT["F"], ei.shape[1]
+    gen = torch.Generator(DEV).manual_seed(505)
+    x = torch.rand((N, F), generator=gen, device=DEV)
+    if red == "max":
+        x = x * 2 - 1
+    res = pg.pyg_propagate(x, None, reduce=red, plan=plan, E=E)
+    out, arg = (res if red == "max" else (res, None))
+    deg = pg.pyg_degree(ei[1], N)
+    hubs = H(torch.topk(deg, 12).indices)
+    empty = H(torch.nonzero(deg == 0).flatten()[:20])
+    rows = _sampled_rows(N, 1500, 6, extra=np.concatenate([hubs, empty]))
+    trows = T(rows)
+    sub, eid = sub_problem(ei, trows, N)
+    ref = oracle.propagate(H(x), sub, n_dst=rows.size, reduce=red)
+    if red == "max":
+        check_exact(H(out[trows]), ref[0])
+        check_exact(H(arg[trows]), map_arg(ref[1], eid, E))
+    else:
+        check_close(H(out[trows]), ref)

@@ -219,6 +219,52 @@ def test_split_hub_rows(pg):
         check_exact(H(res[1]), ref[1][lo:hi])
 
 
+@pytest.mark.parametrize("col_block", [1, 37, 500, 2999])
+def test_source_blocked_plan(pg, col_block):
+    """Source-blocked plans (one pass per block of sources, accumulating in block order) give the
+    oracle's result: sum/mean within tolerance, max/argmax exactly (cross-block ties -> lower id)."""
+    rng = np.random.default_rng(col_block)
+    n_src, n_dst, F = 3000, 700, 12
+    E = 40000
+    src = rng.integers(0, n_src, E + 6000)
+    dst = np.concatenate([rng.integers(0, n_dst, E), np.full(6000, 5)])  # row 5: a hub split across blocks
+    ei = np.stack([src, dst]).astype(np.int64)
+    ei = ei[:, rng.permutation(ei.shape[1])]
+    x = synth.features(n_src, F, 1)
+    xt = rng.integers(-2, 3, (n_src, F)).astype(np.float32)  # tie-heavy for max
+    w = rng.random(ei.shape[1]).astype(np.float32)
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], n_dst, n_src, col_block=col_block)
+    v = plan.view()
+    assert v["n_col_blocks"] == -(-n_src // col_block)
+    for red, xx, ww in (("sum", x, w), ("mean", x, None), ("max", xt, None), ("max", xt, w)):
+        ref = oracle.propagate(xx, ei, n_dst=n_dst, reduce=red, edge_weight=ww, with_abs=True)
+        got = pg.pyg_propagate(T(xx), tei, n_dst=n_dst, reduce=red, edge_weight=T(ww) if ww is not None else None,
+                               plan=plan)
+        if red == "max":
+            compare(got, ref[:2], red, what=f"blocked {col_block}")
+        else:
+            compare(got, ref[0], red, abs_sum=ref[1], what=f"blocked {col_block}")
+        for lo, hi in ((0, 5), (5, 6), (6, 700), (100, 400)):
+            sl = plan.slice(lo, hi)
+            g2 = pg.pyg_propagate(T(xx), tei, n_dst=hi - lo, reduce=red,
+                                  edge_weight=T(ww) if ww is not None else None, plan=sl)
+            if red == "max":
+                check_exact(H(g2[0]), ref[0][lo:hi]); check_exact(H(g2[1]), ref[1][lo:hi])
+            else:
+                check_close(H(g2), ref[0][lo:hi], abs_sum=ref[1][lo:hi])
+    # concatenated x_i block with sum/mean uses the plan's total degree
+    ref = oracle.propagate(x, ei, n_dst=n_dst, reduce="mean", concat_xi=True, x_dst=x[:n_dst])
+    got = pg.pyg_propagate(T(x), tei, n_dst=n_dst, reduce="mean", concat_xi=True, x_dst=T(x[:n_dst]), plan=plan)
+    check_close(H(got), ref)
+    # transposed blocked plan for the backward
+    g = synth.features(n_dst, F, 9, signed=True)
+    planT = pg.pyg_plan_build(tei[0], tei[1], n_src, n_dst, col_block=max(1, col_block // 4))
+    rr = oracle.propagate_backward(x, ei, g, n_dst=n_dst, reduce="mean", edge_weight=w, with_abs=True)
+    gr = pg.pyg_propagate_backward(T(x), tei, T(g), reduce="mean", edge_weight=T(w), plan_T=planT)
+    check_close(H(gr["x_src"]), rr["x_src"], abs_sum=rr["abs_x_src"])
+
+
 def test_segment_is_deterministic(pg):
     rng = np.random.default_rng(1)
     ei = rand_graph(rng, 5000, 5000, 200000)
