@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpygs.so")
+# PYG_LIBPATH selects an experimental build variant of the same library (A/B tuning runs)
+LIB_PATH = os.environ.get("PYG_LIBPATH") or os.path.join(HERE, "libpygs.so")
 
 SUM, MEAN, MAX = 0, 1, 2
 REDUCE = {"sum": SUM, "add": SUM, "mean": MEAN, "max": MAX}

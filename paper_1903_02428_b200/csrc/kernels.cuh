@@ -22,6 +22,10 @@ struct pyg_plan {
     int32_t heavy_threshold = 0, chunk = 0;
     // Source-blocked plans: edges sorted by (source block, target, id); `parts[b]` is the
     // slice of virtual rows of source block b restricted to this plan's target rows.
+    // Light rows are visited in descending degree bucket (floor log2) order, stable by row id:
+    // a CTA's rows then have similar lengths and the longest go first (power-law graphs).
+    const int32_t* row_order = nullptr;  // [order_len] root row ids, or null
+    int64_t order_len = 0;
     int64_t col_block = 0;            // source rows per block (0 = not blocked)
     const int32_t* deg = nullptr;     // [n_rows] total in-degree (blocked plans), offset like rowptr
     std::vector<pyg_plan> parts;
@@ -30,7 +34,7 @@ struct pyg_plan {
 namespace pyg {
 
 constexpr int kHeavyThreshold = 2048;  // rows longer than this are split (reading Q12)
-constexpr int kChunk = 2048;           // positions per chunk of a split row
+constexpr int kChunk = 512;            // positions per chunk of a split row
 
 // ---- CSR segment-reduce ---------------------------------------------------------
 struct SegArgs {
@@ -50,6 +54,9 @@ struct SegArgs {
     int64_t E_sentinel = 0;
     int64_t heavy_threshold = 0;    // light pass skips rows longer than this
     int allow_pad_read = 0;         // X rows may be read up to round_up(ncols, 4)
+    const int32_t* row_order = nullptr;  // light-row visiting order (root row ids), or null
+    int64_t order_len = 0;          // entries of row_order (root rows)
+    int64_t order_offset = 0;       // root row id of this plan's row 0 (slices skip others)
     int accum = 0;                  // add into out/arg (source-blocked passes after the first)
     int finalize = 1;               // apply the mean division in this pass
     const int32_t* deg_total = nullptr;  // mean divisor per row when segments are partial

@@ -77,6 +77,16 @@ __global__ void heavy_compact(const int32_t* __restrict__ flag_heavy, const int3
     GRID_STRIDE(r, n_rows) if (flag_heavy[r]) heavy_rows[pos[r]] = (int32_t)r;
 }
 
+// key = 31 - degree bucket (bucket = bit length of the degree): larger rows sort first
+__global__ void order_keys(const int64_t* __restrict__ rowptr, int64_t n_rows, int32_t* keys, int32_t* vals) {
+    GRID_STRIDE(r, n_rows) {
+        const int64_t d = rowptr[r + 1] - rowptr[r];
+        const int bucket = d > 0 ? 64 - __clzll((unsigned long long)d) : 0;
+        keys[r] = 31 - min(bucket, 31);
+        vals[r] = (int32_t)r;
+    }
+}
+
 __global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_heavy,
                              const int64_t* __restrict__ rowptr, int chunk, int64_t* cnt) {
     GRID_STRIDE(h, n_heavy) {
@@ -89,6 +99,7 @@ __global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_h
 
 struct PlanLayout {
     int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows, *deg;
+    int32_t *order, *okeys, *okeys_out, *ovals;
     int64_t *rowptr, *cnt, *item_ptr;
     int* flags2;
     void* cub_tmp;
@@ -116,12 +127,21 @@ static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, int
     L.flag_heavy = cv.take<int32_t>(v);
     L.pos = cv.take<int32_t>(v);
     L.cnt = cv.take<int64_t>(v + 1);
+    // light-row order (unblocked plans only)
+    const size_t vo = n_blocks == 1 ? v : 1;
+    L.order = cv.take<int32_t>(vo);
+    L.okeys = cv.take<int32_t>(vo);
+    L.okeys_out = cv.take<int32_t>(vo);
+    L.ovals = cv.take<int32_t>(vo);
     size_t b1 = 0, b2 = 0, b3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)e, 0, 32);
     cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)v);
     cub::DeviceScan::ExclusiveSum(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, (int)v + 1);
-    L.cub_bytes = std::max(b1, std::max(b2, b3));
+    size_t b4 = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b4, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, (int)vo, 0, 5);
+    L.cub_bytes = std::max(std::max(b1, b4), std::max(b2, b3));
     L.cub_tmp = cv.take<char>(L.cub_bytes);
     return cv.off;
 }
@@ -174,6 +194,14 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
         LAUNCH_CHECK();
     }
     if (nb > 1) PYG_TRY(coo_degree(row, E, n_rows, L.deg, nullptr, s));
+    if (nb == 1 && V > 0) {
+        order_keys<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, L.okeys, L.ovals);
+        LAUNCH_CHECK();
+        size_t cb = L.cub_bytes;
+        PYG_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.okeys, L.okeys_out, L.ovals, L.order, (int)V, 0, 5,
+                                                 s));
+        PYG_LAUNCHED();
+    }
     int64_t n_heavy = 0;
     if (V > 0) {
         heavy_flags<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, kHeavyThreshold, L.flag_heavy);
@@ -227,6 +255,10 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     root.item_hi = root.h_heavy_item_ptr[(size_t)n_heavy];
     root.heavy_threshold = kHeavyThreshold;
     root.chunk = kChunk;
+    if (nb == 1) {
+        root.row_order = L.order;
+        root.order_len = V;
+    }
     if (nb == 1) {
         *out = new pyg_plan(std::move(root));
         return PYG_OK;

@@ -1,0 +1,359 @@
+// segment_kernel.cuh -- the CSR (target-sorted) segment-reduce kernel: the deterministic
+// strategy for the scatter-reduce BOX of Eq. (1), fused with the gather of x_j
+// and phi (Fig. 1) so the E x F edge space is never materialised.
+//
+// Mapping (sm_100a, 148 SMs, HBM/L2-bound):
+//   * a group of LPR lanes (4..32, compile-time) owns one target row; lane l owns the
+//     vector chunks q = l + ch*LPR (ch < NCH) of V floats (V = 1, 2, 4 or 8 -> 4..32-byte
+//     loads; V = 8 is the sm_100 256-bit LDG.E.ENL2.256), so one column tile is
+//     LPR*NCH*V floats wide (blockIdx.y tiles wider rows) and every chunk address is
+//     `row base + compile-time offset`;
+//   * the group loads the (gathered id, edge id, scale) of LPR positions at once,
+//     coalesced, and broadcasts them with shuffles (scale / edge id only when used);
+//   * U consecutive edges' rows are loaded before any is accumulated: U*NCH independent
+//     loads in flight per lane (memory-level parallelism for a latency-bound gather);
+//   * accumulation is sequential in sorted position order => deterministic; for MAX the
+//     strict '>' keeps the lowest edge id among IEEE-equal maxima (reading Q4);
+//   * rows longer than kHeavyThreshold (power-law hubs) are split into chunks whose fp32
+//     partials are combined in fp64 by combine_kernel (reading Q12);
+//   * accum/finalize let source-blocked plans add pass after pass into `out`.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace pyg {
+namespace seg {
+
+template <int V>
+__device__ __forceinline__ void ld(float (&r)[V], const float* p) {
+    if constexpr (V == 8) {
+        asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+                       "=f"(r[7])
+                     : "l"(p));
+    } else {
+        ldv<V>(r, p);
+    }
+}
+
+template <int V>
+__device__ __forceinline__ void st(float* p, const float (&r)[V], int n, int vec_ok) {
+    if constexpr (V == 8) {
+        if (vec_ok && n == 8) {
+            reinterpret_cast<float4*>(p)[0] = make_float4(r[0], r[1], r[2], r[3]);
+            reinterpret_cast<float4*>(p)[1] = make_float4(r[4], r[5], r[6], r[7]);
+            return;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) if (q < n) p[q] = r[q];
+    } else {
+        if (vec_ok) {
+            stv<V>(p, r, n);
+            return;
+        }
+#pragma unroll
+        for (int q = 0; q < V; ++q) if (q < n) p[q] = r[q];
+    }
+}
+
+// edges whose rows are loaded before accumulation: ~40 floats of loads in flight per lane
+template <int V, int NCH, int LPR>
+struct Unroll {
+    static constexpr int T0 = (V == 8 ? 32 : 40) / (NCH * V);
+    static constexpr int T = T0 < 1 ? 1 : (T0 > 8 ? 8 : T0);
+    static constexpr int U = T < LPR ? T : LPR;
+};
+
+template <int LPR>
+__device__ __forceinline__ unsigned group_mask() {
+    if constexpr (LPR >= 32) {
+        return 0xffffffffu;
+    } else {
+        const int lane = threadIdx.x & 31;
+        return ((1u << LPR) - 1u) << (lane & ~(LPR - 1));
+    }
+}
+
+// Accumulate positions [beg, end) of one segment into registers.
+template <int V, int NCH, int RED, int LPR>
+__device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
+                                           float (&acc)[NCH][V], int (&bi)[NCH][V]) {
+    constexpr int U = Unroll<V, NCH, LPR>::U;
+    const unsigned mask = group_mask<LPR>();
+    const float* __restrict__ X = a.X;
+    const int64_t ldx = a.ldx;
+    const int32_t* __restrict__ gidx = a.gidx;
+    const int32_t* __restrict__ eid = a.eid;
+    const float* __restrict__ w = a.w;
+    const int32_t* __restrict__ gdeg = a.gdeg;
+    const bool scaled = (w != nullptr) || (gdeg != nullptr);
+    // the edge id is only needed for weights, argmax or edge-space rows
+    const bool need_e = (RED == PYG_MAX) || (w != nullptr) || (gidx == nullptr);
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            acc[ch][q] = (RED == PYG_MAX) ? -INFINITY : 0.0f;
+            bi[ch][q] = -1;
+        }
+    const int lane_off = c0 + l * V;
+    bool cv[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) cv[ch] = lane_off + ch * LPR * V < a.ncols;
+    // row address = base + g * row_bytes as one 32x32->64 IMAD.WIDE (row_bytes < 2^32, g < 2^31);
+    // chunk offsets are compile-time immediates
+    const char* __restrict__ Xl = reinterpret_cast<const char*>(X + lane_off);
+    const uint32_t row_bytes = (uint32_t)(ldx * 4);
+    // Loads of invalid chunks (columns >= ncols) are predicated off; their registers keep stale
+    // values that only ever reach accumulators of columns that are never stored.
+    float v[U][NCH][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int q = 0; q < V; ++q) v[u][ch][q] = 0.0f;
+
+    for (int64_t base = beg; base < end; base += LPR) {
+        const int n = (int)min((int64_t)LPR, end - base);
+        int mg = 0, me = 0;
+        float ms = 1.0f;
+        if (l < n) {
+            const int64_t p = base + l;
+            me = (eid && need_e) ? __ldg(eid + p) : (int)p;
+            mg = gidx ? __ldg(gidx + p) : me;
+            if (w) ms = __ldg(w + me);
+            if (gdeg) ms = ms / (float)__ldg(gdeg + mg);
+        }
+        int t = 0;
+        for (; t + U <= n; t += U) {
+            float sv[U];
+            int ev[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int g = __shfl_sync(mask, mg, t + u, LPR);
+                sv[u] = scaled ? __shfl_sync(mask, ms, t + u, LPR) : 1.0f;
+                ev[u] = (RED == PYG_MAX) ? __shfl_sync(mask, me, t + u, LPR) : 0;
+                const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    if (cv[ch]) ld<V>(v[u][ch], row + ch * LPR * V);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        if (RED == PYG_MAX) {
+                            const float m = __fmul_rn(sv[u], v[u][ch][q]);  // s = 1 -> exact
+                            if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }
+                        } else {
+                            acc[ch][q] = fmaf(sv[u], v[u][ch][q], acc[ch][q]);  // s = 1 -> plain add
+                        }
+                    }
+        }
+        for (; t < n; ++t) {
+            const int g = __shfl_sync(mask, mg, t, LPR);
+            const float sc = scaled ? __shfl_sync(mask, ms, t, LPR) : 1.0f;
+            const int e = (RED == PYG_MAX) ? __shfl_sync(mask, me, t, LPR) : 0;
+            const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (cv[ch]) ld<V>(v[0][ch], row + ch * LPR * V);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    if (RED == PYG_MAX) {
+                        const float m = __fmul_rn(sc, v[0][ch][q]);
+                        if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
+                    } else {
+                        acc[ch][q] = fmaf(sc, v[0][ch][q], acc[ch][q]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+struct HeavyArgs {
+    const int32_t* heavy_rows = nullptr;
+    const int64_t* item_ptr = nullptr;
+    int64_t h_lo = 0, h_hi = 0, item_lo = 0, n_items = 0, row_offset = 0;
+    int chunk = 0;
+    float* part = nullptr;
+    int32_t* part_arg = nullptr;
+    int64_t ldp = 0;
+};
+
+// mode 0: light rows (skip rows longer than heavy_threshold), write / accumulate out, arg
+// mode 1: chunks of split rows, write fp32 partials (+ int32 arg partials)
+// resident CTAs per SM requested from ptxas (caps registers at 65536 / (256 * MINB)): 3 (24 warps)
+// measured best for the V*NCH <= 24 float/lane shapes; wider shapes get fewer to avoid spills
+#ifndef PYG_SEG_MINB
+#define PYG_SEG_MINB 3
+#endif
+template <int V, int NCH, int RED>
+struct MinBlocks {
+    static constexpr int base = V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1);
+    static constexpr int value = (RED == PYG_MAX && base > 1) ? base - 1 : base;  // MAX also keeps arg ids
+};
+template <int V, int NCH, int RED, int LPR>
+__global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kernel(SegArgs a, int mode, HeavyArgs h,
+                                                                                  int out_vec_ok) {
+    constexpr int groups = 256 / LPR;
+    const int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / LPR;
+    const int l = threadIdx.x & (LPR - 1);
+    const int c0 = blockIdx.y * (LPR * NCH * V);
+
+    int64_t beg, end, row = -1;
+    if (mode == 0) {
+        if (a.row_order) {
+            if (gid >= a.order_len) return;
+            row = (int64_t)__ldg(a.row_order + gid) - a.order_offset;
+            if (row < 0 || row >= a.n_rows) return;  // a slice visits only its own rows
+        } else {
+            if (gid >= a.n_rows) return;
+            row = gid;
+        }
+        beg = __ldg(a.rowptr + row);
+        end = __ldg(a.rowptr + row + 1);
+        if (end - beg > a.heavy_threshold) return;  // handled by the split path
+    } else {
+        if (gid >= h.n_items) return;
+        const int64_t item = h.item_lo + gid;
+        // heavy row owning this item: last hr with item_ptr[hr] <= item
+        int64_t lo = h.h_lo, hi = h.h_hi - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (__ldg(h.item_ptr + mid) <= item) lo = mid; else hi = mid - 1;
+        }
+        const int64_t r = (int64_t)__ldg(h.heavy_rows + lo) - h.row_offset;
+        const int64_t c = item - __ldg(h.item_ptr + lo);
+        const int64_t rb = __ldg(a.rowptr + r), re = __ldg(a.rowptr + r + 1);
+        beg = rb + c * h.chunk;
+        end = min(beg + h.chunk, re);
+    }
+
+    float acc[NCH][V];
+    int bi[NCH][V];
+    accumulate<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
+
+    if (mode == 0) {
+        const int64_t dseg = end - beg;
+        // accumulate passes (source-blocked plans) have nothing to add for empty segments
+        if (a.accum && dseg == 0 && !(RED == PYG_MEAN && a.finalize)) return;
+        const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            const int col = c0 + l * V + ch * LPR * V;
+            if (col >= a.ncols) continue;
+            const int nv = min(V, a.ncols - col);
+            float* o = a.out + row * a.ldo + col;
+            if (RED != PYG_MAX) {
+                float r[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) r[q] = acc[ch][q];
+                if (a.accum) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) if (q < nv) r[q] += o[q];
+                }
+                if (RED == PYG_MEAN && a.finalize) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
+                }
+                st<V>(o, r, nv, out_vec_ok);
+            } else {
+                int64_t* ap = a.arg + row * a.lda + col;
+                if (!a.accum) {
+                    float r[V];
+#pragma unroll
+                    for (int q = 0; q < V; ++q) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
+                    st<V>(o, r, nv, out_vec_ok);
+#pragma unroll
+                    for (int q = 0; q < V; ++q)
+                        if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
+                } else {
+                    // merge with earlier blocks: larger value wins, IEEE-equal -> lower edge id (Q4)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) {
+                        if (q >= nv || bi[ch][q] < 0) continue;
+                        const int64_t oa = ap[q];
+                        const float ov = o[q];
+                        if (oa == a.E_sentinel || acc[ch][q] > ov || (acc[ch][q] == ov && bi[ch][q] < oa)) {
+                            o[q] = acc[ch][q];
+                            ap[q] = bi[ch][q];
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        float* pp = h.part + gid * h.ldp;
+        int32_t* pa = h.part_arg ? h.part_arg + gid * h.ldp : nullptr;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            const int col = c0 + l * V + ch * LPR * V;
+            if (col >= a.ncols) continue;
+            const int nv = min(V, a.ncols - col);
+#pragma unroll
+            for (int q = 0; q < V; ++q)
+                if (q < nv) {
+                    pp[col + q] = acc[ch][q];
+                    if (RED == PYG_MAX) pa[col + q] = bi[ch][q];
+                }
+        }
+    }
+}
+
+template <int V, int NCH, int RED, int LPR>
+inline pyg_status_t launch_one(const SegArgs& a, int tiles, int mode, const HeavyArgs& h, int ovk,
+                               cudaStream_t s) {
+    constexpr int groups = 256 / LPR;
+    const int64_t units = mode == 0 ? (a.row_order ? a.order_len : a.n_rows) : h.n_items;
+    if (units <= 0) return PYG_OK;
+    dim3 grid((unsigned)cdiv(units, groups), (unsigned)tiles);
+    seg_kernel<V, NCH, RED, LPR><<<grid, 256, 0, s>>>(a, mode, h, ovk);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+template <int V, int RED>
+inline pyg_status_t launch_red(const SegArgs& a, int nch, int lpr, int tiles, int mode, const HeavyArgs& h,
+                               int ovk, cudaStream_t s) {
+    if (nch == 1) {
+        switch (lpr) {
+            case 4: return launch_one<V, 1, RED, 4>(a, tiles, mode, h, ovk, s);
+            case 8: return launch_one<V, 1, RED, 8>(a, tiles, mode, h, ovk, s);
+            case 16: return launch_one<V, 1, RED, 16>(a, tiles, mode, h, ovk, s);
+            default: return launch_one<V, 1, RED, 32>(a, tiles, mode, h, ovk, s);
+        }
+    }
+    switch (nch) {
+        case 2: return launch_one<V, 2, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 3: return launch_one<V, 3, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 4: return launch_one<V, 4, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 5: return launch_one<V, 5, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 6: return launch_one<V, 6, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 8: return launch_one<V, 8, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 12: return launch_one<V, 12, RED, 32>(a, tiles, mode, h, ovk, s);
+        case 16: return launch_one<V, 16, RED, 32>(a, tiles, mode, h, ovk, s);
+        default: return fail(PYG_ERR_INVALID_ARGUMENT, "internal: bad NCH %d", nch);
+    }
+}
+
+// explicit per-V entry points (one translation unit per V for parallel builds)
+template <int V>
+pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, int mode, const HeavyArgs& h,
+                    int ovk, cudaStream_t s) {
+    switch (reduce) {
+        case PYG_SUM: return launch_red<V, PYG_SUM>(a, nch, lpr, tiles, mode, h, ovk, s);
+        case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
+        default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
+    }
+}
+
+}  // namespace seg
+}  // namespace pyg
