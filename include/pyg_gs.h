@@ -71,6 +71,8 @@ typedef enum {
 #define PYG_VALIDATE       (1u << 8)  /* device index-range pre-pass; synchronous */
 #define PYG_FORCE_ATOMIC   (1u << 9)  /* ignore `plan`, use the atomic COO strategy */
 #define PYG_FORCE_SEGMENT  (1u << 10) /* require a plan (error if NULL) */
+#define PYG_NO_TMA         (1u << 11) /* segment path: use the LDG kernel, not the TMA gather4
+                                         pipeline (A/B testing; results are bitwise identical) */
 
 typedef struct pyg_plan pyg_plan_t;   /* opaque host handle */
 

@@ -16,7 +16,7 @@ from typing import Optional
 import torch
 
 from . import _abi
-from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, PHI_CONCAT_XI, SUM, VALIDATE, PygError, check,
+from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, NO_TMA, PHI_CONCAT_XI, SUM, VALIDATE, PygError, check,
                    launch_count, lib)
 
 __all__ = [

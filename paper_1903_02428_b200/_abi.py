@@ -20,6 +20,7 @@ PHI_CONCAT_XI = 1 << 0
 VALIDATE = 1 << 8
 FORCE_ATOMIC = 1 << 9
 FORCE_SEGMENT = 1 << 10
+NO_TMA = 1 << 11
 
 STATUS = {
     0: "PYG_OK", 1: "PYG_ERR_INVALID_ARGUMENT", 2: "PYG_ERR_DIMENSION", 3: "PYG_ERR_INDEX_OUT_OF_BOUNDS",

@@ -307,6 +307,7 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
             a.out = out + off1; a.ldo = ldo; a.arg = arg_out ? arg_out + off1 : nullptr; a.lda = ldo;
             a.n_rows = n_dst; a.E_sentinel = E; a.heavy_threshold = plan->heavy_threshold;
             a.allow_pad_read = 1;
+            a.flags = flags;
             PYG_TRY(segment_reduce(a, reduce, plan, ws, ws_bytes, s));
         }
         if (D > 0) {

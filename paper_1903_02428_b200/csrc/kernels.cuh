@@ -26,6 +26,16 @@ struct pyg_plan {
     // a CTA's rows then have similar lengths and the longest go first (power-law graphs).
     const int32_t* row_order = nullptr;  // [order_len] root row ids, or null
     int64_t order_len = 0;
+    // TMA-pipelined light rows: tasks are runs of consecutive light rows holding <= kTaskPositions
+    // positions (cut at row boundaries and at every split hub row), so task t is the contiguous
+    // position range [task_pos[2t], task_pos[2t+1]); pos_row maps a position to its root row.
+    // Empty rows are the tail of row_order (from empty_begin) and are zero-filled separately.
+    const int64_t* task_pos = nullptr;  // [2 * n_tasks]
+    const int32_t* task_item = nullptr; // [n_tasks] split-row item id of a hub chunk task, -1 light
+    const int32_t* pos_row = nullptr;   // [E]
+    int64_t n_tasks = 0;
+    int64_t n_light_tasks = 0;          // tasks [0, n_light_tasks) are light rows, the rest hub chunks
+    int64_t empty_begin = 0, n_empty = 0;
     int64_t col_block = 0;            // source rows per block (0 = not blocked)
     const int32_t* deg = nullptr;     // [n_rows] total in-degree (blocked plans), offset like rowptr
     std::vector<pyg_plan> parts;
@@ -35,6 +45,7 @@ namespace pyg {
 
 constexpr int kHeavyThreshold = 2048;  // rows longer than this are split (reading Q12)
 constexpr int kChunk = 512;            // positions per chunk of a split row
+constexpr int kTaskPositions = 4096;   // light positions per TMA-pipeline task
 
 // ---- CSR segment-reduce ---------------------------------------------------------
 struct SegArgs {
@@ -57,6 +68,7 @@ struct SegArgs {
     const int32_t* row_order = nullptr;  // light-row visiting order (root row ids), or null
     int64_t order_len = 0;          // entries of row_order (root rows)
     int64_t order_offset = 0;       // root row id of this plan's row 0 (slices skip others)
+    uint32_t flags = 0;             // PYG_NO_TMA, ...
     int accum = 0;                  // add into out/arg (source-blocked passes after the first)
     int finalize = 1;               // apply the mean division in this pass
     const int32_t* deg_total = nullptr;  // mean divisor per row when segments are partial

@@ -78,12 +78,22 @@ __global__ void heavy_compact(const int32_t* __restrict__ flag_heavy, const int3
 }
 
 // key = 31 - degree bucket (bucket = bit length of the degree): larger rows sort first
-__global__ void order_keys(const int64_t* __restrict__ rowptr, int64_t n_rows, int32_t* keys, int32_t* vals) {
+// (also counts empty rows into *n_empty: they sort last, the tail the zero-fill kernel visits)
+__global__ void order_keys(const int64_t* __restrict__ rowptr, int64_t n_rows, int32_t* keys, int32_t* vals,
+                           int* n_empty) {
     GRID_STRIDE(r, n_rows) {
         const int64_t d = rowptr[r + 1] - rowptr[r];
         const int bucket = d > 0 ? 64 - __clzll((unsigned long long)d) : 0;
         keys[r] = 31 - min(bucket, 31);
         vals[r] = (int32_t)r;
+        if (d == 0) atomicAdd(n_empty, 1);
+    }
+}
+
+// pos_row[p] = row owning sorted position p (one thread per row, writes its positions)
+__global__ void pos_row_fill(const int64_t* __restrict__ rowptr, int64_t n_rows, int32_t* pos_row) {
+    GRID_STRIDE(r, n_rows) {
+        for (int64_t p = rowptr[r]; p < rowptr[r + 1]; ++p) pos_row[p] = (int32_t)r;
     }
 }
 
@@ -99,8 +109,9 @@ __global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_h
 
 struct PlanLayout {
     int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows, *deg;
-    int32_t *order, *okeys, *okeys_out, *ovals;
-    int64_t *rowptr, *cnt, *item_ptr;
+    int32_t *order, *okeys, *okeys_out, *ovals, *pos_row, *task_item;
+    int64_t *rowptr, *cnt, *item_ptr, *ldeg, *task_pos;
+    size_t task_cap;
     int* flags2;
     void* cub_tmp;
     size_t cub_bytes;
@@ -133,11 +144,21 @@ static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, int
     L.okeys = cv.take<int32_t>(vo);
     L.okeys_out = cv.take<int32_t>(vo);
     L.ovals = cv.take<int32_t>(vo);
+    L.ldeg = cv.take<int64_t>(1);
+    L.pos_row = n_blocks == 1 ? cv.take<int32_t>(e) : nullptr;
+    // closed tasks hold > kTaskPositions - kHeavyThreshold positions; hub rows add one cut each
+    L.task_cap = n_blocks == 1 ? (e / (kTaskPositions - kHeavyThreshold) + 2 * (e / kHeavyThreshold) + e / kChunk + 4)
+                               : 1;
+    L.task_pos = cv.take<int64_t>(2 * L.task_cap);
+    L.task_item = cv.take<int32_t>(L.task_cap);
     size_t b1 = 0, b2 = 0, b3 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b1, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)e, 0, 32);
     cub::DeviceScan::ExclusiveSum(nullptr, b2, (int32_t*)nullptr, (int32_t*)nullptr, (int)v);
     cub::DeviceScan::ExclusiveSum(nullptr, b3, (int64_t*)nullptr, (int64_t*)nullptr, (int)v + 1);
+    size_t b5 = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b5, (int64_t*)nullptr, (int64_t*)nullptr, (int)vo + 1);
+    b3 = std::max(b3, b5);
     size_t b4 = 0;
     cub::DeviceRadixSort::SortPairs(nullptr, b4, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
                                     (int32_t*)nullptr, (int)vo, 0, 5);
@@ -194,13 +215,20 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
         LAUNCH_CHECK();
     }
     if (nb > 1) PYG_TRY(coo_degree(row, E, n_rows, L.deg, nullptr, s));
+    std::vector<int64_t> h_rowptr;
     if (nb == 1 && V > 0) {
-        order_keys<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, L.okeys, L.ovals);
+        order_keys<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, L.okeys, L.ovals, L.flags2 + 1);
         LAUNCH_CHECK();
         size_t cb = L.cub_bytes;
         PYG_CUDA(cub::DeviceRadixSort::SortPairs(L.cub_tmp, cb, L.okeys, L.okeys_out, L.ovals, L.order, (int)V, 0, 5,
                                                  s));
         PYG_LAUNCHED();
+        if (E > 0) {
+            pos_row_fill<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, L.pos_row);
+            LAUNCH_CHECK();
+        }
+        h_rowptr.resize((size_t)V + 1);
+        PYG_CUDA(cudaMemcpyAsync(h_rowptr.data(), L.rowptr, 8 * ((size_t)V + 1), cudaMemcpyDeviceToHost, s));
     }
     int64_t n_heavy = 0;
     if (V > 0) {
@@ -231,6 +259,50 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     } else {
         PYG_CUDA(cudaMemsetAsync(L.item_ptr, 0, sizeof(int64_t), s));
     }
+    // task partition of the light positions (host greedy over the row pointers; preprocessing):
+    // a task is a run of consecutive light rows with <= kTaskPositions positions, cut before a row
+    // that would overflow it and at every split hub row, so its positions are contiguous.
+    // Hub rows contribute one task per kChunk-position chunk, tagged with its split-row item id
+    // (items are numbered in row order exactly like heavy_item_ptr) so the TMA kernel can write
+    // the chunk's partial for the fp64 combine.
+    int64_t n_tasks = 0, n_light_tasks = 0;
+    if (nb == 1 && V > 0 && E > 0) {
+        std::vector<int64_t> tp, hp;  // light tasks first, then the hub chunk tasks
+        std::vector<int32_t> ti, hi;
+        tp.reserve(2 * (L.task_cap));
+        ti.reserve(L.task_cap);
+        int64_t t0 = -1, t1 = -1, item = 0;
+        auto close = [&]() {
+            if (t0 >= 0) { tp.push_back(t0); tp.push_back(t1); ti.push_back(-1); t0 = -1; }
+        };
+        for (int64_t r = 0; r < V; ++r) {
+            const int64_t b = h_rowptr[(size_t)r], e = h_rowptr[(size_t)r + 1], d = e - b;
+            if (d > kHeavyThreshold) {
+                close();
+                for (int64_t c = b; c < e; c += kChunk) {
+                    hp.push_back(c);
+                    hp.push_back(std::min<int64_t>(c + kChunk, e));
+                    hi.push_back((int32_t)item++);
+                }
+                continue;
+            }
+            if (d == 0) continue;
+            if (t0 >= 0 && (e - t0) > kTaskPositions) close();
+            if (t0 < 0) t0 = b;
+            t1 = e;
+        }
+        close();
+        n_light_tasks = (int64_t)ti.size();
+        tp.insert(tp.end(), hp.begin(), hp.end());
+        ti.insert(ti.end(), hi.begin(), hi.end());
+        n_tasks = (int64_t)ti.size();
+        if ((size_t)n_tasks > L.task_cap) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: task capacity");
+        if (n_tasks > 0) {
+            PYG_CUDA(cudaMemcpyAsync(L.task_pos, tp.data(), tp.size() * 8, cudaMemcpyHostToDevice, s));
+            PYG_CUDA(cudaMemcpyAsync(L.task_item, ti.data(), ti.size() * 4, cudaMemcpyHostToDevice, s));
+        }
+        PYG_CUDA(cudaStreamSynchronize(s));  // tp / ti are locals
+    }
     int flags2[2] = {0, 0};
     PYG_CUDA(cudaMemcpyAsync(flags2, L.flags2, sizeof(flags2), cudaMemcpyDeviceToHost, s));
     pyg_status_t st = validate_flag_check(s, "plan_build: index out of range");
@@ -258,6 +330,13 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     if (nb == 1) {
         root.row_order = L.order;
         root.order_len = V;
+        root.task_pos = n_tasks > 0 ? L.task_pos : nullptr;
+        root.task_item = n_tasks > 0 ? L.task_item : nullptr;
+        root.n_light_tasks = n_light_tasks;
+        root.pos_row = L.pos_row;
+        root.n_tasks = n_tasks;
+        root.n_empty = flags2[1];
+        root.empty_begin = V - flags2[1];
     }
     if (nb == 1) {
         *out = new pyg_plan(std::move(root));

@@ -14,6 +14,10 @@ extern template pyg_status_t launch<4>(const SegArgs&, int, int, int, int, int, 
 extern template pyg_status_t launch<8>(const SegArgs&, int, int, int, int, int, const HeavyArgs&, int, cudaStream_t);
 }  // namespace seg
 
+bool tma_eligible(const SegArgs& a, const pyg_plan* plan);
+pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, unsigned long long* counter,
+                         float* part, int32_t* part_arg, int64_t ldp, cudaStream_t s);
+
 namespace {
 
 // fp64 combine of the chunk partials of each split row (deterministic order).
@@ -127,7 +131,16 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     if (a.heavy_threshold <= 0 || !split) a.heavy_threshold = INT64_MAX;
 
     seg::HeavyArgs h;
-    PYG_TRY(launch(a, reduce, g, 0, h, ovk, s));  // light rows
+    Carver cv(ws, ws_bytes);
+    unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
+    const bool tma = ws && cv.ok() && tma_eligible(a, plan);
+    // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
+    // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel
+    const char* hub_env = getenv("PYG_TMA_HUBS");
+    const bool tma_hubs = tma && split && !(hub_env && atoi(hub_env) == 0);
+    // light rows: TMA gather4 pipeline or the LDG kernel
+    if (tma && !tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, nullptr, nullptr, 0, s));
+    else if (!tma) PYG_TRY(launch(a, reduce, g, 0, h, ovk, s));
     if (!split) return PYG_OK;
 
     // split hub rows: chunk partials, then the fp64 combine
@@ -140,13 +153,13 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     h.row_offset = plan->row_offset;
     h.chunk = plan->chunk;
     h.ldp = (int64_t)align_up((size_t)a.ncols, 4);
-    Carver cv(ws, ws_bytes);
     h.part = cv.take<float>((size_t)h.n_items * h.ldp);
     h.part_arg = reduce == PYG_MAX ? cv.take<int32_t>((size_t)h.n_items * h.ldp) : nullptr;
     if (!ws || !cv.ok())
         return fail(PYG_ERR_NO_MEMORY, "workspace too small for %lld split-row chunks (need %zu bytes)",
                     (long long)h.n_items, segment_ws_bytes(plan, a.ncols, reduce));
-    PYG_TRY(launch(a, reduce, g, 1, h, ovk, s));
+    if (tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, h.part, h.part_arg, h.ldp, s));
+    else PYG_TRY(launch(a, reduce, g, 1, h, ovk, s));  // hub chunks on the LDG kernel (mode 1)
     dim3 grid((unsigned)(h.h_hi - h.h_lo), (unsigned)cdiv(a.ncols, 256));
     switch (reduce) {
         case PYG_SUM: combine_kernel<PYG_SUM><<<grid, 256, 0, s>>>(a, h); break;
@@ -167,10 +180,11 @@ size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce) {
         for (const auto& p : plan->parts) b = std::max(b, segment_ws_bytes(&p, ncols, reduce));
         return b;
     }
+    size_t b = 256;  // TMA task counter
     const int64_t items = plan->item_hi - plan->item_lo;
-    if (items <= 0) return 0;
+    if (items <= 0) return b;
     const size_t ldp = align_up((size_t)ncols, 4);
-    size_t b = align_up((size_t)items * ldp * sizeof(float), 256);
+    b += align_up((size_t)items * ldp * sizeof(float), 256);
     if (reduce == PYG_MAX) b += align_up((size_t)items * ldp * sizeof(int32_t), 256);
     return b;
 }
