@@ -1,23 +1,24 @@
 // segment_tma.cu -- TMA-pipelined CSR segment-reduce for low-reuse graphs (power-law / R-MAT):
 // the gather of x_j rows (Fig. 1) is issued by the Tensor Memory Accelerator with
 // `cp.async.bulk.tensor.2d.tile::gather4` (SASS UTMALDG.2D.GATHER4: 4 arbitrary rows per
-// instruction) into a per-warp ring of shared-memory stages, so each warp keeps (S-1)*4 rows in
+// instruction) into a per-warp ring of S shared-memory stages, so each warp keeps (S-1)*4 rows in
 // flight without spending registers on them -- what a DRAM-latency-bound random-row gather needs.
 //
-//   * work = plan-time tasks: runs of consecutive light rows with <= kTaskPositions positions, i.e.
-//     contiguous position ranges (balanced regardless of degree skew); a warp streams its tasks
-//     back to back without draining the ring;
-//   * producer step (warp-uniform): positions advance 4 per stage; the gathered ids, row ids,
-//     scales and edge ids come from 32-wide coalesced index windows (the next window is
-//     prefetched); lanes 0..3 take their slot's values with ONE shuffle per field and store the
-//     slot metadata to shared memory; lane 0 issues one gather4 per column box on the stage's
-//     mbarrier (arrive.expect_tx);
-//   * consumer step: wait on the stage's mbarrier, accumulate the 4 rows in position order
-//     (same arithmetic as seg_kernel => bitwise-identical results) and flush a row when the next
-//     slot's row differs (mean divides by the count of accumulated positions = the degree, since
-//     tasks never split a row);
-//   * empty rows are zero-filled by `empty_rows_kernel`; rows longer than kHeavyThreshold keep the
-//     split path (seg_kernel mode 1 + fp64 combine).
+//   * work = plan-time tasks: runs of consecutive light rows with <= kTaskPositions positions
+//     (contiguous position ranges), then one task per 512-position chunk of every split hub row;
+//     the first task of a warp is static, the rest come from a global atomic counter;
+//   * producer step (warp-uniform): positions advance 4 per stage; the gathered ids / row ids /
+//     edge ids / scales come from 32-wide coalesced index windows (the next window is prefetched);
+//     lanes 0..3 take their slot's values with ONE shuffle per field and store the slot metadata
+//     (structure-of-arrays: 4 keys | 4 scales | 4 edge ids per stage); lane 0 arms the stage's
+//     mbarrier (arrive.expect_tx) and issues one gather4 per column box;
+//   * consumer step: wait on the mbarrier, accumulate the 4 rows in position order (same
+//     arithmetic as seg_kernel => bitwise-identical results); a full stage inside the current row
+//     takes an unrolled fast path; a row is flushed when the next slot's key differs (mean divides
+//     by the count of accumulated positions = the degree, since tasks never split a light row);
+//     hub-chunk tasks write fp32 partials for the fp64 combine instead;
+//   * S (ring depth) is a template parameter so every stage address and count is compile-time;
+//   * empty rows are zero-filled by `empty_rows_kernel`.
 #include <cuda.h>
 
 #include <cstdlib>
@@ -35,7 +36,7 @@ struct Args {
     const int32_t* task_item;  // hub chunk tasks: split-row item id (partials), else -1
     int64_t n_tasks;
     unsigned long long* next;  // dynamic task counter (zeroed before the launch)
-    float* part;              // [items x ldp] chunk partials (fp32), arg partials (MAX)
+    float* part;               // [items x ldp] chunk partials (fp32), arg partials (MAX)
     int32_t* part_arg;
     int64_t ldp, item_lo;
     int64_t E_root;
@@ -49,19 +50,13 @@ struct Args {
     int ncols;
     int box_w;              // floats per gather4 row (multiple of 8, <= 256)
     int nb;                 // column boxes per row
-    int stages;             // ring depth per warp (<= 16)
     int64_t row_lo, row_hi; // this plan's root rows; out row = r - row_lo
     int64_t E_sentinel;
     int warp_bytes;         // shared memory per warp
     int data_off;           // offset of stage data inside the warp region
 };
 
-struct alignas(16) Meta {
-    int row;
-    float scale;
-    int eid;
-    int pad;
-};
+constexpr int kMetaBytes = 48;  // per stage: int keys[4] | float scales[4] | int eids[4]
 
 __device__ __forceinline__ void bar_init(uint32_t bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
@@ -88,49 +83,64 @@ __device__ __forceinline__ void gather4(uint32_t dst, const CUtensorMap* tmap, i
         "l"(tmap), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
         : "memory");
 }
+__device__ __forceinline__ void sts32(uint32_t addr, int v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+    int4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+    return v;
+}
 
-template <int RED, int NCH>
-__global__ void __launch_bounds__(512) seg_tma_kernel(const __grid_constant__ CUtensorMap tmap, Args a) {
+template <int RED, int NCH, int S>
+__global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CUtensorMap tmap, Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int S = a.stages;
-    unsigned char* region = smem + (size_t)warp * a.warp_bytes;
-    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(region);
-    Meta* meta = reinterpret_cast<Meta*>(region + 128);  // after 16 barriers
-    float* data = reinterpret_cast<float*>(region + a.data_off);
-    const uint32_t data0 = (uint32_t)__cvta_generic_to_shared(data);
-    const int stage_floats = 4 * a.nb * a.box_w;
-    const uint32_t stage_bytes = (uint32_t)stage_floats * 4u;
+    const uint32_t region = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)(warp * a.warp_bytes);
+    const uint32_t bar0 = region;                 // S barriers (8 B each, <= 16)
+    const uint32_t meta0 = region + 128;          // S x kMetaBytes
+    const uint32_t data0 = region + (uint32_t)a.data_off;
+    const int box_w = a.box_w, nb = a.nb;
+    const uint32_t stage_bytes = (uint32_t)(16 * nb * box_w);
+    const uint32_t row_bytes = (uint32_t)(4 * box_w);
 
     if (lane == 0) {
+#pragma unroll
         for (int s = 0; s < S; ++s) bar_init(bar0 + 8 * s);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
 
-    // per-lane smem offsets of its float4 chunks inside a stage (row 0); row i adds i*box_w
-    int coff[NCH];
+    // per-lane byte offsets of its float4 chunks inside a stage (slot 0); slot i adds i*row_bytes
+    uint32_t coff[NCH];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         const int c = 4 * (lane + 32 * ch);
-        const int b = c / a.box_w, cc = c - b * a.box_w;
-        coff[ch] = b < a.nb ? b * 4 * a.box_w + cc : 0;
+        const int b = c / box_w, cc = c - b * box_w;
+        coff[ch] = b < nb ? (uint32_t)(4 * (b * 4 * box_w + cc)) : 0u;
     }
     const bool need_e = (RED == PYG_MAX) || (a.w != nullptr);
+    const bool weighted = a.w != nullptr;
     // this plan's positions (slices restrict the root tasks)
     const int64_t plo = __ldg(a.rowptr + a.row_lo), phi = __ldg(a.rowptr + a.row_hi);
-
     const int64_t twarps = (int64_t)gridDim.x * (blockDim.x >> 5);
     int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
 
     // ---------------- producer state (warp-uniform) ----------------
     int64_t pp = 0, pe = 0;  // position cursor / end of the current task range
     bool done = false;
-    // index windows: lane j holds gathered id / row / edge id / scale of position base + j
     int64_t iwb = 0, nwb = -1;
     int wg = 0, wr = 0, we = 0, ng = 0, nr = 0, ne = 0;
     float ws = 1.0f, ns = 1.0f;
+    int citem = -1;
+    bool first = true;
+
     auto load_window = [&](int64_t base, int& g, int& r, int& e, float& sc) {
         const int64_t p = base + lane;
         g = 0; r = -1; e = 0; sc = 1.0f;
@@ -138,33 +148,8 @@ __global__ void __launch_bounds__(512) seg_tma_kernel(const __grid_constant__ CU
             g = __ldg(a.gidx + p);
             r = __ldg(a.pos_row + p);
             if (need_e) e = a.eid ? __ldg(a.eid + p) : (int)p;
-            if (a.w) sc = __ldg(a.w + e);
+            if (weighted) sc = __ldg(a.w + e);
         }
-    };
-    int citem = -1;  // split-row item of the current task (hub chunk), or -1
-    // first task static (warp id), later ones taken dynamically from a global counter: tasks differ
-    // in cost (size, L2 locality), so static striding leaves a tail
-    bool first = true;
-    auto next_task = [&]() -> bool {
-        for (;;) {
-            if (!first) {
-                unsigned long long t = 0;
-                if (lane == 0) t = atomicAdd(a.next, 1ull);
-                task = twarps + (int64_t)__shfl_sync(0xffffffffu, t, 0);
-            }
-            first = false;
-            if (task >= a.n_tasks) return false;
-            const int64_t t0 = max(__ldg(a.task_pos + 2 * task), plo);
-            const int64_t t1 = min(__ldg(a.task_pos + 2 * task + 1), phi);
-            const int it = a.task_item ? __ldg(a.task_item + task) : -1;
-            if (t0 < t1 && (it < 0 || a.part)) {
-                pp = t0;
-                pe = t1;
-                citem = it;
-                return true;
-            }
-        }
-        return false;
     };
     auto set_window = [&](int64_t base) {
         if (base == nwb) {
@@ -176,35 +161,64 @@ __global__ void __launch_bounds__(512) seg_tma_kernel(const __grid_constant__ CU
         nwb = base + 32;  // speculative prefetch of the continuation
         load_window(nwb, ng, nr, ne, ns);
     };
+    // every task comes from the global counter (a static first task would stall behind CTAs that
+    // are not resident yet)
+    (void)first;
+    (void)twarps;
+    auto next_task = [&]() -> bool {
+        for (;;) {
+            {
+                unsigned long long t = 0;
+                if (lane == 0) t = atomicAdd(a.next, 1ull);
+                task = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+            }
+            if (task >= a.n_tasks) return false;
+            const int64_t t0 = max(__ldg(a.task_pos + 2 * task), plo);
+            const int64_t t1 = min(__ldg(a.task_pos + 2 * task + 1), phi);
+            const int it = a.task_item ? __ldg(a.task_item + task) : -1;
+            if (t0 < t1 && (it < 0 || a.part)) {
+                pp = t0;
+                pe = t1;
+                citem = it;
+                return true;
+            }
+        }
+    };
     if (next_task()) set_window(pp); else done = true;
 
     // fill stage s with the next (up to) 4 positions of the stream; returns the slot count
     auto fill = [&](int s) -> int {
-        if (done) return 0;
+        if (done) {  // mark the stage empty (the consumer stops at a stage without valid slots)
+            if (lane < 4) sts32(meta0 + (uint32_t)(s * kMetaBytes) + 4u * (uint32_t)lane, -1);
+            return 0;
+        }
         if (pp - iwb >= 32) set_window(pp);
-        const int j = (int)(pp - iwb);           // multiple of 4 within the window
+        const int j = (int)(pp - iwb);  // multiple of 4 within the window
         const int cnt = (int)min((int64_t)4, pe - pp);
         const int src = j + (lane & 3);
         const int g = __shfl_sync(0xffffffffu, wg, src);
-        const int r = __shfl_sync(0xffffffffu, wr, src);
-        int e = 0;
-        float sc = 1.0f;
-        if (need_e) e = __shfl_sync(0xffffffffu, we, src);
-        if (a.w) sc = __shfl_sync(0xffffffffu, ws, src);
-        const int g0 = __shfl_sync(0xffffffffu, g, 0);
+        int key = __shfl_sync(0xffffffffu, wr, src);
+        if (citem >= 0) key = -(citem + 2);  // hub chunk: its partial goes to `part`
+        const uint32_t m = meta0 + (uint32_t)(s * kMetaBytes) + 4u * (uint32_t)lane;
+        if (weighted) {
+            const float sc = __shfl_sync(0xffffffffu, ws, src);
+            if (lane < 4) sts32(m + 16, __float_as_int(sc));
+        }
+        if (need_e) {
+            const int e = __shfl_sync(0xffffffffu, we, src);
+            if (lane < 4) sts32(m + 32, e);
+        }
+        if (lane < 4) sts32(m, lane < cnt ? key : -1);
         const int g1 = __shfl_sync(0xffffffffu, g, cnt > 1 ? 1 : 0);
         const int g2 = __shfl_sync(0xffffffffu, g, cnt > 2 ? 2 : 0);
         const int g3 = __shfl_sync(0xffffffffu, g, cnt > 3 ? 3 : 0);
-        // slot key: the root row, or -(item + 2) for a hub chunk (its partial goes to `part`)
-        const int key = citem >= 0 ? -(citem + 2) : r;
-        if (lane < 4) meta[s * 4 + lane] = Meta{lane < cnt ? key : -1, sc, e, 0};
-        __syncwarp();
         if (lane == 0) {
             const uint32_t bar = bar0 + 8 * s;
             bar_expect(bar, stage_bytes);
-            const uint32_t dst = data0 + (uint32_t)(s * stage_floats) * 4u;
-            for (int b = 0; b < a.nb; ++b)
-                gather4(dst + (uint32_t)(b * 4 * a.box_w) * 4u, &tmap, b * a.box_w, g0, g1, g2, g3, bar);
+            const uint32_t dst = data0 + (uint32_t)s * stage_bytes;
+#pragma unroll
+            for (int b = 0; b < NCH; ++b)
+                if (b < nb) gather4(dst + (uint32_t)b * 4u * row_bytes, &tmap, b * box_w, g, g1, g2, g3, bar);
         }
         pp += cnt;
         if (pp >= pe) {
@@ -269,57 +283,72 @@ __global__ void __launch_bounds__(512) seg_tma_kernel(const __grid_constant__ CU
             }
         }
     };
-
-    // prologue: fill the ring; the per-stage slot count is kept in a 16 x 3-bit register array
-    uint64_t cnts = 0;
-    for (int s = 0; s < S; ++s) cnts |= (uint64_t)fill(s) << (3 * s);
-    uint32_t phase = 0;
-    reset();
-    for (int s = 0;;) {
-        const int cnt = (int)((cnts >> (3 * s)) & 7u);
-        if (cnt == 0) break;
-        bar_wait(bar0 + 8 * s, (phase >> s) & 1u);
-        phase ^= 1u << s;
-        const float* st = data + s * stage_floats;
-        const Meta* ms = meta + s * 4;
-        auto slot = [&](const Meta& m, int i) {
+    auto slot = [&](uint32_t st, int i, float sc, int e) {
 #pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-                const float4 v = *reinterpret_cast<const float4*>(st + coff[ch] + i * a.box_w);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
+        for (int ch = 0; ch < NCH; ++ch) {
+            const float4 v = lds128f(st + coff[ch] + (uint32_t)i * row_bytes);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (RED == PYG_MAX) {
-                        const float mm = __fmul_rn(m.scale, vv[q]);
-                        if (bi[ch][q] < 0 || mm > acc[ch][q]) { acc[ch][q] = mm; bi[ch][q] = m.eid; }
-                    } else {
-                        acc[ch][q] = fmaf(m.scale, vv[q], acc[ch][q]);
-                    }
+            for (int q = 0; q < 4; ++q) {
+                if (RED == PYG_MAX) {
+                    const float mm = __fmul_rn(sc, vv[q]);
+                    if (bi[ch][q] < 0 || mm > acc[ch][q]) { acc[ch][q] = mm; bi[ch][q] = e; }
+                } else {
+                    acc[ch][q] = fmaf(sc, vv[q], acc[ch][q]);
                 }
-            }
-        };
-        const Meta m0 = ms[0], m1 = ms[1], m2 = ms[2], m3 = ms[3];
-        if (cnt == 4 && m0.row == crow && m3.row == crow) {
-            // fast path: a full stage inside the current row (rows never interleave in the stream)
-            slot(m0, 0); slot(m1, 1); slot(m2, 2); slot(m3, 3);
-            ccount += 4;
-        } else {
-            for (int i = 0; i < cnt; ++i) {
-                const Meta m = i == 0 ? m0 : (i == 1 ? m1 : (i == 2 ? m2 : m3));
-                if (m.row != crow) {
-                    if (crow != -1) flush();
-                    crow = m.row;
-                    ccount = 0;
-                    reset();
-                }
-                ++ccount;
-                slot(m, i);
             }
         }
-        __syncwarp();  // every lane has read stage s before it is refilled
-        const int nc = fill(s);
-        cnts = (cnts & ~((uint64_t)7 << (3 * s))) | ((uint64_t)nc << (3 * s));
-        s = (s + 1 == S) ? 0 : s + 1;
+    };
+
+    // The ring loop is NOT unrolled: an S-times unrolled body overflows the instruction cache
+    // (measured: S = 8 unrolled ran 2.6x slower than S = 2).  Slot counts live in shared memory
+    // (keys of unused slots are -1).
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) fill(s);
+    __syncwarp();  // slot metadata of the prologue stages visible to every lane
+    reset();
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int s = 0;; s = (s + 1 == S) ? 0 : s + 1) {
+        {
+            const uint32_t m = meta0 + (uint32_t)(s * kMetaBytes);
+            const int4 keys = lds128(m);
+            const int c = (keys.x != -1) + (keys.y != -1) + (keys.z != -1) + (keys.w != -1);
+            if (c == 0) break;
+            bar_wait(bar0 + 8 * s, (phase >> s) & 1u);
+            phase ^= 1u << s;
+            const uint32_t st = data0 + (uint32_t)s * stage_bytes;
+            float4 scs = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
+            int4 eids = make_int4(0, 0, 0, 0);
+            if (weighted) scs = lds128f(m + 16);
+            if (need_e) eids = lds128(m + 32);
+            if (c == 4 && keys.x == crow && keys.w == crow) {
+                // fast path: a full stage inside the current row (rows never interleave)
+                slot(st, 0, scs.x, eids.x);
+                slot(st, 1, scs.y, eids.y);
+                slot(st, 2, scs.z, eids.z);
+                slot(st, 3, scs.w, eids.w);
+                ccount += 4;
+            } else {
+                const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
+                const float ss[4] = {scs.x, scs.y, scs.z, scs.w};
+                const int ee[4] = {eids.x, eids.y, eids.z, eids.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    if (i >= c) break;
+                    if (kk[i] != crow) {
+                        if (crow != -1) flush();
+                        crow = kk[i];
+                        ccount = 0;
+                        reset();
+                    }
+                    ++ccount;
+                    slot(st, i, ss[i], ee[i]);
+                }
+            }
+            __syncwarp();  // every lane has read stage s before it is refilled
+            fill(s);
+        }
     }
     if (crow != -1) flush();
 }
@@ -363,6 +392,51 @@ EncodeFn encode_fn() {
     return fn;
 }
 
+template <int RED, int NCH>
+pyg_status_t launch_s(int S, int64_t want, int threads, int smem, cudaStream_t s, const CUtensorMap& tm,
+                      const Args& t) {
+    void (*k)(const CUtensorMap, Args) = nullptr;
+    switch (S) {
+        case 2: k = seg_tma_kernel<RED, NCH, 2>; break;
+        case 3: k = seg_tma_kernel<RED, NCH, 3>; break;
+        case 4: k = seg_tma_kernel<RED, NCH, 4>; break;
+        case 6: k = seg_tma_kernel<RED, NCH, 6>; break;
+        default: k = seg_tma_kernel<RED, NCH, 8>; break;
+    }
+    PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // Keep >= ~80 KB of the 256 KB unified L1/shared array as L1: the index windows are read
+    // through L1, and a carveout that leaves it smaller made the same kernel 3x slower
+    // (R-MAT sum: 213 KB of stages per SM -> 27.4 ms, 147 KB -> 8.9 ms; ncu long_scoreboard).
+    const int kSmemPerSm = 150 * 1024;
+    int dev = 0, sms = 148, per_sm = 1;
+    PYG_CUDA(cudaGetDevice(&dev));
+    PYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int cap = std::max(1, kSmemPerSm / (smem + 1024));
+    const int carve = std::min(100, (int)cdiv((int64_t)cap * (smem + 1024) * 100, 228 * 1024));
+    PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    PYG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem));
+    per_sm = std::min(per_sm, cap);
+    const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1))));
+    k<<<grid, threads, smem, s>>>(tm, t);
+    return PYG_OK;
+}
+
+template <int RED>
+pyg_status_t launch_nch(int nch, int S, int64_t want, int threads, int smem, cudaStream_t s, const CUtensorMap& tm,
+                        const Args& t) {
+    switch (nch) {
+        case 1: return launch_s<RED, 1>(S, want, threads, smem, s, tm, t);
+        case 2: return launch_s<RED, 2>(S, want, threads, smem, s, tm, t);
+        case 3: return launch_s<RED, 3>(S, want, threads, smem, s, tm, t);
+        case 4: return launch_s<RED, 4>(S, want, threads, smem, s, tm, t);
+        case 5: return launch_s<RED, 5>(S, want, threads, smem, s, tm, t);
+        case 6: return launch_s<RED, 6>(S, want, threads, smem, s, tm, t);
+        case 7: return launch_s<RED, 7>(S, want, threads, smem, s, tm, t);
+        case 8: return launch_s<RED, 8>(S, want, threads, smem, s, tm, t);
+        default: return fail(PYG_ERR_INVALID_ARGUMENT, "internal: no TMA kernel for nch=%d", nch);
+    }
+}
+
 }  // namespace tma
 
 // Whether the TMA path applies: unblocked propagate plan with tasks, 16-byte rows, F in [64, 1024].
@@ -392,17 +466,17 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     const int box_w = (int)align_up((size_t)((F + nb - 1) / nb), 8);  // 128-byte aligned box destinations
     const int nch = (int)cdiv(nb * box_w, 128);
     const int stage_bytes = 16 * nb * box_w;
-    static const int budget = [] {
-        const char* e = getenv("PYG_TMA_WARP_KB");
-        return (e ? atoi(e) : 8) * 1024;  // measured best on R-MAT F=128 (S = 4 stages of 2 KB)
-    }();
-    static const int warps = [] {
-        const char* e = getenv("PYG_TMA_WARPS");
-        const int w = e ? atoi(e) : 8;
-        return (w == 2 || w == 4 || w == 8 || w == 16) ? w : 8;
-    }();
-    const int S = std::max(2, std::min(16, budget / stage_bytes));
-    const int head = 128 + (int)align_up(sizeof(Meta) * 4 * 16, 128);
+    const char* kb_env = getenv("PYG_TMA_WARP_KB");
+    // ring budget per warp: 4 KB (R-MAT F=128 -> S = 2 stages of 2 KB) measured best (sum 10.6 ms
+    // vs 12.9 ms at 8 KB and 22 ms at 12 KB): more resident warps beat deeper rings
+    const int budget = (kb_env ? atoi(kb_env) : 4) * 1024;
+    const char* w_env = getenv("PYG_TMA_WARPS");
+    int warps = w_env ? atoi(w_env) : 8;
+    if (warps != 2 && warps != 4 && warps != 8) warps = 8;
+    int S = std::max(2, std::min(8, budget / stage_bytes));
+    if (S == 5) S = 4;
+    if (S == 7) S = 6;
+    const int head = 128 + (int)align_up((size_t)kMetaBytes * 8, 128);
     const int warp_bytes = (int)align_up((size_t)(head + S * stage_bytes), 128);
     const int smem = warps * warp_bytes;
 
@@ -420,9 +494,9 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     t.rowptr = plan->rowptr - plan->row_offset;
     t.pos_row = plan->pos_row;
     t.task_pos = plan->task_pos;
+    t.task_item = plan->task_item;
     t.n_tasks = part ? plan->n_tasks : plan->n_light_tasks;
     t.next = counter;
-    t.task_item = plan->task_item;
     t.part = part;
     t.part_arg = part_arg;
     t.ldp = ldp;
@@ -438,36 +512,18 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     t.ncols = F;
     t.box_w = box_w;
     t.nb = nb;
-    t.stages = S;
     t.row_lo = plan->row_offset;
     t.row_hi = plan->row_offset + plan->n_rows;
     t.E_sentinel = a.E_sentinel;
     t.warp_bytes = warp_bytes;
     t.data_off = head;
 
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = cdiv(t.n_tasks, warps);
-    const int per_sm = std::max(1, (220 * 1024) / smem);
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * per_sm));
-
-#define PYG_TMA_CASE(R, N)                                                                    \
-    if (reduce == R && nch == N) {                                                            \
-        auto k = seg_tma_kernel<R, N>;                                                        \
-        PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)); \
-        k<<<grid, warps * 32, smem, s>>>(tm, t);                                              \
-        launched = true;                                                                      \
+    switch (reduce) {
+        case PYG_SUM: PYG_TRY(launch_nch<PYG_SUM>(nch, S, want, warps * 32, smem, s, tm, t)); break;
+        case PYG_MEAN: PYG_TRY(launch_nch<PYG_MEAN>(nch, S, want, warps * 32, smem, s, tm, t)); break;
+        default: PYG_TRY(launch_nch<PYG_MAX>(nch, S, want, warps * 32, smem, s, tm, t)); break;
     }
-    bool launched = false;
-    PYG_TMA_CASE(PYG_SUM, 1) PYG_TMA_CASE(PYG_SUM, 2) PYG_TMA_CASE(PYG_SUM, 3) PYG_TMA_CASE(PYG_SUM, 4)
-    PYG_TMA_CASE(PYG_SUM, 5) PYG_TMA_CASE(PYG_SUM, 6) PYG_TMA_CASE(PYG_SUM, 7) PYG_TMA_CASE(PYG_SUM, 8)
-    PYG_TMA_CASE(PYG_MEAN, 1) PYG_TMA_CASE(PYG_MEAN, 2) PYG_TMA_CASE(PYG_MEAN, 3) PYG_TMA_CASE(PYG_MEAN, 4)
-    PYG_TMA_CASE(PYG_MEAN, 5) PYG_TMA_CASE(PYG_MEAN, 6) PYG_TMA_CASE(PYG_MEAN, 7) PYG_TMA_CASE(PYG_MEAN, 8)
-    PYG_TMA_CASE(PYG_MAX, 1) PYG_TMA_CASE(PYG_MAX, 2) PYG_TMA_CASE(PYG_MAX, 3) PYG_TMA_CASE(PYG_MAX, 4)
-    PYG_TMA_CASE(PYG_MAX, 5) PYG_TMA_CASE(PYG_MAX, 6) PYG_TMA_CASE(PYG_MAX, 7) PYG_TMA_CASE(PYG_MAX, 8)
-#undef PYG_TMA_CASE
-    if (!launched) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: no TMA kernel for nch=%d", nch);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
 

@@ -1,0 +1,39 @@
+"""Write profiles/traffic.json from ncu launch lists: DRAM bytes (read + write) summed over the
+launches of ONE propagate call (the last call in the list), keyed like bench.py's roofline key."""
+import csv
+import json
+import os
+import sys
+
+
+def call_traffic(path, n_last):
+    rows = list(csv.reader(open(path)))
+    hdr = [r for r in rows if r and r[0] == "ID"][0]
+    K, M, V, U = (hdr.index(c) for c in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
+    d = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+    for r in rows:
+        if r and r[0].isdigit():
+            d.setdefault(int(r[0]), {"name": r[K]})[r[M]] = float(r[V].replace(",", "")) * scale.get(r[U], 1)
+    ours = [i for i in sorted(d) if "pyg::" in d[i]["name"] or "seg::" in d[i]["name"] or "tma::" in d[i]["name"]]
+    sel = ours[-n_last:]
+    b = sum(d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0) for i in sel)
+    t = sum(d[i].get("gpu__time_duration.sum", 0) for i in sel)
+    return int(b), t / 1e6, [d[i]["name"][:60] for i in sel]
+
+
+if __name__ == "__main__":
+    tag = sys.argv[1]
+    out = {"_note": "DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) summed over the launches of one "
+                    "propagate call, from the ncu launch lists in profiles/; bench.py divides by launches_per_call."}
+    specs = [("reddit-mean-segment-cb21179-n1", f"launches_reddit_mean.csv", 11),
+             ("rmat-sum-segment-cb0-n1", "launches_rmat_sum.csv", 3),
+             ("rmat-max-segment-cb0-n1", "launches_rmat_max.csv", 3)]
+    for key, f, n in specs:
+        p = os.path.join("gpurun_out", tag, f)
+        if os.path.exists(p):
+            b, ms, names = call_traffic(p, n)
+            out[key] = b
+            out[key + "_source"] = f"profiles/{tag}_{f} (last {n} launches: {sorted(set(names))}; {ms:.3f} ms serialized)"
+    json.dump(out, open("profiles/traffic.json", "w"), indent=1)
+    print(json.dumps(out, indent=1))

@@ -1,6 +1,6 @@
 #!/bin/bash
-# One GPU session: parity suite, default bench, ncu launch lists (time + DRAM bytes per launch)
-# and one --set full capture per workload.  Output: gpurun_out/$TAG/
+# One GPU session: parity suite, smoke, default bench, ncu launch lists (time + DRAM bytes per
+# launch) and one --set full capture per headline kernel.  Output: gpurun_out/$TAG/
 set -u
 TAG=${1:-r1}
 O=gpurun_out/$TAG
@@ -15,7 +15,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_
 for red in sum max; do
   timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_rmat_$red.csv python bench.py --config rmat --reduce $red $Q > /dev/null 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 6 -c 2 -o $O/full_rmat_sum python bench.py --config rmat --reduce sum $Q > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_tma -s 3 -c 1 -o $O/full_rmat_sum python bench.py --config rmat --reduce sum $Q > /dev/null 2>&1
 for red in sum max; do
   timeout 600 python bench.py --config rmat --reduce $red --steps 10 --no-e2e --no-cpu --no-variants > $O/bench_rmat_$red.json 2> $O/bench_rmat_$red.err
   timeout 600 python bench.py --config rmat --reduce $red --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_rmat_${red}_atomic.json 2> $O/bench_rmat_${red}_atomic.err
