@@ -230,19 +230,19 @@ def traffic_for(workload_key):
 
 # --------------------------------------------------------------------------- CPU oracle leg
 
-def oracle_sample(ei_cpu, x_cpu, n_rows, reduce, target_s, F):
+def oracle_sample(ei_cpu, x_cpu, n_rows, reduce, target_s, F, w=None):
     """Time the oracle (as it stands) on the edges of the first R target rows, R sized for
     ~target_s seconds from a short calibration run.  Returns (edges*F/s, seconds, E_s, R, out)."""
     import oracle
 
     dst = ei_cpu[1]
-    order_rows = None
 
     def run(R):
         m = dst < R
         sub = ei_cpu[:, m]
+        ws = w[m] if w is not None else None
         t0 = time.perf_counter()
-        out = oracle.propagate(x_cpu, sub, n_dst=R, reduce=reduce)
+        out = oracle.propagate(x_cpu, sub, n_dst=R, reduce=reduce, edge_weight=ws)
         dt = time.perf_counter() - t0
         return sub.shape[1], dt, out
 
@@ -355,11 +355,38 @@ def main():
     ws = torch.empty(max(1, pg.pyg_workspace_size(plan, n_loc, F, red)), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    passes, weighted, prep_ms = 1, False, 0.0
+
+    def compute():
+        pg.pyg_propagate(x_full, None if plan is not None else ei_loc, n_dst=n_loc, reduce=red, plan=plan, out=out,
+                         arg_out=arg, E=E if plan is not None else None, workspace=ws)
+
+    if a.config == "pubmed" and world == 1:
+        # config 2: GCN sym-normalised sum aggregation, forward + backward.  The normalisation
+        # (self-loops + D^-1/2 (A+I) D^-1/2 weights) and both plans are per-graph
+        # preprocessing, as in a cached GCN layer; the step is the forward propagate plus the
+        # backward w.r.t. X (transposed plan).
+        t1 = time.perf_counter()
+        ei, wgt = pg.pyg_gcn_norm(ei, N)
+        E = ei.shape[1]
+        plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N) if a.strategy == "segment" else None
+        planT = pg.pyg_plan_build(ei[0], ei[1], N, N) if a.strategy == "segment" else None
+        torch.cuda.synchronize()
+        prep_ms = (time.perf_counter() - t1) * 1e3
+        g = torch.from_numpy(synth.pubmed_like()[2]).to(dev)
+        gx = torch.empty((N, F), dtype=torch.float32, device=dev)
+        ws = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, red)), dtype=torch.uint8, device=dev)
+        passes, weighted, red = 2, True, "sum"
+
+        def compute():
+            pg.pyg_propagate(x_full, ei, reduce="sum", edge_weight=wgt, plan=plan, out=out, workspace=ws)
+            pg.pyg_propagate_backward(None, ei, g, n_src=N, F=F, reduce="sum", edge_weight=wgt, plan_T=planT,
+                                      grad_x_src=gx)
+
     def step():
         if world > 1:
             gather_x(shard, world, out=xbuf)  # NCCL all-gather of the X shards (dist.py)
-        return pg.pyg_propagate(x_full, None if plan is not None else ei_loc, n_dst=n_loc, reduce=red, plan=plan,
-                                out=out, arg_out=arg, E=E if plan is not None else None, workspace=ws)
+        compute()
 
     # numeric pre-check against the oracle before timing: sampled rows, rank 0 / N=1 below
     for _ in range(a.warmup):
@@ -383,8 +410,7 @@ def main():
         if world > 1:
             gather_x(shard, world, out=xbuf)  # NCCL all-gather of the X shards (dist.py)
         kev[i][0].record(stream)
-        pg.pyg_propagate(x_full, None if plan is not None else ei_loc, n_dst=n_loc, reduce=red, plan=plan, out=out,
-                         arg_out=arg, E=E if plan is not None else None, workspace=ws)
+        compute()
         kev[i][1].record(stream)
         ev[i][1].record(stream)
     t_end.record(stream)
@@ -400,11 +426,11 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, kern_ms = tt.tolist()
     ms_step = total_ms / a.steps
-    units = E * F  # edges*F of the whole job per step (all ranks together)
+    units = passes * E * F  # edges*F of the whole job per step (all ranks together)
     value = units / (ms_step * 1e-3)
 
     peak, peak_src = measured_peak()
-    B = alg_bytes(E_loc if world > 1 else E, n_loc, F, red, a.strategy)
+    B = passes * alg_bytes(E_loc if world > 1 else E, n_loc, F, red, a.strategy, weighted=weighted)
     achieved = B / (kern_ms * 1e-3) / 1e9
     lpc = max(1, int(round(launches / a.steps)))  # launches of the propagate call per step
     wk = f"{a.config}-{red}-{a.strategy}-cb{col_block}-n{world}"
@@ -432,6 +458,10 @@ def main():
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
         "gen_s": gen_s,
     }
+    if passes == 2:
+        result["config"]["step"] = "GCN forward (w = D^-1/2 (A+I) D^-1/2) + backward w.r.t. X"
+        result["config"]["E_with_self_loops"] = E
+        result["gcn_norm_and_plans_ms"] = prep_ms
 
     # ---- numeric pre-check + cpu_baseline (rank 0, N = 1) ----
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -440,7 +470,8 @@ def main():
         oracle.build()
         ei_cpu = ei.cpu().numpy()
         x_cpu = np.ascontiguousarray(x.cpu().numpy())
-        rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F)
+        w_cpu = wgt.cpu().numpy() if weighted else None
+        rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
         got = out[:R].cpu().numpy()
         if red == "max":
             ok = np.array_equal(got, ref[0]) and np.array_equal(arg[:R].cpu().numpy(), ref[1])
@@ -454,7 +485,7 @@ def main():
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
-    if world == 1 and not a.no_e2e:
+    if world == 1 and not a.no_e2e and passes == 1:
         xs = x.as_strided((N, ld), (x.stride(0), 1)) if x.stride(0) == ld else x.contiguous()
         hx = torch.empty(xs.shape, dtype=torch.float32, pin_memory=True)
         hx.copy_(xs)
@@ -489,7 +520,7 @@ def main():
                          "includes": "H2D(X, edge_index) + plan build + propagate + D2H(out)"}
 
     # ---- other reductions on the same resident graph (informational) ----
-    if world == 1 and not a.no_variants:
+    if world == 1 and not a.no_variants and passes == 1:
         var = {}
         for r2 in ("sum", "mean", "max"):
             if r2 == red:

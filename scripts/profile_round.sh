@@ -20,6 +20,12 @@ for red in sum max; do
   timeout 600 python bench.py --config rmat --reduce $red --steps 10 --no-e2e --no-cpu --no-variants > $O/bench_rmat_$red.json 2> $O/bench_rmat_$red.err
   timeout 600 python bench.py --config rmat --reduce $red --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_rmat_${red}_atomic.json 2> $O/bench_rmat_${red}_atomic.err
 done
-for cfg in pubmed clouds cora; do
+for cfg in pubmed clouds cora; do  # pubmed = GCN fwd+bwd
   timeout 300 python bench.py --config $cfg --steps 50 --no-e2e --no-variants > $O/bench_$cfg.json 2> $O/bench_$cfg.err
 done
+# memory-safety evidence: compute-sanitizer memcheck / racecheck on representative small tests
+timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward" \
+  > $O/sanitizer_memcheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck.txt
+timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -q -x \
+  -k "(tma_pipeline and 128) or split_hub" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
