@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
     ap.add_argument("--col-block", default="auto",
                     help="source rows per L2-resident pass: auto (pyg_plan_suggest_col_block), 0 (off) or N")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
+                    help="N > 1 source exchange: NCCL all-gather of X shards, or halo exchange of only the "
+                         "referenced remote rows (auto: halo when it moves < half the all-gather rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -307,7 +310,7 @@ def main():
     dist = init_dist(world, local)
 
     import paper_1903_02428_b200 as pg
-    from paper_1903_02428_b200.dist import gather_x
+    from paper_1903_02428_b200.dist import gather_x, halo_exchange
 
     t0 = time.perf_counter()
     w = make_workload(a.config, dev, a.ld)
@@ -342,13 +345,37 @@ def main():
         ei_loc = ei
     E_loc = int(plan.export()[0][-1].item()) if (plan is not None and world > 1) else ei_loc.shape[1]
 
-    if world > 1:
+    exchange = "none"
+    halo = None
+    if world > 1 and plan is not None and col_block == 0 and a.exchange != "allgather":
+        from paper_1903_02428_b200.dist import halo_setup
+
+        hplan, hids = pg.pyg_halo_build(plan, N, lo, hi, per)
+        nh = torch.tensor([hids.numel()], dtype=torch.int64, device=dev)
+        dist.all_reduce(nh, op=dist.ReduceOp.MAX)
+        if a.exchange == "halo" or int(nh.item()) < 0.5 * (world - 1) * per:
+            send_rows, sc, rc = halo_setup(hids, lo, per, world)
+            halo = dict(plan=hplan, n=hids.numel(), send_rows=send_rows, sc=sc, rc=rc,
+                        sendbuf=torch.empty((send_rows.numel(), ld), dtype=torch.float32, device=dev))
+    if world > 1 and halo is not None:
+        exchange = "halo"
+        xbuf = torch.zeros((per + halo["n"], ld), dtype=torch.float32, device=dev)
+        shard = xbuf[:per]
+        shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
+        x_full = xbuf[:, :F]
+        plan = halo["plan"]
+    elif world > 1:
+        exchange = "allgather"
         xbuf = torch.zeros((per * world, ld), dtype=torch.float32, device=dev)
         shard = torch.zeros((per, ld), dtype=torch.float32, device=dev)
         shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
         x_full = xbuf[:N, :F]
     else:
         x_full = x
+    if world > 1:
+        del x  # every rank keeps only its shard (+ the exchange buffer)
+        w.pop("x")
+        torch.cuda.empty_cache()
     out = torch.empty((n_loc, ((F + 7) // 8 * 8) if a.config == "reddit" else F), dtype=torch.float32,
                       device=dev)[:, :F]
     arg = torch.empty((n_loc, out.stride(0)), dtype=torch.int64, device=dev)[:, :F] if red == "max" else None
@@ -383,9 +410,15 @@ def main():
             pg.pyg_propagate_backward(None, ei, g, n_src=N, F=F, reduce="sum", edge_weight=wgt, plan_T=planT,
                                       grad_x_src=gx)
 
-    def step():
-        if world > 1:
+    def exchange_step():
+        if exchange == "halo":  # pack the requested rows + one NCCL all-to-all (dist.py)
+            halo_exchange(shard, halo["send_rows"], halo["sc"], halo["rc"], xbuf[per:],
+                          pack=lambda xs, rows, o: pg.pyg_gather_rows(xs, rows, out=o), send_buf=halo["sendbuf"])
+        elif exchange == "allgather":
             gather_x(shard, world, out=xbuf)  # NCCL all-gather of the X shards (dist.py)
+
+    def step():
+        exchange_step()
         compute()
 
     # numeric pre-check against the oracle before timing: sampled rows, rank 0 / N=1 below
@@ -407,8 +440,7 @@ def main():
     t_start.record(stream)
     for i in range(a.steps):
         ev[i][0].record(stream)
-        if world > 1:
-            gather_x(shard, world, out=xbuf)  # NCCL all-gather of the X shards (dist.py)
+        exchange_step()
         kev[i][0].record(stream)
         compute()
         kev[i][1].record(stream)
@@ -453,6 +485,8 @@ def main():
                    "strategy": a.strategy, "col_block": col_block,
                    "col_blocks": plan_full.view()["n_col_blocks"] if plan_full is not None else 0,
                    "parallelism": f"dst-range x{world}" if world > 1 else "single",
+                   "exchange": exchange,
+                   "halo_rows": halo["n"] if halo else None,
                    "l2": "inputs larger than L2 (no flush)" if a.config in ("reddit", "rmat")
                    else "L2-resident inputs (warm, back-to-back as in Fig. 3's 1000 runs)"},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,

@@ -148,6 +148,36 @@ pyg_status_t pyg_plan_export(const pyg_plan_t* plan, int64_t* rowptr, int64_t* c
                              void* stream);
 void pyg_plan_destroy(pyg_plan_t* plan);
 
+/* ---- halo exchange of the dst-range partition (north_star (3)) ---- */
+/* For a rank owning targets [own_lo, own_hi) (and the X rows of the same range,
+ * stored as the first own_rows >= own_hi - own_lo rows of a rank-local buffer),
+ * pyg_halo_build derives from `slice` (pyg_plan_slice of an UNBLOCKED forward
+ * plan over n_src sources) the halo: the sources referenced by the slice's
+ * edges that lie outside [own_lo, own_hi), in ascending global id (so grouped
+ * by owner rank when ranks own contiguous ascending ranges).
+ *   halo_ids: (device) int64 capacity n_src; receives the n_halo halo ids.
+ *   n_halo:   (host) receives the halo size.
+ *   halo_plan: a plan equal to `slice` except that every gathered index is
+ *     rank-local: own source j -> j - own_lo, halo source halo_ids[h] ->
+ *     own_rows + h.  A pyg_propagate with this plan reads
+ *     x_src = X_loc [(own_rows + n_halo) x F], the own shard followed by the
+ *     halo rows in halo_ids order; outputs (and max arg edge ids, which stay
+ *     GLOBAL) are bitwise equal to the slice's on the full X.
+ * Workspace (pyg_halo_workspace_size) holds the halo plan's index array and
+ * must outlive it; `slice` (and its root plan) must outlive it too.
+ * SYNCHRONOUS (n_halo is read back).  PYG_ERR_UNSUPPORTED for source-blocked
+ * or scatter plans. */
+pyg_status_t pyg_halo_workspace_size(const pyg_plan_t* slice, int64_t n_src, size_t* bytes);
+pyg_status_t pyg_halo_build(const pyg_plan_t* slice, int64_t n_src, int64_t own_lo, int64_t own_hi,
+                            int64_t own_rows, void* workspace, size_t bytes, pyg_plan_t** halo_plan,
+                            int64_t* halo_ids, int64_t* n_halo, void* stream);
+/* Row gather (the halo "pack": the rows a peer requested, contiguous for the
+ * all-to-all): out[r] = x[rows[r]], r in [0, n).  x [n_x x F] stride ldx;
+ * rows int64 in [0, n_x) (checked synchronously with PYG_VALIDATE);
+ * out [n x F] stride ldo, overwritten.  Asynchronous. */
+pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* rows,
+                             int64_t n, uint32_t flags, float* out, int64_t ldo, void* stream);
+
 /* Scratch needed by pyg_scatter / pyg_propagate / pyg_propagate_backward for
  * an output of F_out columns: fp64-combined partials of split hub rows (plan
  * path) or the in-degree array (atomic path).  bytes may be 0. */

@@ -67,6 +67,10 @@ def lib():
             "orc_gcn_norm": [P, I, I, P, P, P, P, P],
             "orc_collate": [I, P, P, P, P, P, P],
             "orc_global_pool": [P, I, I, P, I, C, P, P],
+            "orc_segment_softmax": [P, I, I, P, I, P],
+            "orc_segment_softmax_backward": [P, P, I, I, P, I, P, P],
+            "orc_gat": [P, I, I, I, P, P, I, P, I, ctypes.c_double, P, P, P],
+            "orc_gat_backward": [P, I, I, I, P, P, I, P, I, ctypes.c_double, P, P, P, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(_lib, name)
@@ -258,3 +262,70 @@ def global_pool(x, batch, G, reduce="sum"):
     _chk(lib().orc_global_pool(_p(x), N, F, _p(_i64(batch)), G, r, _p(out), _p(arg)),
          "global_pool")
     return (out, arg) if r == MAX else out
+
+
+def segment_softmax(src, index, n):
+    """softmax of src [E x H] within each segment of index."""
+    src = _f32(src)
+    src = src.reshape(src.shape[0], -1)
+    E, H = src.shape
+    index = _i64(index)
+    out = np.zeros((E, H), np.float32)
+    _chk(lib().orc_segment_softmax(_p(src), E, H, _p(index), n, _p(out)), "segment_softmax")
+    return out
+
+
+def segment_softmax_backward(out, grad, index, n, with_abs=False):
+    out = _f32(out).reshape(out.shape[0], -1)
+    grad = _f32(grad).reshape(out.shape)
+    E, H = out.shape
+    gs = np.zeros((E, H), np.float32)
+    ab = np.zeros((E, H), np.float64) if with_abs else None
+    _chk(lib().orc_segment_softmax_backward(_p(out), _p(grad), E, H, _p(_i64(index)), n, _p(gs), _p(ab)),
+         "segment_softmax_backward")
+    return (gs, ab) if with_abs else gs
+
+
+def gat(z, s_src, s_dst, edge_index, H, n_dst=None, slope=0.2, with_abs=False):
+    """(out [n_dst x H*C], alpha [E x H]) of the GAT aggregation."""
+    z = _f32(z)
+    n_src, F = z.shape
+    C = F // H
+    assert C * H == F
+    edge_index = _i64(edge_index).reshape(2, -1)
+    E = edge_index.shape[1]
+    s_src = _f32(s_src).reshape(n_src, H)
+    if n_dst is None:
+        n_dst = n_src
+    s_dst = _f32(s_dst).reshape(n_dst, H)
+    out = np.zeros((n_dst, F), np.float32)
+    alpha = np.zeros((E, H), np.float32)
+    ab = np.zeros((n_dst, F), np.float64) if with_abs else None
+    _chk(lib().orc_gat(_p(z), n_src, H, C, _p(s_src), _p(s_dst), n_dst, _p(edge_index), E, float(slope), _p(out),
+                       _p(alpha), _p(ab)), "gat")
+    return (out, alpha, ab) if with_abs else (out, alpha)
+
+
+def gat_backward(z, s_src, s_dst, edge_index, H, grad_out, n_dst=None, slope=0.2, with_abs=False):
+    """dict(z, s_src, s_dst [, abs_z, abs_s_src, abs_s_dst]) of the GAT aggregation's backward."""
+    z = _f32(z)
+    n_src, F = z.shape
+    C = F // H
+    edge_index = _i64(edge_index).reshape(2, -1)
+    E = edge_index.shape[1]
+    if n_dst is None:
+        n_dst = n_src
+    g = _f32(grad_out).reshape(n_dst, F)
+    gz = np.zeros((n_src, F), np.float32)
+    gss = np.zeros((n_src, H), np.float32)
+    gsd = np.zeros((n_dst, H), np.float32)
+    abz = np.zeros((n_src, F), np.float64) if with_abs else None
+    abs_ = np.zeros((n_src, H), np.float64) if with_abs else None
+    abd = np.zeros((n_dst, H), np.float64) if with_abs else None
+    _chk(lib().orc_gat_backward(_p(z), n_src, H, C, _p(_f32(s_src).reshape(n_src, H)),
+                                _p(_f32(s_dst).reshape(n_dst, H)), n_dst, _p(edge_index), E, float(slope), _p(g),
+                                _p(gz), _p(gss), _p(gsd), _p(abz), _p(abs_), _p(abd)), "gat_backward")
+    res = {"z": gz, "s_src": gss, "s_dst": gsd}
+    if with_abs:
+        res.update(abs_z=abz, abs_s_src=abs_, abs_s_dst=abd)
+    return res

@@ -331,3 +331,193 @@ int orc_global_pool(const float* x, int64_t N, int64_t F, const int64_t* batch, 
                     int reduce, float* out, int64_t* arg) {
     return orc_scatter(x, N, F, F, batch, G, reduce, out, arg, NULL);
 }
+
+/* ---- NEXT-1: segment softmax and GAT attention aggregation ---------------- */
+/* segment_softmax (the "optimized sparse softmax kernels" of P:239):
+ * for every segment i = {k : index[k] == i} and column h, with m = max_k src[k][h],
+ *   out[k][h] = exp(src[k][h] - m) / sum_{k' in i} exp(src[k'][h] - m),
+ * in double (three plain passes over the edges: max, sum, divide), rounded once. */
+int orc_segment_softmax(const float* src, int64_t E, int64_t H, const int64_t* index, int64_t n, float* out) {
+    if (E < 0 || H < 0 || n < 0 || (E * H > 0 && (!src || !index || !out))) return ORC_ERR_INVALID;
+    if (check_index(index, E, n)) return ORC_ERR_OOB;
+    size_t nh = (size_t)(n * H > 0 ? n * H : 1);
+    double* m = (double*)malloc(sizeof(double) * nh);
+    double* s = (double*)malloc(sizeof(double) * nh);
+    if (!m || !s) { free(m); free(s); return ORC_ERR_INVALID; }
+    for (size_t t = 0; t < nh; ++t) { m[t] = -INFINITY; s[t] = 0.0; }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) {
+            double v = (double)src[k * H + h];
+            if (v > m[index[k] * H + h]) m[index[k] * H + h] = v;
+        }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) s[index[k] * H + h] += exp((double)src[k * H + h] - m[index[k] * H + h]);
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h)
+            out[k * H + h] = (float)(exp((double)src[k * H + h] - m[index[k] * H + h]) / s[index[k] * H + h]);
+    free(m);
+    free(s);
+    return ORC_OK;
+}
+
+/* softmax backward (chain rule of the definition above, "differentiable"):
+ *   grad_src[k][h] = out[k][h] * (g[k][h] - sum_{k' in seg(k)} out[k'][h] * g[k'][h]).
+ * abs (optional, double [E x H]): out[k][h] * (|g[k][h]| + sum |out g|) -- the magnitude of the
+ * terms, for the summation tolerance (reading Q11). */
+int orc_segment_softmax_backward(const float* out, const float* grad, int64_t E, int64_t H, const int64_t* index,
+                                 int64_t n, float* grad_src, double* abs_out) {
+    if (E < 0 || H < 0 || n < 0 || (E * H > 0 && (!out || !grad || !index || !grad_src))) return ORC_ERR_INVALID;
+    if (check_index(index, E, n)) return ORC_ERR_OOB;
+    size_t nh = (size_t)(n * H > 0 ? n * H : 1);
+    double* t = (double*)calloc(nh, sizeof(double));
+    double* ta = (double*)calloc(nh, sizeof(double));
+    if (!t || !ta) { free(t); free(ta); return ORC_ERR_INVALID; }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) {
+            t[index[k] * H + h] += (double)out[k * H + h] * (double)grad[k * H + h];
+            ta[index[k] * H + h] += fabs((double)out[k * H + h] * (double)grad[k * H + h]);
+        }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) {
+            double a = (double)out[k * H + h];
+            grad_src[k * H + h] = (float)(a * ((double)grad[k * H + h] - t[index[k] * H + h]));
+            if (abs_out) abs_out[k * H + h] = a * (fabs((double)grad[k * H + h]) + ta[index[k] * H + h]);
+        }
+    free(t);
+    free(ta);
+    return ORC_OK;
+}
+
+static double leaky(double v, double slope) { return v > 0.0 ? v : slope * v; }
+
+/* GAT attention coefficients in double: for edge k = (j -> i) and head h,
+ *   logit[k][h] = leaky_relu(s_src[j][h] + s_dst[i][h], slope),
+ *   alpha[k][h] = softmax of the logits over the segment of target i (as orc_segment_softmax). */
+static int gat_alpha(const float* s_src, const float* s_dst, int64_t H, int64_t n_dst, const int64_t* ei, int64_t E,
+                     double slope, double* alpha) {
+    const int64_t* src = ei;
+    const int64_t* dst = ei + E;
+    size_t nh = (size_t)(n_dst * H > 0 ? n_dst * H : 1);
+    double* m = (double*)malloc(sizeof(double) * nh);
+    double* s = (double*)malloc(sizeof(double) * nh);
+    if (!m || !s) { free(m); free(s); return ORC_ERR_INVALID; }
+    for (size_t t = 0; t < nh; ++t) { m[t] = -INFINITY; s[t] = 0.0; }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) {
+            double l = leaky((double)s_src[src[k] * H + h] + (double)s_dst[dst[k] * H + h], slope);
+            alpha[k * H + h] = l;
+            if (l > m[dst[k] * H + h]) m[dst[k] * H + h] = l;
+        }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) {
+            alpha[k * H + h] = exp(alpha[k * H + h] - m[dst[k] * H + h]);
+            s[dst[k] * H + h] += alpha[k * H + h];
+        }
+    for (int64_t k = 0; k < E; ++k)
+        for (int64_t h = 0; h < H; ++h) alpha[k * H + h] /= s[dst[k] * H + h];
+    free(m);
+    free(s);
+    return ORC_OK;
+}
+
+/* GAT aggregation ("output_i = sum alpha z_j (weighted scatter-add)"):
+ *   out[i][h*C + c] = sum_{k : dst_k = i} alpha[k][h] * z[src_k][h*C + c]   (double, rounded once)
+ * z [n_src x H*C] packed; s_src [n_src x H]; s_dst [n_dst x H]; alpha_out [E x H] (optional,
+ * rounded alpha); abs (optional) = sum alpha |z| for the tolerance.  Empty segment -> 0 (Q2). */
+int orc_gat(const float* z, int64_t n_src, int64_t H, int64_t C, const float* s_src, const float* s_dst,
+            int64_t n_dst, const int64_t* ei, int64_t E, double slope, float* out, float* alpha_out,
+            double* abs_out) {
+    if (n_src < 0 || H <= 0 || C < 0 || n_dst < 0 || E < 0) return ORC_ERR_INVALID;
+    if (E > 0 && (!z || !s_src || !s_dst || !ei)) return ORC_ERR_INVALID;
+    if (check_index(ei, E, n_src) || check_index(ei + E, E, n_dst)) return ORC_ERR_OOB;
+    const int64_t F = H * C;
+    double* alpha = (double*)malloc(sizeof(double) * (size_t)(E * H > 0 ? E * H : 1));
+    double* acc = (double*)calloc((size_t)(n_dst * F > 0 ? n_dst * F : 1), sizeof(double));
+    if (!alpha || !acc) { free(alpha); free(acc); return ORC_ERR_INVALID; }
+    int st = gat_alpha(s_src, s_dst, H, n_dst, ei, E, slope, alpha);
+    if (st) { free(alpha); free(acc); return st; }
+    if (abs_out)
+        for (int64_t t = 0; t < n_dst * F; ++t) abs_out[t] = 0.0;
+    for (int64_t k = 0; k < E; ++k) {
+        const int64_t j = ei[k], i = ei[E + k];
+        for (int64_t h = 0; h < H; ++h)
+            for (int64_t c = 0; c < C; ++c) {
+                double v = alpha[k * H + h] * (double)z[j * F + h * C + c];
+                acc[i * F + h * C + c] += v;
+                if (abs_out) abs_out[i * F + h * C + c] += fabs(v);
+            }
+    }
+    for (int64_t t = 0; t < n_dst * F; ++t) out[t] = (float)acc[t];
+    if (alpha_out)
+        for (int64_t t = 0; t < E * H; ++t) alpha_out[t] = (float)alpha[t];
+    free(alpha);
+    free(acc);
+    return ORC_OK;
+}
+
+/* GAT backward (chain rule of orc_gat, double throughout; g = dL/dout [n_dst x H*C]):
+ *   grad_z[j][h*C+c]  = sum_{k: src_k = j} alpha[k][h] * g[dst_k][h*C+c]
+ *   da[k][h]          = sum_c g[dst_k][h*C+c] * z[src_k][h*C+c]            (per-edge SDDMM)
+ *   dl[k][h]          = alpha[k][h] * (da[k][h] - sum_{k' in seg(dst_k)} alpha[k'][h] da[k'][h])
+ *   dp[k][h]          = dl[k][h] * (pre > 0 ? 1 : slope),  pre = s_src[j][h] + s_dst[i][h]
+ *   grad_s_src[j][h]  = sum_{k: src_k = j} dp[k][h];  grad_s_dst[i][h] = sum_{k: dst_k = i} dp[k][h].
+ * abs_* (optional, double): the same sums over the magnitudes of their terms (tolerance). */
+int orc_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, const float* s_src, const float* s_dst,
+                     int64_t n_dst, const int64_t* ei, int64_t E, double slope, const float* g, float* grad_z,
+                     float* grad_s_src, float* grad_s_dst, double* abs_z, double* abs_ssrc, double* abs_sdst) {
+    if (n_src < 0 || H <= 0 || C < 0 || n_dst < 0 || E < 0) return ORC_ERR_INVALID;
+    if (E > 0 && (!z || !s_src || !s_dst || !ei || !g)) return ORC_ERR_INVALID;
+    if (check_index(ei, E, n_src) || check_index(ei + E, E, n_dst)) return ORC_ERR_OOB;
+    const int64_t F = H * C;
+    const size_t eh = (size_t)(E * H > 0 ? E * H : 1), nh = (size_t)(n_dst * H > 0 ? n_dst * H : 1);
+    double* alpha = (double*)malloc(sizeof(double) * eh);
+    double* da = (double*)malloc(sizeof(double) * eh);
+    double* daa = (double*)malloc(sizeof(double) * eh);
+    double* t = (double*)calloc(nh, sizeof(double));
+    double* ta = (double*)calloc(nh, sizeof(double));
+    double* gz = (double*)calloc((size_t)(n_src * F > 0 ? n_src * F : 1), sizeof(double));
+    double* gs = (double*)calloc((size_t)(n_src * H > 0 ? n_src * H : 1), sizeof(double));
+    double* gd = (double*)calloc(nh, sizeof(double));
+    int st = (!alpha || !da || !daa || !t || !ta || !gz || !gs || !gd) ? ORC_ERR_INVALID : ORC_OK;
+    if (!st) st = gat_alpha(s_src, s_dst, H, n_dst, ei, E, slope, alpha);
+    if (!st) {
+        if (abs_z) for (int64_t q = 0; q < n_src * F; ++q) abs_z[q] = 0.0;
+        if (abs_ssrc) for (int64_t q = 0; q < n_src * H; ++q) abs_ssrc[q] = 0.0;
+        if (abs_sdst) for (int64_t q = 0; q < n_dst * H; ++q) abs_sdst[q] = 0.0;
+        for (int64_t k = 0; k < E; ++k) {
+            const int64_t j = ei[k], i = ei[E + k];
+            for (int64_t h = 0; h < H; ++h) {
+                double d = 0.0, dab = 0.0;
+                for (int64_t c = 0; c < C; ++c) {
+                    const double gv = (double)g[i * F + h * C + c];
+                    d += gv * (double)z[j * F + h * C + c];
+                    dab += fabs(gv * (double)z[j * F + h * C + c]);
+                    gz[j * F + h * C + c] += alpha[k * H + h] * gv;
+                    if (abs_z) abs_z[j * F + h * C + c] += alpha[k * H + h] * fabs(gv);
+                }
+                da[k * H + h] = d;
+                daa[k * H + h] = dab;
+                t[i * H + h] += alpha[k * H + h] * d;
+                ta[i * H + h] += alpha[k * H + h] * dab;
+            }
+        }
+        for (int64_t k = 0; k < E; ++k) {
+            const int64_t j = ei[k], i = ei[E + k];
+            for (int64_t h = 0; h < H; ++h) {
+                const double pre = (double)s_src[j * H + h] + (double)s_dst[i * H + h];
+                const double lk = pre > 0.0 ? 1.0 : slope;
+                const double dp = alpha[k * H + h] * (da[k * H + h] - t[i * H + h]) * lk;
+                const double ab = alpha[k * H + h] * (daa[k * H + h] + ta[i * H + h]) * fabs(lk);
+                gs[j * H + h] += dp;
+                gd[i * H + h] += dp;
+                if (abs_ssrc) abs_ssrc[j * H + h] += ab;
+                if (abs_sdst) abs_sdst[i * H + h] += ab;
+            }
+        }
+        if (grad_z) for (int64_t q = 0; q < n_src * F; ++q) grad_z[q] = (float)gz[q];
+        if (grad_s_src) for (int64_t q = 0; q < n_src * H; ++q) grad_s_src[q] = (float)gs[q];
+        if (grad_s_dst) for (int64_t q = 0; q < n_dst * H; ++q) grad_s_dst[q] = (float)gd[q];
+    }
+    free(alpha); free(da); free(daa); free(t); free(ta); free(gz); free(gs); free(gd);
+    return st;
+}

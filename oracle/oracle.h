@@ -101,6 +101,23 @@ int orc_collate(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr,
 int orc_global_pool(const float* x, int64_t N, int64_t F, const int64_t* batch, int64_t G,
                     int reduce, float* out, int64_t* arg);
 
+/* NEXT-1: segment softmax ("optimized sparse
+ * softmax kernels") over [E x H] values grouped by index, and its backward. */
+int orc_segment_softmax(const float* src, int64_t E, int64_t H, const int64_t* index, int64_t n,
+                        float* out);
+int orc_segment_softmax_backward(const float* out, const float* grad, int64_t E, int64_t H,
+                                 const int64_t* index, int64_t n, float* grad_src, double* abs_out);
+/* GAT attention aggregation with H heads of C channels:
+ * alpha = segment softmax over targets of leaky_relu(s_src[j] + s_dst[i]);
+ * out[i] = sum alpha * z[j] per head; and its backward w.r.t. z, s_src, s_dst. */
+int orc_gat(const float* z, int64_t n_src, int64_t H, int64_t C, const float* s_src,
+            const float* s_dst, int64_t n_dst, const int64_t* ei, int64_t E, double slope,
+            float* out, float* alpha_out, double* abs_out);
+int orc_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, const float* s_src,
+                     const float* s_dst, int64_t n_dst, const int64_t* ei, int64_t E, double slope,
+                     const float* g, float* grad_z, float* grad_s_src, float* grad_s_dst,
+                     double* abs_z, double* abs_ssrc, double* abs_sdst);
+
 #ifdef __cplusplus
 }
 #endif

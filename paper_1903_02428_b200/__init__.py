@@ -22,7 +22,7 @@ from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, NO_TMA, PHI_CONCAT_XI
 __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
-    "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_halo_build", "pyg_gather_rows", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
 
@@ -112,6 +112,34 @@ class Plan:
                 self._h = None
         except Exception:
             pass
+
+
+def pyg_halo_build(slice_plan: Plan, n_src: int, own_lo: int, own_hi: int, own_rows: int):
+    """Halo of a rank's plan slice (north_star (3)): (halo_plan, halo_ids [n_halo] int64).
+    halo_plan gathers from X_loc = [own shard (own_rows rows); X[halo_ids]].  Synchronous."""
+    nb = ctypes.c_size_t()
+    check(lib.pyg_halo_workspace_size(slice_plan.handle, n_src, ctypes.byref(nb)), "pyg_halo_workspace_size")
+    dev = slice_plan._device()
+    ws = _workspace(nb.value, dev)
+    ids = torch.empty(max(n_src, 1), dtype=torch.int64, device=dev)
+    h = ctypes.c_void_p()
+    nh = ctypes.c_int64()
+    check(lib.pyg_halo_build(slice_plan.handle, n_src, own_lo, own_hi, own_rows, _ptr(ws), nb.value, ctypes.byref(h),
+                             _ptr(ids), ctypes.byref(nh), _stream(dev)), "pyg_halo_build")
+    return Plan(h, ws, parent=slice_plan), ids[: nh.value]
+
+
+def pyg_gather_rows(x: torch.Tensor, rows: torch.Tensor, out: Optional[torch.Tensor] = None, flags: int = 0):
+    """out[r] = x[rows[r]] (the halo pack)."""
+    n_x, F, ldx = _rows(x, "x")
+    rows = _i64(rows, "rows")
+    n = rows.numel()
+    if out is None:
+        out = torch.empty((n, F), dtype=torch.float32, device=x.device)
+    _, _, ldo = _rows(out, "out") if n > 0 else (0, F, F)
+    check(lib.pyg_gather_rows(_ptr(x), n_x, F, ldx, _ptr(rows), n, flags, _ptr(out), ldo, _stream(x.device)),
+          "pyg_gather_rows")
+    return out
 
 
 def pyg_plan_suggest_col_block(E: int, n_rows: int, n_cols: int, row_bytes: int) -> int:

@@ -75,6 +75,12 @@ pyg_status_t gcn_norm_impl(const int64_t* ei, int64_t E, int64_t N, const float*
 pyg_status_t collate_impl(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr, const int64_t* local,
                           int64_t Et, int64_t Nt, uint32_t flags, int64_t* ei, int64_t* batch, int64_t* node_ptr,
                           cudaStream_t s);
+pyg_status_t halo_workspace_impl(const pyg_plan* p, int64_t n_src, size_t* bytes);
+pyg_status_t halo_build_impl(const pyg_plan* p, int64_t n_src, int64_t own_lo, int64_t own_hi, int64_t own_rows,
+                             void* ws, size_t bytes, pyg_plan** out, int64_t* halo_ids, int64_t* n_halo,
+                             cudaStream_t s);
+pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, int64_t n, float* out,
+                              int64_t ldo, cudaStream_t s);
 
 constexpr int64_t kMaxI32 = 0x7fffffffLL - 1;
 constexpr double kL2BlockFraction = 0.4;  // X block per pass as a fraction of L2
@@ -177,6 +183,43 @@ pyg_status_t pyg_plan_view(const pyg_plan_t* p, pyg_plan_view_t* v) {
 }
 
 void pyg_plan_destroy(pyg_plan_t* p) { delete p; }
+
+pyg_status_t pyg_halo_workspace_size(const pyg_plan_t* slice, int64_t n_src, size_t* bytes) {
+    REQUIRE(slice && bytes && n_src >= 0, PYG_ERR_INVALID_ARGUMENT, "halo_workspace_size: bad args");
+    REQUIRE(slice->col && slice->parts.empty(), PYG_ERR_UNSUPPORTED,
+            "halo: needs an unblocked forward plan (col_index given, col_block = 0)");
+    REQUIRE(slice->n_cols <= n_src, PYG_ERR_DIMENSION, "halo: plan n_cols > n_src");
+    return halo_workspace_impl(slice, n_src, bytes);
+}
+
+pyg_status_t pyg_halo_build(const pyg_plan_t* slice, int64_t n_src, int64_t own_lo, int64_t own_hi, int64_t own_rows,
+                            void* workspace, size_t bytes, pyg_plan_t** halo_plan, int64_t* halo_ids, int64_t* n_halo,
+                            void* stream) {
+    REQUIRE(slice && halo_plan && n_halo && n_src >= 0, PYG_ERR_INVALID_ARGUMENT, "halo_build: bad args");
+    REQUIRE(n_src == 0 || halo_ids, PYG_ERR_INVALID_ARGUMENT, "halo_build: null halo_ids");
+    REQUIRE(slice->col && slice->parts.empty(), PYG_ERR_UNSUPPORTED,
+            "halo: needs an unblocked forward plan (col_index given, col_block = 0)");
+    REQUIRE(0 <= own_lo && own_lo <= own_hi && own_hi <= n_src && own_rows >= own_hi - own_lo, PYG_ERR_DIMENSION,
+            "halo_build: own range [%lld, %lld) / own_rows %lld inconsistent with n_src %lld", (long long)own_lo,
+            (long long)own_hi, (long long)own_rows, (long long)n_src);
+    REQUIRE(slice->n_cols <= n_src, PYG_ERR_DIMENSION, "halo: plan n_cols > n_src");
+    *halo_plan = nullptr;
+    return halo_build_impl(slice, n_src, own_lo, own_hi, own_rows, workspace, bytes, halo_plan, halo_ids, n_halo,
+                           as_stream(stream));
+}
+
+pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* rows, int64_t n,
+                             uint32_t flags, float* out, int64_t ldo, void* stream) {
+    REQUIRE(n_x >= 0 && F >= 0 && n >= 0, PYG_ERR_INVALID_ARGUMENT, "gather_rows: negative size");
+    REQUIRE(ldx >= F && ldo >= F, PYG_ERR_DIMENSION, "gather_rows: leading dimension < F");
+    REQUIRE(n * F == 0 || (x && rows && out), PYG_ERR_INVALID_ARGUMENT, "gather_rows: null pointer");
+    cudaStream_t s = as_stream(stream);
+    if (flags & PYG_VALIDATE) {
+        PYG_TRY(validate_index(rows, n, 0, n_x, s));
+        PYG_TRY(validate_flag_check(s, "gather_rows: row index out of range"));
+    }
+    return gather_rows_impl(x, ldx, F, rows, n, out, ldo, s);
+}
 
 pyg_status_t pyg_plan_export(const pyg_plan_t* p, int64_t* rowptr, int64_t* col, int64_t* perm, void* stream) {
     REQUIRE(p, PYG_ERR_INVALID_ARGUMENT, "plan_export: null plan");

@@ -45,6 +45,44 @@ def reduce_scatter_rows(partial: torch.Tensor, world: int, group=None) -> torch.
     return out
 
 
+def halo_recv_counts(halo_ids: torch.Tensor, per: int, world: int):
+    """Rows this rank receives from each owner: halo ids are ascending, owner = id // per."""
+    owners = torch.div(halo_ids.to("cpu"), per, rounding_mode="floor")
+    return torch.bincount(owners, minlength=world)[:world].tolist()
+
+
+def halo_setup(halo_ids: torch.Tensor, lo: int, per: int, world: int, group=None):
+    """Plan-time request exchange of the halo: every rank tells each owner which
+    of its rows it needs.  Returns (send_rows, send_counts, recv_counts): send_rows are LOCAL row
+    ids of this rank's shard, grouped by requesting rank; recv_counts[q] rows arrive from rank q,
+    in ascending global id, which is the halo_ids order."""
+    recv_counts = halo_recv_counts(halo_ids, per, world)
+    dev = halo_ids.device
+    rc = torch.tensor(recv_counts, dtype=torch.int64, device=dev)
+    sc = torch.empty_like(rc)
+    dist.all_to_all_single(sc, rc, group=group)  # sc[q] = rows rank q wants from me
+    send_counts = sc.tolist()
+    req = torch.empty(sum(send_counts), dtype=torch.int64, device=dev)
+    dist.all_to_all_single(req, halo_ids.contiguous(), send_counts, recv_counts, group=group)
+    return req - lo, send_counts, recv_counts
+
+
+def halo_exchange(x_shard: torch.Tensor, send_rows: torch.Tensor, send_counts, recv_counts, recv_out: torch.Tensor,
+                  pack=None, group=None, send_buf: Optional[torch.Tensor] = None):
+    """Per-call halo exchange: pack the requested rows (pyg_gather_rows on the GPU) and deliver
+    them with one all-to-all into recv_out [n_halo, ld] (contiguous)."""
+    if pack is None:
+        def pack(x, rows, out):
+            return torch.index_select(x, 0, rows, out=out)
+    ld = recv_out.shape[1]
+    if send_buf is None:
+        send_buf = torch.empty((send_rows.numel(), ld), dtype=x_shard.dtype, device=x_shard.device)
+    if send_rows.numel() > 0:
+        pack(x_shard, send_rows, send_buf)
+    dist.all_to_all_single(recv_out, send_buf, recv_counts, send_counts, group=group)
+    return recv_out
+
+
 def local_edges(edge_index: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
     """In-edges of targets [lo, hi) with targets renumbered to [0, hi - lo), in ascending edge id
     (the order the max tie rule refers to).  Used by the atomic strategy and the tests."""
@@ -58,10 +96,14 @@ class DistAggregation:
 
     Every rank holds the full edge_index (it is needed once, to build the plan), builds the global
     plan and keeps the slice of its rows; X arrives as this rank's padded shard.
+    exchange="allgather": every rank receives every shard (dense graphs: Reddit references
+    essentially every row from every partition).  exchange="halo": only the referenced remote rows
+    travel (power-law / sparse cross-partition edges); the local buffer is [own shard ; halo rows]
+    and the plan's gathered ids are rank-local (pyg_halo_build).
     """
 
     def __init__(self, edge_index: torch.Tensor, n: int, world: int, rank: int, group=None,
-                 col_block: Optional[int] = None, ld: Optional[int] = None):
+                 col_block: Optional[int] = None, ld: Optional[int] = None, exchange: str = "allgather"):
         import paper_1903_02428_b200 as pg
 
         self.pg = pg
@@ -75,10 +117,44 @@ class DistAggregation:
         self.plan = self.plan_full.slice(self.lo, self.hi)
         self.edge_index = edge_index
         self._xbuf = None
+        self.exchange = exchange
+        if exchange == "halo":
+            self.halo_plan, self.halo_ids = pg.pyg_halo_build(self.plan, n, self.lo, self.hi, self.per)
+            self.n_halo = self.halo_ids.numel()
+            self.send_rows, self.send_counts, self.recv_counts = halo_setup(self.halo_ids, self.lo, self.per, world,
+                                                                            group)
+            self._sendbuf = None
+
+    def local_buffer(self, ld: int, dtype=torch.float32) -> torch.Tensor:
+        """[per + n_halo, ld] buffer whose first `per` rows are this rank's shard (halo exchange):
+        writing the shard there saves a copy per call."""
+        rows = self.per + self.n_halo
+        if self._xbuf is None or tuple(self._xbuf.shape) != (rows, ld):
+            self._xbuf = torch.empty((rows, ld), dtype=dtype, device=self.edge_index.device)
+        return self._xbuf
+
+    def _forward_halo(self, x_shard, reduce, out, arg_out, edge_weight):
+        F = x_shard.shape[1]
+        ld = x_shard.stride(0)
+        xl = self.local_buffer(ld, x_shard.dtype)
+        full_rows = x_shard.as_strided((x_shard.shape[0], ld), (ld, 1))
+        if full_rows.data_ptr() != xl.data_ptr():
+            xl[: x_shard.shape[0]].copy_(full_rows)
+        if self._sendbuf is None or tuple(self._sendbuf.shape) != (self.send_rows.numel(), ld):
+            self._sendbuf = torch.empty((self.send_rows.numel(), ld), dtype=xl.dtype, device=xl.device)
+        pg = self.pg
+        halo_exchange(xl[: self.per], self.send_rows, self.send_counts, self.recv_counts, xl[self.per:],
+                      pack=lambda x, rows, o: pg.pyg_gather_rows(x, rows, out=o), group=self.group,
+                      send_buf=self._sendbuf)
+        x_loc = xl[:, :F]
+        return pg.pyg_propagate(x_loc, None, n_dst=self.hi - self.lo, reduce=reduce, plan=self.halo_plan, out=out,
+                                arg_out=arg_out, E=self.E, edge_weight=edge_weight)
 
     def forward(self, x_shard: torch.Tensor, reduce="sum", out: Optional[torch.Tensor] = None,
                 arg_out: Optional[torch.Tensor] = None, edge_weight=None):
         """x_shard: [per, F] (row-strided allowed) -> out [hi - lo, F] (+ global-id arg for max)."""
+        if self.exchange == "halo":
+            return self._forward_halo(x_shard, reduce, out, arg_out, edge_weight)
         F = x_shard.shape[1]
         ld = x_shard.stride(0)
         if self._xbuf is None or self._xbuf.shape[1] != ld:
