@@ -292,6 +292,57 @@ pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx,
                              const int64_t* node_ptr, int64_t G, pyg_reduce_t reduce, float* out,
                              int64_t ldo, int64_t* arg_out, void* stream);
 
+/* ---- NEXT-1: segment softmax and GAT attention aggregation ------------------ */
+/* The paper's only other custom kernels: "our own optimized sparse softmax
+ * kernels" for GAT (GAT P:52).  Semantics from S:161-169 / S:421-429.
+ * All deterministic; they run on the CSR plans (no atomic variant).
+ *
+ * pyg_segment_softmax: out[k][h] = exp(src[k][h] - m_i) / sum_{k' : index[k'] = i}
+ *   exp(src[k'][h] - m_i), m_i the segment max, for i = index[k].
+ *   src [E x H] stride lds; out [E x H] stride ldo (overwritten; edges keep their
+ *   ids); plan: the SCATTER plan of index (pyg_plan_build(index, NULL, ...)),
+ *   unblocked; `index` itself is not read (may be NULL).  Empty segments have no
+ *   entries.  Asynchronous. */
+pyg_status_t pyg_segment_softmax(const float* src, int64_t E, int64_t H, int64_t lds,
+                                 const int64_t* index, int64_t dim_size, const pyg_plan_t* plan,
+                                 float* out, int64_t ldo, void* stream);
+/* grad_src[k][h] = out[k][h] * (g[k][h] - sum_{k' in seg(k)} out[k'][h] g[k'][h]);
+ * H <= 8.  Same plan as the forward.  Asynchronous. */
+pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const float* grad_out,
+                                          int64_t ldg, int64_t E, int64_t H, int64_t dim_size,
+                                          const pyg_plan_t* plan, float* grad_src, int64_t lds,
+                                          void* stream);
+/* GAT aggregation with H heads of C channels: for edge k = (j -> i),
+ *   alpha[k][h] = softmax over the in-edges of i of
+ *                 leaky_relu(s_src[j][h] + s_dst[i][h], negative_slope),
+ *   out[i][h*C + c] = sum_k alpha[k][h] * z[j][h*C + c]   (empty segment -> 0).
+ * z [n_src x H*C] stride ldz (the transformed features x W, computed by the
+ * caller); s_src [n_src x H], s_dst [n_dst x H] packed (the attention
+ * projections a_src . z_j and a_dst . z_i per head, computed by the caller);
+ * out [n_dst x H*C] stride ldo; alpha [E x H] packed, OUTPUT (by original edge
+ * id; needed by the backward).  plan: unblocked forward plan (row = target,
+ * col = source).  H <= 8, H*C <= 1024.  Asynchronous. */
+pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
+                               const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
+                               float negative_slope, const pyg_plan_t* plan, float* out,
+                               int64_t ldo, float* alpha, void* stream);
+/* Backward of pyg_gat_propagate, g = grad_out [n_dst x H*C] stride ldg:
+ *   grad_z[j][h*C+c] = sum_{k: src_k = j} alpha[k][h] g[dst_k][h*C+c]     (grad_z optional)
+ *   grad_logit[k][h] = alpha[k][h] (g_i . z_j|_h - sum_{k' in seg(i)} alpha[k'][h] g_i . z_j'|_h)
+ *                      * leaky_relu'(s_src[j][h] + s_dst[i][h])   (dL/d pre-activation; REQUIRED,
+ *                      [E x H] packed, by edge id)
+ *   grad_s_dst[i][h] = sum over i's in-edges of grad_logit     ([n_dst x H] packed, required)
+ *   grad_s_src[j][h] = sum over j's out-edges of grad_logit    ([n_src x H] packed, optional)
+ * plan: the forward plan; plan_T: row_index = sources, col_index = targets.
+ * workspace: pyg_workspace_size(plan_T, n_src, H, PYG_SUM, 0).  Asynchronous. */
+pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
+                              const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
+                              float negative_slope, const float* alpha, const float* grad_out,
+                              int64_t ldg, const pyg_plan_t* plan, const pyg_plan_t* plan_T,
+                              float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst,
+                              float* grad_logit, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 #ifdef __cplusplus
 }
 #endif

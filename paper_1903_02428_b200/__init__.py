@@ -22,7 +22,8 @@ from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, NO_TMA, PHI_CONCAT_XI
 __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
-    "pyg_halo_build", "pyg_gather_rows", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_halo_build", "pyg_gather_rows", "pyg_segment_softmax", "pyg_segment_softmax_backward",
+    "pyg_gat_propagate", "pyg_gat_backward", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
 
@@ -349,3 +350,65 @@ def pyg_global_pool(x: torch.Tensor, node_ptr: torch.Tensor, reduce="sum"):
     check(lib.pyg_global_pool(_ptr(x), N, F, ldx, _ptr(node_ptr), G, r, _ptr(out), F, _ptr(arg), _stream(x.device)),
           "pyg_global_pool")
     return (out, arg) if r == MAX else out
+
+
+def pyg_segment_softmax(src: torch.Tensor, plan: Plan, dim_size: int, out: Optional[torch.Tensor] = None):
+    """softmax of src [E x H] within the segments of the scatter plan's index."""
+    E, H, lds = _rows(src, "src")
+    if out is None:
+        out = torch.empty((E, H), dtype=torch.float32, device=src.device)
+    _, _, ldo = _rows(out, "out")
+    check(lib.pyg_segment_softmax(_ptr(src), E, H, lds, None, dim_size, plan.handle, _ptr(out), ldo,
+                                  _stream(src.device)), "pyg_segment_softmax")
+    return out
+
+
+def pyg_segment_softmax_backward(out: torch.Tensor, grad_out: torch.Tensor, plan: Plan, dim_size: int):
+    E, H, ldo = _rows(out, "out")
+    _, _, ldg = _rows(grad_out, "grad_out")
+    gs = torch.empty((E, H), dtype=torch.float32, device=out.device)
+    check(lib.pyg_segment_softmax_backward(_ptr(out), ldo, _ptr(grad_out), ldg, E, H, dim_size, plan.handle, _ptr(gs),
+                                           H, _stream(out.device)), "pyg_segment_softmax_backward")
+    return gs
+
+
+def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, plan: Plan,
+                      negative_slope: float = 0.2, out: Optional[torch.Tensor] = None,
+                      alpha: Optional[torch.Tensor] = None):
+    """GAT attention aggregation: (out [n_dst x H*C], alpha [E x H])."""
+    n_src, F, ldz = _rows(z, "z")
+    C = F // H
+    assert C * H == F
+    n_dst = s_dst.shape[0]
+    E = plan.view()["E"]
+    s_src = s_src.contiguous()
+    s_dst = s_dst.contiguous()
+    if out is None:
+        out = torch.empty((n_dst, F), dtype=torch.float32, device=z.device)
+    if alpha is None:
+        alpha = torch.empty((E, H), dtype=torch.float32, device=z.device)
+    _, _, ldo = _rows(out, "out")
+    check(lib.pyg_gat_propagate(_ptr(z), n_src, H, C, ldz, _ptr(s_src), _ptr(s_dst), n_dst, E, negative_slope,
+                                plan.handle, _ptr(out), ldo, _ptr(alpha), _stream(z.device)), "pyg_gat_propagate")
+    return out, alpha
+
+
+def pyg_gat_backward(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, alpha: torch.Tensor,
+                     grad_out: torch.Tensor, plan: Plan, plan_T: Plan, negative_slope: float = 0.2):
+    """dict(z, s_src, s_dst, logit) gradients of pyg_gat_propagate."""
+    n_src, F, ldz = _rows(z, "z")
+    C = F // H
+    n_dst = s_dst.shape[0]
+    E = plan.view()["E"]
+    _, _, ldg = _rows(grad_out, "grad_out")
+    dev = z.device
+    gz = torch.empty((n_src, F), dtype=torch.float32, device=dev)
+    gss = torch.empty((n_src, H), dtype=torch.float32, device=dev)
+    gsd = torch.empty((n_dst, H), dtype=torch.float32, device=dev)
+    gl = torch.empty((max(E, 1), H), dtype=torch.float32, device=dev)[:E]
+    ws = _workspace(pyg_workspace_size(plan_T, n_src, H, SUM), dev)
+    check(lib.pyg_gat_backward(_ptr(z), n_src, H, C, ldz, _ptr(s_src.contiguous()), _ptr(s_dst.contiguous()), n_dst,
+                               E, negative_slope, _ptr(alpha), _ptr(grad_out), ldg, plan.handle, plan_T.handle,
+                               _ptr(gz), F, _ptr(gss), _ptr(gsd), _ptr(gl), _ptr(ws), ws.numel(), _stream(dev)),
+          "pyg_gat_backward")
+    return {"z": gz, "s_src": gss, "s_dst": gsd, "logit": gl}

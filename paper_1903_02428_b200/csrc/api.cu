@@ -83,6 +83,7 @@ pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int6
                               int64_t ldo, cudaStream_t s);
 
 constexpr int64_t kMaxI32 = 0x7fffffffLL - 1;
+constexpr int kAttnMaxHeads = 8;
 constexpr double kL2BlockFraction = 0.4;  // X block per pass as a fraction of L2
 
 static size_t coo_ws_bytes(int64_t n_out) { return 2 * align_up((size_t)std::max<int64_t>(n_out, 1) * 4, 256); }
@@ -514,6 +515,100 @@ pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx, 
     a.n_rows = G; a.E_sentinel = N;
     a.heavy_threshold = INT64_MAX;
     return segment_reduce(a, reduce, nullptr, nullptr, 0, as_stream(stream));
+}
+
+// ---- NEXT-1: segment softmax + GAT attention aggregation (attention.cu) ----------
+
+pyg_status_t pyg_segment_softmax(const float* src, int64_t E, int64_t H, int64_t lds, const int64_t* index,
+                                 int64_t dim_size, const pyg_plan_t* plan, float* out, int64_t ldo, void* stream) {
+    (void)index;
+    REQUIRE(E >= 0 && H >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "segment_softmax: negative size");
+    REQUIRE(lds >= H && ldo >= H, PYG_ERR_DIMENSION, "segment_softmax: leading dimension < H");
+    REQUIRE(plan, PYG_ERR_INVALID_ARGUMENT, "segment_softmax: needs a scatter plan over index");
+    REQUIRE(plan->n_rows == dim_size && plan->col == nullptr && plan->parts.empty() && plan->E == E,
+            PYG_ERR_DIMENSION, "segment_softmax: plan is not an unblocked scatter plan over dim_size rows and E edges");
+    REQUIRE(E * H == 0 || (src && out), PYG_ERR_INVALID_ARGUMENT, "segment_softmax: null pointer");
+    if (E == 0 || H == 0) return PYG_OK;
+    return attention_softmax(plan->rowptr, plan->n_rows, nullptr, plan->perm_identity ? nullptr : plan->perm, src, lds,
+                             nullptr, nullptr, (int)H, 0.0f, out, ldo, as_stream(stream));
+}
+
+pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const float* grad_out, int64_t ldg, int64_t E,
+                                          int64_t H, int64_t dim_size, const pyg_plan_t* plan, float* grad_src,
+                                          int64_t lds, void* stream) {
+    REQUIRE(E >= 0 && H >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "segment_softmax_backward: negative size");
+    REQUIRE(ldo >= H && ldg >= H && lds >= H, PYG_ERR_DIMENSION, "segment_softmax_backward: leading dimension < H");
+    REQUIRE(H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "segment_softmax_backward: at most %d columns", kAttnMaxHeads);
+    REQUIRE(plan && plan->n_rows == dim_size && plan->col == nullptr && plan->parts.empty() && plan->E == E,
+            PYG_ERR_DIMENSION, "segment_softmax_backward: needs the scatter plan of the forward");
+    REQUIRE(E * H == 0 || (out && grad_out && grad_src), PYG_ERR_INVALID_ARGUMENT,
+            "segment_softmax_backward: null pointer");
+    if (E == 0 || H == 0) return PYG_OK;
+    return attention_softmax_bwd(plan->rowptr, plan->n_rows, nullptr, plan->perm_identity ? nullptr : plan->perm,
+                                 (int)H, 1, (int)H, out, ldo, grad_out, ldg, nullptr, 0, nullptr, nullptr, 0.0f,
+                                 grad_src, lds, nullptr, as_stream(stream));
+}
+
+pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
+                               const float* s_dst, int64_t n_dst, int64_t E, float negative_slope,
+                               const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, void* stream) {
+    REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
+            "gat_propagate: bad sizes");
+    const int64_t F = H * C;
+    REQUIRE(ldz >= F && ldo >= F, PYG_ERR_DIMENSION, "gat_propagate: leading dimension < H*C");
+    REQUIRE(F <= 1024 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_propagate: H*C <= 1024 and H <= %d",
+            kAttnMaxHeads);
+    REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() &&
+                plan->n_cols <= n_src && plan->E == E,
+            PYG_ERR_DIMENSION, "gat_propagate: needs an unblocked forward plan over n_dst rows and E edges");
+    REQUIRE(n_dst * F == 0 || out, PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null out");
+    REQUIRE(E == 0 || (z && s_src && s_dst && alpha), PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null input");
+    cudaStream_t s = as_stream(stream);
+    const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
+    if (E > 0)
+        PYG_TRY(attention_softmax(plan->rowptr, n_dst, plan->col, eid, nullptr, 0, s_src, s_dst, (int)H,
+                                  negative_slope, alpha, H, s));
+    return attention_headw(plan->rowptr, n_dst, plan->col, eid, z, ldz, (int)F, (int)C, (int)H, alpha, out, ldo, s);
+}
+
+pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
+                              const float* s_dst, int64_t n_dst, int64_t E, float negative_slope, const float* alpha,
+                              const float* grad_out, int64_t ldg, const pyg_plan_t* plan, const pyg_plan_t* plan_T,
+                              float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst, float* grad_logit,
+                              void* ws, size_t ws_bytes, void* stream) {
+    REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
+            "gat_backward: bad sizes");
+    const int64_t F = H * C;
+    REQUIRE(ldz >= F && ldg >= F && (!grad_z || ldgz >= F), PYG_ERR_DIMENSION, "gat_backward: leading dimension < H*C");
+    REQUIRE(F <= 1024 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_backward: H*C <= 1024 and H <= %d",
+            kAttnMaxHeads);
+    REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() && plan->E == E,
+            PYG_ERR_DIMENSION, "gat_backward: `plan` must be the forward plan");
+    REQUIRE(plan_T && plan_T->n_rows == n_src && (plan_T->col || plan_T->E == 0) && plan_T->parts.empty() &&
+                plan_T->n_cols <= n_dst && plan_T->E == E,
+            PYG_ERR_DIMENSION, "gat_backward: plan_T must be built with row_index = sources, col_index = targets");
+    REQUIRE(E == 0 || (z && s_src && s_dst && alpha && grad_out && grad_logit), PYG_ERR_INVALID_ARGUMENT,
+            "gat_backward: null input (grad_logit [E x H] is required)");
+    REQUIRE(n_dst * H == 0 || grad_s_dst, PYG_ERR_INVALID_ARGUMENT, "gat_backward: null grad_s_dst");
+    cudaStream_t s = as_stream(stream);
+    if (n_dst > 0 && E == 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));
+    if (E > 0)
+        PYG_TRY(attention_softmax_bwd(plan->rowptr, n_dst, plan->col, plan->perm_identity ? nullptr : plan->perm,
+                                      (int)H, (int)C, (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst,
+                                      negative_slope, grad_logit, H, grad_s_dst, s));
+    const int32_t* eidT = plan_T->perm_identity ? nullptr : plan_T->perm;
+    if (grad_z) PYG_TRY(attention_headw(plan_T->rowptr, n_src, plan_T->col, eidT, grad_out, ldg, (int)F, (int)C,
+                                        (int)H, alpha, grad_z, ldgz, s));
+    if (grad_s_src && n_src > 0) {
+        SegArgs a;
+        a.X = grad_logit; a.ldx = H; a.ncols = (int)H;
+        a.rowptr = plan_T->rowptr; a.gidx = plan_T->perm; a.eid = nullptr;
+        a.out = grad_s_src; a.ldo = H; a.n_rows = n_src; a.E_sentinel = E;
+        a.heavy_threshold = plan_T->heavy_threshold;
+        a.flags = PYG_NO_TMA;
+        PYG_TRY(segment_reduce(a, PYG_SUM, plan_T, ws, ws_bytes, s));
+    }
+    return PYG_OK;
 }
 
 }  // extern "C"

@@ -127,4 +127,21 @@ pyg_status_t edge_weight_grad(const float* x, int64_t ldx, const float* g, int64
                               int reduce, const int32_t* deg, float* gw, cudaStream_t s);
 pyg_status_t fill_rows(float* out, int64_t ldo, int ncols, int64_t n, cudaStream_t s);
 
+// ---- attention (NEXT-1; attention.cu) ----------------------------------------------
+// alpha[eid][h] = softmax over the row's positions of the logits: values src[eid][h] (s_src
+// null) or GAT leaky_relu(s_src[col][h] + s_dst[row][h], slope).
+pyg_status_t attention_softmax(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
+                               const float* src, int64_t lds, const float* s_src, const float* s_dst, int H,
+                               float slope, float* alpha, int64_t lda, cudaStream_t s);
+// out[r][c] = sum_p alpha[eid_p][c / C] * X[gidx_p][c]
+pyg_status_t attention_headw(const int64_t* rowptr, int64_t n_rows, const int32_t* gidx, const int32_t* eid,
+                             const float* X, int64_t ldx, int F, int C, int H, const float* alpha, float* out,
+                             int64_t ldo, cudaStream_t s);
+// dlogit = alpha (d_alpha - sum alpha d_alpha) per row (* leaky' for GAT, z != null: d_alpha is the
+// SDDMM grad[row] . z[col] per head, and grad_s_dst gets the row sums)
+pyg_status_t attention_softmax_bwd(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
+                                   int H, int C, int F, const float* alpha, int64_t lda, const float* grad, int64_t ldg,
+                                   const float* z, int64_t ldz, const float* s_src, const float* s_dst, float slope,
+                                   float* dlogit, int64_t ldd, float* grad_s_dst, cudaStream_t s);
+
 }  // namespace pyg

@@ -1,0 +1,145 @@
+"""GPU parity of the NEXT-1 attention kernels (segment softmax, GAT aggregation, backward;
+P:52) against the C oracle on the same seeded inputs, through the
+C ABI.  Tolerance (Q11): |got - ref| <= 1e-5 * S + 1e-6 with S the oracle's sum of
+term magnitudes (alpha: S = |alpha|)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from tests.tolerance import check_close
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def _t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _with_loops(ei, n):
+    loops = np.arange(n, dtype=np.int64)
+    return np.concatenate([ei, np.stack([loops, loops])], axis=1)
+
+
+def _case(name):
+    rng = np.random.default_rng(abs(hash(name)) % 2**31)
+    if name == "cora_h8c8":  # config-1 graph + self-loops, GAT's 8 heads x 8 channels
+        ei, _ = synth.cora_like()
+        n = 2708
+        return _with_loops(ei, n), n, n, 8, 8
+    if name == "ragged_h3c5":  # H*C = 15: scalar path, ragged tail
+        n = 500
+        return np.stack([rng.integers(0, n, 4000), rng.integers(0, n, 4000)]).astype(np.int64), n, n, 3, 5
+    if name == "rmat_h4c16":  # power-law rows (long segments: windowed accumulation)
+        n = 4096
+        return synth.rmat_edges_np(scale=12, E=120000, N=n, seed=9), n, n, 4, 16
+    if name == "bipartite_h2c36":  # n_src != n_dst, many empty targets, F = 72 (3 float4 chunks/lane)
+        return np.stack([rng.integers(0, 700, 3000), rng.integers(0, 900, 3000)]).astype(np.int64), 700, 900, 2, 36
+    if name == "wide_h8c64":  # H*C = 512
+        n = 1200
+        return np.stack([rng.integers(0, n, 20000), rng.integers(0, n, 20000)]).astype(np.int64), n, n, 8, 64
+    raise KeyError(name)
+
+
+CASES = ["cora_h8c8", "ragged_h3c5", "rmat_h4c16", "bipartite_h2c36", "wide_h8c64"]
+
+
+def _inputs(name):
+    ei, n_src, n_dst, H, C = _case(name)
+    rng = np.random.default_rng(len(name))
+    z = rng.standard_normal((n_src, H * C)).astype(np.float32)
+    ss = (rng.standard_normal((n_src, H)) * 2).astype(np.float32)
+    sd = (rng.standard_normal((n_dst, H)) * 2).astype(np.float32)
+    g = rng.standard_normal((n_dst, H * C)).astype(np.float32)
+    return ei, n_src, n_dst, H, C, z, ss, sd, g
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gat_forward(name):
+    import paper_1903_02428_b200 as pg
+
+    ei, n_src, n_dst, H, C, z, ss, sd, _ = _inputs(name)
+    ref, ralpha, ab = oracle.gat(z, ss, sd, ei, H, n_dst=n_dst, with_abs=True)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n_dst, n_src)
+    out, alpha = pg.pyg_gat_propagate(_t(z), _t(ss), _t(sd), H, plan)
+    check_close(alpha.cpu().numpy(), ralpha, what="alpha")
+    check_close(out.cpu().numpy(), ref, abs_sum=ab, what="out")
+    # determinism: a second call is bitwise identical
+    out2, alpha2 = pg.pyg_gat_propagate(_t(z), _t(ss), _t(sd), H, plan)
+    assert torch.equal(out, out2) and torch.equal(alpha, alpha2)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_gat_backward(name):
+    import paper_1903_02428_b200 as pg
+
+    ei, n_src, n_dst, H, C, z, ss, sd, g = _inputs(name)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n_dst, n_src)
+    planT = pg.pyg_plan_build(eit[0], eit[1], n_src, n_dst)
+    zt, sst, sdt = _t(z), _t(ss), _t(sd)
+    _, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan)
+    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT)
+    ref = oracle.gat_backward(z, ss, sd, ei, H, g, n_dst=n_dst, with_abs=True)
+    check_close(got["z"].cpu().numpy(), ref["z"], abs_sum=ref["abs_z"], what="grad_z")
+    check_close(got["s_src"].cpu().numpy(), ref["s_src"], abs_sum=ref["abs_s_src"], what="grad_s_src")
+    check_close(got["s_dst"].cpu().numpy(), ref["s_dst"], abs_sum=ref["abs_s_dst"], what="grad_s_dst")
+
+
+def test_gat_zero_attention_equals_mean():
+    """S:428 on the GPU: s = 0 -> uniform attention = the mean aggregation kernel's result."""
+    import paper_1903_02428_b200 as pg
+
+    ei, _ = synth.cora_like()
+    n, H, C = 2708, 2, 16
+    z = synth.features(n, H * C, 5)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n, n)
+    zero = torch.zeros((n, H), device=DEV)
+    out, alpha = pg.pyg_gat_propagate(_t(z), zero, zero, H, plan)
+    mean = pg.pyg_propagate(_t(z), eit, reduce="mean", plan=plan)
+    check_close(out.cpu().numpy(), mean.cpu().numpy(), what="gat(a=0) vs mean")
+
+
+@pytest.mark.parametrize("H", [1, 4, 11])
+def test_segment_softmax(H):
+    import paper_1903_02428_b200 as pg
+
+    rng = np.random.default_rng(H)
+    E, n = 30000, 2000
+    idx = synth.rmat_edges_np(scale=11, E=E, N=n, seed=H)[1]
+    v = (rng.standard_normal((E, H)) * 4).astype(np.float32)
+    ref = oracle.segment_softmax(v, idx, n)
+    plan = pg.pyg_plan_build(_t(idx), None, n)
+    out = pg.pyg_segment_softmax(_t(v), plan, n)
+    check_close(out.cpu().numpy(), ref, what="softmax")
+    if H <= 8:
+        g = rng.standard_normal((E, H)).astype(np.float32)
+        gs, ab = oracle.segment_softmax_backward(out.cpu().numpy(), g, idx, n, with_abs=True)
+        got = pg.pyg_segment_softmax_backward(out, _t(g), plan, n)
+        check_close(got.cpu().numpy(), gs, abs_sum=ab, what="softmax backward")
+
+
+def test_softmax_printed_example():
+    """values [0, 0] in one segment -> [0.5, 0.5]; S:168 single element -> 1."""
+    import paper_1903_02428_b200 as pg
+
+    idx = torch.tensor([0, 0, 2], device=DEV)
+    plan = pg.pyg_plan_build(idx, None, 3)
+    out = pg.pyg_segment_softmax(torch.tensor([[0.0], [0.0], [3.5]], device=DEV), plan, 3)
+    assert out.flatten().tolist() == [0.5, 0.5, 1.0]
+
+
+def test_attention_errors():
+    import paper_1903_02428_b200 as pg
+
+    ei = torch.randint(0, 50, (2, 300), device=DEV)
+    plan = pg.pyg_plan_build(ei[1], ei[0], 50, 50)
+    z = torch.zeros((50, 9 * 4), device=DEV)
+    with pytest.raises(pg.PygError):  # 9 heads > 8
+        pg.pyg_gat_propagate(z, torch.zeros((50, 9), device=DEV), torch.zeros((50, 9), device=DEV), 9, plan)
+    with pytest.raises(pg.PygError):  # forward plan given where a scatter plan is required
+        pg.pyg_segment_softmax(torch.zeros((300, 1), device=DEV), plan, 50)
