@@ -52,6 +52,12 @@ def parse():
     ap.add_argument("--config", default="reddit", choices=list(CONFIGS))
     ap.add_argument("--reduce", default=None, choices=["sum", "mean", "max"])
     ap.add_argument("--strategy", default="segment", choices=["segment", "atomic"])
+    ap.add_argument("--op", default="propagate", choices=["propagate", "gat", "appnp"],
+                    help="gat: GAT attention aggregation forward + backward (NEXT-1) on the config's graph; "
+                         "appnp: K-step APPNP propagation (NEXT-2) with GCN weights")
+    ap.add_argument("--K", type=int, default=10, help="appnp: propagation steps")
+    ap.add_argument("--alpha", type=float, default=0.1, help="appnp: teleport probability")
+    ap.add_argument("--heads", type=int, default=0, help="GAT heads (0: 8 if F %% 8 == 0, else 4, 2 or 1)")
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
     ap.add_argument("--col-block", default="auto",
                     help="source rows per L2-resident pass: auto (pyg_plan_suggest_col_block), 0 (off) or N")
@@ -164,6 +170,18 @@ def alg_bytes(E, n_dst, F, reduce, strategy, weighted=False):
     return b
 
 
+def gat_step_bytes(E, N, F, H):
+    """Algorithmic bytes of one GAT aggregation forward + backward (NEXT-1), every array counted
+    once per kernel that must read or write it: per edge the index pair (col 4 B + edge id 4 B) in
+    each of the five kernels, the gathered rows (z in the forward and the SDDMM, grad_out over the
+    transposed plan: 3 x 4F), the per-edge scalars (s_src gather 4H x 2, alpha write / read x3,
+    dL/dlogit write / read 4H x 2); per node z-out, grad_out, grad_z (4F each), rowptrs (2 x 8),
+    s_dst / grad_s_dst / grad_s_src (4H each)."""
+    per_edge = 5 * 8 + 3 * 4 * F + 4 * H * (2 + 3 + 2)
+    per_node = 3 * 4 * F + 2 * 8 + 3 * 4 * H
+    return E * per_edge + N * per_node
+
+
 # --------------------------------------------------------------------------- clocks
 
 class Clocks:
@@ -256,6 +274,44 @@ def oracle_sample(ei_cpu, x_cpu, n_rows, reduce, target_s, F, w=None):
     R = int(min(n_rows, max(1, target_s * rate / (F * avg))))
     Es, dt, out = run(R)
     return Es * F / dt, dt, Es, R, out
+
+
+def oracle_gat_sample(ei_cpu, z_cpu, ss, sd, H, n_rows, target_s, F):
+    """The GAT oracle (forward) on the in-edges of the first R target rows, R sized for ~target_s."""
+    import oracle
+
+    dst = ei_cpu[1]
+
+    def run(R):
+        m = dst < R
+        sub = ei_cpu[:, m]
+        t0 = time.perf_counter()
+        res = oracle.gat(z_cpu, ss, sd[:R], sub, H, n_dst=R, with_abs=True)
+        return sub.shape[1], time.perf_counter() - t0, res
+
+    R = max(1, min(n_rows, 256))
+    Es, dt, _ = run(R)
+    rate = max(Es * F / max(dt, 1e-6), 1.0)
+    avg = max(ei_cpu.shape[1] / n_rows, 1e-9)
+    R = int(min(n_rows, max(1, target_s * rate / (F * avg))))
+    Es, dt, res = run(R)
+    return Es * F / dt, dt, Es, R, res
+
+
+def oracle_appnp_run(ei_cpu, x_cpu, w_cpu, K, alpha, target_s, F):
+    """The APPNP oracle is a whole-graph recurrence: timed on the full graph when one step of it
+    (estimated from one propagate pass over a sample) fits target_s, else on the sample pass only."""
+    import oracle
+
+    E = ei_cpu.shape[1]
+    n = x_cpu.shape[0]
+    rate, dt, Es, R, _ = oracle_sample(ei_cpu, x_cpu, n, "sum", min(2.0, target_s / 4), F, w=w_cpu)
+    if E * F * K / rate <= 2 * target_s:
+        t0 = time.perf_counter()
+        ref = oracle.appnp(x_cpu, ei_cpu, K=K, alpha=alpha, edge_weight=w_cpu)
+        dt = time.perf_counter() - t0
+        return E * F * K / dt, dt, E * K, n, ref
+    return rate, dt, Es, 0, None
 
 
 def run_reference(a):
@@ -410,6 +466,57 @@ def main():
             pg.pyg_propagate_backward(None, ei, g, n_src=N, F=F, reduce="sum", edge_weight=wgt, plan_T=planT,
                                       grad_x_src=gx)
 
+    gat = None
+    if a.op == "gat":
+        # NEXT-1: GAT layer aggregation, forward (segment softmax of leaky_relu(s_src[j] + s_dst[i]),
+        # alpha-weighted sum per head) + backward (SDDMM + softmax backward, grad_z over the
+        # transposed plan, grad_s_src).  z = the config's X (the transformed features x W); the
+        # attention projections s_src / s_dst are seeded inputs (dense per-node ops, outside the path).
+        assert world == 1 and a.strategy == "segment", "--op gat: one GPU, segment strategy"
+        H = a.heads or next(h for h in (8, 4, 2, 1) if F % h == 0)
+        t1 = time.perf_counter()
+        if plan_full.view()["n_col_blocks"] > 1:
+            plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
+            col_block = 0
+        planT = pg.pyg_plan_build(ei[0], ei[1], N, N)
+        torch.cuda.synchronize()
+        prep_ms = (time.perf_counter() - t1) * 1e3
+        gg = torch.Generator(device=dev)
+        gg.manual_seed(107)
+        s_src = torch.randn((N, H), generator=gg, device=dev) * 2
+        s_dst = torch.randn((N, H), generator=gg, device=dev) * 2
+        gout = torch.randn((N, F), generator=gg, device=dev)
+        zc = x if x.stride(0) == F else x.contiguous()
+        gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
+        passes, red = 2, "gat"
+
+        def compute():
+            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"])
+            gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT)
+
+    appnp = None
+    if a.op == "appnp":
+        # NEXT-2: APPNP propagation z_{k+1} = (1 - alpha) S z_k + alpha h, S = D^-1/2 (A+I) D^-1/2,
+        # K steps on one plan, the teleport term fused into the segment-reduce epilogue.  h = the config's X.
+        assert world == 1 and a.strategy == "segment", "--op appnp: one GPU, segment strategy"
+        t1 = time.perf_counter()
+        if a.config != "pubmed":
+            ei, wgt = pg.pyg_gcn_norm(ei, N)
+            E = ei.shape[1]
+            cb = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4) if a.col_block == "auto" else int(a.col_block)
+            plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb)
+            col_block = cb
+        torch.cuda.synchronize()
+        prep_ms = (time.perf_counter() - t1) * 1e3
+        zbuf = torch.empty((N, ld), dtype=torch.float32, device=dev)[:, :F]
+        obuf = torch.empty((N, ld), dtype=torch.float32, device=dev)[:, :F]
+        ws_a = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, "sum")), dtype=torch.uint8, device=dev)
+        appnp = dict(out=obuf)
+        passes, weighted, red = a.K, True, "sum"
+
+        def compute():
+            pg.pyg_appnp(x_full, plan, K=a.K, alpha=a.alpha, edge_weight=wgt, out=obuf, scratch=zbuf, workspace=ws_a)
+
     def exchange_step():
         if exchange == "halo":  # pack the requested rows + one NCCL all-to-all (dist.py)
             halo_exchange(shard, halo["send_rows"], halo["sc"], halo["rc"], xbuf[per:],
@@ -462,7 +569,12 @@ def main():
     value = units / (ms_step * 1e-3)
 
     peak, peak_src = measured_peak()
-    B = passes * alg_bytes(E_loc if world > 1 else E, n_loc, F, red, a.strategy, weighted=weighted)
+    if gat is not None:
+        B = gat_step_bytes(E, N, F, gat["H"])
+    elif appnp is not None:  # K weighted propagations + the teleport read of h per step
+        B = a.K * (alg_bytes(E, N, F, "sum", a.strategy, weighted=True) + (N * F * 4 if a.alpha else 0))
+    else:
+        B = passes * alg_bytes(E_loc if world > 1 else E, n_loc, F, red, a.strategy, weighted=weighted)
     achieved = B / (kern_ms * 1e-3) / 1e9
     lpc = max(1, int(round(launches / a.steps)))  # launches of the propagate call per step
     wk = f"{a.config}-{red}-{a.strategy}-cb{col_block}-n{world}"
@@ -492,7 +604,21 @@ def main():
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
         "gen_s": gen_s,
     }
-    if passes == 2:
+    if appnp is not None:
+        result["config"]["op"] = "appnp"
+        result["config"]["K"] = a.K
+        result["config"]["alpha"] = a.alpha
+        result["config"]["step"] = "APPNP K-step propagation with GCN weights (K segment-reduce passes, fused teleport)"
+        result["config"]["E_with_self_loops"] = E
+        result["gcn_norm_and_plans_ms"] = prep_ms
+    if gat is not None:
+        result["config"]["op"] = "gat"
+        result["config"]["heads"] = gat["H"]
+        result["config"]["step"] = ("GAT aggregation forward (segment softmax + alpha-weighted sum) + backward "
+                                    "(grad z, s_src, s_dst)")
+        result["plans_ms"] = prep_ms
+        result["roofline"]["note"] = "achieved = algorithmic bytes of the whole step (5 kernels, gat_step_bytes) / step time"
+    elif passes == 2:
         result["config"]["step"] = "GCN forward (w = D^-1/2 (A+I) D^-1/2) + backward w.r.t. X"
         result["config"]["E_with_self_loops"] = E
         result["gcn_norm_and_plans_ms"] = prep_ms
@@ -505,21 +631,39 @@ def main():
         ei_cpu = ei.cpu().numpy()
         x_cpu = np.ascontiguousarray(x.cpu().numpy())
         w_cpu = wgt.cpu().numpy() if weighted else None
-        rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
-        got = out[:R].cpu().numpy()
-        if red == "max":
+        if appnp is not None:
+            rate, dt, Es, R, ref = oracle_appnp_run(ei_cpu, x_cpu, w_cpu, a.K, a.alpha, a.cpu_seconds, F)
+            got = appnp["out"].cpu().numpy() if R else None
+        elif gat is not None:
+            rate, dt, Es, R, ref = oracle_gat_sample(ei_cpu, x_cpu, s_src.cpu().numpy(), s_dst.cpu().numpy(), gat["H"],
+                                                     N, a.cpu_seconds, F)
+            got = gat["out"][:R].cpu().numpy()
+        else:
+            rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
+            got = out[:R].cpu().numpy()
+        if appnp is not None:
+            ok = bool((np.abs(got - ref) <= 1e-5 * np.abs(ref) + 1e-6).all()) if R else None
+        elif gat is not None:
+            ok = bool((np.abs(got - ref[0]) <= 1e-5 * ref[2] + 1e-6).all())
+        elif red == "max":
             ok = np.array_equal(got, ref[0]) and np.array_equal(arg[:R].cpu().numpy(), ref[1])
         else:
             ok = bool((np.abs(got - ref) <= 1e-5 * np.abs(ref) + 1e-6).all())
+        if appnp is not None and R:
+            sample = f"the whole graph, K = {a.K} steps ({Es} edge visits), {dt:.1f} s single-threaded C, fp64 state"
+        elif appnp is not None:
+            sample = (f"one sum propagate pass over the {Es} in-edges of the first target rows ({Es / E:.2%} of E), "
+                      f"{dt:.1f} s single-threaded C (the full K-step recurrence would take hours)")
+        else:
+            sample = (f"{Es} edges of the first {R} target rows ({Es / E:.2%} of E), {dt:.1f} s single-threaded C, "
+                      f"fp64 accumulate")
         result["cpu_baseline"] = {"value": rate, "unit": "edges*F/s", "cores": 1, "kind": "oracle",
-                                  "sample": f"{Es} edges of the first {R} target rows ({Es / E:.2%} of E), "
-                                            f"{dt:.1f} s single-threaded C, fp64 accumulate",
-                                  "parity_on_sample": ok}
+                                  "sample": sample, "parity_on_sample": ok}
         if not ok:
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
-    if world == 1 and not a.no_e2e and passes == 1:
+    if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None:
         xs = x.as_strided((N, ld), (x.stride(0), 1)) if x.stride(0) == ld else x.contiguous()
         hx = torch.empty(xs.shape, dtype=torch.float32, pin_memory=True)
         hx.copy_(xs)
@@ -554,7 +698,7 @@ def main():
                          "includes": "H2D(X, edge_index) + plan build + propagate + D2H(out)"}
 
     # ---- other reductions on the same resident graph (informational) ----
-    if world == 1 and not a.no_variants and passes == 1:
+    if world == 1 and not a.no_variants and passes == 1 and gat is None and appnp is None:
         var = {}
         for r2 in ("sum", "mean", "max"):
             if r2 == red:

@@ -321,11 +321,13 @@ pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const f
  * projections a_src . z_j and a_dst . z_i per head, computed by the caller);
  * out [n_dst x H*C] stride ldo; alpha [E x H] packed, OUTPUT (by original edge
  * id; needed by the backward).  plan: unblocked forward plan (row = target,
- * col = source).  H <= 8, H*C <= 1024.  Asynchronous. */
+ * col = source).  H <= 8.  workspace: pyg_workspace_size(plan, n_dst, H*C,
+ * PYG_SUM, 0) (split hub rows).  Asynchronous. */
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                                const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
                                float negative_slope, const pyg_plan_t* plan, float* out,
-                               int64_t ldo, float* alpha, void* stream);
+                               int64_t ldo, float* alpha, void* workspace, size_t workspace_bytes,
+                               void* stream);
 /* Backward of pyg_gat_propagate, g = grad_out [n_dst x H*C] stride ldg:
  *   grad_z[j][h*C+c] = sum_{k: src_k = j} alpha[k][h] g[dst_k][h*C+c]     (grad_z optional)
  *   grad_logit[k][h] = alpha[k][h] (g_i . z_j|_h - sum_{k' in seg(i)} alpha[k'][h] g_i . z_j'|_h)
@@ -334,7 +336,8 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
  *   grad_s_dst[i][h] = sum over i's in-edges of grad_logit     ([n_dst x H] packed, required)
  *   grad_s_src[j][h] = sum over j's out-edges of grad_logit    ([n_src x H] packed, optional)
  * plan: the forward plan; plan_T: row_index = sources, col_index = targets.
- * workspace: pyg_workspace_size(plan_T, n_src, H, PYG_SUM, 0).  Asynchronous. */
+ * H*C <= 4096.  workspace: pyg_workspace_size(plan_T, n_src, H*C, PYG_SUM, 0).
+ * Asynchronous. */
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                               const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
                               float negative_slope, const float* alpha, const float* grad_out,
@@ -342,6 +345,23 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
                               float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst,
                               float* grad_logit, void* workspace, size_t workspace_bytes,
                               void* stream);
+
+/* ---- NEXT-2: K-step propagation (APPNP; SGC) on one plan ------------------- */
+/* APPNP's propagation: z_0 = h, z_{k+1} = (1 - alpha) S z_k + alpha h,
+ * out = z_K, with S the weighted adjacency of the plan (edge_weight [E] by edge id,
+ * e.g. GCN's D^-1/2 (A+I) D^-1/2 from pyg_gcn_norm; NULL = 1).  alpha = 0 gives
+ * SGC's S^K h.  The teleport term is fused into the segment-reduce
+ * epilogue (no extra pass over z).  The backward w.r.t. h is the same recurrence on
+ * the transposed plan with h := dL/dout (w_K = T^K g + alpha sum_{j<K} T^j g,
+ * T = (1 - alpha) S^T), i.e. pyg_appnp(g, ..., plan_T).
+ *   h [n x F] stride ldh; out [n x F] stride ldo (overwritten); scratch [n x F]
+ *   stride ldo, required for K > 1 (ping-pong buffer); K >= 0 (K = 0 copies h);
+ *   0 <= alpha <= 1.  plan: forward plan over n targets / n sources.  Per-call
+ *   fp32 rounding of every z_k.  workspace: pyg_workspace_size(plan, n, F, SUM).
+ *   Asynchronous. */
+pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const float* edge_weight,
+                       int64_t K, float alpha, const pyg_plan_t* plan, float* out, int64_t ldo,
+                       float* scratch, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -68,6 +68,7 @@ def lib():
             "orc_collate": [I, P, P, P, P, P, P],
             "orc_global_pool": [P, I, I, P, I, C, P, P],
             "orc_segment_softmax": [P, I, I, P, I, P],
+            "orc_appnp": [P, I, I, P, I, P, I, ctypes.c_double, P],
             "orc_segment_softmax_backward": [P, P, I, I, P, I, P, P],
             "orc_gat": [P, I, I, I, P, P, I, P, I, ctypes.c_double, P, P, P],
             "orc_gat_backward": [P, I, I, I, P, P, I, P, I, ctypes.c_double, P, P, P, P, P, P, P],
@@ -329,3 +330,14 @@ def gat_backward(z, s_src, s_dst, edge_index, H, grad_out, n_dst=None, slope=0.2
     if with_abs:
         res.update(abs_z=abz, abs_s_src=abs_, abs_s_dst=abd)
     return res
+
+
+def appnp(h, edge_index, K=10, alpha=0.1, edge_weight=None):
+    """APPNP / SGC propagation z_K."""
+    h = _f32(h)
+    n, F = h.shape
+    edge_index = _i64(edge_index).reshape(2, -1)
+    out = np.zeros((n, F), np.float32)
+    _chk(lib().orc_appnp(_p(h), n, F, _p(edge_index), edge_index.shape[1], _p(_f32(edge_weight)), K, float(alpha),
+                         _p(out)), "appnp")
+    return out

@@ -521,3 +521,34 @@ int orc_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, const 
     free(alpha); free(da); free(daa); free(t); free(ta); free(gz); free(gs); free(gd);
     return st;
 }
+
+/* ---- NEXT-2: APPNP / SGC K-step propagation ---------------------------------- */
+/* APPNP ("Approximate Personalized Propagation of Neural Predictions";
+ * S:439-447): z_0 = h; z_{k+1} = (1 - alpha) * S z_k + alpha * h; out = z_K, with
+ * (S z)[i] = sum_{k : dst_k = i} w_k z[src_k] (w = 1 when edge_weight is NULL).
+ * The state is kept in double through all K steps and rounded once. alpha = 0 is
+ * SGC's S^K h. */
+int orc_appnp(const float* h, int64_t n, int64_t F, const int64_t* ei, int64_t E, const float* edge_weight,
+              int64_t K, double alpha, float* out) {
+    if (n < 0 || F < 0 || E < 0 || K < 0 || (n * F > 0 && (!h || !out)) || (E > 0 && !ei)) return ORC_ERR_INVALID;
+    if (alpha < 0.0 || alpha > 1.0) return ORC_ERR_INVALID;
+    if (check_index(ei, E, n) || check_index(ei + E, E, n)) return ORC_ERR_OOB;
+    size_t nf = (size_t)(n * F > 0 ? n * F : 1);
+    double* z = (double*)malloc(sizeof(double) * nf);
+    double* t = (double*)malloc(sizeof(double) * nf);
+    if (!z || !t) { free(z); free(t); return ORC_ERR_INVALID; }
+    for (int64_t q = 0; q < n * F; ++q) z[q] = (double)h[q];
+    for (int64_t it = 0; it < K; ++it) {
+        for (int64_t q = 0; q < n * F; ++q) t[q] = 0.0;
+        for (int64_t k = 0; k < E; ++k) {
+            const int64_t j = ei[k], i = ei[E + k];
+            const double w = edge_weight ? (double)edge_weight[k] : 1.0;
+            for (int64_t c = 0; c < F; ++c) t[i * F + c] += w * z[j * F + c];
+        }
+        for (int64_t q = 0; q < n * F; ++q) z[q] = (1.0 - alpha) * t[q] + alpha * (double)h[q];
+    }
+    for (int64_t q = 0; q < n * F; ++q) out[q] = (float)z[q];
+    free(z);
+    free(t);
+    return ORC_OK;
+}

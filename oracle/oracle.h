@@ -118,6 +118,11 @@ int orc_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, const 
                      const float* g, float* grad_z, float* grad_s_src, float* grad_s_dst,
                      double* abs_z, double* abs_ssrc, double* abs_sdst);
 
+/* NEXT-2: APPNP / SGC K-step propagation:
+ * z_{k+1} = (1 - alpha) S z_k + alpha h, z_0 = h; out = z_K (double state). */
+int orc_appnp(const float* h, int64_t n, int64_t F, const int64_t* ei, int64_t E,
+              const float* edge_weight, int64_t K, double alpha, float* out);
+
 #ifdef __cplusplus
 }
 #endif

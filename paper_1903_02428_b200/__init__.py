@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
 
@@ -374,7 +374,7 @@ def pyg_segment_softmax_backward(out: torch.Tensor, grad_out: torch.Tensor, plan
 
 def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, plan: Plan,
                       negative_slope: float = 0.2, out: Optional[torch.Tensor] = None,
-                      alpha: Optional[torch.Tensor] = None):
+                      alpha: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
     """GAT attention aggregation: (out [n_dst x H*C], alpha [E x H])."""
     n_src, F, ldz = _rows(z, "z")
     C = F // H
@@ -388,8 +388,11 @@ def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor,
     if alpha is None:
         alpha = torch.empty((E, H), dtype=torch.float32, device=z.device)
     _, _, ldo = _rows(out, "out")
+    if workspace is None:
+        workspace = _workspace(pyg_workspace_size(plan, n_dst, F, SUM), z.device)
     check(lib.pyg_gat_propagate(_ptr(z), n_src, H, C, ldz, _ptr(s_src), _ptr(s_dst), n_dst, E, negative_slope,
-                                plan.handle, _ptr(out), ldo, _ptr(alpha), _stream(z.device)), "pyg_gat_propagate")
+                                plan.handle, _ptr(out), ldo, _ptr(alpha), _ptr(workspace), workspace.numel(),
+                                _stream(z.device)), "pyg_gat_propagate")
     return out, alpha
 
 
@@ -406,9 +409,27 @@ def pyg_gat_backward(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, 
     gss = torch.empty((n_src, H), dtype=torch.float32, device=dev)
     gsd = torch.empty((n_dst, H), dtype=torch.float32, device=dev)
     gl = torch.empty((max(E, 1), H), dtype=torch.float32, device=dev)[:E]
-    ws = _workspace(pyg_workspace_size(plan_T, n_src, H, SUM), dev)
+    ws = _workspace(pyg_workspace_size(plan_T, n_src, F, SUM), dev)
     check(lib.pyg_gat_backward(_ptr(z), n_src, H, C, ldz, _ptr(s_src.contiguous()), _ptr(s_dst.contiguous()), n_dst,
                                E, negative_slope, _ptr(alpha), _ptr(grad_out), ldg, plan.handle, plan_T.handle,
                                _ptr(gz), F, _ptr(gss), _ptr(gsd), _ptr(gl), _ptr(ws), ws.numel(), _stream(dev)),
           "pyg_gat_backward")
     return {"z": gz, "s_src": gss, "s_dst": gsd, "logit": gl}
+
+
+def pyg_appnp(h: torch.Tensor, plan: Plan, K: int = 10, alpha: float = 0.1, edge_weight: Optional[torch.Tensor] = None,
+              out: Optional[torch.Tensor] = None, scratch: Optional[torch.Tensor] = None,
+              workspace: Optional[torch.Tensor] = None):
+    """APPNP / SGC K-step propagation z_{k+1} = (1 - alpha) S z_k + alpha h."""
+    n, F, ldh = _rows(h, "h")
+    dev = h.device
+    if out is None:
+        out = torch.empty((n, F), dtype=torch.float32, device=dev)
+    _, _, ldo = _rows(out, "out")
+    if scratch is None and K > 1:
+        scratch = torch.empty((n, ldo), dtype=torch.float32, device=dev)[:, :F]
+    if workspace is None:
+        workspace = _workspace(pyg_workspace_size(plan, n, F, SUM), dev)
+    check(lib.pyg_appnp(_ptr(h), n, F, ldh, _ptr(edge_weight), K, alpha, plan.handle, _ptr(out), ldo, _ptr(scratch),
+                        _ptr(workspace), workspace.numel(), _stream(dev)), "pyg_appnp")
+    return out

@@ -519,18 +519,22 @@ pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx, 
 
 // ---- NEXT-1: segment softmax + GAT attention aggregation (attention.cu) ----------
 
+static bool scatter_plan_ok(const pyg_plan* p, int64_t n, int64_t E) {
+    return p && p->n_rows == n && p->col == nullptr && p->parts.empty() && p->E == E;
+}
+
 pyg_status_t pyg_segment_softmax(const float* src, int64_t E, int64_t H, int64_t lds, const int64_t* index,
                                  int64_t dim_size, const pyg_plan_t* plan, float* out, int64_t ldo, void* stream) {
     (void)index;
     REQUIRE(E >= 0 && H >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "segment_softmax: negative size");
     REQUIRE(lds >= H && ldo >= H, PYG_ERR_DIMENSION, "segment_softmax: leading dimension < H");
-    REQUIRE(plan, PYG_ERR_INVALID_ARGUMENT, "segment_softmax: needs a scatter plan over index");
-    REQUIRE(plan->n_rows == dim_size && plan->col == nullptr && plan->parts.empty() && plan->E == E,
-            PYG_ERR_DIMENSION, "segment_softmax: plan is not an unblocked scatter plan over dim_size rows and E edges");
+    REQUIRE(H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "segment_softmax: at most %d columns", kAttnMaxHeads);
+    REQUIRE(scatter_plan_ok(plan, dim_size, E), PYG_ERR_DIMENSION,
+            "segment_softmax: needs an unblocked scatter plan over dim_size rows and E edges");
     REQUIRE(E * H == 0 || (src && out), PYG_ERR_INVALID_ARGUMENT, "segment_softmax: null pointer");
     if (E == 0 || H == 0) return PYG_OK;
-    return attention_softmax(plan->rowptr, plan->n_rows, nullptr, plan->perm_identity ? nullptr : plan->perm, src, lds,
-                             nullptr, nullptr, (int)H, 0.0f, out, ldo, as_stream(stream));
+    return attention_softmax(plan, nullptr, plan->perm_identity ? nullptr : plan->perm, src, lds, nullptr, nullptr,
+                             (int)H, 0.0f, out, ldo, as_stream(stream));
 }
 
 pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const float* grad_out, int64_t ldg, int64_t E,
@@ -539,36 +543,50 @@ pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const f
     REQUIRE(E >= 0 && H >= 0 && dim_size >= 0, PYG_ERR_INVALID_ARGUMENT, "segment_softmax_backward: negative size");
     REQUIRE(ldo >= H && ldg >= H && lds >= H, PYG_ERR_DIMENSION, "segment_softmax_backward: leading dimension < H");
     REQUIRE(H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "segment_softmax_backward: at most %d columns", kAttnMaxHeads);
-    REQUIRE(plan && plan->n_rows == dim_size && plan->col == nullptr && plan->parts.empty() && plan->E == E,
-            PYG_ERR_DIMENSION, "segment_softmax_backward: needs the scatter plan of the forward");
+    REQUIRE(scatter_plan_ok(plan, dim_size, E), PYG_ERR_DIMENSION,
+            "segment_softmax_backward: needs the scatter plan of the forward");
     REQUIRE(E * H == 0 || (out && grad_out && grad_src), PYG_ERR_INVALID_ARGUMENT,
             "segment_softmax_backward: null pointer");
     if (E == 0 || H == 0) return PYG_OK;
-    return attention_softmax_bwd(plan->rowptr, plan->n_rows, nullptr, plan->perm_identity ? nullptr : plan->perm,
-                                 (int)H, 1, (int)H, out, ldo, grad_out, ldg, nullptr, 0, nullptr, nullptr, 0.0f,
-                                 grad_src, lds, nullptr, as_stream(stream));
+    return attention_softmax_bwd(plan, nullptr, plan->perm_identity ? nullptr : plan->perm, (int)H, 1, (int)H, out, ldo,
+                                 grad_out, ldg, nullptr, 0, nullptr, nullptr, 0.0f, grad_src, lds, nullptr,
+                                 as_stream(stream));
+}
+
+// alpha-weighted sum over a plan (forward: X = z over the forward plan; grad_z: X = grad_out
+// over the transposed plan): the segment-reduce in mode kRedHeadW
+static pyg_status_t headw_sum(const pyg_plan* p, const float* X, int64_t ldx, int64_t F, int64_t C, int64_t H,
+                              const float* alpha, float* out, int64_t ldo, int64_t n_rows, void* ws, size_t ws_bytes,
+                              cudaStream_t s) {
+    SegArgs a;
+    a.X = X; a.ldx = ldx; a.ncols = (int)F;
+    a.rowptr = p->rowptr; a.gidx = p->col; a.eid = p->perm_identity ? nullptr : p->perm;
+    a.out = out; a.ldo = ldo; a.n_rows = n_rows; a.E_sentinel = p->E;
+    a.heavy_threshold = p->heavy_threshold;
+    a.hw = alpha; a.hH = (int)H; a.hC = (int)C;
+    return segment_reduce(a, kRedHeadW, p, ws, ws_bytes, s);
 }
 
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
                                const float* s_dst, int64_t n_dst, int64_t E, float negative_slope,
-                               const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, void* stream) {
+                               const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, void* ws,
+                               size_t ws_bytes, void* stream) {
     REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
             "gat_propagate: bad sizes");
     const int64_t F = H * C;
     REQUIRE(ldz >= F && ldo >= F, PYG_ERR_DIMENSION, "gat_propagate: leading dimension < H*C");
-    REQUIRE(F <= 1024 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_propagate: H*C <= 1024 and H <= %d",
-            kAttnMaxHeads);
+    REQUIRE(F <= 16384 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_propagate: H <= %d", kAttnMaxHeads);
     REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() &&
                 plan->n_cols <= n_src && plan->E == E,
             PYG_ERR_DIMENSION, "gat_propagate: needs an unblocked forward plan over n_dst rows and E edges");
     REQUIRE(n_dst * F == 0 || out, PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null out");
     REQUIRE(E == 0 || (z && s_src && s_dst && alpha), PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null input");
     cudaStream_t s = as_stream(stream);
-    const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
     if (E > 0)
-        PYG_TRY(attention_softmax(plan->rowptr, n_dst, plan->col, eid, nullptr, 0, s_src, s_dst, (int)H,
-                                  negative_slope, alpha, H, s));
-    return attention_headw(plan->rowptr, n_dst, plan->col, eid, z, ldz, (int)F, (int)C, (int)H, alpha, out, ldo, s);
+        PYG_TRY(attention_softmax(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, nullptr, 0, s_src, s_dst,
+                                  (int)H, negative_slope, alpha, H, s));
+    if (n_dst == 0 || F == 0) return PYG_OK;
+    return headw_sum(plan, z, ldz, F, C, H, alpha, out, ldo, n_dst, ws, ws_bytes, s);
 }
 
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
@@ -580,7 +598,7 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
             "gat_backward: bad sizes");
     const int64_t F = H * C;
     REQUIRE(ldz >= F && ldg >= F && (!grad_z || ldgz >= F), PYG_ERR_DIMENSION, "gat_backward: leading dimension < H*C");
-    REQUIRE(F <= 1024 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_backward: H*C <= 1024 and H <= %d",
+    REQUIRE(F <= 4096 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_backward: H*C <= 4096 and H <= %d",
             kAttnMaxHeads);
     REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() && plan->E == E,
             PYG_ERR_DIMENSION, "gat_backward: `plan` must be the forward plan");
@@ -591,14 +609,13 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
             "gat_backward: null input (grad_logit [E x H] is required)");
     REQUIRE(n_dst * H == 0 || grad_s_dst, PYG_ERR_INVALID_ARGUMENT, "gat_backward: null grad_s_dst");
     cudaStream_t s = as_stream(stream);
-    if (n_dst > 0 && E == 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));
+    if (n_dst > 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));  // rows without in-edges
     if (E > 0)
-        PYG_TRY(attention_softmax_bwd(plan->rowptr, n_dst, plan->col, plan->perm_identity ? nullptr : plan->perm,
-                                      (int)H, (int)C, (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst,
-                                      negative_slope, grad_logit, H, grad_s_dst, s));
-    const int32_t* eidT = plan_T->perm_identity ? nullptr : plan_T->perm;
-    if (grad_z) PYG_TRY(attention_headw(plan_T->rowptr, n_src, plan_T->col, eidT, grad_out, ldg, (int)F, (int)C,
-                                        (int)H, alpha, grad_z, ldgz, s));
+        PYG_TRY(attention_softmax_bwd(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, (int)H, (int)C,
+                                      (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst, negative_slope, grad_logit,
+                                      H, grad_s_dst, s));
+    if (grad_z && n_src > 0 && F > 0)
+        PYG_TRY(headw_sum(plan_T, grad_out, ldg, F, C, H, alpha, grad_z, ldgz, n_src, ws, ws_bytes, s));
     if (grad_s_src && n_src > 0) {
         SegArgs a;
         a.X = grad_logit; a.ldx = H; a.ncols = (int)H;
@@ -607,6 +624,46 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
         a.heavy_threshold = plan_T->heavy_threshold;
         a.flags = PYG_NO_TMA;
         PYG_TRY(segment_reduce(a, PYG_SUM, plan_T, ws, ws_bytes, s));
+    }
+    return PYG_OK;
+}
+
+// ---- NEXT-2: K-step propagation (APPNP / SGC) reusing one plan -------------------
+
+pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const float* edge_weight, int64_t K,
+                       float alpha, const pyg_plan_t* plan, float* out, int64_t ldo, float* scratch, void* ws,
+                       size_t ws_bytes, void* stream) {
+    REQUIRE(n >= 0 && F >= 0 && K >= 0, PYG_ERR_INVALID_ARGUMENT, "appnp: negative size");
+    REQUIRE(alpha >= 0.0f && alpha <= 1.0f, PYG_ERR_INVALID_ARGUMENT, "appnp: alpha outside [0, 1]");
+    REQUIRE(ldh >= F && ldo >= F, PYG_ERR_DIMENSION, "appnp: leading dimension < F");
+    REQUIRE(n <= kMaxI32 && F <= kMaxI32, PYG_ERR_UNSUPPORTED, "appnp: sizes must be < 2^31");
+    REQUIRE(n * F == 0 || (h && out), PYG_ERR_INVALID_ARGUMENT, "appnp: null pointer");
+    REQUIRE(K <= 1 || scratch, PYG_ERR_INVALID_ARGUMENT, "appnp: K > 1 needs scratch [n x F] (stride ldo)");
+    REQUIRE(plan && plan->n_rows == n && plan->n_cols <= n && (plan->col || plan->E == 0), PYG_ERR_DIMENSION,
+            "appnp: needs a forward plan over n targets and n sources");
+    cudaStream_t s = as_stream(stream);
+    if (n == 0 || F == 0) return PYG_OK;
+    if (K == 0) {
+        PYG_CUDA(cudaMemcpy2DAsync(out, (size_t)ldo * 4, h, (size_t)ldh * 4, (size_t)F * 4, (size_t)n,
+                                   cudaMemcpyDeviceToDevice, s));
+        return PYG_OK;
+    }
+    const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
+    const float* z = h;
+    int64_t ldz = ldh;
+    for (int64_t k = 0; k < K; ++k) {
+        // the last iteration writes `out`; earlier ones alternate so that they never read what they write
+        float* dst = ((K - 1 - k) % 2 == 0) ? out : scratch;
+        SegArgs a;
+        a.X = z; a.ldx = ldz; a.ncols = (int)F;
+        a.rowptr = plan->rowptr; a.gidx = plan->col; a.eid = eid; a.w = edge_weight;
+        a.out = dst; a.ldo = ldo; a.n_rows = n; a.E_sentinel = plan->E;
+        a.heavy_threshold = plan->heavy_threshold; a.allow_pad_read = 1;
+        a.blend = alpha != 0.0f ? h : nullptr; a.ldb = ldh;
+        a.blend_a = 1.0f - alpha; a.blend_b = alpha;
+        PYG_TRY(segment_reduce(a, PYG_SUM, plan, ws, ws_bytes, s));
+        z = dst;
+        ldz = ldo;
     }
     return PYG_OK;
 }

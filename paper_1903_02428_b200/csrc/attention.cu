@@ -2,22 +2,25 @@
 // aggregation, "our own optimized sparse softmax kernels" of P:239 (GAT; S:161-169,
 // S:421-429), on the same CSR plans as the segment-reduce.
 //
-//   softmax_fwd_kernel   one warp per target row: per head, max, sum of exp, alpha = exp / sum
-//                        (three passes over the row's logits; logits are GAT's
-//                        leaky_relu(s_src[j] + s_dst[i]) or caller-given values); alpha is written
-//                        per ORIGINAL edge id ([E x H]) because the backward needs it.
-//   headw_kernel         one warp per row: out[r] = sum_p alpha[eid_p][head(c)] * X[gidx_p][c],
-//                        the alpha window of 32 positions staged in shared memory; fp32 partial
-//                        sums per 32-position window added into the row accumulator (chains of
-//                        <= max(32, deg/32) terms, reading Q12).  Forward (X = z over the forward
-//                        plan) and grad_z (X = grad_out over the transposed plan) alike.
-//   softmax_bwd_kernel   one warp per target row: d_alpha per edge (GAT: the SDDMM
-//                        grad_out[i] . z[j] per head, lane per edge, grad_out[i] staged in shared
-//                        memory), t = sum alpha d_alpha, dL/dlogit = alpha (d_alpha - t), times
-//                        leaky_relu' for GAT; grad_s_dst = row sum.  grad_s_src is a segment sum of
-//                        dL/dlogit over the transposed plan (segment_reduce, gathered by edge id).
-// All deterministic (fixed per-row order, fixed warp-reduction trees).  HBM/L2-bound like the
-// segment-reduce: the z-row gather dominates (4*H*C bytes per edge).
+// Every per-row kernel comes in two shapes over the plan's rows: a WARP per light row (rows of
+// <= heavy_threshold positions, visited in the plan's degree-bucket order, longest first) and a
+// 256-thread CTA per split hub row (power-law graphs: a 300k-position row would otherwise serialise
+// one warp), with the same per-thread position assignment in both passes.
+//
+//   softmax_fwd_kernel   pass 1: online (max, sum of exp) per head over the row's logits (all H
+//                        heads per position from one vector load of s_src[j]); a fixed-tree group
+//                        reduction of the (max, sum) pairs; pass 2: alpha = exp(l - max) / sum,
+//                        written per ORIGINAL edge id ([E x H], the backward needs it).  Logits are
+//                        GAT's leaky_relu(s_src[j] + s_dst[i]) or caller-given values.
+//   alpha-weighted sum   the segment-reduce kernels in mode kRedHeadW (weights alpha[eid][c / C]):
+//                        forward (z over the forward plan) and grad_z (grad_out over the transposed
+//                        plan) inherit the hub split, the fp64 combine and the tuned geometry.
+//   softmax_bwd_kernel   pass A: d_alpha per edge (GAT: the SDDMM grad_out[i] . z[j] per head,
+//                        thread per edge, grad_out[i] staged in shared memory) and
+//                        t = sum alpha d_alpha; pass B: dL/dlogit = alpha (d_alpha - t) (times
+//                        leaky_relu'(pre) for GAT), grad_s_dst = row sum.  grad_s_src is a segment
+//                        sum of dL/dlogit over the transposed plan (gathered by edge id).
+// All deterministic (fixed per-row order and reduction trees).
 #include "kernels.cuh"
 
 namespace pyg {
@@ -31,21 +34,131 @@ __device__ __forceinline__ float warp_sum(float v) {
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
 }
-__device__ __forceinline__ float warp_max(float v) {
+
+// (max, sum-of-exp) pair merge; an empty side is (-inf, 0)
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+    const float M = fmaxf(m, m2);
+    if (M == -INFINITY) return;
+    s = s * expf(m - M) + s2 * expf(m2 - M);
+    m = M;
+}
+
+// Group of G threads (32: one warp; 256: one CTA) reducing per-head values in a fixed tree.
+template <int G>
+struct Group {
+    float* red;  // G == 256: shared scratch of 8 warps x kMaxHeads x 2 floats
+    __device__ __forceinline__ void sum(float (&v)[kMaxHeads], int H) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
+        for (int h = 0; h < kMaxHeads; ++h)
+            if (h < H) v[h] = warp_sum(v[h]);
+        if constexpr (G > 32) {
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            __syncthreads();
+            if (lane == 0)
+                for (int h = 0; h < H; ++h) red[w * kMaxHeads + h] = v[h];
+            __syncthreads();
+            for (int h = 0; h < H; ++h) {
+                float t = 0.0f;
+                for (int q = 0; q < G / 32; ++q) t += red[q * kMaxHeads + h];
+                v[h] = t;
+            }
+        }
+    }
+    __device__ __forceinline__ void max_sum(float (&m)[kMaxHeads], float (&s)[kMaxHeads], int H) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) {
+                if (h >= H) continue;
+                const float m2 = __shfl_xor_sync(0xffffffffu, m[h], o);
+                const float s2 = __shfl_xor_sync(0xffffffffu, s[h], o);
+                ms_merge(m[h], s[h], m2, s2);
+            }
+        if constexpr (G > 32) {
+            const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+            __syncthreads();
+            if (lane == 0)
+                for (int h = 0; h < H; ++h) {
+                    red[(w * kMaxHeads + h) * 2] = m[h];
+                    red[(w * kMaxHeads + h) * 2 + 1] = s[h];
+                }
+            __syncthreads();
+            for (int h = 0; h < H; ++h) {
+                float mm = -INFINITY, ss = 0.0f;
+                for (int q = 0; q < G / 32; ++q) ms_merge(mm, ss, red[(q * kMaxHeads + h) * 2], red[(q * kMaxHeads + h) * 2 + 1]);
+                m[h] = mm;
+                s[h] = ss;
+            }
+        }
+    }
+};
+
+// the H (<= 8) per-head values of row `row` of a packed [n x H] array (vector loads when H is 2, 4, 8)
+__device__ __forceinline__ void load_heads(float (&v)[kMaxHeads], const float* base, int64_t row, int H) {
+    const float* p = base + row * H;
+    if (H == 8) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else if (H == 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    } else {
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) v[h] = h < H ? __ldg(p + h) : 0.0f;
+    }
+}
+__device__ __forceinline__ void store_heads(float* base, int64_t row, int H, const float (&v)[kMaxHeads]) {
+    float* p = base + row * H;
+    if (H == 8) {
+        reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else if (H == 4) {
+        reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h)
+            if (h < H) p[h] = v[h];
+    }
+}
+
+struct RowSet {
+    const int64_t* rowptr;      // this plan's rows (offset for slices)
+    int64_t n_rows;
+    const int32_t* order;       // light rows: root ids in degree-bucket order (or null: 0..n_rows)
+    int64_t order_len, order_offset;
+    int64_t thr;                // rows longer than this are hub rows
+    const int32_t* heavy_rows;  // hub rows: root ids
+    int64_t h_lo, h_hi, row_offset;
+};
+
+// the row a group works on in unit u (light: warp-granular; heavy: CTA-granular); -1: skip
+template <int G>
+__device__ __forceinline__ int64_t row_of(const RowSet& rs, int64_t u) {
+    if constexpr (G == 32) {
+        int64_t r;
+        if (rs.order) {
+            if (u >= rs.order_len) return -2;
+            r = (int64_t)rs.order[u] - rs.order_offset;
+            if (r < 0 || r >= rs.n_rows) return -1;
+        } else {
+            if (u >= rs.n_rows) return -2;
+            r = u;
+        }
+        const int64_t d = rs.rowptr[r + 1] - rs.rowptr[r];
+        return (d == 0 || d > rs.thr) ? -1 : r;
+    } else {
+        if (u >= rs.h_hi - rs.h_lo) return -2;
+        return (int64_t)rs.heavy_rows[rs.h_lo + u] - rs.row_offset;
+    }
 }
 
 struct SoftmaxArgs {
-    const int64_t* rowptr;
-    int64_t n_rows;
     const int32_t* col;   // GAT: source of each position
     const int32_t* eid;   // edge id per position (null -> position)
     const float* src;     // values mode: [E x H] stride lds
     int64_t lds;
-    const float* s_src;   // GAT: [n_src x H]
-    const float* s_dst;   // GAT: [n_rows x H]
+    const float* s_src;   // GAT: [n_src x H] packed
+    const float* s_dst;   // GAT: [n_rows x H] packed
     int H;
     float slope;
     float* alpha;         // [E x H] stride lda
@@ -53,121 +166,64 @@ struct SoftmaxArgs {
 };
 
 template <bool GAT>
-__device__ __forceinline__ float logit(const SoftmaxArgs& a, int64_t r, int64_t p, int h) {
+__device__ __forceinline__ void logits(const SoftmaxArgs& a, int64_t p, int64_t k, const float (&sd)[kMaxHeads],
+                                       float (&l)[kMaxHeads]) {
     if constexpr (GAT) {
-        const float pre = __ldg(a.s_src + (int64_t)a.col[p] * a.H + h) + __ldg(a.s_dst + r * a.H + h);
-        return pre > 0.0f ? pre : a.slope * pre;
+        load_heads(l, a.s_src, a.col[p], a.H);
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) {
+            const float pre = l[h] + sd[h];
+            l[h] = pre > 0.0f ? pre : a.slope * pre;
+        }
     } else {
-        const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-        return __ldg(a.src + k * a.lds + h);
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) l[h] = h < a.H ? __ldg(a.src + k * a.lds + h) : 0.0f;
     }
 }
 
-template <bool GAT>
-__global__ void __launch_bounds__(256) softmax_fwd_kernel(SoftmaxArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n_rows; r += nw) {
-        const int64_t b = a.rowptr[r], e = a.rowptr[r + 1];
-        if (b == e) continue;
-        for (int h = 0; h < a.H; ++h) {
-            float m = -INFINITY;
-            for (int64_t p = b + lane; p < e; p += 32) m = fmaxf(m, logit<GAT>(a, r, p, h));
-            m = warp_max(m);
-            float s = 0.0f;
-            for (int64_t p = b + lane; p < e; p += 32) s += expf(logit<GAT>(a, r, p, h) - m);
-            s = warp_sum(s);
-            for (int64_t p = b + lane; p < e; p += 32) {
-                const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-                a.alpha[k * a.lda + h] = expf(logit<GAT>(a, r, p, h) - m) / s;
+template <int G, bool GAT>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(SoftmaxArgs a, RowSet rs) {
+    __shared__ float red[8 * kMaxHeads * 2];
+    Group<G> grp{red};
+    const int t = G == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    const int64_t units = G == 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
+    int64_t u = G == 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
+    for (;; u += units) {
+        const int64_t r = row_of<G>(rs, u);
+        if (r == -2) break;
+        if (r < 0) continue;
+        const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
+        float sd[kMaxHeads];
+        if (GAT) load_heads(sd, a.s_dst, r, a.H);
+        float m[kMaxHeads], s[kMaxHeads], l[kMaxHeads];
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) { m[h] = -INFINITY; s[h] = 0.0f; }
+        for (int64_t p = b + t; p < e; p += G) {
+            const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
+            logits<GAT>(a, p, k, sd, l);
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) {
+                if (h >= a.H) continue;
+                if (l[h] > m[h]) { s[h] = s[h] * expf(m[h] - l[h]) + 1.0f; m[h] = l[h]; }
+                else s[h] += expf(l[h] - m[h]);
             }
         }
-    }
-}
-
-struct HeadwArgs {
-    const int64_t* rowptr;
-    int64_t n_rows;
-    const int32_t* gidx;  // gathered row per position
-    const int32_t* eid;   // edge id per position (null -> position)
-    const float* X;
-    int64_t ldx;
-    int F, C, H;
-    const float* alpha;   // [E x H] packed
-    float* out;
-    int64_t ldo;
-};
-
-// V floats per lane access (4: float4 when F % 4 == 0 and rows are 16-byte aligned; else 1);
-// lane l owns columns [V*(l + 32*ch), +V) for ch < NCH.
-template <int V, int NCH>
-__global__ void __launch_bounds__(256) headw_kernel(HeadwArgs a) {
-    __shared__ float s_alpha[8][32 * kMaxHeads];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float* sa = s_alpha[wib];
-    int hd[NCH][V];
+        grp.max_sum(m, s, a.H);
+        for (int64_t p = b + t; p < e; p += G) {
+            const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
+            logits<GAT>(a, p, k, sd, l);
 #pragma unroll
-    for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-        for (int q = 0; q < V; ++q) {
-            const int c = V * (lane + 32 * ch) + q;
-            hd[ch][q] = c < a.F ? c / a.C : 0;
-        }
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n_rows; r += nw) {
-        const int64_t b = a.rowptr[r], e = a.rowptr[r + 1];
-        float acc[NCH][V];
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-            for (int q = 0; q < V; ++q) acc[ch][q] = 0.0f;
-        for (int64_t w = b; w < e; w += 32) {
-            const int64_t p = w + lane;
-            int g = 0;
-            if (p < e) {
-                g = a.gidx[p];
-                const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-                for (int h = 0; h < a.H; ++h) sa[lane * kMaxHeads + h] = __ldg(a.alpha + k * a.H + h);
+            for (int h = 0; h < kMaxHeads; ++h) l[h] = h < a.H ? expf(l[h] - m[h]) / s[h] : 0.0f;
+            if (a.lda == a.H) {
+                store_heads(a.alpha, k, a.H, l);
+            } else {
+                for (int h = 0; h < a.H; ++h) a.alpha[k * a.lda + h] = l[h];
             }
-            __syncwarp();
-            const int n = (int)min((int64_t)32, e - w);
-            float wacc[NCH][V];
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-                for (int q = 0; q < V; ++q) wacc[ch][q] = 0.0f;
-            for (int t = 0; t < n; ++t) {
-                const int j = __shfl_sync(0xffffffffu, g, t);
-                const float* xr = a.X + (int64_t)j * a.ldx;
-                const float* at = sa + t * kMaxHeads;
-#pragma unroll
-                for (int ch = 0; ch < NCH; ++ch) {
-                    const int c = V * (lane + 32 * ch);
-                    if (c >= a.F) continue;
-                    float v[V];
-                    ldv<V>(v, xr + c);
-#pragma unroll
-                    for (int q = 0; q < V; ++q) wacc[ch][q] = fmaf(at[hd[ch][q]], v[q], wacc[ch][q]);
-                }
-            }
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch)
-#pragma unroll
-                for (int q = 0; q < V; ++q) acc[ch][q] += wacc[ch][q];
-            __syncwarp();
-        }
-        float* o = a.out + r * a.ldo;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-            const int c = V * (lane + 32 * ch);
-            if (c < a.F) stv<V>(o + c, acc[ch], min(V, a.F - c));
         }
     }
 }
 
 struct SoftmaxBwdArgs {
-    const int64_t* rowptr;
-    int64_t n_rows;
     const int32_t* col;     // GAT: source per position
     const int32_t* eid;     // edge id per position (null -> position)
     int H, C, F;
@@ -186,26 +242,33 @@ struct SoftmaxBwdArgs {
     float* grad_s_dst;      // GAT: [n_rows x H]
 };
 
-template <bool GAT>
-__global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a) {
-    extern __shared__ float s_g[];  // GAT: grad_out row of the warp's target, F floats per warp
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    float* sg = s_g + (GAT ? (int64_t)wib * a.F : 0);
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < a.n_rows; r += nw) {
-        const int64_t b = a.rowptr[r], e = a.rowptr[r + 1];
+template <int G, bool GAT>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowSet rs) {
+    __shared__ float red[8 * kMaxHeads * 2];
+    extern __shared__ float s_g[];  // GAT: grad_out row of the group's target, F floats per group
+    Group<G> grp{red};
+    const int t = G == 32 ? (threadIdx.x & 31) : threadIdx.x;
+    float* sg = s_g + (G == 32 ? (int64_t)(threadIdx.x >> 5) * a.F : 0);
+    const int64_t units = G == 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
+    int64_t u = G == 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
+    for (;; u += units) {
+        const int64_t r = row_of<G>(rs, u);
+        if (r == -2) break;
+        if (r < 0) continue;
+        const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
+        float sd[kMaxHeads];
         if (GAT) {
-            __syncwarp();
-            for (int c = lane; c < a.F; c += 32) sg[c] = a.grad[r * a.ldg + c];
-            __syncwarp();
+            load_heads(sd, a.s_dst, r, a.H);
+            if (G == 32) __syncwarp(); else __syncthreads();
+            for (int c = t; c < a.F; c += G) sg[c] = a.grad[r * a.ldg + c];
+            if (G == 32) __syncwarp(); else __syncthreads();
         }
-        float tp[kMaxHeads];
+        float tp[kMaxHeads], al[kMaxHeads], da[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) tp[h] = 0.0f;
         // pass A: d_alpha per edge and head, t = sum alpha * d_alpha
-        for (int64_t p = b + lane; p < e; p += 32) {
+        for (int64_t p = b + t; p < e; p += G) {
             const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-            float da[kMaxHeads];
             if constexpr (GAT) {
 #pragma unroll
                 for (int h = 0; h < kMaxHeads; ++h) da[h] = 0.0f;
@@ -214,8 +277,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a) {
                     for (int c = 0; c < a.F; c += 4) {
                         const float4 zv = __ldg(reinterpret_cast<const float4*>(zr + c));
                         const int hh = c / a.C;
-                        float d = 0.0f;
-                        d = fmaf(sg[c], zv.x, d);
+                        float d = sg[c] * zv.x;
                         d = fmaf(sg[c + 1], zv.y, d);
                         d = fmaf(sg[c + 2], zv.z, d);
                         d = fmaf(sg[c + 3], zv.w, d);
@@ -232,122 +294,254 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a) {
                             if (h == hh) da[h] += d;
                     }
                 }
-#pragma unroll
-                for (int h = 0; h < kMaxHeads; ++h)
-                    if (h < a.H) a.dlogit[k * a.ldd + h] = da[h];
+                store_heads(a.dlogit, k, a.H, da);  // scratch, re-read by this thread in pass B
             } else {
 #pragma unroll
                 for (int h = 0; h < kMaxHeads; ++h) da[h] = h < a.H ? __ldg(a.grad + k * a.ldg + h) : 0.0f;
             }
+            if (a.lda == a.H) {
+                load_heads(al, a.alpha, k, a.H);
+            } else {
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h)
-                if (h < a.H) tp[h] = fmaf(__ldg(a.alpha + k * a.lda + h), da[h], tp[h]);
+                for (int h = 0; h < kMaxHeads; ++h) al[h] = h < a.H ? __ldg(a.alpha + k * a.lda + h) : 0.0f;
+            }
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) tp[h] = fmaf(al[h], da[h], tp[h]);
         }
-#pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < a.H) tp[h] = warp_sum(tp[h]);
-        __syncwarp();  // pass A's d_alpha stores visible to the lanes re-reading them
+        grp.sum(tp, a.H);
         // pass B: dL/dlogit = alpha * (d_alpha - t) (* leaky_relu' for GAT); grad_s_dst = row sum
         float gs[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) gs[h] = 0.0f;
-        for (int64_t p = b + lane; p < e; p += 32) {
+        for (int64_t p = b + t; p < e; p += G) {
             const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
+            if constexpr (GAT) {
+                float ss[kMaxHeads];
+                load_heads(da, a.dlogit, k, a.H);
+                load_heads(al, a.alpha, k, a.H);
+                load_heads(ss, a.s_src, a.col[p], a.H);
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) {
-                if (h >= a.H) continue;
-                const float da = GAT ? a.dlogit[k * a.ldd + h] : __ldg(a.grad + k * a.ldg + h);
-                float d = __ldg(a.alpha + k * a.lda + h) * (da - tp[h]);
-                if constexpr (GAT) {
-                    const float pre = __ldg(a.s_src + (int64_t)a.col[p] * a.H + h) + __ldg(a.s_dst + r * a.H + h);
-                    if (!(pre > 0.0f)) d *= a.slope;
+                for (int h = 0; h < kMaxHeads; ++h) {
+                    float d = al[h] * (da[h] - tp[h]);
+                    if (!(ss[h] + sd[h] > 0.0f)) d *= a.slope;
+                    da[h] = d;
                     gs[h] += d;
                 }
-                a.dlogit[k * a.ldd + h] = d;
+                store_heads(a.dlogit, k, a.H, da);
+            } else {
+                for (int h = 0; h < a.H; ++h)
+                    a.dlogit[k * a.ldd + h] = __ldg(a.alpha + k * a.lda + h) * (__ldg(a.grad + k * a.ldg + h) - tp[h]);
             }
         }
         if constexpr (GAT) {
+            grp.sum(gs, a.H);
+            if (t == 0)
+                for (int h = 0; h < a.H; ++h) a.grad_s_dst[r * a.H + h] = gs[h];
+        }
+        if (G > 32) __syncthreads();  // shared scratch reused by the next row
+    }
+}
+
+// GAT backward, warp-cooperative SDDMM (C % 4 == 0 and C a power of two <= 128 or a multiple of
+// 128; float4-aligned z / grad_out): a warp walks 32-position windows of its row, loading U z rows
+// at a time with lane l holding float4 chunk (l + 32 ch) of a row (coalesced), dotted with the
+// lane's chunk of grad_out[i] (registers, loaded once per row) and reduced over the C/4 lanes of
+// each head by a butterfly; the per-(position, head) d_alpha goes through shared memory to the
+// lane owning the position, which continues exactly like softmax_bwd_kernel (same position
+// assignment, so pass B is shared).
+template <int G, int NCH>
+__global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, RowSet rs) {
+    __shared__ float red[8 * kMaxHeads * 2];
+    __shared__ float sda[8][32 * kMaxHeads];
+    constexpr int U = NCH >= 8 ? 1 : 8 / NCH;
+    Group<G> grp{red};
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int t = G == 32 ? lane : threadIdx.x;
+    float* sd_w = sda[wib];
+    const int CL = a.C >= 128 ? 32 : a.C / 4;
+    int hch[NCH];
+    bool cvalid[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int c = 4 * (lane + 32 * ch);
+        cvalid[ch] = c < a.F;
+        hch[ch] = cvalid[ch] ? c / a.C : 0;
+    }
+    const bool leader = (lane % CL) == 0;
+    const int64_t units = G == 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
+    int64_t u = G == 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
+    for (;; u += units) {
+        const int64_t r = row_of<G>(rs, u);
+        if (r == -2) break;
+        if (r < 0) continue;
+        const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
+        float sd[kMaxHeads];
+        load_heads(sd, a.s_dst, r, a.H);
+        float4 gv[NCH];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            gv[ch] = cvalid[ch] ? __ldg(reinterpret_cast<const float4*>(a.grad + r * a.ldg) + lane + 32 * ch)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+        float tp[kMaxHeads], al[kMaxHeads], da[kMaxHeads];
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) tp[h] = 0.0f;
+        // pass A: windows of 32 positions; this thread owns position w + lane
+        for (int64_t w = b + (G == 32 ? 0 : 32 * wib); w < e; w += G) {
+            const int64_t p = w + lane;
+            const bool valid = p < e;
+            const int j = valid ? a.col[p] : 0;
+            const int64_t k = valid ? (a.eid ? (int64_t)a.eid[p] : p) : 0;
+#pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) sd_w[lane * kMaxHeads + h] = 0.0f;
+            __syncwarp();
+            const int n = (int)min((int64_t)32, e - w);
+            for (int t0 = 0; t0 < n; t0 += U) {
+                float4 zc[U][NCH];
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+                    const int jt = __shfl_sync(0xffffffffu, j, (t0 + uu) & 31);
+                    const float4* zr = reinterpret_cast<const float4*>(a.z + (int64_t)jt * a.ldz);
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch)
+                        zc[uu][ch] = (cvalid[ch] && t0 + uu < n) ? __ldg(zr + lane + 32 * ch)
+                                                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int uu = 0; uu < U; ++uu) {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        float d = gv[ch].x * zc[uu][ch].x;
+                        d = fmaf(gv[ch].y, zc[uu][ch].y, d);
+                        d = fmaf(gv[ch].z, zc[uu][ch].z, d);
+                        d = fmaf(gv[ch].w, zc[uu][ch].w, d);
+                        for (int o = 1; o < CL; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+                        if (leader && cvalid[ch] && t0 + uu < n) sd_w[(t0 + uu) * kMaxHeads + hch[ch]] += d;
+                    }
+                }
+            }
+            __syncwarp();
+            if (valid) {
+#pragma unroll
+                for (int h = 0; h < kMaxHeads; ++h) da[h] = sd_w[lane * kMaxHeads + h];
+                store_heads(a.dlogit, k, a.H, da);  // scratch, re-read by this thread in pass B
+                load_heads(al, a.alpha, k, a.H);
+#pragma unroll
+                for (int h = 0; h < kMaxHeads; ++h) tp[h] = fmaf(al[h], da[h], tp[h]);
+            }
+            __syncwarp();
+        }
+        grp.sum(tp, a.H);
+        // pass B (as softmax_bwd_kernel): position p = b + t + i*G is this thread's in both passes
+        float gs[kMaxHeads];
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) gs[h] = 0.0f;
+        for (int64_t p = b + t; p < e; p += G) {
+            const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
+            float ss[kMaxHeads];
+            load_heads(da, a.dlogit, k, a.H);
+            load_heads(al, a.alpha, k, a.H);
+            load_heads(ss, a.s_src, a.col[p], a.H);
 #pragma unroll
             for (int h = 0; h < kMaxHeads; ++h) {
-                if (h >= a.H) continue;
-                const float v = warp_sum(gs[h]);
-                if (lane == 0) a.grad_s_dst[r * a.H + h] = v;
+                float d = al[h] * (da[h] - tp[h]);
+                if (!(ss[h] + sd[h] > 0.0f)) d *= a.slope;
+                da[h] = d;
+                gs[h] += d;
             }
+            store_heads(a.dlogit, k, a.H, da);
         }
+        grp.sum(gs, a.H);
+        if (t == 0)
+            for (int h = 0; h < a.H; ++h) a.grad_s_dst[r * a.H + h] = gs[h];
+        if (G > 32) __syncthreads();
     }
 }
 
-int warp_grid(int64_t rows) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, 8), 148 * 8));
+RowSet row_set(const pyg_plan* p) {
+    RowSet rs;
+    rs.rowptr = p->rowptr;
+    rs.n_rows = p->n_rows;
+    rs.order = p->row_order;
+    rs.order_len = p->row_order ? p->order_len : p->n_rows;
+    rs.order_offset = p->row_offset;
+    const bool split = p->item_hi > p->item_lo && p->heavy_rows;
+    rs.thr = split ? p->heavy_threshold : INT64_MAX;
+    rs.heavy_rows = p->heavy_rows;
+    rs.h_lo = split ? p->h_lo : 0;
+    rs.h_hi = split ? p->h_hi : 0;
+    rs.row_offset = p->row_offset;
+    return rs;
 }
 
-template <int V>
-pyg_status_t launch_headw(const HeadwArgs& a, cudaStream_t s) {
-    const int nch = (int)cdiv(a.F, 32 * V);
-    const int grid = warp_grid(a.n_rows);
-    switch (nch) {
-        case 1: headw_kernel<V, 1><<<grid, 256, 0, s>>>(a); break;
-        case 2: headw_kernel<V, 2><<<grid, 256, 0, s>>>(a); break;
-        case 3: headw_kernel<V, 3><<<grid, 256, 0, s>>>(a); break;
-        case 4: headw_kernel<V, 4><<<grid, 256, 0, s>>>(a); break;
-        case 5: headw_kernel<V, 5><<<grid, 256, 0, s>>>(a); break;
-        case 6: headw_kernel<V, 6><<<grid, 256, 0, s>>>(a); break;
-        case 7: headw_kernel<V, 7><<<grid, 256, 0, s>>>(a); break;
-        case 8: headw_kernel<V, 8><<<grid, 256, 0, s>>>(a); break;
-        default: return fail(PYG_ERR_UNSUPPORTED, "attention: feature width %d too large", a.F);
-    }
-    PYG_LAUNCHED();
-    PYG_CUDA(cudaGetLastError());
-    return PYG_OK;
-}
+int warp_grid(int64_t units) { return (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(units, 8), 148 * 8)); }
+int cta_grid(int64_t units) { return (int)std::max<int64_t>(1, std::min<int64_t>(units, 148 * 8)); }
 
 }  // namespace
 
-pyg_status_t attention_headw(const int64_t* rowptr, int64_t n_rows, const int32_t* gidx, const int32_t* eid,
-                             const float* X, int64_t ldx, int F, int C, int H, const float* alpha, float* out,
-                             int64_t ldo, cudaStream_t s) {
-    if (n_rows <= 0 || F <= 0) return PYG_OK;
-    HeadwArgs a{rowptr, n_rows, gidx, eid, X, ldx, F, C, H, alpha, out, ldo};
-    const bool v4 = (F % 4 == 0) && (ldx % 4 == 0) && (ldo % 4 == 0) && !(reinterpret_cast<uintptr_t>(X) & 15) &&
-                    !(reinterpret_cast<uintptr_t>(out) & 15);
-    if (v4) return launch_headw<4>(a, s);
-    return launch_headw<1>(a, s);
-}
-
-pyg_status_t attention_softmax(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
-                               const float* src, int64_t lds, const float* s_src, const float* s_dst, int H,
-                               float slope, float* alpha, int64_t lda, cudaStream_t s) {
-    if (n_rows <= 0 || H <= 0) return PYG_OK;
-    SoftmaxArgs a{rowptr, n_rows, col, eid, src, lds, s_src, s_dst, H, slope, alpha, lda};
-    if (s_src) softmax_fwd_kernel<true><<<warp_grid(n_rows), 256, 0, s>>>(a);
-    else softmax_fwd_kernel<false><<<warp_grid(n_rows), 256, 0, s>>>(a);
-    PYG_LAUNCHED();
+pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const int32_t* eid, const float* src,
+                               int64_t lds, const float* s_src, const float* s_dst, int H, float slope, float* alpha,
+                               int64_t lda, cudaStream_t s) {
+    if (plan->n_rows <= 0 || H <= 0) return PYG_OK;
+    if (H > kMaxHeads) return fail(PYG_ERR_UNSUPPORTED, "softmax: at most %d heads / columns", kMaxHeads);
+    SoftmaxArgs a{col, eid, src, lds, s_src, s_dst, H, slope, alpha, lda};
+    const RowSet rs = row_set(plan);
+    const int64_t light = rs.order_len, heavy = rs.h_hi - rs.h_lo;
+    if (s_src) {
+        softmax_fwd_kernel<32, true><<<warp_grid(light), 256, 0, s>>>(a, rs);
+        PYG_LAUNCHED();
+        if (heavy > 0) { softmax_fwd_kernel<256, true><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
+    } else {
+        softmax_fwd_kernel<32, false><<<warp_grid(light), 256, 0, s>>>(a, rs);
+        PYG_LAUNCHED();
+        if (heavy > 0) { softmax_fwd_kernel<256, false><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
+    }
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;
 }
 
-pyg_status_t attention_softmax_bwd(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
-                                   int H, int C, int F, const float* alpha, int64_t lda, const float* grad, int64_t ldg,
-                                   const float* z, int64_t ldz, const float* s_src, const float* s_dst, float slope,
-                                   float* dlogit, int64_t ldd, float* grad_s_dst, cudaStream_t s) {
-    if (n_rows <= 0 || H <= 0) return PYG_OK;
+pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, const int32_t* eid, int H, int C, int F,
+                                   const float* alpha, int64_t lda, const float* grad, int64_t ldg, const float* z,
+                                   int64_t ldz, const float* s_src, const float* s_dst, float slope, float* dlogit,
+                                   int64_t ldd, float* grad_s_dst, cudaStream_t s) {
+    if (plan->n_rows <= 0 || H <= 0) return PYG_OK;
+    if (H > kMaxHeads) return fail(PYG_ERR_UNSUPPORTED, "softmax backward: at most %d heads / columns", kMaxHeads);
     SoftmaxBwdArgs a;
-    a.rowptr = rowptr; a.n_rows = n_rows; a.col = col; a.eid = eid;
+    a.col = col; a.eid = eid;
     a.H = H; a.C = C; a.F = F; a.alpha = alpha; a.lda = lda; a.grad = grad; a.ldg = ldg;
     a.z = z; a.ldz = ldz; a.s_src = s_src; a.s_dst = s_dst; a.slope = slope;
     a.vec = z && (F % 4 == 0) && (C % 4 == 0) && (ldz % 4 == 0) && !(reinterpret_cast<uintptr_t>(z) & 15);
     a.dlogit = dlogit; a.ldd = ldd; a.grad_s_dst = grad_s_dst;
-    const int grid = warp_grid(n_rows);
-    if (z) {
-        const size_t smem = (size_t)8 * F * sizeof(float);
-        if (smem > 48 * 1024)
-            PYG_CUDA(cudaFuncSetAttribute(softmax_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)smem));
-        softmax_bwd_kernel<true><<<grid, 256, smem, s>>>(a);
+    const RowSet rs = row_set(plan);
+    const int64_t light = rs.order_len, heavy = rs.h_hi - rs.h_lo;
+    const bool pow2 = C > 0 && (C & (C - 1)) == 0;
+    const bool coop = z && a.vec && (ldg % 4 == 0) && !(reinterpret_cast<uintptr_t>(grad) & 15) &&
+                      ((pow2 && C >= 4 && C <= 128) || C % 128 == 0) && F <= 1024;
+    if (coop) {
+        if (ldd != H || lda != H) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: GAT backward arrays must be packed");
+        const int nch = (int)cdiv(F, 128);
+        auto go = [&](auto kl, auto kh) {
+            kl<<<warp_grid(light), 256, 0, s>>>(a, rs);
+            PYG_LAUNCHED();
+            if (heavy > 0) { kh<<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
+        };
+        if (nch == 1) go(gat_bwd_coop_kernel<32, 1>, gat_bwd_coop_kernel<256, 1>);
+        else if (nch == 2) go(gat_bwd_coop_kernel<32, 2>, gat_bwd_coop_kernel<256, 2>);
+        else if (nch <= 4) go(gat_bwd_coop_kernel<32, 4>, gat_bwd_coop_kernel<256, 4>);
+        else go(gat_bwd_coop_kernel<32, 8>, gat_bwd_coop_kernel<256, 8>);
+    } else if (z) {
+        if (ldd != H || lda != H) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: GAT backward arrays must be packed");
+        const size_t smem_w = (size_t)8 * F * sizeof(float), smem_c = (size_t)F * sizeof(float);
+        if (smem_w > 48 * 1024)
+            PYG_CUDA(cudaFuncSetAttribute(softmax_bwd_kernel<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem_w));
+        softmax_bwd_kernel<32, true><<<warp_grid(light), 256, smem_w, s>>>(a, rs);
+        PYG_LAUNCHED();
+        if (heavy > 0) { softmax_bwd_kernel<256, true><<<cta_grid(heavy), 256, smem_c, s>>>(a, rs); PYG_LAUNCHED(); }
     } else {
-        softmax_bwd_kernel<false><<<grid, 256, 0, s>>>(a);
+        softmax_bwd_kernel<32, false><<<warp_grid(light), 256, 0, s>>>(a, rs);
+        PYG_LAUNCHED();
+        if (heavy > 0) { softmax_bwd_kernel<256, false><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
     }
-    PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;
 }

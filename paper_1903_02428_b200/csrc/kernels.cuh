@@ -46,6 +46,8 @@ namespace pyg {
 constexpr int kHeavyThreshold = 2048;  // rows longer than this are split (reading Q12)
 constexpr int kChunk = 512;            // positions per chunk of a split row
 constexpr int kTaskPositions = 4096;   // light positions per TMA-pipeline task
+constexpr int kRedHeadW = 3;           // internal reduce mode: SUM with per-(edge, head) weights
+                                       // hw[eid * hH + c / hC] (GAT alpha-weighted aggregation)
 
 // ---- CSR segment-reduce ---------------------------------------------------------
 struct SegArgs {
@@ -72,6 +74,13 @@ struct SegArgs {
     int accum = 0;                  // add into out/arg (source-blocked passes after the first)
     int finalize = 1;               // apply the mean division in this pass
     const int32_t* deg_total = nullptr;  // mean divisor per row when segments are partial
+    // APPNP blend epilogue (SUM/MEAN, finalize pass): out = blend_a * reduced + blend_b * blend[row]
+    const float* blend = nullptr;
+    int64_t ldb = 0;
+    float blend_a = 1.0f, blend_b = 0.0f;
+    // kRedHeadW: weights [E x hH] by edge id; column c belongs to head c / hC (hC % V == 0)
+    const float* hw = nullptr;
+    int hH = 0, hC = 0;
 };
 // Full segment reduce of a block of columns: light rows, split hub rows (plan
 // may be null for plan-free segment inputs such as pooling), fp64 combine.
@@ -128,20 +137,17 @@ pyg_status_t edge_weight_grad(const float* x, int64_t ldx, const float* g, int64
 pyg_status_t fill_rows(float* out, int64_t ldo, int ncols, int64_t n, cudaStream_t s);
 
 // ---- attention (NEXT-1; attention.cu) ----------------------------------------------
-// alpha[eid][h] = softmax over the row's positions of the logits: values src[eid][h] (s_src
-// null) or GAT leaky_relu(s_src[col][h] + s_dst[row][h], slope).
-pyg_status_t attention_softmax(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
-                               const float* src, int64_t lds, const float* s_src, const float* s_dst, int H,
-                               float slope, float* alpha, int64_t lda, cudaStream_t s);
-// out[r][c] = sum_p alpha[eid_p][c / C] * X[gidx_p][c]
-pyg_status_t attention_headw(const int64_t* rowptr, int64_t n_rows, const int32_t* gidx, const int32_t* eid,
-                             const float* X, int64_t ldx, int F, int C, int H, const float* alpha, float* out,
-                             int64_t ldo, cudaStream_t s);
+// alpha[eid][h] = softmax over each row's positions of the logits: values src[eid][h] (s_src
+// null) or GAT leaky_relu(s_src[col][h] + s_dst[row][h], slope).  Warp per light row, CTA per
+// split hub row of `plan`.
+pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const int32_t* eid, const float* src,
+                               int64_t lds, const float* s_src, const float* s_dst, int H, float slope, float* alpha,
+                               int64_t lda, cudaStream_t s);
 // dlogit = alpha (d_alpha - sum alpha d_alpha) per row (* leaky' for GAT, z != null: d_alpha is the
 // SDDMM grad[row] . z[col] per head, and grad_s_dst gets the row sums)
-pyg_status_t attention_softmax_bwd(const int64_t* rowptr, int64_t n_rows, const int32_t* col, const int32_t* eid,
-                                   int H, int C, int F, const float* alpha, int64_t lda, const float* grad, int64_t ldg,
-                                   const float* z, int64_t ldz, const float* s_src, const float* s_dst, float slope,
-                                   float* dlogit, int64_t ldd, float* grad_s_dst, cudaStream_t s);
+pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, const int32_t* eid, int H, int C, int F,
+                                   const float* alpha, int64_t lda, const float* grad, int64_t ldg, const float* z,
+                                   int64_t ldz, const float* s_src, const float* s_dst, float slope, float* dlogit,
+                                   int64_t ldd, float* grad_s_dst, cudaStream_t s);
 
 }  // namespace pyg

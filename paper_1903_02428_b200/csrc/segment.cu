@@ -51,6 +51,8 @@ __global__ void combine_kernel(SegArgs a, seg::HeavyArgs h) {
             for (int64_t it = i0; it < i1; ++it) s += (double)h.part[it * ldp + col];
             if (a.accum) s += (double)a.out[r * a.ldo + col];
             if (RED == PYG_MEAN && a.finalize) s = deg > 0 ? s / (double)deg : 0.0;
+            if (a.blend && a.finalize)
+                s = (double)a.blend_a * s + (double)a.blend_b * (double)a.blend[r * a.ldb + col];
             a.out[r * a.ldo + col] = (float)s;
         }
     }
@@ -83,6 +85,7 @@ Geometry geometry(int64_t ncols, int V) {
 }
 
 bool v_ok(const SegArgs& a, int V) {
+    if (a.hw && a.hC % V) return false;  // per-head weights: a vector chunk must stay inside one head
     const bool cols_ok = (a.ncols % V == 0) ||
                          (a.allow_pad_read && V >= 4 && a.ldx >= (int64_t)align_up(a.ncols, V));
     return cols_ok && a.ldx % V == 0 && aligned(a.X, 4 * V);
@@ -164,6 +167,7 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     switch (reduce) {
         case PYG_SUM: combine_kernel<PYG_SUM><<<grid, 256, 0, s>>>(a, h); break;
         case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, 256, 0, s>>>(a, h); break;
+        case kRedHeadW: combine_kernel<kRedHeadW><<<grid, 256, 0, s>>>(a, h); break;
         default: combine_kernel<PYG_MAX><<<grid, 256, 0, s>>>(a, h); break;
     }
     PYG_LAUNCHED();

@@ -88,7 +88,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
     const int32_t* __restrict__ gdeg = a.gdeg;
     const bool scaled = (w != nullptr) || (gdeg != nullptr);
     // the edge id is only needed for weights, argmax or edge-space rows
-    const bool need_e = (RED == PYG_MAX) || (w != nullptr) || (gidx == nullptr);
+    const bool need_e = (RED == PYG_MAX) || (RED == kRedHeadW) || (w != nullptr) || (gidx == nullptr);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
@@ -100,6 +100,12 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
     bool cv[NCH];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) cv[ch] = lane_off + ch * LPR * V < a.ncols;
+    // kRedHeadW: the head of each chunk (a V-chunk never straddles heads: hC % V == 0)
+    int hch[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) hch[ch] = (RED == kRedHeadW && cv[ch]) ? (lane_off + ch * LPR * V) / a.hC : 0;
+    const float* __restrict__ hw = a.hw;
+    const int64_t hH = a.hH;
     // row address = base + g * row_bytes as one 32x32->64 IMAD.WIDE (row_bytes < 2^32, g < 2^31);
     // chunk offsets are compile-time immediates
     const char* __restrict__ Xl = reinterpret_cast<const char*>(X + lane_off);
@@ -133,7 +139,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
             for (int u = 0; u < U; ++u) {
                 const int g = __shfl_sync(mask, mg, t + u, LPR);
                 sv[u] = scaled ? __shfl_sync(mask, ms, t + u, LPR) : 1.0f;
-                ev[u] = (RED == PYG_MAX) ? __shfl_sync(mask, me, t + u, LPR) : 0;
+                ev[u] = (RED == PYG_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t + u, LPR) : 0;
                 const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -142,32 +148,39 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
 #pragma unroll
             for (int u = 0; u < U; ++u)
 #pragma unroll
-                for (int ch = 0; ch < NCH; ++ch)
+                for (int ch = 0; ch < NCH; ++ch) {
+                    const float hwv = (RED == kRedHeadW) ? __ldg(hw + (int64_t)ev[u] * hH + hch[ch]) : 1.0f;
 #pragma unroll
                     for (int q = 0; q < V; ++q) {
                         if (RED == PYG_MAX) {
                             const float m = __fmul_rn(sv[u], v[u][ch][q]);  // s = 1 -> exact
                             if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }
+                        } else if (RED == kRedHeadW) {
+                            acc[ch][q] = fmaf(hwv, v[u][ch][q], acc[ch][q]);
                         } else {
                             acc[ch][q] = fmaf(sv[u], v[u][ch][q], acc[ch][q]);  // s = 1 -> plain add
                         }
                     }
+                }
         }
         for (; t < n; ++t) {
             const int g = __shfl_sync(mask, mg, t, LPR);
             const float sc = scaled ? __shfl_sync(mask, ms, t, LPR) : 1.0f;
-            const int e = (RED == PYG_MAX) ? __shfl_sync(mask, me, t, LPR) : 0;
+            const int e = (RED == PYG_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t, LPR) : 0;
             const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
                 if (cv[ch]) ld<V>(v[0][ch], row + ch * LPR * V);
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
+                const float hwv = (RED == kRedHeadW) ? __ldg(hw + (int64_t)e * hH + hch[ch]) : 1.0f;
 #pragma unroll
                 for (int q = 0; q < V; ++q) {
                     if (RED == PYG_MAX) {
                         const float m = __fmul_rn(sc, v[0][ch][q]);
                         if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
+                    } else if (RED == kRedHeadW) {
+                        acc[ch][q] = fmaf(hwv, v[0][ch][q], acc[ch][q]);
                     } else {
                         acc[ch][q] = fmaf(sc, v[0][ch][q], acc[ch][q]);
                     }
@@ -243,7 +256,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
     if (mode == 0) {
         const int64_t dseg = end - beg;
         // accumulate passes (source-blocked plans) have nothing to add for empty segments
-        if (a.accum && dseg == 0 && !(RED == PYG_MEAN && a.finalize)) return;
+        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || a.blend) && a.finalize)) return;
         const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -262,6 +275,11 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
                 if (RED == PYG_MEAN && a.finalize) {
 #pragma unroll
                     for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
+                }
+                if (a.blend && a.finalize) {
+                    const float* hb = a.blend + row * a.ldb + col;
+#pragma unroll
+                    for (int q = 0; q < V; ++q) if (q < nv) r[q] = fmaf(a.blend_b, hb[q], a.blend_a * r[q]);
                 }
                 st<V>(o, r, nv, out_vec_ok);
             } else {
@@ -351,6 +369,7 @@ pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, i
     switch (reduce) {
         case PYG_SUM: return launch_red<V, PYG_SUM>(a, nch, lpr, tiles, mode, h, ovk, s);
         case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
+        case kRedHeadW: return launch_red<V, kRedHeadW>(a, nch, lpr, tiles, mode, h, ovk, s);
         default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
     }
 }

@@ -158,3 +158,55 @@ def test_gat_empty_segments_and_errors():
     assert np.array_equal(alpha, np.full((2, 1), 0.5, np.float32))
     with pytest.raises(oracle.OracleError):
         oracle.gat(np.ones((3, 2), np.float32), np.zeros((3, 1)), np.zeros((3, 1)), np.array([[0], [3]]), 1)
+
+
+# ---- NEXT-2: APPNP / SGC --------------------------------------------------
+
+def _gcn_graph(seed, n=40, E=160):
+    rng = np.random.default_rng(seed)
+    ei = np.stack([rng.integers(0, n, E), rng.integers(0, n, E)]).astype(np.int64)
+    ei = ei[:, ei[0] != ei[1]]
+    ei = np.concatenate([ei, ei[::-1]], axis=1)  # symmetric
+    ei2, w = oracle.gcn_norm(ei, n)
+    S = np.zeros((n, n))
+    np.add.at(S, (ei2[1], ei2[0]), w.astype(np.float64))  # S[i][j] = sum of w over j -> i
+    return ei2, w, S
+
+
+def test_appnp_printed_special_cases():
+    """S:445 alpha = 1 -> h for any K; S:446 K = 1, alpha = 0 -> one GCN propagation."""
+    ei, w, _ = _gcn_graph(1)
+    h = np.random.default_rng(2).random((40, 3)).astype(np.float32)
+    assert np.array_equal(oracle.appnp(h, ei, K=7, alpha=1.0, edge_weight=w), h)
+    one = oracle.appnp(h, ei, K=1, alpha=0.0, edge_weight=w)
+    assert np.array_equal(one, oracle.propagate(h, ei, reduce="sum", edge_weight=w))
+    assert np.array_equal(oracle.appnp(h, ei, K=0, alpha=0.3, edge_weight=w), h)
+    with pytest.raises(oracle.OracleError):
+        oracle.appnp(h, ei, K=2, alpha=1.5, edge_weight=w)
+
+
+def test_appnp_dense_power_iteration_and_fixed_point():
+    """S:447 dense power-iteration oracle; the K -> inf limit is the closed form
+    alpha (I - (1 - alpha) S)^-1 h (APPNP's personalized-PageRank fixed point), reached to
+    within (1 - alpha)^K; SGC (alpha = 0, K = 2) equals the dense S^2 h."""
+    ei, w, S = _gcn_graph(3)
+    h = np.random.default_rng(4).random((40, 5)).astype(np.float32)
+    hd = h.astype(np.float64)
+    z = hd.copy()
+    for _ in range(10):
+        z = 0.9 * (S @ z) + 0.1 * hd
+    assert np.allclose(oracle.appnp(h, ei, K=10, alpha=0.1, edge_weight=w), z, rtol=1e-6, atol=1e-7)
+    fixed = 0.1 * np.linalg.solve(np.eye(40) - 0.9 * S, hd)
+    assert np.allclose(oracle.appnp(h, ei, K=300, alpha=0.1, edge_weight=w), fixed, rtol=1e-5, atol=1e-6)
+    assert np.allclose(oracle.appnp(h, ei, K=2, alpha=0.0, edge_weight=w), S @ (S @ hd), rtol=1e-6, atol=1e-7)
+
+
+def test_appnp_constant_fixed_point():
+    """complete graph with self-loops, constant features -> unchanged (stochastic matrix)."""
+    n = 6
+    src, dst = np.meshgrid(np.arange(n), np.arange(n))
+    ei = np.stack([src.ravel(), dst.ravel()]).astype(np.int64)
+    ei2, w = oracle.gcn_norm(ei, n)
+    h = np.full((n, 2), 0.75, np.float32)
+    out = oracle.appnp(h, ei2, K=5, alpha=0.2, edge_weight=w)
+    assert np.allclose(out, h, rtol=1e-7)
