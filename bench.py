@@ -52,10 +52,11 @@ def parse():
     ap.add_argument("--config", default="reddit", choices=list(CONFIGS))
     ap.add_argument("--reduce", default=None, choices=["sum", "mean", "max"])
     ap.add_argument("--strategy", default="segment", choices=["segment", "atomic"])
-    ap.add_argument("--op", default="propagate", choices=["propagate", "gat", "appnp"],
+    ap.add_argument("--op", default="propagate", choices=["propagate", "gat", "appnp", "gcn"],
                     help="gat: GAT attention aggregation forward + backward (NEXT-1) on the config's graph; "
                          "appnp: K-step APPNP propagation (NEXT-2) with GCN weights")
     ap.add_argument("--K", type=int, default=10, help="appnp: propagation steps")
+    ap.add_argument("--hidden", type=int, default=128, help="gcn: output width of the layer's transform")
     ap.add_argument("--alpha", type=float, default=0.1, help="appnp: teleport probability")
     ap.add_argument("--heads", type=int, default=0, help="GAT heads (0: 8 if F %% 8 == 0, else 4, 2 or 1)")
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
@@ -314,6 +315,38 @@ def oracle_appnp_run(ei_cpu, x_cpu, w_cpu, K, alpha, target_s, F):
     return rate, dt, Es, 0, None
 
 
+def oracle_gcn_sample(ei_cpu, x_cpu, W, b, n_rows, target_s):
+    """The oracle GCN layer (fp64 transform of the needed source rows, gcn_norm-weighted propagate, bias)
+    on the in-edges of the first R target rows; edges*F counted at the hidden width."""
+    import oracle
+
+    ei2, w2 = oracle.gcn_norm(ei_cpu, n_rows)
+    dst = ei2[1]
+    Fh = W.shape[0]
+
+    def run(R):
+        m = dst < R
+        sub = ei2[:, m]
+        t0 = time.perf_counter()
+        srcs = np.unique(sub[0])
+        h, hab = oracle.dense_transform(x_cpu[srcs], W, with_abs=True)
+        remap = np.zeros(n_rows, np.int64)
+        remap[srcs] = np.arange(srcs.size)
+        loc = np.stack([remap[sub[0]], sub[1]])
+        out = oracle.propagate(h, loc, n_dst=R, reduce="sum", edge_weight=w2[m]) + b
+        bound = oracle.propagate(hab.astype(np.float32), loc, n_dst=R, reduce="sum", edge_weight=w2[m])
+        s_abs = oracle.propagate(np.abs(h), loc, n_dst=R, reduce="sum", edge_weight=w2[m]) + np.abs(b)
+        return sub.shape[1], time.perf_counter() - t0, (out, bound, s_abs)
+
+    R = max(1, min(n_rows, 64))
+    Es, dt, _ = run(R)
+    rate = max(Es * Fh / max(dt, 1e-6), 1.0)
+    avg = max(ei2.shape[1] / n_rows, 1e-9)
+    R = int(min(n_rows, max(1, target_s * rate / (Fh * avg))))
+    Es, dt, res = run(R)
+    return Es * Fh / dt, dt, Es, R, res
+
+
 def run_reference(a):
     world, rank, local = dist_env()
     if rank != 0:
@@ -517,6 +550,39 @@ def main():
         def compute():
             pg.pyg_appnp(x_full, plan, K=a.K, alpha=a.alpha, edge_weight=wgt, out=obuf, scratch=zbuf, workspace=ws_a)
 
+    gcn = None
+    if a.op == "gcn":
+        # NEXT-2: one GCN layer D^-1/2 (A+I) D^-1/2 X W^T + b: the transform on the tcgen05
+        # tensor cores (TF32, D^-1/2 row scale fused), then the unweighted aggregation over A+I at the
+        # hidden width with the D^-1/2 row scale and the bias fused into its epilogue.
+        assert world == 1 and a.strategy == "segment", "--op gcn: one GPU, segment strategy"
+        t1 = time.perf_counter()
+        if a.config != "pubmed":
+            ei, _ = pg.pyg_gcn_norm(ei, N)
+            E = ei.shape[1]
+        plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
+        col_block = 0
+        torch.cuda.synchronize()
+        prep_ms = (time.perf_counter() - t1) * 1e3
+        gg = torch.Generator(device=dev)
+        gg.manual_seed(108)
+        Wt = torch.randn((a.hidden, ld), generator=gg, device=dev) / (F ** 0.5)
+        bias = torch.randn(a.hidden, generator=gg, device=dev)
+        gout = torch.empty((N, a.hidden), dtype=torch.float32, device=dev)
+        nbw = pg.lib.pyg_gcn_layer_workspace_size  # size query through the binding
+        ws_g = None
+        gcn = dict(out=gout, W=Wt[:, :F], b=bias)
+        passes, red = 1, "sum"
+        pg.pyg_gcn_layer(x_full, gcn["W"], plan, bias=bias, out=gout)  # allocates the workspace once
+
+        import ctypes as _ct
+        _nb = _ct.c_size_t()
+        pg._abi.check(nbw(plan.handle, N, a.hidden, _ct.byref(_nb)), "pyg_gcn_layer_workspace_size")
+        ws_g = torch.empty(max(1, _nb.value), dtype=torch.uint8, device=dev)
+
+        def compute():
+            pg.pyg_gcn_layer(x_full, gcn["W"], plan, bias=gcn["b"], out=gcn["out"], workspace=ws_g)
+
     def exchange_step():
         if exchange == "halo":  # pack the requested rows + one NCCL all-to-all (dist.py)
             halo_exchange(shard, halo["send_rows"], halo["sc"], halo["rc"], xbuf[per:],
@@ -565,12 +631,16 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms, kern_ms = tt.tolist()
     ms_step = total_ms / a.steps
-    units = passes * E * F  # edges*F of the whole job per step (all ranks together)
+    units = passes * E * (a.hidden if a.op == "gcn" else F)  # edges*F of the whole job per step (all ranks)
     value = units / (ms_step * 1e-3)
 
     peak, peak_src = measured_peak()
     if gat is not None:
         B = gat_step_bytes(E, N, F, gat["H"])
+    elif gcn is not None:  # transform (X once, W, H write) + unweighted aggregation at the hidden width
+        Fh = a.hidden
+        B = N * F * 4 + Fh * F * 4 + N * Fh * 4 + (E * Fh * 4 + E * 4 + 8 * (N + 1) + N * Fh * 4 + 2 * N * 4)
+        result_flops = 2.0 * N * F * Fh
     elif appnp is not None:  # K weighted propagations + the teleport read of h per step
         B = a.K * (alg_bytes(E, N, F, "sum", a.strategy, weighted=True) + (N * F * 4 if a.alpha else 0))
     else:
@@ -604,6 +674,15 @@ def main():
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
         "gen_s": gen_s,
     }
+    if gcn is not None:
+        result["config"]["op"] = "gcn"
+        result["config"]["hidden"] = a.hidden
+        result["config"]["E_with_self_loops"] = E
+        result["config"]["step"] = ("GCN layer: tcgen05 TF32 transform X W^T (D^-1/2 rows fused) + unweighted "
+                                    "aggregation over A+I at the hidden width (D^-1/2 and bias fused)")
+        result["gcn_norm_and_plans_ms"] = prep_ms
+        result["transform_tflops_per_step"] = result_flops / 1e12
+        result["units_note"] = "edges*F counts E x hidden (the aggregation width) per step"
     if appnp is not None:
         result["config"]["op"] = "appnp"
         result["config"]["K"] = a.K
@@ -631,7 +710,11 @@ def main():
         ei_cpu = ei.cpu().numpy()
         x_cpu = np.ascontiguousarray(x.cpu().numpy())
         w_cpu = wgt.cpu().numpy() if weighted else None
-        if appnp is not None:
+        if gcn is not None:
+            rate, dt, Es, R, ref = oracle_gcn_sample(ei_cpu, x_cpu, gcn["W"].cpu().numpy(), gcn["b"].cpu().numpy(), N,
+                                                     a.cpu_seconds)
+            got = gcn["out"][:R].cpu().numpy()
+        elif appnp is not None:
             rate, dt, Es, R, ref = oracle_appnp_run(ei_cpu, x_cpu, w_cpu, a.K, a.alpha, a.cpu_seconds, F)
             got = appnp["out"].cpu().numpy() if R else None
         elif gat is not None:
@@ -641,7 +724,9 @@ def main():
         else:
             rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
             got = out[:R].cpu().numpy()
-        if appnp is not None:
+        if gcn is not None:
+            ok = bool((np.abs(got - ref[0]) <= 2.5e-3 * ref[1] + 1e-5 * ref[2] + 1e-6).all())
+        elif appnp is not None:
             ok = bool((np.abs(got - ref) <= 1e-5 * np.abs(ref) + 1e-6).all()) if R else None
         elif gat is not None:
             ok = bool((np.abs(got - ref[0]) <= 1e-5 * ref[2] + 1e-6).all())
@@ -663,7 +748,7 @@ def main():
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
-    if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None:
+    if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None and gcn is None:
         xs = x.as_strided((N, ld), (x.stride(0), 1)) if x.stride(0) == ld else x.contiguous()
         hx = torch.empty(xs.shape, dtype=torch.float32, pin_memory=True)
         hx.copy_(xs)
@@ -698,7 +783,7 @@ def main():
                          "includes": "H2D(X, edge_index) + plan build + propagate + D2H(out)"}
 
     # ---- other reductions on the same resident graph (informational) ----
-    if world == 1 and not a.no_variants and passes == 1 and gat is None and appnp is None:
+    if world == 1 and not a.no_variants and passes == 1 and gat is None and appnp is None and gcn is None:
         var = {}
         for r2 in ("sum", "mean", "max"):
             if r2 == red:

@@ -363,6 +363,35 @@ pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const 
                        int64_t K, float alpha, const pyg_plan_t* plan, float* out, int64_t ldo,
                        float* scratch, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- NEXT-2: dense feature transform on the tensor cores ------------------------ */
+/* Y[m][n] = row_scale[m] * sum_k X[m][k] W[n][k] + bias[n]: the x W of GCN / SGC /
+ * APPNP layers, on tcgen05 tensor cores in TF32 with fp32 accumulation (both
+ * operands keep 10 mantissa bits: |error| <= ~2^-9 sum_k |X[m][k] W[n][k]|, A7).
+ *   X [M x K] stride ldx (row-major; 16-byte aligned, ldx % 4 == 0);
+ *   W [N x K] stride ldw (the torch.nn.Linear weight layout [out x in]; same alignment);
+ *   bias [N] or NULL; row_scale [M] or NULL (e.g. GCN's D^-1/2, applied before the bias);
+ *   Y [M x N] stride ldy, overwritten.  1 <= K, N <= 256.  Asynchronous. */
+pyg_status_t pyg_dense_transform(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W,
+                                 int64_t N, int64_t ldw, const float* bias, const float* row_scale,
+                                 float* Y, int64_t ldy, void* stream);
+
+/* GCN layer (Kipf & Welling's operator): out = D^-1/2 (A+I) D^-1/2 X W^T + bias,
+ * with d_i = the in-degree in `plan` (which must already contain the self-loops, e.g. a
+ * plan of pyg_gcn_norm's edge_index; reading Q7/Q8).  Transform first on the tensor cores
+ * (pyg_dense_transform, rows scaled by D^-1/2 in its epilogue, so the aggregation runs at
+ * width F_out), then an UNWEIGHTED segment sum over the plan whose epilogue scales rows by
+ * D^-1/2 and adds the bias: no per-edge weights or edge ids are read.
+ *   X [n x K] stride ldx, W [F_out x K] stride ldw (alignment as pyg_dense_transform),
+ *   bias [F_out] or NULL, out [n x F_out] stride ldo.  plan: unblocked forward plan, n x n.
+ *   workspace: pyg_gcn_layer_workspace_size (D^-1/2, the transformed rows, split rows).
+ *   Asynchronous. */
+pyg_status_t pyg_gcn_layer_workspace_size(const pyg_plan_t* plan, int64_t n, int64_t F_out,
+                                          size_t* bytes);
+pyg_status_t pyg_gcn_layer(const float* X, int64_t n, int64_t K, int64_t ldx, const float* W,
+                           int64_t F_out, int64_t ldw, const float* bias, const pyg_plan_t* plan,
+                           float* out, int64_t ldo, void* workspace, size_t workspace_bytes,
+                           void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -68,6 +68,7 @@ def lib():
             "orc_collate": [I, P, P, P, P, P, P],
             "orc_global_pool": [P, I, I, P, I, C, P, P],
             "orc_segment_softmax": [P, I, I, P, I, P],
+            "orc_dense_transform": [P, I, I, P, I, P, P, P, P],
             "orc_appnp": [P, I, I, P, I, P, I, ctypes.c_double, P],
             "orc_segment_softmax_backward": [P, P, I, I, P, I, P, P],
             "orc_gat": [P, I, I, I, P, P, I, P, I, ctypes.c_double, P, P, P],
@@ -341,3 +342,17 @@ def appnp(h, edge_index, K=10, alpha=0.1, edge_weight=None):
     _chk(lib().orc_appnp(_p(h), n, F, _p(edge_index), edge_index.shape[1], _p(_f32(edge_weight)), K, float(alpha),
                          _p(out)), "appnp")
     return out
+
+
+def dense_transform(x, weight, bias=None, row_scale=None, with_abs=False):
+    """Y = diag(row_scale) x weight^T + bias (weight [F_out x F_in])."""
+    x = _f32(x)
+    weight = _f32(weight)
+    M, K = x.shape
+    N = weight.shape[0]
+    assert weight.shape[1] == K
+    y = np.zeros((M, N), np.float32)
+    ab = np.zeros((M, N), np.float64) if with_abs else None
+    _chk(lib().orc_dense_transform(_p(x), M, K, _p(weight), N, _p(_f32(bias)), _p(_f32(row_scale)), _p(y), _p(ab)),
+         "dense_transform")
+    return (y, ab) if with_abs else y

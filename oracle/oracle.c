@@ -552,3 +552,25 @@ int orc_appnp(const float* h, int64_t n, int64_t F, const int64_t* ei, int64_t E
     free(t);
     return ORC_OK;
 }
+
+/* ---- NEXT-2: dense feature transform ------------------------------------------ */
+/* Y[m][n] = row_scale[m] * sum_k X[m][k] W[n][k] + bias[n] (the x W of GCN / SGC / APPNP, P:49-54;
+ * W in the [out x in] layout), in double, rounded once; abs = sum_k |X[m][k] W[n][k]| * |row_scale|. */
+int orc_dense_transform(const float* X, int64_t M, int64_t K, const float* W, int64_t N, const float* bias,
+                        const float* row_scale, float* Y, double* abs_out) {
+    if (M < 0 || K < 0 || N < 0 || (M * N > 0 && (!X || !W || !Y))) return ORC_ERR_INVALID;
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0, ab = 0.0;
+            for (int64_t k = 0; k < K; ++k) {
+                const double p = (double)X[m * K + k] * (double)W[n * K + k];
+                acc += p;
+                ab += fabs(p);
+            }
+            const double rs = row_scale ? (double)row_scale[m] : 1.0;
+            acc = acc * rs + (bias ? (double)bias[n] : 0.0);
+            Y[m * N + n] = (float)acc;
+            if (abs_out) abs_out[m * N + n] = ab * fabs(rs);
+        }
+    return ORC_OK;
+}

@@ -123,6 +123,10 @@ int orc_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, const 
 int orc_appnp(const float* h, int64_t n, int64_t F, const int64_t* ei, int64_t E,
               const float* edge_weight, int64_t K, double alpha, float* out);
 
+/* NEXT-2: dense transform Y = diag(row_scale) X W^T + bias, double. */
+int orc_dense_transform(const float* X, int64_t M, int64_t K, const float* W, int64_t N,
+                        const float* bias, const float* row_scale, float* Y, double* abs_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
 
@@ -432,4 +432,38 @@ def pyg_appnp(h: torch.Tensor, plan: Plan, K: int = 10, alpha: float = 0.1, edge
         workspace = _workspace(pyg_workspace_size(plan, n, F, SUM), dev)
     check(lib.pyg_appnp(_ptr(h), n, F, ldh, _ptr(edge_weight), K, alpha, plan.handle, _ptr(out), ldo, _ptr(scratch),
                         _ptr(workspace), workspace.numel(), _stream(dev)), "pyg_appnp")
+    return out
+
+
+def pyg_dense_transform(x: torch.Tensor, weight: torch.Tensor, bias: Optional[torch.Tensor] = None,
+                        row_scale: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None):
+    """Y = diag(row_scale) x weight^T + bias on tcgen05 tensor cores (TF32, fp32 accumulate).
+    weight: [F_out x F_in] (torch.nn.Linear layout)."""
+    M, K, ldx = _rows(x, "x")
+    N, K2, ldw = _rows(weight, "weight")
+    assert K2 == K
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=x.device)
+    _, _, ldy = _rows(out, "out")
+    check(lib.pyg_dense_transform(_ptr(x), M, K, ldx, _ptr(weight), N, ldw, _ptr(bias), _ptr(row_scale), _ptr(out),
+                                  ldy, _stream(x.device)), "pyg_dense_transform")
+    return out
+
+
+def pyg_gcn_layer(x: torch.Tensor, weight: torch.Tensor, plan: Plan, bias: Optional[torch.Tensor] = None,
+                  out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+    """GCN layer D^-1/2 (A+I) D^-1/2 x weight^T + bias; `plan` over edges incl. self-loops."""
+    n, K, ldx = _rows(x, "x")
+    F_out, K2, ldw = _rows(weight, "weight")
+    assert K2 == K
+    dev = x.device
+    if out is None:
+        out = torch.empty((n, F_out), dtype=torch.float32, device=dev)
+    _, _, ldo = _rows(out, "out")
+    if workspace is None:
+        nb = ctypes.c_size_t()
+        check(lib.pyg_gcn_layer_workspace_size(plan.handle, n, F_out, ctypes.byref(nb)), "pyg_gcn_layer_workspace_size")
+        workspace = _workspace(nb.value, dev)
+    check(lib.pyg_gcn_layer(_ptr(x), n, K, ldx, _ptr(weight), F_out, ldw, _ptr(bias), plan.handle, _ptr(out), ldo,
+                            _ptr(workspace), workspace.numel(), _stream(dev)), "pyg_gcn_layer")
     return out

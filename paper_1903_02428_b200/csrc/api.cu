@@ -79,6 +79,10 @@ pyg_status_t halo_workspace_impl(const pyg_plan* p, int64_t n_src, size_t* bytes
 pyg_status_t halo_build_impl(const pyg_plan* p, int64_t n_src, int64_t own_lo, int64_t own_hi, int64_t own_rows,
                              void* ws, size_t bytes, pyg_plan** out, int64_t* halo_ids, int64_t* n_halo,
                              cudaStream_t s);
+pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W, int64_t N,
+                                  int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
+                                  cudaStream_t s);
+pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_t s);
 pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, int64_t n, float* out,
                               int64_t ldo, cudaStream_t s);
 
@@ -666,6 +670,80 @@ pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const 
         ldz = ldo;
     }
     return PYG_OK;
+}
+
+// ---- NEXT-2: dense feature transform on tcgen05 (transform.cu) -------------------------
+
+pyg_status_t pyg_dense_transform(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W, int64_t N,
+                                 int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
+                                 void* stream) {
+    REQUIRE(M >= 0 && K >= 1 && N >= 0, PYG_ERR_INVALID_ARGUMENT, "dense_transform: bad sizes (K >= 1)");
+    REQUIRE(ldx >= K && ldw >= K && ldy >= N, PYG_ERR_DIMENSION, "dense_transform: leading dimension too small");
+    REQUIRE(N <= 256, PYG_ERR_UNSUPPORTED, "dense_transform: F_out <= 256 (one UMMA N)");
+    REQUIRE(M <= kMaxI32 && K <= kMaxI32, PYG_ERR_UNSUPPORTED, "dense_transform: sizes must be < 2^31");
+    REQUIRE(M * N == 0 || (X && W && Y), PYG_ERR_INVALID_ARGUMENT, "dense_transform: null pointer");
+    REQUIRE((reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&
+                (ldx % 4 == 0) && (ldw % 4 == 0),
+            PYG_ERR_ALIGNMENT, "dense_transform: X and W must be 16-byte aligned with ld %% 4 == 0 (TMA)");
+    return dense_transform_impl(X, M, K, ldx, W, N, ldw, bias, row_scale, Y, ldy, as_stream(stream));
+}
+
+// GCN layer: out = D^-1/2 (A+I) D^-1/2 X W^T + b, with the normalisation fused into the
+// epilogues: the transform scales its rows by D^-1/2 and the unweighted aggregation over A+I scales
+// its output rows by D^-1/2 and adds b -- no per-edge weights are read.
+static void gcn_layer_layout(const pyg_plan* plan, int64_t n, int64_t F_out, Carver& cv, float** dinv, float** H,
+                             int64_t* ldh, void** seg_ws, size_t* seg_bytes) {
+    *dinv = cv.take<float>((size_t)std::max<int64_t>(n, 1));
+    *ldh = (int64_t)align_up((size_t)std::max<int64_t>(F_out, 1), 8);
+    *H = cv.take<float>((size_t)std::max<int64_t>(n, 1) * (size_t)*ldh);
+    const size_t sb = segment_ws_bytes(plan, F_out, PYG_SUM) + 256;
+    *seg_ws = cv.take<char>(sb);
+    *seg_bytes = sb;
+}
+
+pyg_status_t pyg_gcn_layer_workspace_size(const pyg_plan_t* plan, int64_t n, int64_t F_out, size_t* bytes) {
+    REQUIRE(plan && bytes && n >= 0 && F_out >= 0, PYG_ERR_INVALID_ARGUMENT, "gcn_layer_workspace_size: bad args");
+    Carver cv(nullptr, 0);
+    float *dinv, *H;
+    int64_t ldh;
+    void* sw;
+    size_t sb;
+    gcn_layer_layout(plan, n, F_out, cv, &dinv, &H, &ldh, &sw, &sb);
+    *bytes = cv.off + 256;
+    return PYG_OK;
+}
+
+pyg_status_t pyg_gcn_layer(const float* X, int64_t n, int64_t K, int64_t ldx, const float* W, int64_t F_out,
+                           int64_t ldw, const float* bias, const pyg_plan_t* plan, float* out, int64_t ldo, void* ws,
+                           size_t ws_bytes, void* stream) {
+    REQUIRE(n >= 0 && K >= 1 && F_out >= 0, PYG_ERR_INVALID_ARGUMENT, "gcn_layer: bad sizes");
+    REQUIRE(ldo >= F_out, PYG_ERR_DIMENSION, "gcn_layer: ldo < F_out");
+    REQUIRE(plan && plan->n_rows == n && plan->n_cols <= n && (plan->col || plan->E == 0), PYG_ERR_DIMENSION,
+            "gcn_layer: needs a forward plan over n nodes (edges incl. self-loops, e.g. from pyg_gcn_norm)");
+    REQUIRE(n * F_out == 0 || out, PYG_ERR_INVALID_ARGUMENT, "gcn_layer: null out");
+    Carver cv(ws, ws_bytes);
+    float *dinv, *H;
+    int64_t ldh;
+    void* sw;
+    size_t sb;
+    gcn_layer_layout(plan, n, F_out, cv, &dinv, &H, &ldh, &sw, &sb);
+    REQUIRE(ws && cv.ok(), PYG_ERR_NO_MEMORY, "gcn_layer: workspace too small (pyg_gcn_layer_workspace_size)");
+    if (n == 0 || F_out == 0) return PYG_OK;
+    cudaStream_t s = as_stream(stream);
+    // degrees of A+I: the plan's row lengths (all source blocks together for blocked plans)
+    if (plan->parts.empty()) {
+        PYG_TRY(gcn_dinv(plan->rowptr, n, dinv, s));
+    } else {
+        return fail(PYG_ERR_UNSUPPORTED, "gcn_layer: source-blocked plans are not supported (aggregate width F_out is small)");
+    }
+    PYG_TRY(pyg_dense_transform(X, n, K, ldx, W, F_out, ldw, nullptr, dinv, H, ldh, stream));
+    SegArgs a;
+    a.X = H; a.ldx = ldh; a.ncols = (int)F_out;
+    a.rowptr = plan->rowptr; a.gidx = plan->col; a.eid = nullptr;
+    a.out = out; a.ldo = ldo; a.n_rows = n; a.E_sentinel = plan->E;
+    a.heavy_threshold = plan->heavy_threshold; a.allow_pad_read = 1;
+    a.row_scale = dinv; a.col_bias = bias;
+    return segment_reduce(a, PYG_SUM, plan, sw, sb, s);
 }
 
 }  // extern "C"

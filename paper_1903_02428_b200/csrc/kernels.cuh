@@ -78,6 +78,10 @@ struct SegArgs {
     const float* blend = nullptr;
     int64_t ldb = 0;
     float blend_a = 1.0f, blend_b = 0.0f;
+    // GCN-layer epilogue (SUM/MEAN, finalize pass): out = row_scale[row] * reduced (+ col_bias[c]);
+    // order: mean divide, row scale, blend, column bias
+    const float* row_scale = nullptr;
+    const float* col_bias = nullptr;
     // kRedHeadW: weights [E x hH] by edge id; column c belongs to head c / hC (hC % V == 0)
     const float* hw = nullptr;
     int hH = 0, hC = 0;

@@ -51,8 +51,10 @@ __global__ void combine_kernel(SegArgs a, seg::HeavyArgs h) {
             for (int64_t it = i0; it < i1; ++it) s += (double)h.part[it * ldp + col];
             if (a.accum) s += (double)a.out[r * a.ldo + col];
             if (RED == PYG_MEAN && a.finalize) s = deg > 0 ? s / (double)deg : 0.0;
+            if (a.row_scale && a.finalize) s *= (double)a.row_scale[r];
             if (a.blend && a.finalize)
                 s = (double)a.blend_a * s + (double)a.blend_b * (double)a.blend[r * a.ldb + col];
+            if (a.col_bias && a.finalize) s += (double)a.col_bias[col];
             a.out[r * a.ldo + col] = (float)s;
         }
     }

@@ -256,7 +256,8 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
     if (mode == 0) {
         const int64_t dseg = end - beg;
         // accumulate passes (source-blocked plans) have nothing to add for empty segments
-        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || a.blend) && a.finalize)) return;
+        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || a.blend || a.col_bias) && a.finalize)) return;
+        const float rsc = (a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
         const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -276,10 +277,18 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
 #pragma unroll
                     for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
                 }
+                if (a.row_scale && a.finalize) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) r[q] *= rsc;
+                }
                 if (a.blend && a.finalize) {
                     const float* hb = a.blend + row * a.ldb + col;
 #pragma unroll
                     for (int q = 0; q < V; ++q) if (q < nv) r[q] = fmaf(a.blend_b, hb[q], a.blend_a * r[q]);
+                }
+                if (a.col_bias && a.finalize) {
+#pragma unroll
+                    for (int q = 0; q < V; ++q) if (q < nv) r[q] += __ldg(a.col_bias + col + q);
                 }
                 st<V>(o, r, nv, out_vec_ok);
             } else {

@@ -52,6 +52,8 @@ struct Args {
     int nb;                 // column boxes per row
     int64_t row_lo, row_hi; // this plan's root rows; out row = r - row_lo
     int64_t E_sentinel;
+    const float* row_scale; // GCN-layer epilogue: v *= row_scale[row], then + col_bias[c]
+    const float* col_bias;
     const float* blend;     // APPNP epilogue (light rows): out = blend_a * v + blend_b * blend[row]
     int64_t ldb;
     float blend_a, blend_b;
@@ -277,7 +279,9 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
                 if (RED == PYG_MAX) v = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
                 else if (RED == PYG_MEAN) v = acc[ch][q] / (float)ccount;
                 else v = acc[ch][q];
+                if (RED != PYG_MAX && a.row_scale) v *= __ldg(a.row_scale + orow);
                 if (RED != PYG_MAX && a.blend) v = fmaf(a.blend_b, a.blend[orow * a.ldb + col + q], a.blend_a * v);
+                if (RED != PYG_MAX && a.col_bias) v += __ldg(a.col_bias + col + q);
                 o[q] = v;
             }
             if (RED == PYG_MAX) {
@@ -360,16 +364,18 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
 // one warp per empty row: out = 0 (float4 stores when aligned), arg = E
 __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
                                   int64_t row_hi, int ncols, float* out, int64_t ldo, int64_t* arg, int64_t lda,
-                                  int64_t E, int vec_ok, const float* blend, int64_t ldb, float blend_b) {
+                                  int64_t E, int vec_ok, const float* blend, int64_t ldb, float blend_b,
+                                  const float* col_bias) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t k = begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < end; k += warps) {
         const int64_t r = (int64_t)order[k];
         if (r < row_lo || r >= row_hi) continue;
         float* o = out + (r - row_lo) * ldo;
-        if (blend) {  // APPNP: an empty row keeps only the teleport term
-            const float* hb = blend + (r - row_lo) * ldb;
-            for (int c = lane; c < ncols; c += 32) o[c] = fmaf(blend_b, hb[c], 0.0f);
+        if (blend || col_bias) {  // APPNP: an empty row keeps only the teleport term; GCN: the bias
+            const float* hb = blend ? blend + (r - row_lo) * ldb : nullptr;
+            for (int c = lane; c < ncols; c += 32)
+                o[c] = (hb ? fmaf(blend_b, hb[c], 0.0f) : 0.0f) + (col_bias ? __ldg(col_bias + c) : 0.0f);
         } else if (vec_ok) {
             for (int c = 4 * lane; c < ncols; c += 128) *reinterpret_cast<float4*>(o + c) = make_float4(0, 0, 0, 0);
         } else {
@@ -522,6 +528,8 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     t.row_lo = plan->row_offset;
     t.row_hi = plan->row_offset + plan->n_rows;
     t.E_sentinel = a.E_sentinel;
+    t.row_scale = a.row_scale;
+    t.col_bias = a.col_bias;
     t.blend = a.blend;
     t.ldb = a.ldb;
     t.blend_a = a.blend_a;
@@ -546,7 +554,7 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
         empty_rows_kernel<<<blocks, 256, 0, s>>>(plan->row_order, plan->empty_begin, plan->empty_begin + n_empty,
                                                  plan->row_offset, plan->row_offset + plan->n_rows, F, a.out, a.ldo,
                                                  reduce == PYG_MAX ? a.arg : nullptr, a.lda, a.E_sentinel, vec_ok,
-                                                 a.blend, a.ldb, a.blend_b);
+                                                 a.blend, a.ldb, a.blend_b, reduce == PYG_MAX ? nullptr : a.col_bias);
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
     }

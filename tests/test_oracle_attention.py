@@ -210,3 +210,22 @@ def test_appnp_constant_fixed_point():
     h = np.full((n, 2), 0.75, np.float32)
     out = oracle.appnp(h, ei2, K=5, alpha=0.2, edge_weight=w)
     assert np.allclose(out, h, rtol=1e-7)
+
+
+# ---- NEXT-2: dense transform --------------------------------------------------------
+
+def test_dense_transform_vs_numpy_and_special_cases():
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((37, 23)).astype(np.float32)
+    w = rng.standard_normal((11, 23)).astype(np.float32)
+    b = rng.standard_normal(11).astype(np.float32)
+    rs = rng.random(37).astype(np.float32)
+    y, ab = oracle.dense_transform(x, w, bias=b, row_scale=rs, with_abs=True)
+    ref = rs[:, None].astype(np.float64) * (x.astype(np.float64) @ w.T.astype(np.float64)) + b
+    assert np.allclose(y, ref, rtol=1e-6, atol=1e-6)
+    assert (ab >= np.abs(ref - b) - 1e-9).all()
+    # identity weight -> copy (exact); zero weight -> bias
+    eye = np.eye(23, dtype=np.float32)
+    assert np.array_equal(oracle.dense_transform(x, eye), x)
+    assert np.array_equal(oracle.dense_transform(x, np.zeros((4, 23), np.float32), bias=b[:4]),
+                          np.broadcast_to(b[:4], (37, 4)))
