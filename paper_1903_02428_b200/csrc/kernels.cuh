@@ -48,6 +48,9 @@ constexpr int kChunk = 512;            // positions per chunk of a split row
 constexpr int kTaskPositions = 4096;   // light positions per TMA-pipeline task
 constexpr int kRedHeadW = 3;           // internal reduce mode: SUM with per-(edge, head) weights
                                        // hw[eid * hH + c / hC] (GAT alpha-weighted aggregation)
+constexpr int kRedSumEpi = 4;          // internal TMA-kernel mode: SUM with the row-scale / blend /
+                                       // bias epilogue (a separate instantiation keeps the plain SUM
+                                       // kernel at its register count)
 
 // ---- CSR segment-reduce ---------------------------------------------------------
 struct SegArgs {

@@ -138,7 +138,8 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     seg::HeavyArgs h;
     Carver cv(ws, ws_bytes);
     unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
-    const bool tma = ws && cv.ok() && tma_eligible(a, plan);
+    const bool extras = a.row_scale || a.blend || a.col_bias;
+    const bool tma = ws && cv.ok() && tma_eligible(a, plan) && !(extras && reduce != PYG_SUM);
     // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
     // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel
     const char* hub_env = getenv("PYG_TMA_HUBS");
