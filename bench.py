@@ -58,13 +58,19 @@ def parse():
     ap.add_argument("--K", type=int, default=10, help="appnp: propagation steps")
     ap.add_argument("--hidden", type=int, default=128, help="gcn: output width of the layer's transform")
     ap.add_argument("--alpha", type=float, default=0.1, help="appnp: teleport probability")
-    ap.add_argument("--heads", type=int, default=0, help="GAT heads (0: 8 if F %% 8 == 0, else 4, 2 or 1)")
+    ap.add_argument("--heads", type=int, default=0, help="GAT heads (0: 8)")
+    ap.add_argument("--gat-c", type=int, default=0, help="GAT channels per head (0: 8 on citation graphs, F/8 else)")
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
     ap.add_argument("--col-block", default="auto",
                     help="source rows per L2-resident pass: auto (pyg_plan_suggest_col_block), 0 (off) or N")
     ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
                     help="N > 1 source exchange: NCCL all-gather of X shards, or halo exchange of only the "
                          "referenced remote rows (auto: halo when it moves < half the all-gather rows)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as a CUDA graph (auto: on for the launch-bound L2-resident configs)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo stages the exchange through host memory: only for exercising the N > 1 path "
+                         "with several ranks on one GPU (tests); nccl is the measured backend")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -92,7 +98,7 @@ def init_dist(world, local, backend="nccl"):
 
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     if backend == "nccl":
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local % max(1, torch.cuda.device_count())))
     else:
         dist.init_process_group(backend)
     return dist
@@ -137,12 +143,27 @@ def make_workload(cfg, dev, ld_arg):
         import paper_1903_02428_b200 as pg
 
         nn, eptr, local, x_np = synth.clouds_like()
-        ei, _, _ = pg.pyg_collate(torch.from_numpy(nn).to(dev), torch.from_numpy(eptr).to(dev),
-                                  torch.from_numpy(local).to(dev))
+        args = (torch.from_numpy(nn).to(dev), torch.from_numpy(eptr).to(dev), torch.from_numpy(local).to(dev))
+        ei, _, _ = pg.pyg_collate(*args)
+        # the mini-batch collate (a9) timed on its own: CUDA events, median of 20 calls
+        ts = []
+        for _ in range(23):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pg.pyg_collate(*args, N_total=int(nn.sum()))
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        cms = float(np.median(ts[3:]))
+        Et, Nt, G = local.shape[1], int(nn.sum()), nn.size
+        cbytes = 2 * (2 * Et * 8) + Nt * 8 + (G + 1) * 8 * 2 + G * 8  # edges in/out, batch, ptrs
+        extra = {"collate_ms": cms, "collate_GBps": cbytes / (cms * 1e-3) / 1e9, "collate_alg_bytes": cbytes,
+                 "collate_note": "pyg_collate of 64 graphs (1,048,576 edges, 65,536 nodes), incl. binding overhead"}
         x = torch.from_numpy(x_np).to(dev)
         F = x_np.shape[1]
         ld = F
         w = None
+        return dict(ei=ei, x=x, N=x.shape[0], E=ei.shape[1], F=F, ld=ld, w=w, extra=extra)
     else:
         ei_np, x_np = synth.cora_like()
         ei = torch.from_numpy(ei_np).to(dev)
@@ -394,9 +415,11 @@ def main():
     world, rank, local = dist_env()
     if world > 1 and a.gpus != world:
         a.gpus = world
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist = init_dist(world, local)
+    # several ranks may share one GPU in the gloo test mode (--dist-backend gloo)
+    gpu = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    dist = init_dist(world, local, backend=a.dist_backend)
 
     import paper_1903_02428_b200 as pg
     from paper_1903_02428_b200.dist import gather_x, halo_exchange
@@ -440,7 +463,7 @@ def main():
         from paper_1903_02428_b200.dist import halo_setup
 
         hplan, hids = pg.pyg_halo_build(plan, N, lo, hi, per)
-        nh = torch.tensor([hids.numel()], dtype=torch.int64, device=dev)
+        nh = torch.tensor([hids.numel()], dtype=torch.int64, device=dev if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(nh, op=dist.ReduceOp.MAX)
         if a.exchange == "halo" or int(nh.item()) < 0.5 * (world - 1) * per:
             send_rows, sc, rc = halo_setup(hids, lo, per, world)
@@ -506,7 +529,10 @@ def main():
         # transposed plan, grad_s_src).  z = the config's X (the transformed features x W); the
         # attention projections s_src / s_dst are seeded inputs (dense per-node ops, outside the path).
         assert world == 1 and a.strategy == "segment", "--op gat: one GPU, segment strategy"
-        H = a.heads or next(h for h in (8, 4, 2, 1) if F % h == 0)
+        # z = x W: the GAT paper's 8 heads x 8 channels on the citation graphs, 8 x F/8 on
+        # the large graphs; z is a seeded input (the transform is the tcgen05 path, --op gcn)
+        H = a.heads or 8
+        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, F // H))
         t1 = time.perf_counter()
         if plan_full.view()["n_col_blocks"] > 1:
             plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
@@ -518,8 +544,9 @@ def main():
         gg.manual_seed(107)
         s_src = torch.randn((N, H), generator=gg, device=dev) * 2
         s_dst = torch.randn((N, H), generator=gg, device=dev) * 2
+        F = H * C
+        zc = torch.randn((N, F), generator=gg, device=dev)
         gout = torch.randn((N, F), generator=gg, device=dev)
-        zc = x if x.stride(0) == F else x.contiguous()
         gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
         passes, red = 2, "gat"
 
@@ -599,9 +626,26 @@ def main():
         step()
     torch.cuda.synchronize()
 
+    # CUDA graph of the step (single GPU): the small configs (Cora, PubMed, point clouds) take tens of
+    # microseconds per call, so host launch overhead would otherwise dominate the device timeline
+    # (all K timed steps are captured into ONE graph and replayed once, so the device runs them back
+    # to back; per-step time = total / K)
+    use_graph = (a.graph == "on" or (a.graph == "auto" and a.config in ("cora", "pubmed", "clouds"))) and world == 1
+    launches_per_replay = 0
+    if use_graph:
+        l0 = pg.launch_count()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for _ in range(a.steps):
+                compute()
+        torch.cuda.synchronize()
+        launches_per_replay = pg.launch_count() - l0
+        graph.replay()  # untimed: uploads the graph
+        torch.cuda.synchronize()
+
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    clocks = Clocks(local)
+    clocks = Clocks(gpu)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -611,25 +655,34 @@ def main():
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
-    for i in range(a.steps):
-        ev[i][0].record(stream)
-        exchange_step()
-        kev[i][0].record(stream)
-        compute()
-        kev[i][1].record(stream)
-        ev[i][1].record(stream)
+    if use_graph:
+        graph.replay()
+    else:
+        for i in range(a.steps):
+            ev[i][0].record(stream)
+            exchange_step()
+            kev[i][0].record(stream)
+            compute()
+            kev[i][1].record(stream)
+            ev[i][1].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
-    launches = pg.launch_count() - launches0
+    launches = pg.launch_count() - launches0 + launches_per_replay
     clk = clocks.stop()
     if dist:
         dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
-    kern_ms = float(np.mean([s.elapsed_time(e) for s, e in kev]))
+    if use_graph:
+        kern_ms = step_ms = total_ms / a.steps
+    else:
+        kern_ms = float(np.mean([s.elapsed_time(e) for s, e in kev]))
+        step_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
     if dist:
-        tt = torch.tensor([total_ms, kern_ms], device=dev)
+        tt = torch.tensor([total_ms, kern_ms, step_ms - kern_ms], device=dev if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms, kern_ms = tt.tolist()
+        total_ms, kern_ms, xchg_ms = tt.tolist()
+    else:
+        xchg_ms = 0.0
     ms_step = total_ms / a.steps
     units = passes * E * (a.hidden if a.op == "gcn" else F)  # edges*F of the whole job per step (all ranks)
     value = units / (ms_step * 1e-3)
@@ -668,12 +721,16 @@ def main():
                    "col_blocks": plan_full.view()["n_col_blocks"] if plan_full is not None else 0,
                    "parallelism": f"dst-range x{world}" if world > 1 else "single",
                    "exchange": exchange,
+                   "cuda_graph": bool(use_graph),
                    "halo_rows": halo["n"] if halo else None,
                    "l2": "inputs larger than L2 (no flush)" if a.config in ("reddit", "rmat")
                    else "L2-resident inputs (warm, back-to-back as in Fig. 3's 1000 runs)"},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
+        "exchange_ms": xchg_ms, "compute_ms": kern_ms,
         "gen_s": gen_s,
     }
+    if w.get("extra"):
+        result.update(w["extra"])
     if gcn is not None:
         result["config"]["op"] = "gcn"
         result["config"]["hidden"] = a.hidden
@@ -718,8 +775,8 @@ def main():
             rate, dt, Es, R, ref = oracle_appnp_run(ei_cpu, x_cpu, w_cpu, a.K, a.alpha, a.cpu_seconds, F)
             got = appnp["out"].cpu().numpy() if R else None
         elif gat is not None:
-            rate, dt, Es, R, ref = oracle_gat_sample(ei_cpu, x_cpu, s_src.cpu().numpy(), s_dst.cpu().numpy(), gat["H"],
-                                                     N, a.cpu_seconds, F)
+            rate, dt, Es, R, ref = oracle_gat_sample(ei_cpu, zc.cpu().numpy(), s_src.cpu().numpy(), s_dst.cpu().numpy(),
+                                                     gat["H"], N, a.cpu_seconds, F)
             got = gat["out"][:R].cpu().numpy()
         else:
             rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)

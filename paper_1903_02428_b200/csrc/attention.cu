@@ -28,6 +28,7 @@ namespace pyg {
 namespace {
 
 constexpr int kMaxHeads = 8;
+constexpr int64_t kShortRow = 16;  // softmax rows up to this length use 8-lane groups
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -49,8 +50,15 @@ struct Group {
     float* red;  // G == 256: shared scratch of 8 warps x kMaxHeads x 2 floats
     __device__ __forceinline__ void sum(float (&v)[kMaxHeads], int H) {
 #pragma unroll
-        for (int h = 0; h < kMaxHeads; ++h)
-            if (h < H) v[h] = warp_sum(v[h]);
+        for (int h = 0; h < kMaxHeads; ++h) {
+            if (h >= H) continue;
+            if constexpr (G >= 32) {
+                v[h] = warp_sum(v[h]);
+            } else {
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) v[h] += __shfl_xor_sync(0xffffffffu, v[h], o);
+            }
+        }
         if constexpr (G > 32) {
             const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
             __syncthreads();
@@ -66,7 +74,7 @@ struct Group {
     }
     __device__ __forceinline__ void max_sum(float (&m)[kMaxHeads], float (&s)[kMaxHeads], int H) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+        for (int o = (G >= 32 ? 16 : G / 2); o > 0; o >>= 1)
 #pragma unroll
             for (int h = 0; h < kMaxHeads; ++h) {
                 if (h >= H) continue;
@@ -127,6 +135,7 @@ struct RowSet {
     const int32_t* order;       // light rows: root ids in degree-bucket order (or null: 0..n_rows)
     int64_t order_len, order_offset;
     int64_t thr;                // rows longer than this are hub rows
+    int64_t dlo, dhi;           // light-row kernels: rows with dlo < degree <= dhi (and <= thr)
     const int32_t* heavy_rows;  // hub rows: root ids
     int64_t h_lo, h_hi, row_offset;
 };
@@ -134,7 +143,7 @@ struct RowSet {
 // the row a group works on in unit u (light: warp-granular; heavy: CTA-granular); -1: skip
 template <int G>
 __device__ __forceinline__ int64_t row_of(const RowSet& rs, int64_t u) {
-    if constexpr (G == 32) {
+    if constexpr (G <= 32) {
         int64_t r;
         if (rs.order) {
             if (u >= rs.order_len) return -2;
@@ -145,7 +154,7 @@ __device__ __forceinline__ int64_t row_of(const RowSet& rs, int64_t u) {
             r = u;
         }
         const int64_t d = rs.rowptr[r + 1] - rs.rowptr[r];
-        return (d == 0 || d > rs.thr) ? -1 : r;
+        return (d == 0 || d > rs.thr || d <= rs.dlo || d > rs.dhi) ? -1 : r;
     } else {
         if (u >= rs.h_hi - rs.h_lo) return -2;
         return (int64_t)rs.heavy_rows[rs.h_lo + u] - rs.row_offset;
@@ -185,16 +194,24 @@ template <int G, bool GAT>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(SoftmaxArgs a, RowSet rs) {
     __shared__ float red[8 * kMaxHeads * 2];
     Group<G> grp{red};
-    const int t = G == 32 ? (threadIdx.x & 31) : threadIdx.x;
-    const int64_t units = G == 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
-    int64_t u = G == 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
+    // G < 32: 32 / G rows per warp (short rows); the row loop stays warp-uniform (a group without a
+    // row joins the shuffles with an empty range) because the reductions shuffle across the warp
+    constexpr int GPW = G < 32 ? 32 / G : 1;
+    const int t = G <= 32 ? (threadIdx.x & (G - 1)) : threadIdx.x;
+    const int64_t units = G <= 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
+    int64_t u = G <= 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
     for (;; u += units) {
-        const int64_t r = row_of<G>(rs, u);
-        if (r == -2) break;
-        if (r < 0) continue;
-        const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
+        const int64_t r = row_of<G>(rs, G < 32 ? u * GPW + ((threadIdx.x & 31) / G) : u);
+        if constexpr (G < 32) {
+            if (__all_sync(0xffffffffu, r == -2)) break;
+            if (__all_sync(0xffffffffu, r < 0)) continue;
+        } else {
+            if (r == -2) break;
+            if (r < 0) continue;
+        }
+        const int64_t b = r >= 0 ? rs.rowptr[r] : 0, e = r >= 0 ? rs.rowptr[r + 1] : 0;
         float sd[kMaxHeads];
-        if (GAT) load_heads(sd, a.s_dst, r, a.H);
+        if (GAT && r >= 0) load_heads(sd, a.s_dst, r, a.H);
         float m[kMaxHeads], s[kMaxHeads], l[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) { m[h] = -INFINITY; s[h] = 0.0f; }
@@ -351,59 +368,79 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowS
 // assignment, so pass B is shared).
 template <int G, int NCH>
 __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, RowSet rs) {
+    // G = 8: 8-lane subgroups, one short row each (4 rows per warp); G = 32: a warp per row;
+    // G = 256: a CTA per hub row, each warp a subgroup walking every 8th 32-position window.
+    constexpr int LS = G >= 32 ? 32 : G;       // lanes per subgroup (one window = LS positions)
+    constexpr int GPW = G < 32 ? 32 / G : 1;   // rows per warp
     __shared__ float red[8 * kMaxHeads * 2];
     __shared__ float sda[8][32 * kMaxHeads];
     constexpr int U = NCH >= 8 ? 1 : 8 / NCH;
     Group<G> grp{red};
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int t = G == 32 ? lane : threadIdx.x;
-    float* sd_w = sda[wib];
-    const int CL = a.C >= 128 ? 32 : a.C / 4;
+    const int sl = lane & (LS - 1);            // lane within the subgroup
+    const int sbase = lane & ~(LS - 1);        // first lane of the subgroup
+    const int t = G <= 32 ? sl : threadIdx.x;
+    float* sd_w = sda[wib] + sbase * kMaxHeads;
+    const int CL = a.C >= 4 * LS ? LS : a.C / 4;  // lanes sharing a head inside one chunk row
     int hch[NCH];
     bool cvalid[NCH];
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
-        const int c = 4 * (lane + 32 * ch);
+        const int c = 4 * (sl + LS * ch);
         cvalid[ch] = c < a.F;
         hch[ch] = cvalid[ch] ? c / a.C : 0;
     }
-    const bool leader = (lane % CL) == 0;
-    const int64_t units = G == 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
-    int64_t u = G == 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
+    const bool leader = (sl % CL) == 0;
+    const int64_t units = G <= 32 ? (((int64_t)gridDim.x * blockDim.x) >> 5) : gridDim.x;
+    int64_t u = G <= 32 ? (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) : blockIdx.x;
     for (;; u += units) {
-        const int64_t r = row_of<G>(rs, u);
-        if (r == -2) break;
-        if (r < 0) continue;
-        const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
+        // warp-uniform row loop (the subgroups of a warp shuffle together)
+        const int64_t r = row_of<G>(rs, G < 32 ? u * GPW + lane / LS : u);
+        if constexpr (G < 32) {
+            if (__all_sync(0xffffffffu, r == -2)) break;
+            if (__all_sync(0xffffffffu, r < 0)) continue;
+        } else {
+            if (r == -2) break;
+            if (r < 0) continue;
+        }
+        const bool rok = r >= 0;
+        const int64_t b = rok ? rs.rowptr[r] : 0, e = rok ? rs.rowptr[r + 1] : 0;
         float sd[kMaxHeads];
-        load_heads(sd, a.s_dst, r, a.H);
+        if (rok) load_heads(sd, a.s_dst, r, a.H);
         float4 gv[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-            gv[ch] = cvalid[ch] ? __ldg(reinterpret_cast<const float4*>(a.grad + r * a.ldg) + lane + 32 * ch)
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
+            gv[ch] = (rok && cvalid[ch]) ? __ldg(reinterpret_cast<const float4*>(a.grad + r * a.ldg) + sl + LS * ch)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
         float tp[kMaxHeads], al[kMaxHeads], da[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) tp[h] = 0.0f;
-        // pass A: windows of 32 positions; this thread owns position w + lane
-        for (int64_t w = b + (G == 32 ? 0 : 32 * wib); w < e; w += G) {
-            const int64_t p = w + lane;
+        // pass A: windows of LS positions; this thread owns position w + sl
+        const int64_t w_first = b + (G > 32 ? 32 * wib : 0);
+        for (int64_t w = w_first; __any_sync(0xffffffffu, w < e); w += (G > 32 ? G : LS)) {
+            const int64_t p = w + sl;
             const bool valid = p < e;
             const int j = valid ? a.col[p] : 0;
             const int64_t k = valid ? (a.eid ? (int64_t)a.eid[p] : p) : 0;
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) sd_w[lane * kMaxHeads + h] = 0.0f;
+            for (int h = 0; h < kMaxHeads; ++h) sd_w[sl * kMaxHeads + h] = 0.0f;
             __syncwarp();
-            const int n = (int)min((int64_t)32, e - w);
-            for (int t0 = 0; t0 < n; t0 += U) {
+            const int n = w < e ? (int)min((int64_t)LS, e - w) : 0;
+            // warp-uniform trip count: the longest window of the warp's subgroups
+            int nmax = n;
+            if constexpr (G < 32) {
+#pragma unroll
+                for (int o = LS; o < 32; o <<= 1) nmax = max(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+            }
+            for (int t0 = 0; t0 < nmax; t0 += U) {
                 float4 zc[U][NCH];
 #pragma unroll
                 for (int uu = 0; uu < U; ++uu) {
-                    const int jt = __shfl_sync(0xffffffffu, j, (t0 + uu) & 31);
+                    const int jt = __shfl_sync(0xffffffffu, j, sbase + ((t0 + uu) & (LS - 1)));
                     const float4* zr = reinterpret_cast<const float4*>(a.z + (int64_t)jt * a.ldz);
 #pragma unroll
                     for (int ch = 0; ch < NCH; ++ch)
-                        zc[uu][ch] = (cvalid[ch] && t0 + uu < n) ? __ldg(zr + lane + 32 * ch)
+                        zc[uu][ch] = (cvalid[ch] && t0 + uu < n) ? __ldg(zr + sl + LS * ch)
                                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
 #pragma unroll
@@ -422,7 +459,7 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
             __syncwarp();
             if (valid) {
 #pragma unroll
-                for (int h = 0; h < kMaxHeads; ++h) da[h] = sd_w[lane * kMaxHeads + h];
+                for (int h = 0; h < kMaxHeads; ++h) da[h] = sd_w[sl * kMaxHeads + h];
                 store_heads(a.dlogit, k, a.H, da);  // scratch, re-read by this thread in pass B
                 load_heads(al, a.alpha, k, a.H);
 #pragma unroll
@@ -431,11 +468,12 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
             __syncwarp();
         }
         grp.sum(tp, a.H);
-        // pass B (as softmax_bwd_kernel): position p = b + t + i*G is this thread's in both passes
+        // pass B (as softmax_bwd_kernel): position p = b + t + i*G' is this thread's in both passes
+        // (G' = LS for subgroups, G for the CTA)
         float gs[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) gs[h] = 0.0f;
-        for (int64_t p = b + t; p < e; p += G) {
+        for (int64_t p = b + t; p < e; p += (G > 32 ? G : LS)) {
             const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
             float ss[kMaxHeads];
             load_heads(da, a.dlogit, k, a.H);
@@ -451,7 +489,7 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
             store_heads(a.dlogit, k, a.H, da);
         }
         grp.sum(gs, a.H);
-        if (t == 0)
+        if (t == 0 && rok)
             for (int h = 0; h < a.H; ++h) a.grad_s_dst[r * a.H + h] = gs[h];
         if (G > 32) __syncthreads();
     }
@@ -466,6 +504,8 @@ RowSet row_set(const pyg_plan* p) {
     rs.order_offset = p->row_offset;
     const bool split = p->item_hi > p->item_lo && p->heavy_rows;
     rs.thr = split ? p->heavy_threshold : INT64_MAX;
+    rs.dlo = 0;
+    rs.dhi = INT64_MAX;
     rs.heavy_rows = p->heavy_rows;
     rs.h_lo = split ? p->h_lo : 0;
     rs.h_hi = split ? p->h_hi : 0;
@@ -486,12 +526,20 @@ pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const i
     SoftmaxArgs a{col, eid, src, lds, s_src, s_dst, H, slope, alpha, lda};
     const RowSet rs = row_set(plan);
     const int64_t light = rs.order_len, heavy = rs.h_hi - rs.h_lo;
+    // rows of <= kShortRow positions: 8-lane groups (4 rows per warp); longer light rows: a warp
+    RowSet rs_short = rs, rs_long = rs;
+    rs_short.dhi = kShortRow;
+    rs_long.dlo = kShortRow;
     if (s_src) {
-        softmax_fwd_kernel<32, true><<<warp_grid(light), 256, 0, s>>>(a, rs);
+        softmax_fwd_kernel<8, true><<<warp_grid(cdiv(light, 4)), 256, 0, s>>>(a, rs_short);
+        softmax_fwd_kernel<32, true><<<warp_grid(light), 256, 0, s>>>(a, rs_long);
+        PYG_LAUNCHED();
         PYG_LAUNCHED();
         if (heavy > 0) { softmax_fwd_kernel<256, true><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
     } else {
-        softmax_fwd_kernel<32, false><<<warp_grid(light), 256, 0, s>>>(a, rs);
+        softmax_fwd_kernel<8, false><<<warp_grid(cdiv(light, 4)), 256, 0, s>>>(a, rs_short);
+        softmax_fwd_kernel<32, false><<<warp_grid(light), 256, 0, s>>>(a, rs_long);
+        PYG_LAUNCHED();
         PYG_LAUNCHED();
         if (heavy > 0) { softmax_fwd_kernel<256, false><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
     }
@@ -519,8 +567,26 @@ pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, con
     if (coop) {
         if (ldd != H || lda != H) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: GAT backward arrays must be packed");
         const int nch = (int)cdiv(F, 128);
+        // short rows (<= kShortRow positions) on 8-lane subgroups when a head's columns tile an
+        // 8-lane chunk row (C a power of two <= 32 or a multiple of 32) and F <= 256
+        const bool short8 = ((pow2 && C <= 32) || C % 32 == 0) && F <= 256;
+        RowSet rs_long = rs;
+        if (short8) {
+            RowSet rs_short = rs;
+            rs_short.dhi = kShortRow;
+            rs_long.dlo = kShortRow;
+            const int n8 = (int)cdiv(F, 32);
+            auto g8 = [&](auto k8) {
+                k8<<<warp_grid(cdiv(light, 4)), 256, 0, s>>>(a, rs_short);
+                PYG_LAUNCHED();
+            };
+            if (n8 <= 1) g8(gat_bwd_coop_kernel<8, 1>);
+            else if (n8 <= 2) g8(gat_bwd_coop_kernel<8, 2>);
+            else if (n8 <= 4) g8(gat_bwd_coop_kernel<8, 4>);
+            else g8(gat_bwd_coop_kernel<8, 8>);
+        }
         auto go = [&](auto kl, auto kh) {
-            kl<<<warp_grid(light), 256, 0, s>>>(a, rs);
+            kl<<<warp_grid(light), 256, 0, s>>>(a, rs_long);
             PYG_LAUNCHED();
             if (heavy > 0) { kh<<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
         };

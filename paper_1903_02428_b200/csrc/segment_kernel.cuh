@@ -154,7 +154,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
                     for (int q = 0; q < V; ++q) {
                         if (RED == PYG_MAX) {
                             const float m = __fmul_rn(sv[u], v[u][ch][q]);  // s = 1 -> exact
-                            if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }
+                            if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }  // acc starts at -inf (Q5: finite inputs)
                         } else if (RED == kRedHeadW) {
                             acc[ch][q] = fmaf(hwv, v[u][ch][q], acc[ch][q]);
                         } else {
@@ -178,7 +178,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
                 for (int q = 0; q < V; ++q) {
                     if (RED == PYG_MAX) {
                         const float m = __fmul_rn(sc, v[0][ch][q]);
-                        if (bi[ch][q] < 0 || m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
+                        if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
                     } else if (RED == kRedHeadW) {
                         acc[ch][q] = fmaf(hwv, v[0][ch][q], acc[ch][q]);
                     } else {

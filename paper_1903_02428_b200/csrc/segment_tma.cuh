@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
             for (int q = 0; q < 4; ++q) {
                 if (RR == PYG_MAX) {
                     const float mm = __fmul_rn(sc, vv[q]);
-                    if (bi[ch][q] < 0 || mm > acc[ch][q]) { acc[ch][q] = mm; bi[ch][q] = e; }
+                    if (mm > acc[ch][q]) { acc[ch][q] = mm; bi[ch][q] = e; }  // acc starts at -inf (Q5: finite inputs)
                 } else {
                     acc[ch][q] = fmaf(sc, vv[q], acc[ch][q]);
                 }

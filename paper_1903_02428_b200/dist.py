@@ -21,6 +21,12 @@ import torch
 import torch.distributed as dist
 
 
+def _staged(group, *tensors) -> bool:
+    """gloo cannot run these collectives on CUDA tensors: stage them through host memory (used to
+    exercise the N > 1 path with several processes on one GPU; NCCL is the production backend)."""
+    return dist.get_backend(group) == "gloo" and any(t.is_cuda for t in tensors)
+
+
 def partition_rows(n: int, world: int):
     """Contiguous destination ranges [lo, hi) per rank, equal shards of ceil(n / world) rows
     (the last ones may be short or empty).  Returns (ranges, rows_per_shard)."""
@@ -33,6 +39,11 @@ def gather_x(x_shard: torch.Tensor, world: int, group=None, out: Optional[torch.
     per = x_shard.shape[0]
     if out is None:
         out = torch.empty((per * world,) + tuple(x_shard.shape[1:]), dtype=x_shard.dtype, device=x_shard.device)
+    if _staged(group, x_shard, out):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.all_gather_into_tensor(h, x_shard.contiguous().cpu(), group=group)
+        out.copy_(h)
+        return out
     dist.all_gather_into_tensor(out, x_shard.contiguous(), group=group)
     return out
 
@@ -41,6 +52,11 @@ def reduce_scatter_rows(partial: torch.Tensor, world: int, group=None) -> torch.
     """Sum [per * world, F] partials over ranks and return this rank's [per, F] shard."""
     per = partial.shape[0] // world
     out = torch.empty((per,) + tuple(partial.shape[1:]), dtype=partial.dtype, device=partial.device)
+    if _staged(group, partial):
+        h = torch.empty(out.shape, dtype=out.dtype)
+        dist.reduce_scatter_tensor(h, partial.contiguous().cpu(), group=group)
+        out.copy_(h)
+        return out
     dist.reduce_scatter_tensor(out, partial.contiguous(), group=group)
     return out
 
@@ -58,13 +74,14 @@ def halo_setup(halo_ids: torch.Tensor, lo: int, per: int, world: int, group=None
     in ascending global id, which is the halo_ids order."""
     recv_counts = halo_recv_counts(halo_ids, per, world)
     dev = halo_ids.device
-    rc = torch.tensor(recv_counts, dtype=torch.int64, device=dev)
+    cdev = "cpu" if _staged(group, halo_ids) else dev
+    rc = torch.tensor(recv_counts, dtype=torch.int64, device=cdev)
     sc = torch.empty_like(rc)
     dist.all_to_all_single(sc, rc, group=group)  # sc[q] = rows rank q wants from me
     send_counts = sc.tolist()
-    req = torch.empty(sum(send_counts), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(req, halo_ids.contiguous(), send_counts, recv_counts, group=group)
-    return req - lo, send_counts, recv_counts
+    req = torch.empty(sum(send_counts), dtype=torch.int64, device=cdev)
+    dist.all_to_all_single(req, halo_ids.contiguous().to(cdev), send_counts, recv_counts, group=group)
+    return (req - lo).to(dev), send_counts, recv_counts
 
 
 def halo_exchange(x_shard: torch.Tensor, send_rows: torch.Tensor, send_counts, recv_counts, recv_out: torch.Tensor,
@@ -79,6 +96,11 @@ def halo_exchange(x_shard: torch.Tensor, send_rows: torch.Tensor, send_counts, r
         send_buf = torch.empty((send_rows.numel(), ld), dtype=x_shard.dtype, device=x_shard.device)
     if send_rows.numel() > 0:
         pack(x_shard, send_rows, send_buf)
+    if _staged(group, send_buf, recv_out):
+        h = torch.empty(recv_out.shape, dtype=recv_out.dtype)
+        dist.all_to_all_single(h, send_buf.cpu(), recv_counts, send_counts, group=group)
+        recv_out.copy_(h)
+        return recv_out
     dist.all_to_all_single(recv_out, send_buf, recv_counts, send_counts, group=group)
     return recv_out
 

@@ -30,7 +30,7 @@ if __name__ == "__main__":
              ("rmat-sum-segment-cb0-n1", "launches_rmat_sum.csv", 3),
              ("rmat-max-segment-cb0-n1", "launches_rmat_max.csv", 3)]
     for key, f, n in specs:
-        p = os.path.join("gpurun_out", tag, f)
+        p = os.path.join("profiles", f"{tag}_{f}")
         if os.path.exists(p):
             b, ms, names = call_traffic(p, n)
             out[key] = b

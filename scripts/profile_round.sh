@@ -1,31 +1,69 @@
 #!/bin/bash
-# One GPU session: parity suite, smoke, default bench, ncu launch lists (time + DRAM bytes per
-# launch) and one --set full capture per headline kernel.  Output: gpurun_out/$TAG/
+# One GPU session: parity suite, smoke, the bench lines of every config / op, ncu launch lists
+# (time + DRAM bytes per launch) and one --set full capture per headline kernel, the Fig. 3 study,
+# compute-sanitizer on representative tests.  Output: gpurun_out/$TAG/
 set -u
 TAG=${1:-r1}
 O=gpurun_out/$TAG
 mkdir -p $O
+# gpurun copies back at most 64 MiB: every --set full report is exported to CSV (raw metrics +
+# details page) and deleted; launch lists are gzipped
+export_rep() {
+  if [ -f "$1.ncu-rep" ]; then
+    ncu -i "$1.ncu-rep" --page raw --csv > "$1.raw.csv" 2>/dev/null
+    ncu -i "$1.ncu-rep" --page details --csv > "$1.details.csv" 2>/dev/null
+    rm -f "$1.ncu-rep"
+  fi
+}
 timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -15 > $O/pytest_gpu.txt
 timeout 300 python __graft_entry__.py smoke > $O/smoke.txt 2>&1
 timeout 600 python bench.py > $O/bench_default.json 2> $O/bench_default.err
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum
 Q="--steps 1 --warmup 3 --no-e2e --no-cpu --no-variants"
+FULL="ncu --set full --clock-control none --import-source on"
 timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_reddit_mean.csv python bench.py $Q > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_kernel -s 33 -c 1 -o $O/full_reddit_mean python bench.py $Q > /dev/null 2>&1
+timeout 900 $FULL -k regex:seg_kernel -s 33 -c 1 -o $O/full_reddit_mean python bench.py $Q > /dev/null 2>&1
+export_rep $O/full_reddit_mean
 for red in sum max; do
   timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_rmat_$red.csv python bench.py --config rmat --reduce $red $Q > /dev/null 2>&1
+  timeout 900 $FULL -k regex:seg_tma -s 3 -c 1 -o $O/full_rmat_$red python bench.py --config rmat --reduce $red $Q > /dev/null 2>&1
+  export_rep $O/full_rmat_$red
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:seg_tma -s 3 -c 1 -o $O/full_rmat_sum python bench.py --config rmat --reduce sum $Q > /dev/null 2>&1
+# atomic COO strategy: atomic throughput evidence (north_star: "atomic throughput")
+timeout 900 $FULL -k regex:coo_kernel -s 3 -c 1 -o $O/full_rmat_sum_atomic python bench.py --config rmat --reduce sum --strategy atomic $Q > /dev/null 2>&1
+export_rep $O/full_rmat_sum_atomic
+timeout 900 $FULL -k regex:coo_kernel -s 3 -c 1 -o $O/full_reddit_mean_atomic python bench.py --strategy atomic $Q > /dev/null 2>&1
+export_rep $O/full_reddit_mean_atomic
 for red in sum max; do
   timeout 600 python bench.py --config rmat --reduce $red --steps 10 --no-e2e --no-cpu --no-variants > $O/bench_rmat_$red.json 2> $O/bench_rmat_$red.err
   timeout 600 python bench.py --config rmat --reduce $red --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_rmat_${red}_atomic.json 2> $O/bench_rmat_${red}_atomic.err
 done
+timeout 600 python bench.py --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_reddit_mean_atomic.json 2> $O/bench_reddit_mean_atomic.err
 for cfg in pubmed clouds cora; do  # pubmed = GCN fwd+bwd
   timeout 300 python bench.py --config $cfg --steps 50 --no-e2e --no-variants > $O/bench_$cfg.json 2> $O/bench_$cfg.err
 done
+# NEXT rows: GAT (NEXT-1), APPNP and the GCN layer with the tcgen05 transform (NEXT-2)
+for cfg in rmat pubmed; do
+  timeout 600 python bench.py --config $cfg --op gat --steps 10 > $O/bench_gat_$cfg.json 2> $O/bench_gat_$cfg.err
+done
+for cfg in reddit pubmed; do
+  timeout 600 python bench.py --config $cfg --op appnp --steps 5 > $O/bench_appnp_$cfg.json 2> $O/bench_appnp_$cfg.err
+done
+for cfg in reddit rmat pubmed; do
+  timeout 600 python bench.py --config $cfg --op gcn --steps 10 > $O/bench_gcn_$cfg.json 2> $O/bench_gcn_$cfg.err
+done
+timeout 600 ncu --metrics $M --clock-control none -k regex:"softmax|seg_|combine|gat_" --csv --log-file $O/launches_gat_rmat.csv python bench.py --config rmat --op gat $Q > /dev/null 2>&1
+timeout 900 $FULL -k regex:gat_bwd_coop -c 1 -o $O/full_gat_bwd_rmat python bench.py --config rmat --op gat $Q > /dev/null 2>&1
+export_rep $O/full_gat_bwd_rmat
+timeout 600 ncu --metrics $M --clock-control none -k regex:"tf32|seg_|combine|deg_rsqrt" --csv --log-file $O/launches_gcn_reddit.csv python bench.py --config reddit --op gcn $Q > /dev/null 2>&1
+timeout 900 $FULL -k regex:tf32 -s 1 -c 1 -o $O/full_tf32_reddit python bench.py --config reddit --op gcn $Q > /dev/null 2>&1
+export_rep $O/full_tf32_reddit
+timeout 600 python scripts/fig3.py --out $O/fig3.json > $O/fig3.log 2>&1
 # memory-safety evidence: compute-sanitizer memcheck / racecheck on representative small tests
-timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -q -x \
-  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward" \
+timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_appnp.py tests/test_gpu_transform.py tests/test_gpu_dist.py -q -x \
+  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward or cora or rmat_h4c16 or softmax or power_law or pubmed_shaped or (transform and 300) or gcn_layer or halo_plan" \
   > $O/sanitizer_memcheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck.txt
-timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py -q -x \
-  -k "(tma_pipeline and 128) or split_hub" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
+timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_transform.py -q -x \
+  -k "(tma_pipeline and 128) or split_hub or rmat_h4c16 or (transform and 1000)" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
+
+gzip -f $O/launches_*.csv

@@ -79,3 +79,15 @@ def test_appnp_errors():
     plan = pg.pyg_plan_build(ei[1], ei[0], 30, 30)
     with pytest.raises(pg.PygError):
         pg.pyg_appnp(torch.zeros((30, 4), device=DEV), plan, K=2, alpha=1.5)
+
+
+def test_appnp_no_edges():
+    """E = 0: S z = 0, so z_K = alpha h for K >= 1 (and h for K = 0)."""
+    import paper_1903_02428_b200 as pg
+
+    h = torch.rand((37, 5), device=DEV)
+    ei = torch.zeros((2, 0), dtype=torch.int64, device=DEV)
+    plan = pg.pyg_plan_build(ei[1], ei[0], 37, 37)
+    out = pg.pyg_appnp(h, plan, K=3, alpha=0.25)
+    assert torch.allclose(out, 0.25 * h, rtol=0, atol=0)
+    assert torch.equal(pg.pyg_appnp(h, plan, K=0, alpha=0.25), h)

@@ -145,3 +145,32 @@ def test_attention_errors():
     splan = pg.pyg_plan_build(ei[1], None, 50)
     with pytest.raises(pg.PygError):  # more than 8 columns
         pg.pyg_segment_softmax(torch.zeros((300, 9), device=DEV), splan, 50)
+
+
+def test_gat_empty_graph_and_single_edge():
+    """Degenerate cases: E = 0 (every segment empty -> out 0, all gradients 0) and one edge
+    (alpha = 1, out = z_j, d alpha = 0 -> zero attention gradients)."""
+    import paper_1903_02428_b200 as pg
+
+    n, H, C = 10, 2, 4
+    z = torch.randn((n, H * C), device=DEV)
+    ss = torch.randn((n, H), device=DEV)
+    sd = torch.randn((n, H), device=DEV)
+    g = torch.randn((n, H * C), device=DEV)
+    ei = torch.zeros((2, 0), dtype=torch.int64, device=DEV)
+    plan = pg.pyg_plan_build(ei[1], ei[0], n, n)
+    planT = pg.pyg_plan_build(ei[0], ei[1], n, n)
+    out, alpha = pg.pyg_gat_propagate(z, ss, sd, H, plan)
+    assert alpha.shape == (0, H) and torch.equal(out, torch.zeros_like(out))
+    gr = pg.pyg_gat_backward(z, ss, sd, H, alpha, g, plan, planT)
+    for k in ("z", "s_src", "s_dst"):
+        assert torch.equal(gr[k], torch.zeros_like(gr[k])), k
+    ei1 = torch.tensor([[3], [7]], device=DEV)
+    plan1 = pg.pyg_plan_build(ei1[1], ei1[0], n, n)
+    planT1 = pg.pyg_plan_build(ei1[0], ei1[1], n, n)
+    out1, a1 = pg.pyg_gat_propagate(z, ss, sd, H, plan1)
+    assert torch.equal(a1, torch.ones_like(a1))
+    assert torch.equal(out1[7], z[3]) and torch.equal(out1[:7], torch.zeros_like(out1[:7]))
+    gr1 = pg.pyg_gat_backward(z, ss, sd, H, a1, g, plan1, planT1)
+    assert torch.equal(gr1["z"][3], g[7])
+    assert gr1["s_src"].abs().max().item() == 0 and gr1["s_dst"].abs().max().item() == 0

@@ -111,3 +111,19 @@ def test_gcn_layer_fused_normalisation(cfg, monkeypatch):
     s_abs = oracle.propagate(np.abs(h), rei, reduce="sum", edge_weight=rw) + np.abs(b)
     err = np.abs(got - ref) - (TF32_RTOL * bound + 1e-5 * s_abs + 1e-6)
     assert (err <= 0).all(), float(err.max())
+
+
+def test_dense_transform_degenerate_shapes():
+    """M = 1 (one row of a 128-row tile), K = 1 (one 32-wide K block, zero-filled), N = 1, and an
+    exactly representable case (small integers: the TF32 products and sums are exact)."""
+    import paper_1903_02428_b200 as pg
+
+    x = torch.zeros((1, 4), device=DEV)
+    x[0, 0] = 3.0
+    w = torch.zeros((1, 4), device=DEV)
+    w[0, 0] = -2.0
+    y = pg.pyg_dense_transform(x[:, :1], w[:, :1], bias=torch.tensor([0.5], device=DEV))
+    assert y.shape == (1, 1) and y.item() == -5.5
+    xi = torch.randint(-4, 5, (300, 40), device=DEV).float()
+    wi = torch.randint(-4, 5, (24, 40), device=DEV).float()
+    assert torch.equal(pg.pyg_dense_transform(xi, wi), (xi.double() @ wi.double().T).float())
