@@ -52,7 +52,7 @@ def _rows(x: torch.Tensor, name: str):
         raise ValueError(f"{name}: expected a float32 CUDA tensor")
     if x.shape[1] > 1 and x.stride(1) != 1:
         raise ValueError(f"{name}: columns must be contiguous")
-    ld = x.stride(0) if x.shape[0] > 1 else x.shape[1]
+    ld = x.stride(0) if x.shape[0] >= 1 else x.shape[1]
     return x.shape[0], x.shape[1], max(ld, x.shape[1])
 
 

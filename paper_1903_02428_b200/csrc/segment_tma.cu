@@ -10,6 +10,7 @@ extern template pyg_status_t launch_nch<PYG_SUM>(int, int, int64_t, int, int, cu
 extern template pyg_status_t launch_nch<PYG_MEAN>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<PYG_MAX>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<kRedSumEpi>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
+extern template pyg_status_t launch_nch<kRedHeadW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 
 // one warp per empty row: out = 0 (float4 stores when aligned), arg = E
 __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
@@ -60,7 +61,8 @@ bool tma_eligible(const SegArgs& a, const pyg_plan* plan) {
     if (mode == 0 || (a.flags & PYG_NO_TMA) || !plan || !plan->parts.empty() || plan->n_tasks <= 0 ||
         !plan->task_pos || !plan->pos_row)
         return false;
-    if (!a.gidx || a.gdeg || a.accum || a.deg_total || a.hw) return false;
+    if (!a.gidx || a.gdeg || a.accum || a.deg_total) return false;
+    if (a.hw && a.hC % 4) return false;  // a float4 chunk must stay inside one head
     if (a.ncols < 64 || a.ncols > 1024) return false;
     // enough tasks to keep every SM's warps streaming (small graphs are launch/latency-bound and
     // faster on the LDG kernel: PubMed-shaped measured 0.046 ms LDG vs 1.16 ms TMA)
@@ -131,6 +133,9 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     t.E_sentinel = a.E_sentinel;
     t.row_scale = a.row_scale;
     t.col_bias = a.col_bias;
+    t.hw = a.hw;
+    t.hH = a.hH;
+    t.hC = a.hC;
     t.blend = a.blend;
     t.ldb = a.ldb;
     t.blend_a = a.blend_a;
@@ -141,8 +146,10 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     const int64_t want = cdiv(t.n_tasks, warps);
     const bool extras = a.row_scale || a.blend || a.col_bias;
     if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: TMA epilogue extras need SUM");
+    if (extras && a.hw) return fail(PYG_ERR_UNSUPPORTED, "internal: TMA epilogue extras with head weights");
     switch (extras ? kRedSumEpi : reduce) {
         case kRedSumEpi: PYG_TRY(launch_nch<kRedSumEpi>(nch, S, want, warps * 32, smem, s, tm, t)); break;
+        case kRedHeadW: PYG_TRY(launch_nch<kRedHeadW>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         case PYG_SUM: PYG_TRY(launch_nch<PYG_SUM>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         case PYG_MEAN: PYG_TRY(launch_nch<PYG_MEAN>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         default: PYG_TRY(launch_nch<PYG_MAX>(nch, S, want, warps * 32, smem, s, tm, t)); break;

@@ -59,6 +59,8 @@ struct Args {
     const float* blend;     // APPNP epilogue (light rows): out = blend_a * v + blend_b * blend[row]
     int64_t ldb;
     float blend_a, blend_b;
+    const float* hw;        // kRedHeadW: alpha [E x hH] by edge id, column c in head c / hC
+    int hH, hC;
     int warp_bytes;         // shared memory per warp
     int data_off;           // offset of stage data inside the warp region
 };
@@ -107,7 +109,8 @@ __device__ __forceinline__ float4 lds128f(uint32_t addr) {
 template <int RED, int NCH, int S>
 __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CUtensorMap tmap, Args a) {
     constexpr bool EPI = RED == kRedSumEpi;        // SUM + row scale / blend / bias epilogue
-    constexpr int RR = EPI ? PYG_SUM : RED;        // the reduction itself
+    constexpr bool HW = RED == kRedHeadW;          // SUM with per-(edge, head) weights (GAT)
+    constexpr int RR = (EPI || HW) ? PYG_SUM : RED; // the reduction itself
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -134,8 +137,11 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
         const int b = c / box_w, cc = c - b * box_w;
         coff[ch] = b < nb ? (uint32_t)(4 * (b * 4 * box_w + cc)) : 0u;
     }
-    const bool need_e = (RR == PYG_MAX) || (a.w != nullptr);
+    const bool need_e = (RR == PYG_MAX) || (a.w != nullptr) || HW;
     const bool weighted = a.w != nullptr;
+    int hch[NCH];  // kRedHeadW: head of each float4 chunk (hC % 4 == 0)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) hch[ch] = HW ? min(4 * (lane + 32 * ch), a.ncols - 1) / a.hC : 0;
     // this plan's positions (slices restrict the root tasks)
     const int64_t plo = __ldg(a.rowptr + a.row_lo), phi = __ldg(a.rowptr + a.row_hi);
     const int64_t twarps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -308,6 +314,7 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
     auto slot = [&](uint32_t st, int i, float sc, int e) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
+            if constexpr (HW) sc = __ldg(a.hw + (int64_t)e * a.hH + hch[ch]);  // alpha of this chunk's head
             const float4 v = lds128f(st + coff[ch] + (uint32_t)i * row_bytes);
             const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll

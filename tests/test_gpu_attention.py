@@ -56,9 +56,15 @@ def _inputs(name):
     return ei, n_src, n_dst, H, C, z, ss, sd, g
 
 
+@pytest.mark.parametrize("tma", ["auto", "1"])
 @pytest.mark.parametrize("name", CASES)
-def test_gat_forward(name):
+def test_gat_forward(name, tma, monkeypatch):
+    """tma = "1" forces the TMA gather4 kernel for the alpha-weighted sum wherever it applies
+    (C % 4 == 0, F >= 64); "auto" lets the library choose (the LDG kernel at these sizes)."""
     import paper_1903_02428_b200 as pg
+
+    if tma == "1":
+        monkeypatch.setenv("PYG_SEG_TMA", "1")
 
     ei, n_src, n_dst, H, C, z, ss, sd, _ = _inputs(name)
     ref, ralpha, ab = oracle.gat(z, ss, sd, ei, H, n_dst=n_dst, with_abs=True)
@@ -72,9 +78,13 @@ def test_gat_forward(name):
     assert torch.equal(out, out2) and torch.equal(alpha, alpha2)
 
 
+@pytest.mark.parametrize("tma", ["auto", "1"])
 @pytest.mark.parametrize("name", CASES)
-def test_gat_backward(name):
+def test_gat_backward(name, tma, monkeypatch):
     import paper_1903_02428_b200 as pg
+
+    if tma == "1":
+        monkeypatch.setenv("PYG_SEG_TMA", "1")
 
     ei, n_src, n_dst, H, C, z, ss, sd, g = _inputs(name)
     eit = _t(ei)
