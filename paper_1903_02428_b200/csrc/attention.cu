@@ -29,7 +29,6 @@ namespace {
 
 constexpr int kMaxHeads = 8;
 constexpr int64_t kShortRow = 16;  // softmax rows up to this length use 8-lane groups
-constexpr int64_t kMidRow = 64;    // ... up to this length 16-lane groups (then a warp)
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -528,23 +527,18 @@ pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const i
     const RowSet rs = row_set(plan);
     const int64_t light = rs.order_len, heavy = rs.h_hi - rs.h_lo;
     // rows of <= kShortRow positions: 8-lane groups (4 rows per warp); longer light rows: a warp
-    RowSet rs_short = rs, rs_mid = rs, rs_long = rs;
+    RowSet rs_short = rs, rs_long = rs;
     rs_short.dhi = kShortRow;
-    rs_mid.dlo = kShortRow;
-    rs_mid.dhi = kMidRow;
-    rs_long.dlo = kMidRow;
+    rs_long.dlo = kShortRow;
     if (s_src) {
         softmax_fwd_kernel<8, true><<<warp_grid(cdiv(light, 4)), 256, 0, s>>>(a, rs_short);
-        softmax_fwd_kernel<16, true><<<warp_grid(cdiv(light, 2)), 256, 0, s>>>(a, rs_mid);
         softmax_fwd_kernel<32, true><<<warp_grid(light), 256, 0, s>>>(a, rs_long);
         if (heavy > 0) { softmax_fwd_kernel<256, true><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
     } else {
         softmax_fwd_kernel<8, false><<<warp_grid(cdiv(light, 4)), 256, 0, s>>>(a, rs_short);
-        softmax_fwd_kernel<16, false><<<warp_grid(cdiv(light, 2)), 256, 0, s>>>(a, rs_mid);
         softmax_fwd_kernel<32, false><<<warp_grid(light), 256, 0, s>>>(a, rs_long);
         if (heavy > 0) { softmax_fwd_kernel<256, false><<<cta_grid(heavy), 256, 0, s>>>(a, rs); PYG_LAUNCHED(); }
     }
-    PYG_LAUNCHED();
     PYG_LAUNCHED();
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
@@ -574,7 +568,6 @@ pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, con
         // short rows (<= kShortRow positions) on 8-lane subgroups when a head's columns tile an
         // 8-lane chunk row (C a power of two <= 32 or a multiple of 32) and F <= 256
         const bool short8 = ((pow2 && C <= 32) || C % 32 == 0) && F <= 256;
-        const bool mid16 = ((pow2 && C <= 64) || C % 64 == 0) && F <= 512;
         RowSet rs_long = rs;
         if (short8) {
             RowSet rs_short = rs;
@@ -589,21 +582,6 @@ pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, con
             else if (n8 <= 2) g8(gat_bwd_coop_kernel<8, 2>);
             else if (n8 <= 4) g8(gat_bwd_coop_kernel<8, 4>);
             else g8(gat_bwd_coop_kernel<8, 8>);
-        }
-        if (short8 && mid16) {
-            RowSet rs_mid = rs;
-            rs_mid.dlo = kShortRow;
-            rs_mid.dhi = kMidRow;
-            rs_long.dlo = kMidRow;
-            const int n16 = (int)cdiv(F, 64);
-            auto g16 = [&](auto k16) {
-                k16<<<warp_grid(cdiv(light, 2)), 256, 0, s>>>(a, rs_mid);
-                PYG_LAUNCHED();
-            };
-            if (n16 <= 1) g16(gat_bwd_coop_kernel<16, 1>);
-            else if (n16 <= 2) g16(gat_bwd_coop_kernel<16, 2>);
-            else if (n16 <= 4) g16(gat_bwd_coop_kernel<16, 4>);
-            else g16(gat_bwd_coop_kernel<16, 8>);
         }
         auto go = [&](auto kl, auto kh) {
             kl<<<warp_grid(light), 256, 0, s>>>(a, rs_long);

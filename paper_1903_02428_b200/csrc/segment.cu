@@ -107,6 +107,19 @@ Geometry choose(const SegArgs& a) {
         Geometry g = geometry(a.ncols, V);
         if (g.util >= best.util - 1e-9 || (V <= 4 && g.util >= 0.75)) best = g;
     }
+    // Few rows with narrow features (e.g. 10,000 rows x 16 columns): one group of LPR lanes per row
+    // leaves most of the GPU idle (4 lanes per row at V = 4 -> 40k threads).  Narrow the vector
+    // while that raises the thread count toward ~148 SMs x 1,024 threads (a row's positions stay
+    // sequential; more lanes per row split its columns finer).
+    const int64_t rows = a.row_order ? a.order_len : a.n_rows;
+    const int64_t want = 148LL * 1024;
+    while (best.V > 1 && rows * best.lpr * best.tiles < want) {
+        const int V2 = best.V / 2;
+        if (!v_ok(a, V2)) break;
+        const Geometry g = geometry(a.ncols, V2);
+        if (g.lpr * g.tiles <= best.lpr * best.tiles) break;  // no more lanes per row to gain
+        best = g;
+    }
     return best;
 }
 

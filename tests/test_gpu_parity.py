@@ -472,3 +472,16 @@ def test_batching_equivalence_on_gpu(pg):
         check_exact(full_out[lo:hi], o)
         a = np.where(a == le.shape[1], ei.shape[1], a + eptr[g])
         check_exact(full_arg[lo:hi], a)
+
+
+def test_suggest_col_block_decisions(pg):
+    """pyg_plan_suggest_col_block (host logic + the device's L2 size): X that fits L2 -> 0 (one
+    pass); Reddit-shaped reuse (E / n = 492, |X| = 566 MB) -> blocks of about 0.4 x L2; R-MAT-shaped
+    low reuse (average degree 20, |X| = 5.1 GB) -> 0, since the extra read+write of out per pass
+    costs more than the DRAM it saves."""
+    l2 = torch.cuda.get_device_properties(0).L2_cache_size
+    assert pg.pyg_plan_suggest_col_block(1_000_000, 10_000, 10_000, 512) == 0  # 5 MB of X
+    cb = pg.pyg_plan_suggest_col_block(114_615_892, 232_965, 232_965, 608 * 4)
+    assert cb > 0
+    assert 0.2 * l2 <= cb * 608 * 4 <= 0.45 * l2
+    assert pg.pyg_plan_suggest_col_block(200_000_000, 10_000_000, 10_000_000, 128 * 4) == 0
