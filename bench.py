@@ -63,9 +63,10 @@ def parse():
     ap.add_argument("--ld", type=int, default=0, help="X row stride (0: padded to a multiple of 8 floats)")
     ap.add_argument("--col-block", default="auto",
                     help="source rows per L2-resident pass: auto (pyg_plan_suggest_col_block), 0 (off) or N")
-    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo"],
+    ap.add_argument("--exchange", default="auto", choices=["auto", "allgather", "halo", "push"],
                     help="N > 1 source exchange: NCCL all-gather of X shards, or halo exchange of only the "
-                         "referenced remote rows (auto: halo when it moves < half the all-gather rows)")
+                         "referenced remote rows (auto: halo when it moves < half the all-gather rows); push: "
+                         "the halo rows stored into the peers' buffers over NVLink by one kernel (CUDA IPC)")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph (auto: on for the launch-bound L2-resident configs)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -459,7 +460,7 @@ def main():
 
     exchange = "none"
     halo = None
-    if world > 1 and plan is not None and col_block == 0 and a.exchange != "allgather":
+    if world > 1 and plan is not None and col_block == 0 and a.exchange not in ("allgather", "push"):
         from paper_1903_02428_b200.dist import halo_setup
 
         hplan, hids = pg.pyg_halo_build(plan, N, lo, hi, per)
@@ -469,7 +470,20 @@ def main():
             send_rows, sc, rc = halo_setup(hids, lo, per, world)
             halo = dict(plan=hplan, n=hids.numel(), send_rows=send_rows, sc=sc, rc=rc,
                         sendbuf=torch.empty((send_rows.numel(), ld), dtype=torch.float32, device=dev))
-    if world > 1 and halo is not None:
+    hpush = None
+    if world > 1 and a.exchange == "push":
+        assert plan is not None and col_block == 0, "--exchange push: segment strategy, unblocked plan"
+        from paper_1903_02428_b200.dist import HaloPush
+
+        hpush = HaloPush(plan, N, lo, hi, per, ld, world, rank)
+        halo = None
+    if hpush is not None:
+        exchange = "push"
+        hpush.shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
+        x_full = hpush.xloc[:, :F]
+        plan = hpush.plans[0]
+        halo = dict(n=hpush.n_halo)
+    elif world > 1 and halo is not None:
         exchange = "halo"
         xbuf = torch.zeros((per + halo["n"], ld), dtype=torch.float32, device=dev)
         shard = xbuf[:per]
@@ -496,9 +510,12 @@ def main():
 
     passes, weighted, prep_ms = 1, False, 0.0
 
+    cur = {"plan": plan}
+
     def compute():
-        pg.pyg_propagate(x_full, None if plan is not None else ei_loc, n_dst=n_loc, reduce=red, plan=plan, out=out,
-                         arg_out=arg, E=E if plan is not None else None, workspace=ws)
+        p = cur["plan"]
+        pg.pyg_propagate(x_full, None if p is not None else ei_loc, n_dst=n_loc, reduce=red, plan=p, out=out,
+                         arg_out=arg, E=E if p is not None else None, workspace=ws)
 
     if a.config == "pubmed" and world == 1:
         # config 2: GCN sym-normalised sum aggregation, forward + backward.  The normalisation
@@ -611,7 +628,9 @@ def main():
             pg.pyg_gcn_layer(x_full, gcn["W"], plan, bias=gcn["b"], out=gcn["out"], workspace=ws_g)
 
     def exchange_step():
-        if exchange == "halo":  # pack the requested rows + one NCCL all-to-all (dist.py)
+        if exchange == "push":  # one kernel stores the requested rows into the peers' X_loc (dist.py)
+            cur["plan"] = hpush.exchange()
+        elif exchange == "halo":  # pack the requested rows + one NCCL all-to-all (dist.py)
             halo_exchange(shard, halo["send_rows"], halo["sc"], halo["rc"], xbuf[per:],
                           pack=lambda xs, rows, o: pg.pyg_gather_rows(xs, rows, out=o), send_buf=halo["sendbuf"])
         elif exchange == "allgather":

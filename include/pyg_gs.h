@@ -177,6 +177,24 @@ pyg_status_t pyg_halo_build(const pyg_plan_t* slice, int64_t n_src, int64_t own_
  * out [n x F] stride ldo, overwritten.  Asynchronous. */
 pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* rows,
                              int64_t n, uint32_t flags, float* out, int64_t ldo, void* stream);
+/* Peer-store halo (the alternative to pack + NCCL all-to-all): the owner stores the rows each
+ * peer requested straight into the peer's X_loc over NVLink (one kernel: gather + transfer).
+ * Peers' buffers are mapped with CUDA IPC (same node):
+ *   pyg_ipc_handle: (host) 64-byte handle of the allocation containing dev_ptr + the byte offset
+ *     of dev_ptr inside it;  pyg_ipc_open: map a peer's (handle, offset) -> dev_ptr (peer access
+ *     enabled lazily);  pyg_ipc_close: unmap (dev_ptr, offset as opened).
+ *   pyg_halo_push: for peer q < n_peers (<= 16): local rows send_rows[send_ptr[q] ..
+ *     send_ptr[q+1]) of x [n_x x F] (stride ldx) are stored to rows dst_row[q] + i of dst[q]
+ *     (stride ldd).  send_ptr [n_peers + 1], dst [n_peers] (device pointers, e.g. from
+ *     pyg_ipc_open) and dst_row [n_peers] are HOST arrays; send_rows is a device array.
+ *     Asynchronous; the caller orders the peers' reads after the pushes (stream sync + a
+ *     process-group barrier). */
+pyg_status_t pyg_ipc_handle(const void* dev_ptr, void* handle, int64_t* offset);
+pyg_status_t pyg_ipc_open(const void* handle, int64_t offset, void** dev_ptr);
+pyg_status_t pyg_ipc_close(void* dev_ptr, int64_t offset);
+pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* send_rows,
+                           const int64_t* send_ptr, void* const* dst, const int64_t* dst_row,
+                           int64_t ldd, int n_peers, void* stream);
 
 /* Scratch needed by pyg_scatter / pyg_propagate / pyg_propagate_backward for
  * an output of F_out columns: fp64-combined partials of split hub rows (plan

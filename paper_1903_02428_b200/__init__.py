@@ -22,7 +22,7 @@ from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, NO_TMA, PHI_CONCAT_XI
 __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
-    "pyg_halo_build", "pyg_gather_rows", "pyg_segment_softmax", "pyg_segment_softmax_backward",
+    "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
     "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
@@ -467,3 +467,35 @@ def pyg_gcn_layer(x: torch.Tensor, weight: torch.Tensor, plan: Plan, bias: Optio
     check(lib.pyg_gcn_layer(_ptr(x), n, K, ldx, _ptr(weight), F_out, ldw, _ptr(bias), plan.handle, _ptr(out), ldo,
                             _ptr(workspace), workspace.numel(), _stream(dev)), "pyg_gcn_layer")
     return out
+
+
+def pyg_ipc_handle(t: torch.Tensor) -> bytes:
+    """72 bytes: the CUDA IPC handle of the allocation holding t (64) + t's byte offset in it (8)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    check(lib.pyg_ipc_handle(_ptr(t), h, ctypes.byref(off)), "pyg_ipc_handle")
+    return h.raw + off.value.to_bytes(8, "little")
+
+
+def pyg_ipc_open(handle: bytes) -> int:
+    """Map a peer's buffer (from pyg_ipc_handle); returns its device address."""
+    p = ctypes.c_void_p()
+    off = int.from_bytes(handle[64:72], "little")
+    check(lib.pyg_ipc_open(ctypes.c_char_p(handle[:64]), off, ctypes.byref(p)), "pyg_ipc_open")
+    return p.value
+
+
+def pyg_ipc_close(ptr: int, handle: bytes):
+    check(lib.pyg_ipc_close(ctypes.c_void_p(ptr), int.from_bytes(handle[64:72], "little")), "pyg_ipc_close")
+
+
+def pyg_halo_push(x: torch.Tensor, send_rows: torch.Tensor, send_ptr, dst_ptrs, dst_rows, ldd: int):
+    """Store x[send_rows[send_ptr[q]:send_ptr[q+1]]] into rows dst_rows[q].. of peer q's buffer dst_ptrs[q]."""
+    n_x, F, ldx = _rows(x, "x")
+    send_rows = _i64(send_rows, "send_rows") if send_rows.numel() else send_rows
+    n = len(dst_ptrs)
+    sp = (ctypes.c_int64 * (n + 1))(*send_ptr)
+    dp = (ctypes.c_void_p * max(n, 1))(*[p or None for p in dst_ptrs])
+    dr = (ctypes.c_int64 * max(n, 1))(*dst_rows)
+    check(lib.pyg_halo_push(_ptr(x), n_x, F, ldx, _ptr(send_rows) if send_rows.numel() else None, sp, dp, dr, ldd, n,
+                            _stream(x.device)), "pyg_halo_push")

@@ -66,6 +66,10 @@ SIGNATURES = {
     "pyg_plan_destroy": ([P], None),
     "pyg_halo_workspace_size": ([P, I64, ctypes.POINTER(SZ)], C),
     "pyg_halo_build": ([P, I64, I64, I64, I64, P, SZ, PP, P, ctypes.POINTER(I64), P], C),
+    "pyg_ipc_handle": ([P, P, ctypes.POINTER(I64)], C),
+    "pyg_ipc_open": ([P, I64, PP], C),
+    "pyg_ipc_close": ([P, I64], C),
+    "pyg_halo_push": ([P, I64, I64, I64, P, P, P, P, I64, C, P], C),
     "pyg_gather_rows": ([P, I64, I64, I64, P, I64, U32, P, I64, P], C),
     "pyg_workspace_size": ([P, I64, I64, C, U32, ctypes.POINTER(SZ)], C),
     "pyg_scatter": ([P, I64, I64, I64, P, I64, C, U32, P, I64, P, P, P, SZ, P], C),

@@ -83,6 +83,11 @@ pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t 
                                   int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
                                   cudaStream_t s);
 pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_t s);
+pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, const int64_t* ptr,
+                            void* const* dst, const int64_t* dst_row, int64_t ldd, int n_peers, cudaStream_t s);
+pyg_status_t ipc_handle_impl(const void* ptr, void* handle, int64_t* offset);
+pyg_status_t ipc_open_impl(const void* handle, int64_t offset, void** ptr);
+pyg_status_t ipc_close_impl(void* ptr, int64_t offset);
 pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, int64_t n, float* out,
                               int64_t ldo, cudaStream_t s);
 
@@ -211,6 +216,35 @@ pyg_status_t pyg_halo_build(const pyg_plan_t* slice, int64_t n_src, int64_t own_
     *halo_plan = nullptr;
     return halo_build_impl(slice, n_src, own_lo, own_hi, own_rows, workspace, bytes, halo_plan, halo_ids, n_halo,
                            as_stream(stream));
+}
+
+pyg_status_t pyg_ipc_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+    REQUIRE(dev_ptr && handle && offset, PYG_ERR_INVALID_ARGUMENT, "ipc_handle: null pointer");
+    return ipc_handle_impl(dev_ptr, handle, offset);
+}
+
+pyg_status_t pyg_ipc_open(const void* handle, int64_t offset, void** dev_ptr) {
+    REQUIRE(handle && dev_ptr && offset >= 0, PYG_ERR_INVALID_ARGUMENT, "ipc_open: bad args");
+    return ipc_open_impl(handle, offset, dev_ptr);
+}
+
+pyg_status_t pyg_ipc_close(void* dev_ptr, int64_t offset) {
+    REQUIRE(dev_ptr && offset >= 0, PYG_ERR_INVALID_ARGUMENT, "ipc_close: bad args");
+    return ipc_close_impl(dev_ptr, offset);
+}
+
+pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* send_rows,
+                           const int64_t* send_ptr, void* const* dst, const int64_t* dst_row, int64_t ldd, int n_peers,
+                           void* stream) {
+    REQUIRE(n_x >= 0 && F >= 0 && n_peers >= 0, PYG_ERR_INVALID_ARGUMENT, "halo_push: negative size");
+    REQUIRE(ldx >= F && ldd >= F, PYG_ERR_DIMENSION, "halo_push: leading dimension < F");
+    REQUIRE(n_peers == 0 || (send_ptr && dst && dst_row), PYG_ERR_INVALID_ARGUMENT, "halo_push: null host array");
+    for (int q = 0; q < n_peers; ++q)
+        REQUIRE(send_ptr[q] <= send_ptr[q + 1] && (send_ptr[q] == send_ptr[q + 1] || dst[q]) && dst_row[q] >= 0,
+                PYG_ERR_INVALID_ARGUMENT, "halo_push: bad peer %d", q);
+    REQUIRE(n_peers == 0 || send_ptr[n_peers] == 0 || (x && send_rows), PYG_ERR_INVALID_ARGUMENT,
+            "halo_push: null x / send_rows");
+    return halo_push_impl(x, ldx, F, send_rows, send_ptr, dst, dst_row, ldd, n_peers, as_stream(stream));
 }
 
 pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* rows, int64_t n,

@@ -178,3 +178,125 @@ pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int6
 }
 
 }  // namespace pyg
+
+// ---- halo push over peer memory (NVLink P2P stores) ------------------------------------------
+// The owner writes the rows each peer asked for straight into the peer's X_loc halo block through
+// a CUDA-IPC mapping of that buffer: the gather of the rows and their transfer are one kernel, with
+// no staging buffer and no NCCL call (the peer-store alternative to pack + all-to-all).
+namespace pyg {
+
+namespace {
+
+constexpr int kMaxPeers = 16;
+
+struct PushArgs {
+    const float* x;
+    int64_t ldx;
+    int F;
+    const int64_t* rows;      // local row ids, grouped by destination peer
+    int n_peers;
+    int64_t ptr[kMaxPeers + 1];   // rows[ptr[q] .. ptr[q+1]) go to peer q
+    float* dst[kMaxPeers];        // peer q's X_loc (mapped)
+    int64_t dst_row[kMaxPeers];   // first halo row of this owner's block at peer q
+    int64_t ldd;
+    int vec;
+};
+
+__global__ void halo_push_kernel(PushArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t total = a.ptr[a.n_peers];
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < total; i += nw) {
+        int q = 0;
+        while (q + 1 < a.n_peers && i >= a.ptr[q + 1]) ++q;  // <= 16 peers
+        const float* src = a.x + a.rows[i] * a.ldx;
+        float* d = a.dst[q] + (a.dst_row[q] + (i - a.ptr[q])) * a.ldd;
+        if (a.vec) {
+            const int nv = a.F >> 2;
+            for (int c = lane; c < nv; c += 32)
+                reinterpret_cast<float4*>(d)[c] = __ldg(reinterpret_cast<const float4*>(src) + c);
+            for (int c = 4 * nv + lane; c < a.F; c += 32) d[c] = __ldg(src + c);
+        } else {
+            for (int c = lane; c < a.F; c += 32) d[c] = __ldg(src + c);
+        }
+    }
+}
+
+}  // namespace
+
+pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, const int64_t* ptr,
+                            void* const* dst, const int64_t* dst_row, int64_t ldd, int n_peers, cudaStream_t s) {
+    if (n_peers > kMaxPeers) return fail(PYG_ERR_UNSUPPORTED, "halo_push: at most %d peers", kMaxPeers);
+    PushArgs a;
+    a.x = x; a.ldx = ldx; a.F = (int)F; a.rows = rows; a.n_peers = n_peers; a.ldd = ldd;
+    bool aligned = (ldx % 4 == 0) && (ldd % 4 == 0) && !(reinterpret_cast<uintptr_t>(x) & 15);
+    for (int q = 0; q <= n_peers; ++q) a.ptr[q] = ptr[q];
+    for (int q = 0; q < n_peers; ++q) {
+        a.dst[q] = static_cast<float*>(dst[q]);
+        a.dst_row[q] = dst_row[q];
+        if (reinterpret_cast<uintptr_t>(dst[q]) & 15) aligned = false;
+    }
+    a.vec = aligned;
+    const int64_t total = ptr[n_peers];
+    if (total <= 0 || F <= 0) return PYG_OK;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 8), 148 * 16));
+    halo_push_kernel<<<blocks, 256, 0, s>>>(a);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+}  // namespace pyg
+
+// ---- CUDA IPC for the peer-store halo ---------------------------------------------------------
+#include <cuda.h>
+
+#include <mutex>
+
+namespace pyg {
+
+namespace {
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+AddrRangeFn addr_range_fn() {
+    static AddrRangeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddrRangeFn>(p);
+    });
+    return fn;
+}
+}  // namespace
+
+pyg_status_t ipc_handle_impl(const void* ptr, void* handle, int64_t* offset) {
+    if (!addr_range_fn()) return fail(PYG_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (addr_range_fn()(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(PYG_ERR_INVALID_ARGUMENT, "ipc_handle: not a device allocation");
+    cudaIpcMemHandle_t h;
+    PYG_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    memcpy(handle, &h, 64);
+    *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(ptr) - base);
+    return PYG_OK;
+}
+
+pyg_status_t ipc_open_impl(const void* handle, int64_t offset, void** ptr) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    void* base = nullptr;
+    PYG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *ptr = static_cast<char*>(base) + offset;
+    return PYG_OK;
+}
+
+pyg_status_t ipc_close_impl(void* ptr, int64_t offset) {
+    PYG_CUDA(cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset));
+    return PYG_OK;
+}
+
+}  // namespace pyg

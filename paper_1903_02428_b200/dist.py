@@ -105,6 +105,68 @@ def halo_exchange(x_shard: torch.Tensor, send_rows: torch.Tensor, send_counts, r
     return recv_out
 
 
+class HaloPush:
+    """Peer-store halo exchange (north_star (3)): each owner writes the rows its peers
+    requested straight into their X_loc buffers over NVLink with one kernel (pyg_halo_push: gather +
+    transfer, no staging buffer, no NCCL), the buffers mapped once with CUDA IPC.  The halo block is
+    double-buffered -- X_loc = [own shard (per rows) ; halo A ; halo B], one halo plan per block --
+    so a step needs a single host barrier: a push of step k+1 can only start after every peer has
+    synchronised step k, whose stream also finished that peer's step k-1 propagate (the last
+    reader of the block being overwritten)."""
+
+    def __init__(self, slice_plan, n: int, lo: int, hi: int, per: int, ld: int, world: int, rank: int, group=None,
+                 dtype=torch.float32):
+        import paper_1903_02428_b200 as pg
+
+        self.pg, self.world, self.rank, self.group, self.per = pg, world, rank, group, per
+        plan_a, ids = pg.pyg_halo_build(slice_plan, n, lo, hi, per)
+        self.n_halo = ids.numel()
+        plan_b, _ = pg.pyg_halo_build(slice_plan, n, lo, hi, per + self.n_halo)
+        self.plans = (plan_a, plan_b)
+        self.send_rows, self.send_counts, recv_counts = halo_setup(ids, lo, per, world, group)
+        dev = ids.device
+        self.xloc = torch.zeros((per + 2 * self.n_halo, ld), dtype=dtype, device=dev)
+        # where my block of rows lands in each peer's halo: per + parity * n_halo_q + (rows q gets
+        # from owners < me); each rank tells every owner its offset (all-to-all) and its n_halo
+        cdev = "cpu" if _staged(group, ids) else dev
+        offs = torch.tensor([per + sum(recv_counts[:o]) for o in range(world)], dtype=torch.int64, device=cdev)
+        got = torch.empty_like(offs)
+        dist.all_to_all_single(got, offs, group=group)
+        nh = [None] * world
+        dist.all_gather_object(nh, self.n_halo, group=group)
+        self.dst_row = [[int(got[q]) + b * int(nh[q]) for q in range(world)] for b in (0, 1)]
+        handles = [None] * world
+        dist.all_gather_object(handles, pg.pyg_ipc_handle(self.xloc), group=group)
+        self.handles = handles
+        self.dst = [0 if (q == rank or self.send_counts[q] == 0) else pg.pyg_ipc_open(handles[q]) for q in range(world)]
+        self.send_ptr = [0]
+        for c in self.send_counts:
+            self.send_ptr.append(self.send_ptr[-1] + c)
+        self.step = 0
+
+    @property
+    def shard(self) -> torch.Tensor:
+        """This rank's X rows (write the shard here)."""
+        return self.xloc[: self.per]
+
+    def exchange(self):
+        """Push this step's halo rows to every peer, then wait for every peer's push into mine.
+        Returns the halo plan to propagate with (X_loc = self.xloc)."""
+        b = self.step & 1
+        self.pg.pyg_halo_push(self.shard, self.send_rows, self.send_ptr, self.dst, self.dst_row[b],
+                              self.xloc.stride(0))
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group)
+        self.step += 1
+        return self.plans[b]
+
+    def close(self):
+        for q, p in enumerate(self.dst):
+            if p:
+                self.pg.pyg_ipc_close(p, self.handles[q])
+        self.dst = [0] * self.world
+
+
 def local_edges(edge_index: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
     """In-edges of targets [lo, hi) with targets renumbered to [0, hi - lo), in ascending edge id
     (the order the max tie rule refers to).  Used by the atomic strategy and the tests."""

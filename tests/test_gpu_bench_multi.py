@@ -23,7 +23,7 @@ def _port():
 
 
 @pytest.mark.parametrize("cfg,exchange,reduce", [("cora", "allgather", "sum"), ("cora", "halo", "max"),
-                                                 ("pubmed", "auto", "mean")])
+                                                 ("pubmed", "auto", "mean"), ("cora", "push", "sum")])
 def test_bench_two_ranks(cfg, exchange, reduce):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
@@ -35,7 +35,7 @@ def test_bench_two_ranks(cfg, exchange, reduce):
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dst-range x2"
-    want = {"allgather": "allgather", "halo": "halo"}.get(exchange)
+    want = {"allgather": "allgather", "halo": "halo", "push": "push"}.get(exchange)
     if want:
         assert d["config"]["exchange"] == want
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] > 0
