@@ -264,12 +264,25 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def traffic_for(workload_key):
+def _profile_lookup(fname, workload_key):
+    """Entry of profiles/<fname> for this workload; the col_block part of the key may differ between
+    boxes (it follows the L2 size), so fall back to the same config / reduce / strategy / N."""
     try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(workload_key)
+        with open(os.path.join(ROOT, "profiles", fname)) as f:
+            d = json.load(f)
     except Exception:
         return None
+    if workload_key in d:
+        return d[workload_key]
+    head, tail = workload_key.split("-cb")[0], workload_key.rsplit("-", 1)[-1]
+    for k, v in d.items():
+        if k.startswith(head + "-cb") and k.endswith("-" + tail):
+            return v
+    return None
+
+
+def traffic_for(workload_key):
+    return _profile_lookup("traffic.json", workload_key)
 
 
 # --------------------------------------------------------------------------- CPU oracle leg
@@ -729,7 +742,8 @@ def main():
             "alg_bytes_per_launch": B / lpc, "launches_per_call": lpc, "kernel_ms_per_launch": kern_ms / lpc,
             "alg_bytes_per_call": B, "call_ms": kern_ms, "traffic_per_call": tr,
             "note": "achieved counts every gathered x_j row (north_star byte model); source-blocked passes serve "
-                    "repeats from L2, so achieved can exceed the HBM copy peak while DRAM traffic stays below it"}
+                    "repeats from L2, so achieved can exceed the HBM copy peak while DRAM traffic stays below it",
+            "ncu": _profile_lookup("ncu_summary.json", wk)}
 
     result = {
         "metric": "aggregation edges*F/s", "value": value, "unit": "edges*F/s", "n_gpus": world,
