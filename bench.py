@@ -274,9 +274,9 @@ def _profile_lookup(fname, workload_key):
         return None
     if workload_key in d:
         return d[workload_key]
-    head, tail = workload_key.split("-cb")[0], workload_key.rsplit("-", 1)[-1]
+    head, tail = workload_key.split("-cb")[0], workload_key.split("-cb", 1)[-1].split("-", 1)[-1]
     for k, v in d.items():
-        if k.startswith(head + "-cb") and k.endswith("-" + tail):
+        if k.startswith(head + "-cb") and k.split("-cb", 1)[-1].split("-", 1)[-1] == tail:
             return v
     return None
 
@@ -732,7 +732,7 @@ def main():
         B = passes * alg_bytes(E_loc if world > 1 else E, n_loc, F, red, a.strategy, weighted=weighted)
     achieved = B / (kern_ms * 1e-3) / 1e9
     lpc = max(1, int(round(launches / a.steps)))  # launches of the propagate call per step
-    wk = f"{a.config}-{red}-{a.strategy}-cb{col_block}-n{world}"
+    wk = f"{a.config}-{red}-{a.strategy}-cb{col_block}-n{world}" + ("" if a.op == "propagate" else f"-{a.op}")
     tr = traffic_for(wk)
     # The dominant kernel is the segment-reduce (or COO) kernel family of one propagate call (one
     # launch per source-blocked pass, plus the split-hub chunk/combine launches).  achieved =

@@ -48,6 +48,8 @@ constexpr int kChunk = 512;            // positions per chunk of a split row
 constexpr int kTaskPositions = 4096;   // light positions per TMA-pipeline task
 constexpr int kRedHeadW = 3;           // internal reduce mode: SUM with per-(edge, head) weights
                                        // hw[eid * hH + c / hC] (GAT alpha-weighted aggregation)
+constexpr int kRedMaxW = 5;            // internal TMA-kernel mode: MAX of weighted messages (the plain
+                                       // PYG_MAX instantiation assumes w == null: no multiply)
 constexpr int kRedSumEpi = 4;          // internal TMA-kernel mode: SUM with the row-scale / blend /
                                        // bias epilogue (a separate instantiation keeps the plain SUM
                                        // kernel at its register count)

@@ -11,6 +11,7 @@ extern template pyg_status_t launch_nch<PYG_MEAN>(int, int, int64_t, int, int, c
 extern template pyg_status_t launch_nch<PYG_MAX>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<kRedSumEpi>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<kRedHeadW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
+extern template pyg_status_t launch_nch<kRedMaxW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 
 // one warp per empty row: out = 0 (float4 stores when aligned), arg = E
 __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
@@ -147,7 +148,9 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     const bool extras = a.row_scale || a.blend || a.col_bias;
     if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: TMA epilogue extras need SUM");
     if (extras && a.hw) return fail(PYG_ERR_UNSUPPORTED, "internal: TMA epilogue extras with head weights");
-    switch (extras ? kRedSumEpi : reduce) {
+    const int mode = extras ? kRedSumEpi : (reduce == PYG_MAX && a.w) ? kRedMaxW : reduce;
+    switch (mode) {
+        case kRedMaxW: PYG_TRY(launch_nch<kRedMaxW>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         case kRedSumEpi: PYG_TRY(launch_nch<kRedSumEpi>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         case kRedHeadW: PYG_TRY(launch_nch<kRedHeadW>(nch, S, want, warps * 32, smem, s, tm, t)); break;
         case PYG_SUM: PYG_TRY(launch_nch<PYG_SUM>(nch, S, want, warps * 32, smem, s, tm, t)); break;

@@ -110,7 +110,8 @@ template <int RED, int NCH, int S>
 __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CUtensorMap tmap, Args a) {
     constexpr bool EPI = RED == kRedSumEpi;        // SUM + row scale / blend / bias epilogue
     constexpr bool HW = RED == kRedHeadW;          // SUM with per-(edge, head) weights (GAT)
-    constexpr int RR = (EPI || HW) ? PYG_SUM : RED; // the reduction itself
+    constexpr bool MAXW = RED == kRedMaxW;         // MAX of weighted messages
+    constexpr int RR = (EPI || HW) ? PYG_SUM : (MAXW ? PYG_MAX : RED);  // the reduction itself
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
         coff[ch] = b < nb ? (uint32_t)(4 * (b * 4 * box_w + cc)) : 0u;
     }
     const bool need_e = (RR == PYG_MAX) || (a.w != nullptr) || HW;
-    const bool weighted = a.w != nullptr;
+    const bool weighted = RED != PYG_MAX && a.w != nullptr;  // PYG_MAX instantiation: unweighted
     int hch[NCH];  // kRedHeadW: head of each float4 chunk (hC % 4 == 0)
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) hch[ch] = HW ? min(4 * (lane + 32 * ch), a.ncols - 1) / a.hC : 0;
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(256) seg_tma_kernel(const __grid_constant__ CU
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (RR == PYG_MAX) {
-                    const float mm = __fmul_rn(sc, vv[q]);
+                    const float mm = RED == PYG_MAX ? vv[q] : __fmul_rn(sc, vv[q]);
                     if (mm > acc[ch][q]) { acc[ch][q] = mm; bi[ch][q] = e; }  // acc starts at -inf (Q5: finite inputs)
                 } else {
                     acc[ch][q] = fmaf(sc, vv[q], acc[ch][q]);
