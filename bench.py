@@ -161,6 +161,21 @@ def make_workload(cfg, dev, ld_arg):
         extra = {"collate_ms": cms, "collate_GBps": cbytes / (cms * 1e-3) / 1e9, "collate_alg_bytes": cbytes,
                  "collate_note": "pyg_collate of 64 graphs (1,048,576 edges, 65,536 nodes), incl. binding overhead"}
         x = torch.from_numpy(x_np).to(dev)
+        # global max pooling readout over the batch (NEXT-3): 65,536 x 64 -> 64 x 64 (+ arg)
+        _, _, node_ptr = pg.pyg_collate(*args)
+        ts = []
+        for _ in range(23):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            pg.pyg_global_pool(x, node_ptr, reduce="max")
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        pms = float(np.median(ts[3:]))
+        pbytes = x.numel() * 4 + G * x.shape[1] * 12 + (G + 1) * 8
+        extra.update({"global_pool_max_ms": pms, "global_pool_GBps": pbytes / (pms * 1e-3) / 1e9,
+                      "global_pool_note": "pyg_global_pool max over 64 graphs x 1,024 nodes x 64 features, incl. "
+                                          "binding overhead"})
         F = x_np.shape[1]
         ld = F
         w = None
