@@ -410,6 +410,18 @@ pyg_status_t pyg_gcn_layer(const float* X, int64_t n, int64_t K, int64_t ldx, co
                            float* out, int64_t ldo, void* workspace, size_t workspace_bytes,
                            void* stream);
 
+/* GAT transform: z = X W^T on the tensor cores (as pyg_dense_transform, TF32) with
+ * the attention projections fused into the epilogue:
+ *   s_src[m][h] = sum_{c < C} z[m][h*C + c] att_src[h*C + c],  s_dst likewise with att_dst
+ * (the split form of S:424's [z_i || z_j] . a; the inputs of pyg_gat_propagate).
+ *   X [M x K] stride ldx; W [H*C x K] stride ldw (alignment as pyg_dense_transform); att_src /
+ *   att_dst [H*C]; Z [M x H*C] stride ldz; s_src / s_dst [M x H] packed.  H <= 8, H*C <= 256.
+ *   The projections use the fp32 z values before they are stored.  Asynchronous. */
+pyg_status_t pyg_gat_transform(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W,
+                               int64_t H, int64_t C, int64_t ldw, const float* att_src,
+                               const float* att_dst, float* Z, int64_t ldz, float* s_src, float* s_dst,
+                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version",
 ]
 
@@ -499,3 +499,19 @@ def pyg_halo_push(x: torch.Tensor, send_rows: torch.Tensor, send_ptr, dst_ptrs, 
     dr = (ctypes.c_int64 * max(n, 1))(*dst_rows)
     check(lib.pyg_halo_push(_ptr(x), n_x, F, ldx, _ptr(send_rows) if send_rows.numel() else None, sp, dp, dr, ldd, n,
                             _stream(x.device)), "pyg_halo_push")
+
+
+def pyg_gat_transform(x: torch.Tensor, weight: torch.Tensor, att_src: torch.Tensor, att_dst: torch.Tensor, H: int):
+    """(z, s_src, s_dst): z = x weight^T on the tensor cores with GAT's per-head attention projections
+    fused into the epilogue.  weight [H*C x K]."""
+    M, K, ldx = _rows(x, "x")
+    N, K2, ldw = _rows(weight, "weight")
+    assert K2 == K and N % H == 0
+    dev = x.device
+    z = torch.empty((M, N), dtype=torch.float32, device=dev)
+    ss = torch.empty((M, H), dtype=torch.float32, device=dev)
+    sd = torch.empty((M, H), dtype=torch.float32, device=dev)
+    check(lib.pyg_gat_transform(_ptr(x), M, K, ldx, _ptr(weight), H, N // H, ldw, _ptr(att_src.contiguous()),
+                                _ptr(att_dst.contiguous()), _ptr(z), N, _ptr(ss), _ptr(sd), _stream(dev)),
+          "pyg_gat_transform")
+    return z, ss, sd

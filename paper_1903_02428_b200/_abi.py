@@ -81,6 +81,7 @@ SIGNATURES = {
     "pyg_gcn_norm": ([P, I64, I64, P, U32, P, P, ctypes.POINTER(I64), P, SZ, P], C),
     "pyg_collate": ([I64, P, P, P, I64, I64, U32, P, P, P, P], C),
     "pyg_global_pool": ([P, I64, I64, I64, P, I64, C, P, I64, P, P], C),
+    "pyg_gat_transform": ([P, I64, I64, I64, P, I64, I64, I64, P, P, P, I64, P, P, P], C),
     "pyg_dense_transform": ([P, I64, I64, I64, P, I64, I64, P, P, P, I64, P], C),
     "pyg_gcn_layer_workspace_size": ([P, I64, I64, ctypes.POINTER(SZ)], C),
     "pyg_gcn_layer": ([P, I64, I64, I64, P, I64, I64, P, P, P, I64, P, SZ, P], C),

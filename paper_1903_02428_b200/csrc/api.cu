@@ -81,7 +81,8 @@ pyg_status_t halo_build_impl(const pyg_plan* p, int64_t n_src, int64_t own_lo, i
                              cudaStream_t s);
 pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W, int64_t N,
                                   int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
-                                  cudaStream_t s);
+                                  cudaStream_t s, const float* att_src = nullptr, const float* att_dst = nullptr,
+                                  float* s_src = nullptr, float* s_dst = nullptr, int heads = 0);
 pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_t s);
 pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, const int64_t* ptr,
                             void* const* dst, const int64_t* dst_row, int64_t ldd, int n_peers, cudaStream_t s);
@@ -778,6 +779,26 @@ pyg_status_t pyg_gcn_layer(const float* X, int64_t n, int64_t K, int64_t ldx, co
     a.heavy_threshold = plan->heavy_threshold; a.allow_pad_read = 1;
     a.row_scale = dinv; a.col_bias = bias;
     return segment_reduce(a, PYG_SUM, plan, sw, sb, s);
+}
+
+// GAT transform: z = X W^T on the tensor cores with the attention projections of every head fused
+// into the epilogue ("z = xW; logit = leaky_relu([z_i || z_j] . a)")
+pyg_status_t pyg_gat_transform(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W, int64_t H,
+                               int64_t C, int64_t ldw, const float* att_src, const float* att_dst, float* Z, int64_t ldz,
+                               float* s_src, float* s_dst, void* stream) {
+    REQUIRE(M >= 0 && K >= 1 && H >= 1 && C >= 1, PYG_ERR_INVALID_ARGUMENT, "gat_transform: bad sizes");
+    const int64_t N = H * C;
+    REQUIRE(H <= kAttnMaxHeads && N <= 256, PYG_ERR_UNSUPPORTED, "gat_transform: H <= %d and H*C <= 256",
+            kAttnMaxHeads);
+    REQUIRE(ldx >= K && ldw >= K && ldz >= N, PYG_ERR_DIMENSION, "gat_transform: leading dimension too small");
+    REQUIRE(M == 0 || (X && W && Z && att_src && att_dst && s_src && s_dst), PYG_ERR_INVALID_ARGUMENT,
+            "gat_transform: null pointer");
+    REQUIRE((reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&
+                (ldx % 4 == 0) && (ldw % 4 == 0),
+            PYG_ERR_ALIGNMENT, "gat_transform: X and W must be 16-byte aligned with ld %% 4 == 0 (TMA)");
+    if (M == 0) return PYG_OK;
+    return dense_transform_impl(X, M, K, ldx, W, N, ldw, nullptr, nullptr, Z, ldz, as_stream(stream), att_src,
+                                att_dst, s_src, s_dst, (int)H);
 }
 
 }  // extern "C"

@@ -87,6 +87,12 @@ struct Args {
     int64_t ldy;
     const float* bias;       // [N] or null
     const float* row_scale;  // [M] or null
+    // GAT attention projections fused into the epilogue: s_src[m][h] = sum_{c in head h} y[m][c] a_src[c]
+    const float* att_src;    // [N] or null
+    const float* att_dst;    // [N] or null
+    float* s_src;            // [M x heads] packed
+    float* s_dst;
+    int heads, hc;           // heads and channels per head (N = heads * hc)
 };
 
 __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_constant__ CUtensorMap map_x,
@@ -172,6 +178,9 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
     const int64_t row = m0 + warp * 32 + lane;
     const float rs = (a.row_scale && row < a.M) ? __ldg(a.row_scale + row) : 1.0f;
     const bool vec = ((a.ldy & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.Y) & 15) == 0);
+    float ps[8], pd[8];  // per-head projections of this thread's row (heads <= 8)
+#pragma unroll
+    for (int h = 0; h < 8; ++h) { ps[h] = 0.0f; pd[h] = 0.0f; }
     for (int c0 = 0; c0 < a.N; c0 += 16) {
         uint32_t v[16];
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
@@ -187,6 +196,17 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
 #pragma unroll
             for (int q = 0; q < 16; ++q)
                 r[q] = __uint_as_float(v[q]) * rs + ((a.bias && c0 + q < a.N) ? __ldg(a.bias + c0 + q) : 0.0f);
+            if (a.att_src) {
+#pragma unroll
+                for (int q = 0; q < 16; ++q) {
+                    if (c0 + q >= a.N) break;
+                    const int hh = (c0 + q) / a.hc;
+                    const float vs = r[q] * __ldg(a.att_src + c0 + q), vd = r[q] * __ldg(a.att_dst + c0 + q);
+#pragma unroll
+                    for (int h = 0; h < 8; ++h)
+                        if (h == hh) { ps[h] += vs; pd[h] += vd; }
+                }
+            }
             float* y = a.Y + row * a.ldy + c0;
             if (vec && c0 + 16 <= a.N) {
 #pragma unroll
@@ -196,6 +216,12 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
                 for (int q = 0; q < 16; ++q)
                     if (c0 + q < a.N) y[q] = r[q];
             }
+        }
+    }
+    if (a.att_src && row < a.M) {
+        for (int h = 0; h < a.heads; ++h) {
+            a.s_src[row * a.heads + h] = ps[h];
+            a.s_dst[row * a.heads + h] = pd[h];
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -244,7 +270,8 @@ pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_
 
 pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W, int64_t N,
                                   int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, const float* att_src, const float* att_dst, float* s_src,
+                                  float* s_dst, int heads) {
     using namespace xform;
     if (M == 0 || N == 0) return PYG_OK;
     if (!encode_fn()) return fail(PYG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -255,6 +282,9 @@ pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t 
     while (a.tmem_cols < a.UN) a.tmem_cols <<= 1;
     a.kb = (int)cdiv(std::max<int64_t>(K, 1), kBK);
     a.Y = Y; a.ldy = ldy; a.bias = bias; a.row_scale = row_scale;
+    a.att_src = att_src; a.att_dst = att_dst; a.s_src = s_src; a.s_dst = s_dst;
+    a.heads = heads > 0 ? heads : 1;
+    a.hc = (int)(N / a.heads);
     const int stage_bytes = kBM * kBK * 4 + a.UN * kBK * 4;
     // ~100 KB of stages per CTA so that two CTAs share an SM: one's epilogue (TMEM -> global)
     // overlaps the other's TMA / MMA main loop (measured: 1 CTA/SM with 6 stages ran at 2.7 TB/s)

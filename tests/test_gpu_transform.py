@@ -127,3 +127,30 @@ def test_dense_transform_degenerate_shapes():
     xi = torch.randint(-4, 5, (300, 40), device=DEV).float()
     wi = torch.randint(-4, 5, (24, 40), device=DEV).float()
     assert torch.equal(pg.pyg_dense_transform(xi, wi), (xi.double() @ wi.double().T).float())
+
+
+@pytest.mark.parametrize("M,K,H,C", [(2708, 1433, 8, 8), (1000, 64, 4, 16), (333, 100, 1, 64), (130, 36, 8, 32)])
+def test_gat_transform_fused_projections(M, K, H, C):
+    """pyg_gat_transform: z = x W^T (TF32 bound, A7) and the per-head attention projections
+    s = z . a fused into the epilogue, against the fp64 oracle transform contracted with a."""
+    import paper_1903_02428_b200 as pg
+
+    rng = np.random.default_rng(M + H)
+    x = rng.standard_normal((M, K)).astype(np.float32)
+    w = (rng.standard_normal((H * C, K)) / np.sqrt(K)).astype(np.float32)
+    a_s = rng.standard_normal(H * C).astype(np.float32)
+    a_d = rng.standard_normal(H * C).astype(np.float32)
+    ref, ab = oracle.dense_transform(x, w, with_abs=True)
+    ldk = (K + 3) // 4 * 4
+    xb = torch.zeros((M, ldk), device=DEV)
+    xb[:, :K] = _t(x)
+    wb = torch.zeros((H * C, ldk), device=DEV)
+    wb[:, :K] = _t(w)
+    z, ss, sd = pg.pyg_gat_transform(xb[:, :K], wb[:, :K], _t(a_s), _t(a_d), H)
+    check_close(z.cpu().numpy(), ref, abs_sum=ab, rtol=TF32_RTOL, what="z")
+    z64 = ref.astype(np.float64).reshape(M, H, C)
+    for got, a in ((ss, a_s), (sd, a_d)):
+        a64 = a.astype(np.float64).reshape(H, C)
+        want = (z64 * a64).sum(-1)
+        bound = TF32_RTOL * (ab.reshape(M, H, C) * np.abs(a64)).sum(-1) + 1e-5 * np.abs(z64 * a64).sum(-1) + 1e-6
+        assert (np.abs(got.cpu().numpy() - want) <= bound).all()
