@@ -89,6 +89,8 @@ pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_
 pyg_status_t ipc_handle_impl(const void* ptr, void* handle, int64_t* offset);
 pyg_status_t ipc_open_impl(const void* handle, int64_t offset, void** ptr);
 pyg_status_t ipc_close_impl(void* ptr, int64_t offset);
+pyg_status_t global_pool_impl(const float* x, int64_t ldx, int F, const int64_t* node_ptr, int64_t G, int reduce,
+                              float* out, int64_t ldo, int64_t* arg, int64_t N, cudaStream_t s);
 pyg_status_t gather_rows_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, int64_t n, float* out,
                               int64_t ldo, cudaStream_t s);
 
@@ -547,13 +549,7 @@ pyg_status_t pyg_global_pool(const float* x, int64_t N, int64_t F, int64_t ldx, 
     REQUIRE(G * F == 0 || (out && node_ptr), PYG_ERR_INVALID_ARGUMENT, "global_pool: null pointer");
     REQUIRE(reduce != PYG_MAX || G * F == 0 || arg_out, PYG_ERR_INVALID_ARGUMENT, "global_pool: max needs arg_out");
     if (G == 0 || F == 0) return PYG_OK;
-    SegArgs a;
-    a.X = x; a.ldx = ldx; a.ncols = (int)F;
-    a.rowptr = node_ptr;
-    a.out = out; a.ldo = ldo; a.arg = arg_out; a.lda = ldo;
-    a.n_rows = G; a.E_sentinel = N;
-    a.heavy_threshold = INT64_MAX;
-    return segment_reduce(a, reduce, nullptr, nullptr, 0, as_stream(stream));
+    return global_pool_impl(x, ldx, (int)F, node_ptr, G, reduce, out, ldo, arg_out, N, as_stream(stream));
 }
 
 // ---- NEXT-1: segment softmax + GAT attention aggregation (attention.cu) ----------

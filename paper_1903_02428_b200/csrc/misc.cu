@@ -369,3 +369,119 @@ pyg_status_t collate_impl(int64_t G, const int64_t* num_nodes, const int64_t* ed
 }
 
 }  // namespace pyg
+
+// ---- global pooling readout (NEXT-3) -----------------------------------------------
+// out[g] = BOX over the contiguous node segment [node_ptr[g], node_ptr[g+1]) of x.  The readout
+// has few, long segments (64 point clouds x 1,024 nodes): a thread-block CLUSTER of 8 CTAs shares
+// each segment, every CTA reducing one eighth of its rows (256 threads = 4 row stripes x 64
+// columns), and the cluster's rank-0 CTA combines the 8 partials through distributed shared memory
+// in rank order (fp64 for sum/mean; strict > for max, so ties keep the lowest node id).  One kernel,
+// no workspace, deterministic.
+#include <cooperative_groups.h>
+
+namespace pyg {
+namespace {
+
+namespace cg = cooperative_groups;
+constexpr int kPoolCluster = 8;
+constexpr int kPoolCols = 64;      // columns per column tile (threads per row stripe)
+constexpr int kPoolStripes = 4;    // row stripes per CTA
+
+template <int RED>
+__global__ void __cluster_dims__(1, kPoolCluster, 1) __launch_bounds__(256)
+    pool_kernel(const float* __restrict__ x, int64_t ldx, int F, const int64_t* __restrict__ node_ptr,
+                float* out, int64_t ldo, int64_t* arg, int64_t N) {
+    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ double s_part[kPoolCols];   // this CTA's partial of the current column tile
+    __shared__ float s_val[kPoolStripes][kPoolCols];
+    __shared__ int64_t s_arg[kPoolStripes][kPoolCols];
+    __shared__ int64_t s_parg[kPoolCols];
+    const int g = blockIdx.x;
+    const int rank = (int)cluster.block_rank();
+    const int col_in = threadIdx.x % kPoolCols, stripe = threadIdx.x / kPoolCols;
+    const int64_t b = node_ptr[g], e = node_ptr[g + 1];
+    const int64_t len = e - b, chunk = (len + kPoolCluster - 1) / kPoolCluster;
+    const int64_t cb = b + min(len, (int64_t)rank * chunk), ce = b + min(len, (int64_t)(rank + 1) * chunk);
+    for (int c0 = 0; c0 < F; c0 += kPoolCols) {
+        const int c = c0 + col_in;
+        // 1. stripe partial over this CTA's rows
+        float acc = RED == PYG_MAX ? -INFINITY : 0.0f;
+        int64_t best = -1;
+        if (c < F) {
+            for (int64_t r = cb + stripe; r < ce; r += kPoolStripes) {
+                const float v = __ldg(x + r * ldx + c);
+                if (RED == PYG_MAX) {
+                    if (v > acc) { acc = v; best = r; }  // rows ascend: strict > keeps the lowest id (Q4)
+                } else {
+                    acc += v;
+                }
+            }
+        }
+        s_val[stripe][col_in] = acc;
+        s_arg[stripe][col_in] = best;
+        __syncthreads();
+        // 2. the CTA partial (stripes combined in order)
+        if (stripe == 0) {
+            if (RED == PYG_MAX) {
+                float bv = s_val[0][col_in];
+                int64_t ba = s_arg[0][col_in];
+                for (int q = 1; q < kPoolStripes; ++q) {
+                    const float v = s_val[q][col_in];
+                    const int64_t av = s_arg[q][col_in];
+                    if (av >= 0 && (ba < 0 || v > bv || (v == bv && av < ba))) { bv = v; ba = av; }
+                }
+                s_part[col_in] = bv;
+                s_parg[col_in] = ba;
+            } else {
+                double t = 0.0;
+                for (int q = 0; q < kPoolStripes; ++q) t += (double)s_val[q][col_in];
+                s_part[col_in] = t;
+            }
+        }
+        cluster.sync();  // every CTA's partial of this tile is visible cluster-wide
+        // 3. rank 0 combines the cluster's partials in rank order (distributed shared memory)
+        if (rank == 0 && stripe == 0 && c < F) {
+            double t = 0.0, bv = 0.0;
+            int64_t ba = -1;
+            for (int q = 0; q < kPoolCluster; ++q) {
+                const double v = *cluster.map_shared_rank(&s_part[col_in], q);
+                if (RED == PYG_MAX) {
+                    const int64_t av = *cluster.map_shared_rank(&s_parg[col_in], q);
+                    if (av >= 0 && (ba < 0 || v > bv || (v == bv && av < ba))) { bv = v; ba = av; }
+                } else {
+                    t += v;
+                }
+            }
+            float r;
+            if (RED == PYG_MAX) {
+                r = ba >= 0 ? (float)bv : 0.0f;
+                arg[(int64_t)g * ldo + c] = ba >= 0 ? ba : N;
+            } else if (RED == PYG_MEAN) {
+                r = len > 0 ? (float)(t / (double)len) : 0.0f;
+            } else {
+                r = (float)t;
+            }
+            out[(int64_t)g * ldo + c] = r;
+        }
+        cluster.sync();  // rank 0 is done reading before the partials are overwritten / CTAs exit
+    }
+}
+
+}  // namespace
+
+pyg_status_t global_pool_impl(const float* x, int64_t ldx, int F, const int64_t* node_ptr, int64_t G, int reduce,
+                              float* out, int64_t ldo, int64_t* arg, int64_t N, cudaStream_t s) {
+    if (G <= 0 || F <= 0) return PYG_OK;
+    if (G > 0x7fffffff) return fail(PYG_ERR_UNSUPPORTED, "global_pool: too many graphs");
+    const dim3 grid((unsigned)G, kPoolCluster);
+    switch (reduce) {
+        case PYG_SUM: pool_kernel<PYG_SUM><<<grid, 256, 0, s>>>(x, ldx, F, node_ptr, out, ldo, arg, N); break;
+        case PYG_MEAN: pool_kernel<PYG_MEAN><<<grid, 256, 0, s>>>(x, ldx, F, node_ptr, out, ldo, arg, N); break;
+        default: pool_kernel<PYG_MAX><<<grid, 256, 0, s>>>(x, ldx, F, node_ptr, out, ldo, arg, N); break;
+    }
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+}  // namespace pyg

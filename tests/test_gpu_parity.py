@@ -485,3 +485,25 @@ def test_suggest_col_block_decisions(pg):
     assert cb > 0
     assert 0.2 * l2 <= cb * 608 * 4 <= 0.45 * l2
     assert pg.pyg_plan_suggest_col_block(200_000_000, 10_000_000, 10_000_000, 128 * 4) == 0
+
+
+@pytest.mark.parametrize("sizes,F", [([1024] * 64, 64), ([0, 100_003, 7, 0, 2048], 19), ([3, 1, 0, 9], 300)])
+def test_global_pool_long_segments(pg, sizes, F):
+    """The readout with few long segments (the point-cloud batch: 64 x 1,024) and ragged / empty
+    ones: one 8-CTA cluster per segment, partials combined through distributed shared memory in
+    rank order.  max: exact value and lowest node id on ties (tie-heavy integer data)."""
+    nn = np.array(sizes, np.int64)
+    N = int(nn.sum())
+    rng = np.random.default_rng(len(sizes) + F)
+    x = synth.features(N, F, 5, signed=True)
+    xt = rng.integers(-3, 4, (N, F)).astype(np.float32)
+    node_ptr = np.concatenate([[0], np.cumsum(nn)])
+    batch = np.repeat(np.arange(nn.size), nn)
+    for red, xx in (("sum", x), ("mean", x), ("max", xt)):
+        ref = oracle.global_pool(xx, batch, nn.size, red)
+        got = pg.pyg_global_pool(T(xx), T(node_ptr), red)
+        if red == "max":
+            check_exact(H(got[0]), ref[0])
+            check_exact(H(got[1]), ref[1])
+        else:
+            check_close(H(got), ref, abs_sum=oracle.global_pool(np.abs(xx), batch, nn.size, red))
