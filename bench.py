@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo stages the exchange through host memory: only for exercising the N > 1 path "
                          "with several ranks on one GPU (tests); nccl is the measured backend")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="N > 1 with a source-blocked plan: one all-gather, then the propagate (no per-owner overlap)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -463,20 +465,28 @@ def main():
     # dst-range partition (N > 1): rank owns targets [lo, hi) and their in-edges; X is sharded by
     # the same ranges and all-gathered every step (NCCL over NVLink).
     ranges, per = partition_rows(N, world)
-    lo, hi = ranges[rank]
-    n_loc = hi - lo
 
     t0 = time.perf_counter()
     plan_full = None
     col_block = 0
+    overlap = False
     if a.strategy == "segment":
         if a.col_block == "auto":
             col_block = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4)
         else:
             col_block = int(a.col_block)
+        if world > 1 and col_block > 0 and not a.no_overlap and a.exchange in ("auto", "allgather"):
+            # source blocks aligned with the shards: block b's rows come from one owner, so its pass can
+            # run as soon as that owner's broadcast has landed (dist.OverlappedGather)
+            from paper_1903_02428_b200.dist import aligned_partition
+
+            ranges, per, col_block = aligned_partition(N, world, col_block)
+            overlap = True
         plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=col_block)
         torch.cuda.synchronize()
     plan_ms = (time.perf_counter() - t0) * 1e3
+    lo, hi = ranges[rank]
+    n_loc = hi - lo
     plan = plan_full.slice(lo, hi) if (plan_full is not None and world > 1) else plan_full
     if a.strategy == "atomic" and world > 1:
         m = (ei[1] >= lo) & (ei[1] < hi)
@@ -484,7 +494,8 @@ def main():
         ei_loc[1] -= lo
     else:
         ei_loc = ei
-    E_loc = int(plan.export()[0][-1].item()) if (plan is not None and world > 1) else ei_loc.shape[1]
+    # edges owned by this rank (byte accounting only; source-blocked plans have no single CSR to export)
+    E_loc = int(((ei[1] >= lo) & (ei[1] < hi)).sum().item()) if world > 1 else ei_loc.shape[1]
 
     exchange = "none"
     halo = None
@@ -518,6 +529,15 @@ def main():
         shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
         x_full = xbuf[:, :F]
         plan = halo["plan"]
+    elif world > 1 and overlap:
+        from paper_1903_02428_b200.dist import OverlappedGather
+
+        exchange = "allgather-overlap"
+        xbuf = torch.zeros((per * world, ld), dtype=torch.float32, device=dev)
+        ovg = OverlappedGather(plan, xbuf, per, col_block, world, rank)
+        shard = ovg.shard(rank)
+        shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
+        x_full = xbuf[:N, :F]
     elif world > 1:
         exchange = "allgather"
         xbuf = torch.zeros((per * world, ld), dtype=torch.float32, device=dev)
@@ -540,10 +560,15 @@ def main():
 
     cur = {"plan": plan}
 
-    def compute():
-        p = cur["plan"]
+    def one(p):
         pg.pyg_propagate(x_full, None if p is not None else ei_loc, n_dst=n_loc, reduce=red, plan=p, out=out,
                          arg_out=arg, E=E if p is not None else None, workspace=ws)
+
+    def compute():
+        if exchange == "allgather-overlap":  # the broadcasts and the per-owner passes interleave
+            ovg.step(one)
+        else:
+            one(cur["plan"])
 
     if a.config == "pubmed" and world == 1:
         # config 2: GCN sym-normalised sum aggregation, forward + backward.  The normalisation

@@ -139,6 +139,14 @@ pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_col
  * slice is global row row_lo + r; arg outputs stay GLOBAL edge ids. */
 pyg_status_t pyg_plan_slice(const pyg_plan_t* plan, int64_t row_lo, int64_t row_hi,
                             pyg_plan_t** slice);
+/* Pass view of a SOURCE-BLOCKED plan (or a slice of one): the source blocks [pass_lo, pass_hi)
+ * only.  Calls made with the views of consecutive block ranges, in order and on one stream, give
+ * exactly the result of one call with the whole plan (the root's first block writes `out`, later
+ * blocks accumulate, its last block finalizes) -- so a multi-GPU step can run block b as soon as
+ * the X rows of block b have arrived (compute / communication overlap).  Zero-copy; the parent
+ * must outlive the view.  CONCAT_XI is not supported with views. */
+pyg_status_t pyg_plan_passes(const pyg_plan_t* plan, int64_t pass_lo, int64_t pass_hi,
+                             pyg_plan_t** view);
 pyg_status_t pyg_plan_view(const pyg_plan_t* plan, pyg_plan_view_t* view);
 /* Copy a plan's CSR arrays into caller device buffers (any may be NULL):
  * rowptr [n_rows + 1] int64 (positions relative to the plan's first row),

@@ -88,6 +88,12 @@ class Plan:
         check(lib.pyg_plan_slice(self._h, lo, hi, ctypes.byref(h)), "pyg_plan_slice")
         return Plan(h, None, parent=self)
 
+    def passes(self, lo: int, hi: int) -> "Plan":
+        """View of the source blocks [lo, hi) of a source-blocked plan (pyg_plan_passes)."""
+        h = ctypes.c_void_p()
+        check(lib.pyg_plan_passes(self._h, lo, hi, ctypes.byref(h)), "pyg_plan_passes")
+        return Plan(h, None, parent=self)
+
     def export(self):
         """(rowptr, col or None, perm) as int64 CUDA tensors (test helper)."""
         v = self.view()

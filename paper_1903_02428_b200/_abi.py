@@ -61,6 +61,7 @@ SIGNATURES = {
     "pyg_plan_build": ([P, P, I64, I64, I64, I64, U32, P, SZ, PP, P], C),
     "pyg_plan_suggest_col_block": ([I64, I64, I64, I64, ctypes.POINTER(I64)], C),
     "pyg_plan_slice": ([P, I64, I64, PP], C),
+    "pyg_plan_passes": ([P, I64, I64, PP], C),
     "pyg_plan_view": ([P, ctypes.POINTER(PlanView)], C),
     "pyg_plan_export": ([P, P, P, P, P], C),
     "pyg_plan_destroy": ([P], None),

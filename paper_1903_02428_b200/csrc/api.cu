@@ -69,6 +69,7 @@ pyg_status_t plan_workspace(int64_t E, int64_t n_rows, int64_t n_cols, int64_t c
 pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, int64_t n_rows, int64_t n_cols,
                              int64_t col_block, void* ws, size_t bytes, pyg_plan** out, cudaStream_t s);
 pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out);
+pyg_status_t plan_passes_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out);
 pyg_status_t plan_export_impl(const pyg_plan* p, int64_t* rowptr, int64_t* col, int64_t* perm, cudaStream_t s);
 pyg_status_t gcn_norm_impl(const int64_t* ei, int64_t E, int64_t N, const float* w, int64_t* eo, float* wo,
                            int64_t* E_out, void* ws, size_t bytes, cudaStream_t s, size_t* need);
@@ -174,6 +175,15 @@ pyg_status_t pyg_plan_slice(const pyg_plan_t* plan, int64_t lo, int64_t hi, pyg_
     REQUIRE(0 <= lo && lo <= hi && hi <= plan->n_rows, PYG_ERR_DIMENSION, "plan_slice: rows [%lld, %lld) outside [0, %lld)",
             (long long)lo, (long long)hi, (long long)plan->n_rows);
     return plan_slice_impl(plan, lo, hi, slice);
+}
+
+pyg_status_t pyg_plan_passes(const pyg_plan_t* plan, int64_t pass_lo, int64_t pass_hi, pyg_plan_t** view) {
+    REQUIRE(plan && view, PYG_ERR_INVALID_ARGUMENT, "plan_passes: null");
+    REQUIRE(!plan->parts.empty(), PYG_ERR_UNSUPPORTED, "plan_passes: needs a source-blocked plan (col_block > 0)");
+    REQUIRE(0 <= pass_lo && pass_lo < pass_hi && pass_hi <= (int64_t)plan->parts.size(), PYG_ERR_DIMENSION,
+            "plan_passes: passes [%lld, %lld) outside [0, %lld)", (long long)pass_lo, (long long)pass_hi,
+            (long long)plan->parts.size());
+    return plan_passes_impl(plan, pass_lo, pass_hi, view);
 }
 
 pyg_status_t pyg_plan_view(const pyg_plan_t* p, pyg_plan_view_t* v) {
@@ -379,6 +389,7 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
         if (cat && !plan->parts.empty()) {
             REQUIRE(reduce != PYG_MAX, PYG_ERR_UNSUPPORTED, "propagate: CONCAT_XI + MAX needs an unblocked plan");
+            REQUIRE(plan->n_passes == 0, PYG_ERR_UNSUPPORTED, "propagate: CONCAT_XI needs the whole plan, not a pass view");
             PYG_TRY(xi_block(xd, ldd, (int)F, n_dst, nullptr, nullptr, plan->deg, nullptr, reduce, out, ldo, arg_out,
                              ldo, E, s));
         } else if (cat) {

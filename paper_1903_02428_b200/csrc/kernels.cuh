@@ -37,6 +37,8 @@ struct pyg_plan {
     int64_t n_light_tasks = 0;          // tasks [0, n_light_tasks) are light rows, the rest hub chunks
     int64_t empty_begin = 0, n_empty = 0;
     int64_t col_block = 0;            // source rows per block (0 = not blocked)
+    int64_t pass_base = 0;            // pass views: global index of parts[0] among the source blocks
+    int64_t n_passes = 0;             // total source blocks of the root plan (0: parts.size())
     const int32_t* deg = nullptr;     // [n_rows] total in-degree (blocked plans), offset like rowptr
     std::vector<pyg_plan> parts;
 };

@@ -400,6 +400,8 @@ pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan
         q->heavy_threshold = p->heavy_threshold;
         q->chunk = p->chunk;
         q->col_block = p->col_block;
+        q->pass_base = p->pass_base;
+        q->n_passes = p->n_passes;
         q->deg = p->deg + lo;
         for (const auto& part : p->parts) {
             pyg_plan* sub = nullptr;
@@ -428,6 +430,23 @@ pyg_status_t plan_slice_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan
     q->h_hi = std::max(a, b);
     q->item_lo = p->h_heavy_item_ptr[(size_t)q->h_lo];
     q->item_hi = p->h_heavy_item_ptr[(size_t)q->h_hi];
+    *out = q;
+    return PYG_OK;
+}
+
+// Pass view: the source blocks [lo, hi) of a source-blocked plan (or of a slice of one); calls made
+// with the views of consecutive ranges, in order, equal one call with the whole plan.
+pyg_status_t plan_passes_impl(const pyg_plan* p, int64_t lo, int64_t hi, pyg_plan** out) {
+    pyg_plan* q = new pyg_plan(*p);
+    q->parts.assign(p->parts.begin() + lo, p->parts.begin() + hi);
+    q->n_passes = p->n_passes > 0 ? p->n_passes : (int64_t)p->parts.size();
+    q->pass_base = p->pass_base + lo;
+    q->rowptr = q->parts.empty() ? p->rowptr : q->parts[0].rowptr;
+    q->item_lo = q->item_hi = q->h_lo = q->h_hi = 0;
+    for (const auto& r : q->parts) {
+        q->item_hi += r.item_hi - r.item_lo;
+        q->h_hi += r.h_hi - r.h_lo;
+    }
     *out = q;
     return PYG_OK;
 }

@@ -215,13 +215,17 @@ size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce) {
 pyg_status_t segment_reduce(const SegArgs& a0, int reduce, const pyg_plan* plan, void* ws, size_t ws_bytes,
                             cudaStream_t s) {
     if (!plan || plan->parts.empty()) return segment_reduce_one(a0, reduce, plan, ws, ws_bytes, s);
+    // a pass view (pyg_plan_passes) holds a consecutive range of the root's source blocks: the first
+    // block of the root writes, later ones accumulate, the root's last one finalizes
     const size_t nb = plan->parts.size();
+    const int64_t total = plan->n_passes > 0 ? plan->n_passes : (int64_t)nb;
     for (size_t b = 0; b < nb; ++b) {
         SegArgs a = a0;
         const pyg_plan& p = plan->parts[b];
+        const int64_t gb = plan->pass_base + (int64_t)b;
         a.rowptr = p.rowptr;
-        a.accum = b > 0;
-        a.finalize = (b + 1 == nb);
+        a.accum = gb > 0;
+        a.finalize = (gb + 1 == total);
         a.deg_total = plan->deg;
         a.heavy_threshold = p.heavy_threshold;
         PYG_TRY(segment_reduce_one(a, reduce, &p, ws, ws_bytes, s));

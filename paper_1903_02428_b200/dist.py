@@ -34,6 +34,52 @@ def partition_rows(n: int, world: int):
     return [(min(r * per, n), min((r + 1) * per, n)) for r in range(world)], per
 
 
+def aligned_partition(n: int, world: int, block_rows: int):
+    """dst ranges whose boundaries are source-block boundaries: per = k * cb with cb <= block_rows,
+    so every source block of a plan built with col_block = cb lies inside one rank's shard.
+    Returns (ranges, per, cb)."""
+    per0 = (n + world - 1) // world if world > 0 else 0
+    k = max(1, -(-per0 // max(1, block_rows)))
+    cb = max(1, -(-per0 // k))
+    per = k * cb
+    return [(min(q * per, n), min((q + 1) * per, n)) for q in range(world)], per, cb
+
+
+class OverlappedGather:
+    """The all-gather of the X shards as one broadcast per owner, overlapped with the source-blocked
+    propagate (SURVEY 8(e) "Overlap"): the plan's source blocks are aligned with the shards
+    (aligned_partition), all P broadcasts are issued at once on NCCL's stream, and the compute stream
+    runs owner q's blocks (a pass view) as soon as owner q's rows have landed -- in ascending block
+    order, so the result is bitwise the one-GPU result.  Only the first shard's transfer is exposed."""
+
+    def __init__(self, plan_slice, xbuf: torch.Tensor, per: int, cb: int, world: int, rank: int, group=None):
+        self.xbuf, self.per, self.world, self.rank, self.group = xbuf, per, world, rank, group
+        nb = plan_slice.view()["n_col_blocks"]
+        k = per // cb
+        self.views = [plan_slice.passes(q * k, min((q + 1) * k, nb)) if q * k < nb else None for q in range(world)]
+
+    def shard(self, q: int) -> torch.Tensor:
+        return self.xbuf[q * self.per: (q + 1) * self.per]
+
+    def step(self, compute):
+        """compute(view) runs one pass view of the plan on the current stream."""
+        if _staged(self.group, self.xbuf):  # gloo test mode: synchronous host-staged broadcasts
+            for q in range(self.world):
+                h = self.shard(q).cpu()
+                dist.broadcast(h, src=q, group=self.group)
+                self.shard(q).copy_(h)
+            for v in self.views:
+                if v is not None:
+                    compute(v)
+            return
+        works = [dist.broadcast(self.shard(q), src=q, group=self.group, async_op=True) for q in range(self.world)]
+        for q, v in enumerate(self.views):
+            if q != self.rank:
+                works[q].wait()  # the compute stream waits for owner q's rows (host not blocked)
+            if v is not None:
+                compute(v)
+
+
 def gather_x(x_shard: torch.Tensor, world: int, group=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """All-gather equal row shards [per, ld] into [per * world, ld] (rank order = row order)."""
     per = x_shard.shape[0]

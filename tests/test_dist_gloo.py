@@ -192,3 +192,12 @@ def test_halo_exchange_equals_single_process(N):
             assert np.array_equal(res["outs"][red], full[red][lo:hi]), red
         assert np.array_equal(res["outs"]["max"][0], full["max"][0][lo:hi])
         assert np.array_equal(res["outs"]["max"][1], full["max"][1][lo:hi])
+
+
+def test_aligned_partition():
+    from paper_1903_02428_b200.dist import aligned_partition
+
+    for n, w, b in ((232965, 8, 21179), (10, 3, 2), (6001, 2, 1100), (5, 8, 100)):
+        ranges, per, cb = aligned_partition(n, w, b)
+        assert per % cb == 0 and cb <= max(b, 1) and per * w >= n
+        assert ranges[0][0] == 0 and ranges[-1][1] == n

@@ -22,13 +22,16 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("cfg,exchange,reduce", [("cora", "allgather", "sum"), ("cora", "halo", "max"),
-                                                 ("pubmed", "auto", "mean"), ("cora", "push", "sum")])
-def test_bench_two_ranks(cfg, exchange, reduce):
+@pytest.mark.parametrize("cfg,exchange,reduce,extra", [
+    ("cora", "allgather", "sum", []), ("cora", "halo", "max", []), ("pubmed", "auto", "mean", []),
+    ("cora", "push", "sum", []),
+    # source-blocked plan: shard-aligned blocks, per-owner broadcasts overlapped with the block passes
+    ("cora", "auto", "max", ["--col-block", "500"]), ("pubmed", "allgather", "sum", ["--col-block", "3000"])])
+def test_bench_two_ranks(cfg, exchange, reduce, extra):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "2",
            "--config", cfg, "--reduce", reduce, "--steps", "3", "--warmup", "3", "--dist-backend", "gloo",
-           "--exchange", exchange]
+           "--exchange", exchange] + extra
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
@@ -36,6 +39,8 @@ def test_bench_two_ranks(cfg, exchange, reduce):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "dst-range x2"
     want = {"allgather": "allgather", "halo": "halo", "push": "push"}.get(exchange)
+    if extra:
+        want = "allgather-overlap"
     if want:
         assert d["config"]["exchange"] == want
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] > 0

@@ -507,3 +507,29 @@ def test_global_pool_long_segments(pg, sizes, F):
             check_exact(H(got[1]), ref[1])
         else:
             check_close(H(got), ref, abs_sum=oracle.global_pool(np.abs(xx), batch, nn.size, red))
+
+
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_plan_pass_views_equal_whole_plan(pg, red):
+    """pyg_plan_passes: running the source blocks of a blocked plan as consecutive views (in order,
+    one stream; what the multi-GPU overlap does as each block's rows arrive) equals one call with the
+    whole plan bitwise -- also for a slice of it."""
+    rng = np.random.default_rng(3)
+    n_src, n_dst, F, E = 4000, 900, 24, 50000
+    ei = np.stack([rng.integers(0, n_src, E), rng.integers(0, n_dst, E)]).astype(np.int64)
+    x = rng.integers(-3, 4, (n_src, F)).astype(np.float32) if red == "max" else synth.features(n_src, F, 2)
+    tei = T(ei)
+    plan = pg.pyg_plan_build(tei[1], tei[0], n_dst, n_src, col_block=700)
+    nb = plan.view()["n_col_blocks"]
+    assert nb == 6
+    for p, n, lo in ((plan, n_dst, 0), (plan.slice(100, 700), 600, 100)):
+        whole = pg.pyg_propagate(T(x), None, n_dst=n, reduce=red, plan=p, E=E)
+        out = torch.empty((n, F), device="cuda")
+        arg = torch.empty((n, F), dtype=torch.int64, device="cuda") if red == "max" else None
+        for b0, b1 in ((0, 2), (2, 3), (3, 6)):
+            pg.pyg_propagate(T(x), None, n_dst=n, reduce=red, plan=p.passes(b0, b1), E=E, out=out, arg_out=arg)
+        if red == "max":
+            check_exact(H(out), H(whole[0]))
+            check_exact(H(arg), H(whole[1]))
+        else:
+            check_exact(H(out), H(whole))
