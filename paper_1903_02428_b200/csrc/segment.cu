@@ -152,14 +152,16 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     Carver cv(ws, ws_bytes);
     unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
     const bool extras = a.row_scale || a.blend || a.col_bias;
-    const bool tma = ws && cv.ok() && tma_eligible(a, plan) && !(extras && reduce != PYG_SUM);
+    if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: epilogue extras need SUM");
+    const int red_k = extras ? kRedSumEpi : reduce;  // LDG / combine instantiation
+    const bool tma = ws && cv.ok() && tma_eligible(a, plan);
     // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
     // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel
     const char* hub_env = getenv("PYG_TMA_HUBS");
     const bool tma_hubs = tma && split && !(hub_env && atoi(hub_env) == 0);
     // light rows: TMA gather4 pipeline or the LDG kernel
     if (tma && !tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, nullptr, nullptr, 0, s));
-    else if (!tma) PYG_TRY(launch(a, reduce, g, 0, h, ovk, s));
+    else if (!tma) PYG_TRY(launch(a, red_k, g, 0, h, ovk, s));
     if (!split) return PYG_OK;
 
     // split hub rows: chunk partials, then the fp64 combine
@@ -178,10 +180,11 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
         return fail(PYG_ERR_NO_MEMORY, "workspace too small for %lld split-row chunks (need %zu bytes)",
                     (long long)h.n_items, segment_ws_bytes(plan, a.ncols, reduce));
     if (tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, h.part, h.part_arg, h.ldp, s));
-    else PYG_TRY(launch(a, reduce, g, 1, h, ovk, s));  // hub chunks on the LDG kernel (mode 1)
+    else PYG_TRY(launch(a, red_k, g, 1, h, ovk, s));  // hub chunks on the LDG kernel (mode 1)
     dim3 grid((unsigned)(h.h_hi - h.h_lo), (unsigned)cdiv(a.ncols, 256));
-    switch (reduce) {
+    switch (red_k) {
         case PYG_SUM: combine_kernel<PYG_SUM><<<grid, 256, 0, s>>>(a, h); break;
+        case kRedSumEpi: combine_kernel<kRedSumEpi><<<grid, 256, 0, s>>>(a, h); break;
         case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, 256, 0, s>>>(a, h); break;
         case kRedHeadW: combine_kernel<kRedHeadW><<<grid, 256, 0, s>>>(a, h); break;
         default: combine_kernel<PYG_MAX><<<grid, 256, 0, s>>>(a, h); break;

@@ -210,7 +210,8 @@ struct HeavyArgs {
 template <int V, int NCH, int RED>
 struct MinBlocks {
     static constexpr int base = V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1);
-    static constexpr int value = (RED == PYG_MAX && base > 1) ? base - 1 : base;  // MAX also keeps arg ids
+    // MAX also keeps arg ids, the head-weighted sum a head index per chunk: one CTA fewer
+    static constexpr int value = ((RED == PYG_MAX || RED == kRedHeadW) && base > 1) ? base - 1 : base;
 };
 template <int V, int NCH, int RED, int LPR>
 __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kernel(SegArgs a, int mode, HeavyArgs h,
@@ -256,8 +257,11 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
     if (mode == 0) {
         const int64_t dseg = end - beg;
         // accumulate passes (source-blocked plans) have nothing to add for empty segments
-        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || a.blend || a.col_bias) && a.finalize)) return;
-        const float rsc = (a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
+        // the GCN / APPNP epilogue extras exist only in the kRedSumEpi instantiation, so the plain
+        // SUM / MEAN kernels keep their register budget
+        constexpr bool EPI = RED == kRedSumEpi;
+        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || (EPI && (a.blend || a.col_bias))) && a.finalize)) return;
+        const float rsc = (EPI && a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
         const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch) {
@@ -277,16 +281,16 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
 #pragma unroll
                     for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
                 }
-                if (a.row_scale && a.finalize) {
+                if (EPI && a.row_scale && a.finalize) {
 #pragma unroll
                     for (int q = 0; q < V; ++q) r[q] *= rsc;
                 }
-                if (a.blend && a.finalize) {
+                if (EPI && a.blend && a.finalize) {
                     const float* hb = a.blend + row * a.ldb + col;
 #pragma unroll
                     for (int q = 0; q < V; ++q) if (q < nv) r[q] = fmaf(a.blend_b, hb[q], a.blend_a * r[q]);
                 }
-                if (a.col_bias && a.finalize) {
+                if (EPI && a.col_bias && a.finalize) {
 #pragma unroll
                     for (int q = 0; q < V; ++q) if (q < nv) r[q] += __ldg(a.col_bias + col + q);
                 }
@@ -379,6 +383,7 @@ pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, i
         case PYG_SUM: return launch_red<V, PYG_SUM>(a, nch, lpr, tiles, mode, h, ovk, s);
         case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedHeadW: return launch_red<V, kRedHeadW>(a, nch, lpr, tiles, mode, h, ovk, s);
+        case kRedSumEpi: return launch_red<V, kRedSumEpi>(a, nch, lpr, tiles, mode, h, ovk, s);
         default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
     }
 }
