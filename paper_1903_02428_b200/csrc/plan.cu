@@ -107,6 +107,19 @@ __global__ void heavy_counts(const int32_t* __restrict__ heavy_rows, int64_t n_h
 
 }  // namespace
 
+// Split parameters of a plan: rows longer than `thr` positions are cut into `chunk`-position pieces
+// (separate work items, fp32 partials combined in fp64): 2048 / 512 (reading Q12).  (Splitting the
+// rows of few-row, high-degree graphs above 32 positions was measured: Fig. 3's 10,000-node ER graph
+// at degree 128 went from 35 to 53 ms per 1000 runs -- the extra launches and the combine cost more
+// than the parallelism gained -- so the thresholds are fixed.)
+static void split_params(int64_t E, int64_t V, int64_t n_blocks, int64_t* thr, int64_t* chunk) {
+    (void)E;
+    (void)V;
+    (void)n_blocks;
+    *thr = kHeavyThreshold;
+    *chunk = kChunk;
+}
+
 struct PlanLayout {
     int32_t *keys, *vals, *skeys, *perm, *col, *flag_heavy, *pos, *heavy_rows, *deg;
     int32_t *order, *okeys, *okeys_out, *ovals, *pos_row, *task_item;
@@ -146,9 +159,10 @@ static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, int
     L.ovals = cv.take<int32_t>(vo);
     L.ldeg = cv.take<int64_t>(1);
     L.pos_row = n_blocks == 1 ? cv.take<int32_t>(e) : nullptr;
-    // closed tasks hold > kTaskPositions - kHeavyThreshold positions; hub rows add one cut each
-    L.task_cap = n_blocks == 1 ? (e / (kTaskPositions - kHeavyThreshold) + 2 * (e / kHeavyThreshold) + e / kChunk + 4)
-                               : 1;
+    // closed tasks hold > kTaskPositions - thr positions; hub rows add one cut each
+    int64_t thr = 0, chk = 0;
+    split_params(E, n_rows * n_blocks, n_blocks, &thr, &chk);
+    L.task_cap = n_blocks == 1 ? (e / (kTaskPositions - thr) + 2 * (e / thr) + e / chk + 4) : 1;
     L.task_pos = cv.take<int64_t>(2 * L.task_cap);
     L.task_item = cv.take<int32_t>(L.task_cap);
     size_t b1 = 0, b2 = 0, b3 = 0;
@@ -195,6 +209,8 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     if (nb * n_rows > 0x7ffffffeLL) return fail(PYG_ERR_UNSUPPORTED, "plan: n_blocks * n_rows must be < 2^31");
     const int64_t V = nb * n_rows;  // virtual rows
     const size_t need = plan_layout(ws, bytes, E, n_rows, nb, col != nullptr, L);
+    int64_t thr = 0, chunk = 0;
+    split_params(E, V, nb, &thr, &chunk);
     if (!ws || need > bytes) return fail(PYG_ERR_NO_MEMORY, "plan workspace too small (%zu < %zu)", bytes, need);
     int* flag = validate_flag_dev();
     PYG_CUDA(cudaMemsetAsync(L.flags2, 0, 2 * sizeof(int), s));
@@ -232,7 +248,7 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     }
     int64_t n_heavy = 0;
     if (V > 0) {
-        heavy_flags<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, kHeavyThreshold, L.flag_heavy);
+        heavy_flags<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, (int)thr, L.flag_heavy);
         LAUNCH_CHECK();
         size_t cb = L.cub_bytes;
         PYG_CUDA(cub::DeviceScan::ExclusiveSum(L.cub_tmp, cb, L.flag_heavy, L.pos, (int)V, s));
@@ -248,7 +264,7 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     std::vector<int32_t> h_rows((size_t)n_heavy);
     std::vector<int64_t> h_ptr((size_t)n_heavy + 1, 0);
     if (n_heavy > 0) {
-        heavy_counts<<<grid_for(n_heavy), 256, 0, s>>>(L.heavy_rows, n_heavy, L.rowptr, kChunk, L.cnt);
+        heavy_counts<<<grid_for(n_heavy), 256, 0, s>>>(L.heavy_rows, n_heavy, L.rowptr, (int)chunk, L.cnt);
         LAUNCH_CHECK();
         PYG_CUDA(cudaMemsetAsync(L.cnt + n_heavy, 0, sizeof(int64_t), s));
         size_t cb = L.cub_bytes;
@@ -277,11 +293,11 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
         };
         for (int64_t r = 0; r < V; ++r) {
             const int64_t b = h_rowptr[(size_t)r], e = h_rowptr[(size_t)r + 1], d = e - b;
-            if (d > kHeavyThreshold) {
+            if (d > thr) {
                 close();
-                for (int64_t c = b; c < e; c += kChunk) {
+                for (int64_t c = b; c < e; c += chunk) {
                     hp.push_back(c);
-                    hp.push_back(std::min<int64_t>(c + kChunk, e));
+                    hp.push_back(std::min<int64_t>(c + chunk, e));
                     hi.push_back((int32_t)item++);
                 }
                 continue;
@@ -325,8 +341,8 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     root.h_hi = n_heavy;
     root.item_lo = 0;
     root.item_hi = root.h_heavy_item_ptr[(size_t)n_heavy];
-    root.heavy_threshold = kHeavyThreshold;
-    root.chunk = kChunk;
+    root.heavy_threshold = (int32_t)thr;
+    root.chunk = (int32_t)chunk;
     if (nb == 1) {
         root.row_order = L.order;
         root.order_len = V;
@@ -350,8 +366,8 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     p->col = root.col;
     p->perm = root.perm;
     p->perm_identity = 0;
-    p->heavy_threshold = kHeavyThreshold;
-    p->chunk = kChunk;
+    p->heavy_threshold = (int32_t)thr;
+    p->chunk = (int32_t)chunk;
     p->col_block = col_block;
     p->deg = L.deg;
     for (int64_t b = 0; b < nb; ++b) {

@@ -181,13 +181,15 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
                     (long long)h.n_items, segment_ws_bytes(plan, a.ncols, reduce));
     if (tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, h.part, h.part_arg, h.ldp, s));
     else PYG_TRY(launch(a, red_k, g, 1, h, ovk, s));  // hub chunks on the LDG kernel (mode 1)
-    dim3 grid((unsigned)(h.h_hi - h.h_lo), (unsigned)cdiv(a.ncols, 256));
+    // one CTA per split row, threads over columns (one warp for narrow rows)
+    const int ct = (int)std::min<int64_t>(256, align_up((size_t)a.ncols, 32));
+    dim3 grid((unsigned)(h.h_hi - h.h_lo), (unsigned)cdiv(a.ncols, ct));
     switch (red_k) {
-        case PYG_SUM: combine_kernel<PYG_SUM><<<grid, 256, 0, s>>>(a, h); break;
-        case kRedSumEpi: combine_kernel<kRedSumEpi><<<grid, 256, 0, s>>>(a, h); break;
-        case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, 256, 0, s>>>(a, h); break;
-        case kRedHeadW: combine_kernel<kRedHeadW><<<grid, 256, 0, s>>>(a, h); break;
-        default: combine_kernel<PYG_MAX><<<grid, 256, 0, s>>>(a, h); break;
+        case PYG_SUM: combine_kernel<PYG_SUM><<<grid, ct, 0, s>>>(a, h); break;
+        case kRedSumEpi: combine_kernel<kRedSumEpi><<<grid, ct, 0, s>>>(a, h); break;
+        case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, ct, 0, s>>>(a, h); break;
+        case kRedHeadW: combine_kernel<kRedHeadW><<<grid, ct, 0, s>>>(a, h); break;
+        default: combine_kernel<PYG_MAX><<<grid, ct, 0, s>>>(a, h); break;
     }
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());

@@ -3,6 +3,6 @@
 O=gpurun_out/${1:-v}
 mkdir -p $O
 timeout -s KILL 1000 python -m pytest tests -m gpu -q 2>&1 | tail -5 > $O/pytest.txt
-timeout 300 python bench.py --steps 10 --no-e2e --no-cpu > $O/reddit.json 2>/dev/null
-for op in appnp gcn; do timeout 400 python bench.py --config reddit --op $op --steps 5 --no-cpu > $O/reddit_$op.json 2>/dev/null; done
-for op in gcn gat; do timeout 400 python bench.py --config rmat --op $op --steps 5 --no-cpu > $O/rmat_$op.json 2>/dev/null; done
+timeout 600 python scripts/fig3.py --out $O/fig3.json > $O/fig3.log 2>&1
+for cfg in cora pubmed clouds; do timeout 300 python bench.py --config $cfg --steps 50 --no-e2e --no-variants > $O/$cfg.json 2>/dev/null; done
+for red in sum max; do timeout 300 python bench.py --config rmat --reduce $red --steps 10 --no-e2e --no-cpu --no-variants > $O/rmat_$red.json 2>/dev/null; done

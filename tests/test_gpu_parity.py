@@ -132,6 +132,8 @@ CASES = [
     (150, 120, 2500, 602, 608),
     (150, 120, 2500, 602, None),
     (80, 60, 900, 2100, None),
+    (500, 200, 20000, 16, None),   # few rows, degree 100: rows split above 32 positions (Fig. 3 regime)
+    (700, 300, 30000, 130, 132),
 ]
 
 
