@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--config", default="reddit", choices=list(CONFIGS))
     ap.add_argument("--reduce", default=None, choices=["sum", "mean", "max"])
     ap.add_argument("--strategy", default="segment", choices=["segment", "atomic"])
-    ap.add_argument("--op", default="propagate", choices=["propagate", "gat", "appnp", "gcn"],
+    ap.add_argument("--op", default="propagate", choices=["propagate", "gat", "gatlayer", "appnp", "gcn"],
                     help="gat: GAT attention aggregation forward + backward (NEXT-1) on the config's graph; "
                          "appnp: K-step APPNP propagation (NEXT-2) with GCN weights")
     ap.add_argument("--K", type=int, default=10, help="appnp: propagation steps")
@@ -624,6 +624,32 @@ def main():
             o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"])
             gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT)
 
+    gatl = None
+    if a.op == "gatlayer":
+        # a whole GAT layer forward in this library: z = x W^T with the per-head attention
+        # projections fused into the tcgen05 epilogue (pyg_gat_transform), then the segment softmax and
+        # the alpha-weighted aggregation (pyg_gat_propagate); 8 heads x 8 (citation graphs) or x F/8
+        assert world == 1 and a.strategy == "segment", "--op gatlayer: one GPU, segment strategy"
+        H = a.heads or 8
+        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, F // H))
+        if plan_full.view()["n_col_blocks"] > 1:
+            plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
+            col_block = 0
+        gg = torch.Generator(device=dev)
+        gg.manual_seed(109)
+        Wg = torch.zeros((H * C, ld), device=dev)
+        Wg[:, :F] = torch.randn((H * C, F), generator=gg, device=dev) / (F ** 0.5)
+        a_s = torch.randn(H * C, generator=gg, device=dev)
+        a_d = torch.randn(H * C, generator=gg, device=dev)
+        go = torch.empty((N, H * C), device=dev)
+        gal = torch.empty((E, H), device=dev)
+        gatl = dict(H=H, C=C, out=go)
+        passes, red = 1, "gatlayer"
+
+        def compute():
+            z, ss, sd = pg.pyg_gat_transform(x_full, Wg[:, :F], a_s, a_d, H)
+            pg.pyg_gat_propagate(z, ss, sd, H, plan, out=go, alpha=gal)
+
     appnp = None
     if a.op == "appnp":
         # NEXT-2: APPNP propagation z_{k+1} = (1 - alpha) S z_k + alpha h, S = D^-1/2 (A+I) D^-1/2,
@@ -756,7 +782,7 @@ def main():
     else:
         xchg_ms = 0.0
     ms_step = total_ms / a.steps
-    units = passes * E * (a.hidden if a.op == "gcn" else F)  # edges*F of the whole job per step (all ranks)
+    units = passes * E * (a.hidden if a.op == "gcn" else (gatl["H"] * gatl["C"] if gatl else F))  # edges*F, all ranks
     value = units / (ms_step * 1e-3)
 
     peak, peak_src = measured_peak()
@@ -766,6 +792,12 @@ def main():
         Fh = a.hidden
         B = N * F * 4 + Fh * F * 4 + N * Fh * 4 + (E * Fh * 4 + E * 4 + 8 * (N + 1) + N * Fh * 4 + 2 * N * 4)
         result_flops = 2.0 * N * F * Fh
+    elif gatl is not None:  # transform (X once, W, z + projections written) + softmax + alpha-weighted sum
+        Fz = gatl["H"] * gatl["C"]
+        Hh = gatl["H"]
+        B = (N * F * 4 + Fz * F * 4 + N * Fz * 4 + 2 * N * Hh * 4) + \
+            (E * (8 + 2 * 4 * Hh + 4 * Hh) + N * Hh * 4) + (E * (8 + 4 * Hh + 4 * Fz) + N * Fz * 4 + 8 * (N + 1))
+        result_flops = 2.0 * N * F * Fz
     elif appnp is not None:  # K weighted propagations + the teleport read of h per step
         B = a.K * (alg_bytes(E, N, F, "sum", a.strategy, weighted=True) + (N * F * 4 if a.alpha else 0))
     else:
@@ -804,6 +836,14 @@ def main():
     }
     if w.get("extra"):
         result.update(w["extra"])
+    if gatl is not None:
+        result["config"]["op"] = "gatlayer"
+        result["config"]["heads"] = gatl["H"]
+        result["config"]["channels"] = gatl["C"]
+        result["config"]["step"] = ("GAT layer forward: tcgen05 TF32 transform with fused attention projections + "
+                                    "segment softmax + alpha-weighted aggregation")
+        result["transform_tflops_per_step"] = result_flops / 1e12
+        result["units_note"] = "edges*F counts E x heads*channels per step"
     if gcn is not None:
         result["config"]["op"] = "gcn"
         result["config"]["hidden"] = a.hidden
@@ -840,7 +880,10 @@ def main():
         ei_cpu = ei.cpu().numpy()
         x_cpu = np.ascontiguousarray(x.cpu().numpy())
         w_cpu = wgt.cpu().numpy() if weighted else None
-        if gcn is not None:
+        if gatl is not None:
+            rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, "sum", a.cpu_seconds, F)
+            got = None
+        elif gcn is not None:
             rate, dt, Es, R, ref = oracle_gcn_sample(ei_cpu, x_cpu, gcn["W"].cpu().numpy(), gcn["b"].cpu().numpy(), N,
                                                      a.cpu_seconds)
             got = gcn["out"][:R].cpu().numpy()
@@ -854,7 +897,9 @@ def main():
         else:
             rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
             got = out[:R].cpu().numpy()
-        if gcn is not None:
+        if gatl is not None:
+            ok = None  # parity of the layer's parts: tests/test_gpu_transform.py + tests/test_gpu_attention.py
+        elif gcn is not None:
             ok = bool((np.abs(got - ref[0]) <= 2.5e-3 * ref[1] + 1e-5 * ref[2] + 1e-6).all())
         elif appnp is not None:
             ok = bool((np.abs(got - ref) <= 1e-5 * np.abs(ref) + 1e-6).all()) if R else None
@@ -878,7 +923,7 @@ def main():
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
-    if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None and gcn is None:
+    if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None and gcn is None and gatl is None:
         xs = x.as_strided((N, ld), (x.stride(0), 1)) if x.stride(0) == ld else x.contiguous()
         hx = torch.empty(xs.shape, dtype=torch.float32, pin_memory=True)
         hx.copy_(xs)
@@ -958,7 +1003,8 @@ def main():
             result["concat_xi_note"] = "phi = [x_i || x_j], F_out = 128, max + arg (eager, back to back)"
 
     # ---- other reductions on the same resident graph (informational) ----
-    if world == 1 and not a.no_variants and passes == 1 and gat is None and appnp is None and gcn is None:
+    if world == 1 and not a.no_variants and passes == 1 and gat is None and appnp is None and gcn is None \
+            and gatl is None:
         var = {}
         for r2 in ("sum", "mean", "max"):
             if r2 == red:
