@@ -546,6 +546,19 @@ def main():
         x_full = xbuf[:N, :F]
     else:
         x_full = x
+    e2e_host = None
+    if world > 1 and not a.no_e2e and a.op == "propagate" and a.strategy == "segment":
+        # N > 1 end-to-end leg (below): this rank's X rows and the edge list in pinned host memory
+        from paper_1903_02428_b200.dist import partition_rows as _pr
+
+        lo_e, hi_e = _pr(N, world)[0][rank]
+        xs_all = x.as_strided((N, ld), (x.stride(0), 1))
+        e2e_host = dict(lo=lo_e, hi=hi_e,
+                        hx=torch.empty((hi_e - lo_e, ld), dtype=torch.float32, pin_memory=True),
+                        hei=torch.empty(ei.shape, dtype=torch.int64, pin_memory=True))
+        e2e_host["hx"].copy_(xs_all[lo_e:hi_e])
+        e2e_host["hei"].copy_(ei)
+        del xs_all
     if world > 1:
         del x  # every rank keeps only its shard (+ the exchange buffer)
         w.pop("x")
@@ -921,6 +934,46 @@ def main():
                                   "sample": sample, "parity_on_sample": ok}
         if not ok:
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
+
+    # ---- e2e at N > 1: every step the edge list and this rank's X rows come from pinned host memory,
+    # the global plan is built and sliced, X is all-gathered (NCCL), the rank's rows are propagated and
+    # copied back (dist.DistAggregation: the user-facing multi-GPU call); max over ranks ----
+    if e2e_host is not None:
+        from paper_1903_02428_b200.dist import DistAggregation
+
+        dei = torch.empty(e2e_host["hei"].shape, dtype=torch.int64, device=dev)
+        dxs = torch.empty(e2e_host["hx"].shape, dtype=torch.float32, device=dev)
+        cb_e = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4) if a.col_block == "auto" else int(a.col_block)
+        hout_e = torch.empty((e2e_host["hi"] - e2e_host["lo"], F), dtype=torch.float32, pin_memory=True)
+
+        def e2e_dist_step():
+            dei.copy_(e2e_host["hei"], non_blocking=True)
+            dxs.copy_(e2e_host["hx"], non_blocking=True)
+            da = DistAggregation(dei, N, world, rank, col_block=cb_e)
+            shard_e = torch.zeros((da.per, ld), dtype=torch.float32, device=dev)
+            shard_e[: da.hi - da.lo] = dxs
+            r = da.forward(shard_e[:, :F], reduce=red)
+            o = r[0] if isinstance(r, tuple) else r
+            hout_e.copy_(o, non_blocking=True)
+
+        e2e_dist_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        k2 = max(2, min(a.steps, 3))
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(k2):
+            e2e_dist_step()
+        s1.record()
+        torch.cuda.synchronize()
+        tt = torch.tensor([s0.elapsed_time(s1) / k2], device=dev if a.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt.item())
+        result["e2e"] = {"value": units / (e_ms * 1e-3), "unit": "edges*F/s",
+                         "h2d_bytes_per_step": int(e2e_host["hx"].numel() * 4 + e2e_host["hei"].numel() * 8),
+                         "d2h_bytes_per_step": int(hout_e.numel() * 4), "ms_per_step": e_ms, "steps": k2,
+                         "includes": "per rank: H2D(edge list, own X rows) + global plan build + slice + NCCL "
+                                     "all-gather of X + propagate + D2H(own out rows); max over ranks"}
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
     if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None and gcn is None and gatl is None:

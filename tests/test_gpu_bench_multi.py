@@ -46,3 +46,4 @@ def test_bench_two_ranks(cfg, exchange, reduce, extra):
     assert d["value"] > 0 and d["ms_per_step"] > 0 and d["gpu_launches"] > 0
     for k in ("roofline", "clocks", "steps", "warmup", "metric", "unit"):
         assert k in d
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0  # the N > 1 end-to-end leg
