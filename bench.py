@@ -667,7 +667,7 @@ def main():
         # the alpha-weighted aggregation (pyg_gat_propagate); 8 heads x 8 (citation graphs) or x F/8
         assert world == 1 and a.strategy == "segment", "--op gatlayer: one GPU, segment strategy"
         H = a.heads or 8
-        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, F // H))
+        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, min(F, 256) // H))
         if plan_full.view()["n_col_blocks"] > 1:
             plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
             col_block = 0

@@ -396,7 +396,8 @@ pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const 
  *   X [M x K] stride ldx (row-major; 16-byte aligned, ldx % 4 == 0);
  *   W [N x K] stride ldw (the torch.nn.Linear weight layout [out x in]; same alignment);
  *   bias [N] or NULL; row_scale [M] or NULL (e.g. GCN's D^-1/2, applied before the bias);
- *   Y [M x N] stride ldy, overwritten.  1 <= K, N <= 256.  Asynchronous. */
+ *   Y [M x N] stride ldy, overwritten.  K >= 1; N > 256 runs as several 256-column tiles (X is
+ *   then read once per tile).  Asynchronous. */
 pyg_status_t pyg_dense_transform(const float* X, int64_t M, int64_t K, int64_t ldx, const float* W,
                                  int64_t N, int64_t ldw, const float* bias, const float* row_scale,
                                  float* Y, int64_t ldy, void* stream);

@@ -721,7 +721,7 @@ pyg_status_t pyg_dense_transform(const float* X, int64_t M, int64_t K, int64_t l
                                  void* stream) {
     REQUIRE(M >= 0 && K >= 1 && N >= 0, PYG_ERR_INVALID_ARGUMENT, "dense_transform: bad sizes (K >= 1)");
     REQUIRE(ldx >= K && ldw >= K && ldy >= N, PYG_ERR_DIMENSION, "dense_transform: leading dimension too small");
-    REQUIRE(N <= 256, PYG_ERR_UNSUPPORTED, "dense_transform: F_out <= 256 (one UMMA N)");
+    REQUIRE(N <= 65535LL * 256, PYG_ERR_UNSUPPORTED, "dense_transform: F_out too large");
     REQUIRE(M <= kMaxI32 && K <= kMaxI32, PYG_ERR_UNSUPPORTED, "dense_transform: sizes must be < 2^31");
     REQUIRE(M * N == 0 || (X && W && Y), PYG_ERR_INVALID_ARGUMENT, "dense_transform: null pointer");
     REQUIRE((reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&

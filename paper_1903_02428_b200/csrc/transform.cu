@@ -108,6 +108,8 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + (size_t)a.stages * stage_bytes + 8 * (2 * a.stages + 1));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t m0 = (int64_t)blockIdx.x * kBM;
+    const int n0 = blockIdx.y * a.UN;            // this CTA's output-column tile (N > 256: several)
+    const int nl = min(a.UN, a.N - n0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < a.stages; ++s) {
@@ -137,7 +139,7 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
             const uint32_t sa = base + (uint32_t)s * stage_bytes;
             mbar_expect_tx(bars + 8 * s, stage_bytes);
             tma_load_2d(sa, &map_x, kb * kBK, (int)m0, bars + 8 * s);
-            tma_load_2d(sa + a_bytes, &map_w, kb * kBK, 0, bars + 8 * s);
+            tma_load_2d(sa + a_bytes, &map_w, kb * kBK, n0, bars + 8 * s);
         }
     } else if (warp == 1 && lane == 0) {
         // ---- MMA issuer ----
@@ -181,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
     float ps[8], pd[8];  // per-head projections of this thread's row (heads <= 8)
 #pragma unroll
     for (int h = 0; h < 8; ++h) { ps[h] = 0.0f; pd[h] = 0.0f; }
-    for (int c0 = 0; c0 < a.N; c0 += 16) {
+    for (int c0 = 0; c0 < nl; c0 += 16) {
         uint32_t v[16];
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
         asm volatile(
@@ -195,26 +197,26 @@ __global__ void __launch_bounds__(kThreads) tf32_gemm_kernel(const __grid_consta
             float r[16];
 #pragma unroll
             for (int q = 0; q < 16; ++q)
-                r[q] = __uint_as_float(v[q]) * rs + ((a.bias && c0 + q < a.N) ? __ldg(a.bias + c0 + q) : 0.0f);
+                r[q] = __uint_as_float(v[q]) * rs + ((a.bias && c0 + q < nl) ? __ldg(a.bias + n0 + c0 + q) : 0.0f);
             if (a.att_src) {
 #pragma unroll
                 for (int q = 0; q < 16; ++q) {
-                    if (c0 + q >= a.N) break;
-                    const int hh = (c0 + q) / a.hc;
-                    const float vs = r[q] * __ldg(a.att_src + c0 + q), vd = r[q] * __ldg(a.att_dst + c0 + q);
+                    if (c0 + q >= nl) break;
+                    const int hh = (n0 + c0 + q) / a.hc;
+                    const float vs = r[q] * __ldg(a.att_src + n0 + c0 + q), vd = r[q] * __ldg(a.att_dst + n0 + c0 + q);
 #pragma unroll
                     for (int h = 0; h < 8; ++h)
                         if (h == hh) { ps[h] += vs; pd[h] += vd; }
                 }
             }
-            float* y = a.Y + row * a.ldy + c0;
-            if (vec && c0 + 16 <= a.N) {
+            float* y = a.Y + row * a.ldy + n0 + c0;
+            if (vec && c0 + 16 <= nl) {
 #pragma unroll
                 for (int q = 0; q < 16; q += 4) *reinterpret_cast<float4*>(y + q) = make_float4(r[q], r[q + 1], r[q + 2], r[q + 3]);
             } else {
 #pragma unroll
                 for (int q = 0; q < 16; ++q)
-                    if (c0 + q < a.N) y[q] = r[q];
+                    if (c0 + q < nl) y[q] = r[q];
             }
         }
     }
@@ -277,7 +279,7 @@ pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t 
     if (!encode_fn()) return fail(PYG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     Args a;
     a.M = M; a.K = K; a.N = (int)N;
-    a.UN = (int)align_up((size_t)N, 16);
+    a.UN = (int)std::min<size_t>(256, align_up((size_t)N, 16));  // UMMA N per CTA; more columns -> grid.y
     a.tmem_cols = 32;
     while (a.tmem_cols < a.UN) a.tmem_cols <<= 1;
     a.kb = (int)cdiv(std::max<int64_t>(K, 1), kBK);
@@ -317,7 +319,9 @@ pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t 
         if (r != CUDA_SUCCESS) return fail(PYG_ERR_CUDA, "tensor map for W failed (%d)", (int)r);
     }
     PYG_CUDA(cudaFuncSetAttribute(tf32_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    tf32_gemm_kernel<<<(unsigned)cdiv(M, kBM), kThreads, smem, s>>>(mx, mw, a);
+    const dim3 grid((unsigned)cdiv(M, kBM), (unsigned)cdiv(N, a.UN));
+    if (att_src && grid.y > 1) return fail(PYG_ERR_UNSUPPORTED, "gat_transform: H*C <= 256");
+    tf32_gemm_kernel<<<grid, kThreads, smem, s>>>(mx, mw, a);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;

@@ -19,7 +19,8 @@ def _t(a):
 
 
 @pytest.mark.parametrize("M,K,N", [(19717, 500, 16), (300, 37, 3), (1000, 64, 64), (129, 128, 128),
-                                   (4096, 602, 256), (5, 8, 100), (2708, 1433, 16)])
+                                   (4096, 602, 256), (5, 8, 100), (2708, 1433, 16),
+                                   (1000, 64, 300), (300, 128, 600), (129, 37, 513)])  # N > 256: column tiles
 @pytest.mark.parametrize("epi", ["plain", "bias_scale"])
 def test_dense_transform(M, K, N, epi):
     import paper_1903_02428_b200 as pg
@@ -69,8 +70,9 @@ def test_dense_transform_errors():
     import paper_1903_02428_b200 as pg
 
     x = torch.zeros((10, 8), device=DEV)
-    with pytest.raises(pg.PygError):
-        pg.pyg_dense_transform(x, torch.zeros((300, 8), device=DEV))  # N > 256
+    with pytest.raises(pg.PygError):  # GAT projections need the heads in one 256-column tile
+        pg.pyg_gat_transform(x, torch.zeros((300, 8), device=DEV), torch.zeros(300, device=DEV),
+                             torch.zeros(300, device=DEV), 5)
     with pytest.raises(pg.PygError):
         pg.pyg_dense_transform(torch.zeros((10, 9), device=DEV)[:, 1:], torch.zeros((4, 8), device=DEV))  # unaligned
 
