@@ -589,7 +589,8 @@ def main():
     out = torch.empty((n_loc, ((F + 7) // 8 * 8) if a.config == "reddit" else F), dtype=torch.float32,
                       device=dev)[:, :F]
     arg = torch.empty((n_loc, out.stride(0)), dtype=torch.int64, device=dev)[:, :F] if red == "max" else None
-    ws = torch.empty(max(1, pg.pyg_workspace_size(plan, n_loc, F, red)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(max(1, pg.pyg_workspace_size(plan, n_loc, F, red, E=ei_loc.shape[1])), dtype=torch.uint8,
+                     device=dev)
     stream = torch.cuda.current_stream()
 
     passes, weighted, prep_ms = 1, False, 0.0
@@ -620,7 +621,7 @@ def main():
         prep_ms = (time.perf_counter() - t1) * 1e3
         g = torch.from_numpy(synth.pubmed_like()[2]).to(dev)
         gx = torch.empty((N, F), dtype=torch.float32, device=dev)
-        ws = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, red)), dtype=torch.uint8, device=dev)
+        ws = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, red, E=ei.shape[1])), dtype=torch.uint8, device=dev)
         passes, weighted, red = 2, True, "sum"
 
         def compute():
@@ -1086,7 +1087,7 @@ def main():
             if r2 == red:
                 continue
             a2 = torch.empty((N, out.stride(0)), dtype=torch.int64, device=dev)[:, :F] if r2 == "max" else None
-            ws2 = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, r2)), dtype=torch.uint8, device=dev)
+            ws2 = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, r2, E=E)), dtype=torch.uint8, device=dev)
             for _ in range(3):
                 pg.pyg_propagate(x, None if plan else ei, reduce=r2, plan=plan, out=out, arg_out=a2, E=E,
                                  workspace=ws2)

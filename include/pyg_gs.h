@@ -205,9 +205,16 @@ pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, 
                            int64_t ldd, int n_peers, void* stream);
 
 /* Scratch needed by pyg_scatter / pyg_propagate / pyg_propagate_backward for
- * an output of F_out columns: fp64-combined partials of split hub rows (plan
- * path) or the in-degree array (atomic path).  bytes may be 0. */
-pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t n_out, int64_t F_out,
+ * an output of n_out rows x F_out columns over E edges.
+ *   plan path: the fp32 partials of split hub rows, combined in fp64 (reading Q12).
+ *   atomic path (plan NULL or PYG_FORCE_ATOMIC): the in-degree array and, for
+ *   SUM / MEAN, the hub slots -- rows with more than 2048 entries spread their
+ *   edges over slots of <= 1024 entries (one atomic counter per hub hands out
+ *   positions) whose fp32 partials are combined in fp64, so no fp32 atomic chain
+ *   exceeds 1024 terms (Q12).  The size is the worst case for E edges
+ *   (E/1024 + E/2049 slots x F_out floats); a MAX call needs none of it.
+ * For pyg_propagate_backward pass (plan_T, E, n_src, F).  Host-only. */
+pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t E, int64_t n_out, int64_t F_out,
                                 pyg_reduce_t reduce, uint32_t flags, size_t* bytes);
 
 /* ---- scatter: edge space -> node space -------------- */
@@ -219,8 +226,10 @@ pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t n_out, int64_t F
  *     empty segments (Q3).  (On the atomic path it doubles as the 64-bit key
  *     buffer before being decoded in place.)
  *   plan: built with row_index = index, col_index = NULL -> deterministic
- *     CSR segment-reduce; NULL -> atomic COO (red.global.add.v4.f32 /
- *     64-bit atomicMax keys), non-deterministic for sum/mean. */
+ *     CSR segment-reduce; NULL -> atomic COO (warp-aggregated
+ *     red.global.add.v4.f32, hub rows through fp64-combined slots / 64-bit
+ *     atomicMax keys), non-deterministic for sum/mean.
+ *   workspace: pyg_workspace_size(plan, E, dim_size, F, reduce, flags). */
 pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, const int64_t* index,
                          int64_t dim_size, pyg_reduce_t reduce, uint32_t flags, float* out,
                          int64_t ldo, int64_t* arg_out, const pyg_plan_t* plan, void* workspace,

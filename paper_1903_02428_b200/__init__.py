@@ -175,9 +175,14 @@ def pyg_plan_build(row_index: torch.Tensor, col_index: Optional[torch.Tensor], n
     return Plan(h, ws)
 
 
-def pyg_workspace_size(plan: Optional[Plan], n_out: int, F_out: int, reduce, flags: int = 0) -> int:
+def pyg_workspace_size(plan: Optional[Plan], n_out: int, F_out: int, reduce, flags: int = 0,
+                       E: Optional[int] = None) -> int:
+    """Scratch bytes of a scatter / propagate / backward call; E (edges) sizes the atomic path's hub
+    slots and defaults to the plan's edge count."""
+    if E is None:
+        E = plan.view()["E"] if plan is not None else 0
     nb = ctypes.c_size_t()
-    check(lib.pyg_workspace_size(plan.handle if plan else None, n_out, F_out, _red(reduce), flags,
+    check(lib.pyg_workspace_size(plan.handle if plan else None, E, n_out, F_out, _red(reduce), flags,
                                  ctypes.byref(nb)), "pyg_workspace_size")
     return nb.value
 
@@ -203,7 +208,7 @@ def pyg_scatter(src: torch.Tensor, index: torch.Tensor, dim_size: int, reduce="s
         arg_out = torch.empty((dim_size, F), dtype=torch.int64, device=dev)
     _, _, ldo = _rows(out, "out")
     if workspace is None:
-        workspace = _workspace(pyg_workspace_size(plan, dim_size, F, r, flags), dev)
+        workspace = _workspace(pyg_workspace_size(plan, dim_size, F, r, flags, E=E), dev)
     check(lib.pyg_scatter(_ptr(src), E, F, lds, _ptr(index), dim_size, r, flags, _ptr(out), ldo, _ptr(arg_out),
                           plan.handle if plan else None, _ptr(workspace), workspace.numel(), _stream(dev)),
           "pyg_scatter")
@@ -261,7 +266,7 @@ def pyg_propagate(x_src: torch.Tensor, edge_index: Optional[torch.Tensor], n_dst
         arg_out = torch.empty((n_dst, F_out), dtype=torch.int64, device=dev)
     _, _, ldo = _rows(out, "out")
     if workspace is None:
-        workspace = _workspace(pyg_workspace_size(plan, n_dst, F_out, r, flags), dev)
+        workspace = _workspace(pyg_workspace_size(plan, n_dst, F_out, r, flags, E=E), dev)
     check(lib.pyg_propagate(_ptr(x_src), n_src, F, ldx, _ptr(x_dst), ldxd, n_dst, _ptr(edge_index), E,
                             _ptr(edge_attr), D, lde, _ptr(edge_weight), r, flags, _ptr(out), ldo, _ptr(arg_out),
                             plan.handle if plan else None, _ptr(workspace), workspace.numel(), _stream(dev)),
@@ -297,7 +302,7 @@ def pyg_propagate_backward(x_src: Optional[torch.Tensor], edge_index: torch.Tens
     gxd = torch.empty((n_dst, F), dtype=torch.float32, device=dev) if (need_x_dst and concat_xi) else None
     gea = torch.empty((E, D), dtype=torch.float32, device=dev) if (need_edge_attr and D > 0) else None
     gew = torch.empty(E, dtype=torch.float32, device=dev) if need_edge_weight else None
-    ws = _workspace(pyg_workspace_size(plan_T, n_src, F, SUM, flags), dev)
+    ws = _workspace(pyg_workspace_size(plan_T, n_src, F, SUM, flags, E=E), dev)
     check(lib.pyg_propagate_backward(_ptr(x_src), n_src, F, ldx, n_dst, _ptr(edge_index), E, D, _ptr(edge_weight), r,
                                      flags, _ptr(grad_out), ldg, _ptr(arg_out), _ptr(deg_dst), _ptr(gxs),
                                      gxs.stride(0) if gxs is not None else 0, _ptr(gxd), F, _ptr(gea), D, _ptr(gew),

@@ -72,7 +72,7 @@ SIGNATURES = {
     "pyg_ipc_close": ([P, I64], C),
     "pyg_halo_push": ([P, I64, I64, I64, P, P, P, P, I64, C, P], C),
     "pyg_gather_rows": ([P, I64, I64, I64, P, I64, U32, P, I64, P], C),
-    "pyg_workspace_size": ([P, I64, I64, C, U32, ctypes.POINTER(SZ)], C),
+    "pyg_workspace_size": ([P, I64, I64, I64, C, U32, ctypes.POINTER(SZ)], C),
     "pyg_scatter": ([P, I64, I64, I64, P, I64, C, U32, P, I64, P, P, P, SZ, P], C),
     "pyg_scatter_backward": ([P, I64, P, I64, I64, I64, C, P, P, P, I64, P], C),
     "pyg_propagate": ([P, I64, I64, I64, P, I64, I64, P, I64, P, I64, I64, P, C, U32, P, I64, P, P, P, SZ, P], C),

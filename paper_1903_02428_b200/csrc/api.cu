@@ -5,7 +5,6 @@
 #include <stdio.h>
 
 #include <cmath>
-#include <mutex>
 #include <string>
 
 #include "kernels.cuh"
@@ -38,26 +37,40 @@ pyg_status_t cuda_check(cudaError_t e, const char* what) {
     return fail(PYG_ERR_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
 }
 
-static std::mutex g_flag_mu;
-static int* g_flag = nullptr;
+// PYG_VALIDATE flag: one pinned, mapped int per host thread (so concurrent calls on other threads
+// never consume each other's errors).  validate_begin() clears it before a validating call launches
+// its checking kernels (every earlier use on this thread ended with the synchronising check).
+namespace {
+struct MappedFlag {
+    int* p = nullptr;
+    ~MappedFlag() {
+        if (p) cudaFreeHost(p);
+    }
+};
+thread_local MappedFlag t_flag;
+}  // namespace
 
 int* validate_flag_dev() {
-    std::lock_guard<std::mutex> lk(g_flag_mu);
-    if (!g_flag) {
-        if (cudaHostAlloc(reinterpret_cast<void**>(&g_flag), sizeof(int),
+    if (!t_flag.p) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&t_flag.p), sizeof(int),
                           cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-            g_flag = nullptr;
+            t_flag.p = nullptr;
             return nullptr;
         }
-        *g_flag = 0;
+        *t_flag.p = 0;
     }
-    return g_flag;  // UVA: the host pointer is valid on the device
+    return t_flag.p;  // UVA: the host pointer is valid on the device
+}
+
+void validate_begin() {
+    int* f = validate_flag_dev();
+    if (f) *reinterpret_cast<volatile int*>(f) = 0;
 }
 
 pyg_status_t validate_flag_check(cudaStream_t s, const char* what) {
     PYG_CUDA(cudaStreamSynchronize(s));
     int* f = validate_flag_dev();
-    const int v = f ? *f : 0;
+    const int v = f ? *reinterpret_cast<volatile int*>(f) : 0;
     if (f) *f = 0;
     if (v == 1) return fail(PYG_ERR_INDEX_OUT_OF_BOUNDS, "%s", what);
     if (v == 2) return fail(PYG_ERR_DIMENSION, "%s", what);
@@ -99,7 +112,8 @@ constexpr int64_t kMaxI32 = 0x7fffffffLL - 1;
 constexpr int kAttnMaxHeads = 8;
 constexpr double kL2BlockFraction = 0.4;  // X block per pass as a fraction of L2
 
-static size_t coo_ws_bytes(int64_t n_out) { return 2 * align_up((size_t)std::max<int64_t>(n_out, 1) * 4, 256); }
+// deg + first edge per target (atomic propagate with CONCAT_XI / MEAN), carved before coo_reduce's own
+static size_t coo_deg_bytes(int64_t n_out) { return 2 * align_up((size_t)std::max<int64_t>(n_out, 1) * 4, 256); }
 
 static bool use_plan(const pyg_plan* plan, uint32_t flags) { return plan && !(flags & PYG_FORCE_ATOMIC); }
 
@@ -124,6 +138,7 @@ pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t fla
     REQUIRE(E <= kMaxI32 && n <= kMaxI32, PYG_ERR_UNSUPPORTED, "degree: sizes must be < 2^31");
     cudaStream_t s = as_stream(stream);
     if (flags & PYG_VALIDATE) {
+        validate_begin();
         PYG_TRY(validate_index(index, E, 0, n, s));
         PYG_TRY(validate_flag_check(s, "degree: index out of range"));
     }
@@ -267,6 +282,7 @@ pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx
     REQUIRE(n * F == 0 || (x && rows && out), PYG_ERR_INVALID_ARGUMENT, "gather_rows: null pointer");
     cudaStream_t s = as_stream(stream);
     if (flags & PYG_VALIDATE) {
+        validate_begin();
         PYG_TRY(validate_index(rows, n, 0, n_x, s));
         PYG_TRY(validate_flag_check(s, "gather_rows: row index out of range"));
     }
@@ -280,11 +296,13 @@ pyg_status_t pyg_plan_export(const pyg_plan_t* p, int64_t* rowptr, int64_t* col,
     return plan_export_impl(p, rowptr, col, perm, as_stream(stream));
 }
 
-pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t n_out, int64_t F_out, pyg_reduce_t reduce,
-                                uint32_t flags, size_t* bytes) {
-    REQUIRE(bytes && n_out >= 0 && F_out >= 0, PYG_ERR_INVALID_ARGUMENT, "workspace_size: bad args");
-    size_t b = coo_ws_bytes(n_out);
-    if (use_plan(plan, flags)) b = std::max(b, segment_ws_bytes(plan, F_out, (int)reduce));
+pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t E, int64_t n_out, int64_t F_out,
+                                pyg_reduce_t reduce, uint32_t flags, size_t* bytes) {
+    REQUIRE(bytes && E >= 0 && n_out >= 0 && F_out >= 0, PYG_ERR_INVALID_ARGUMENT, "workspace_size: bad args");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "workspace_size: bad reduce");
+    size_t b;
+    if (use_plan(plan, flags)) b = std::max(coo_deg_bytes(n_out), segment_ws_bytes(plan, F_out, (int)reduce));
+    else b = coo_deg_bytes(n_out) + coo_ws_bytes(E, n_out, F_out, (int)reduce);
     *bytes = b + 256;
     return PYG_OK;
 }
@@ -302,6 +320,7 @@ pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, co
     REQUIRE(!(flags & PYG_FORCE_SEGMENT) || plan, PYG_ERR_INVALID_ARGUMENT, "scatter: FORCE_SEGMENT without plan");
     cudaStream_t s = as_stream(stream);
     if (flags & PYG_VALIDATE) {
+        validate_begin();
         PYG_TRY(validate_index(index, E, 0, dim_size, s));
         PYG_TRY(validate_flag_check(s, "scatter: index out of range"));
     }
@@ -324,17 +343,7 @@ pyg_status_t pyg_scatter(const float* src, int64_t E, int64_t F, int64_t lds, co
     c.out = out; c.ldo = ldo;
     c.keys = reinterpret_cast<unsigned long long*>(arg_out); c.ldk = ldo;
     c.E = E; c.n_out = dim_size;
-    PYG_TRY(coo_reduce(c, reduce, s));
-    if (reduce == PYG_MEAN) {
-        Carver cv(ws, ws_bytes);
-        int32_t* deg = cv.take<int32_t>((size_t)dim_size);
-        REQUIRE(ws && cv.ok(), PYG_ERR_NO_MEMORY, "scatter: workspace too small for mean");
-        PYG_TRY(coo_degree(index, E, dim_size, deg, nullptr, s));
-        PYG_TRY(mean_divide(out, ldo, (int)F, dim_size, deg, s));
-    } else if (reduce == PYG_MAX) {
-        PYG_TRY(max_decode(c.keys, ldo, out, ldo, (int)F, dim_size, E, s));
-    }
-    return PYG_OK;
+    return coo_reduce(c, reduce, ws, ws_bytes, s);
 }
 
 pyg_status_t pyg_scatter_backward(const float* grad_out, int64_t ldg, const int64_t* index, int64_t E, int64_t F,
@@ -379,7 +388,7 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         PYG_TRY(validate_flag_check(s, "propagate: edge_index out of range"));
     }
     if (n_dst == 0 || F_out == 0) return PYG_OK;
-    const float* xd = x_dst ? x_dst : x_src;
+    const float* xd = x_dst ? x_dst : x_src;  // (offset below for slices)
     const int64_t ldd = x_dst ? ldxd : ldx;
     const int64_t off1 = cat ? F : 0, off2 = off1 + F;
 
@@ -387,6 +396,12 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         REQUIRE(plan->n_rows == n_dst && (plan->col != nullptr || plan->E == 0) && plan->n_cols <= n_src, PYG_ERR_DIMENSION,
                 "propagate: plan does not match (n_rows %lld vs n_dst %lld)", (long long)plan->n_rows, (long long)n_dst);
         const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
+        if (cat && !x_dst && plan->row_offset > 0) {
+            // a slice's output row r is global row row_offset + r: its x_i is x_src[row_offset + r]
+            REQUIRE(plan->row_offset + n_dst <= n_src, PYG_ERR_DIMENSION,
+                    "propagate: CONCAT_XI on a slice with x_dst = NULL needs row_offset + n_dst <= n_src");
+            xd = x_src + plan->row_offset * ldx;
+        }
         if (cat && !plan->parts.empty()) {
             REQUIRE(reduce != PYG_MAX, PYG_ERR_UNSUPPORTED, "propagate: CONCAT_XI + MAX needs an unblocked plan");
             REQUIRE(plan->n_passes == 0, PYG_ERR_UNSUPPORTED, "propagate: CONCAT_XI needs the whole plan, not a pass view");
@@ -435,10 +450,8 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         c.keys = arg_out ? reinterpret_cast<unsigned long long*>(arg_out + off) : nullptr; c.ldk = ldo;
         c.E = E; c.n_out = n_dst;
         c.allow_pad_read = (X == x_src);
-        PYG_TRY(coo_reduce(c, reduce, s));
-        if (reduce == PYG_MEAN) PYG_TRY(mean_divide(out + off, ldo, (int)nc, n_dst, deg, s));
-        if (reduce == PYG_MAX) PYG_TRY(max_decode(c.keys, ldo, out + off, ldo, (int)nc, n_dst, E, s));
-        return PYG_OK;
+        c.deg = need_deg ? deg : nullptr;
+        return coo_reduce(c, reduce, cv.rest(), cv.rest_bytes(), s);
     };
     if (F > 0) PYG_TRY(block(x_src, ldx, F, edge_index, edge_weight, off1));
     if (D > 0) PYG_TRY(block(edge_attr, lde, D, nullptr, nullptr, off2));
@@ -468,6 +481,7 @@ pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F
             PYG_ERR_INVALID_ARGUMENT, "propagate_backward: deg_dst required");
     cudaStream_t s = as_stream(stream);
     if (flags & PYG_VALIDATE) {
+        validate_begin();
         PYG_TRY(validate_index(edge_index, E, 0, n_src, s));
         PYG_TRY(validate_index(edge_index + E, E, 0, n_dst, s));
         PYG_TRY(validate_flag_check(s, "propagate_backward: edge_index out of range"));
@@ -503,7 +517,7 @@ pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F
             c.X = grad_out + off1; c.ldx = ldg; c.ncols = (int)F;
             c.gidx = dst; c.sidx = src; c.w = edge_weight; c.gdeg = reduce == PYG_MEAN ? deg_dst : nullptr;
             c.out = grad_x_src; c.ldo = ldgx; c.E = E; c.n_out = n_src;
-            PYG_TRY(coo_reduce(c, PYG_SUM, s));
+            PYG_TRY(coo_reduce(c, PYG_SUM, ws, ws_bytes, s));
         }
     }
     if (grad_edge_attr && D > 0) {
@@ -533,6 +547,7 @@ pyg_status_t pyg_gcn_norm(const int64_t* edge_index, int64_t E, int64_t N, const
     REQUIRE(E + N <= kMaxI32, PYG_ERR_UNSUPPORTED, "gcn_norm: sizes must be < 2^31");
     cudaStream_t s = as_stream(stream);
     if (flags & PYG_VALIDATE) {
+        validate_begin();
         PYG_TRY(validate_index(edge_index, 2 * E, 0, N, s));
         PYG_TRY(validate_flag_check(s, "gcn_norm: edge_index out of range"));
     }

@@ -45,10 +45,14 @@ struct Carver {
         return p;
     }
     bool ok() const { return off <= cap; }
+    // the uncarved tail (for a callee that carves its own buffers)
+    void* rest() const { return base ? base + align_up(off, 256) : nullptr; }
+    size_t rest_bytes() const { return cap > align_up(off, 256) ? cap - align_up(off, 256) : 0; }
 };
 
 // Device-side validation flag (pinned, mapped) -- PYG_VALIDATE paths.
 int* validate_flag_dev();
+void validate_begin();  // clear this thread's flag before launching checking kernels
 pyg_status_t validate_flag_check(cudaStream_t s, const char* what);
 pyg_status_t validate_index(const int64_t* idx, int64_t n, int64_t lo, int64_t hi,
                             cudaStream_t s);

@@ -3,22 +3,34 @@
 //
 //   * a group of `lpr` lanes walks a contiguous run of `epg` edges in input order,
 //     fusing the gather of x_j and phi;
-//   * equal consecutive targets are aggregated in registers and flushed with one
-//     vector red.global.add.v{2,4}.f32 (REDG.E.ADD.F32x4) per run -- for
-//     target-sorted ("coalesced") input this removes almost all atomics,
-//     for unsorted input it degrades to one RED per element, which is the
-//     paper's scheme ("GS is always fast, nevertheless of the input being
-//     coalesced");
+//   * warp-aggregated atomics: each batch of lpr edges is matched on its targets
+//     (__match_any_sync) and visited in grouped order, so edges with equal targets --
+//     consecutive (target-sorted, "coalesced" input) or not (unsorted input) --
+//     are summed in registers and flushed with ONE vector red.global.add.v{2,4}.f32
+//     (REDG.E.ADD.F32x4) per distinct target; for unsorted input with distinct
+//     targets this is one RED per element, the paper's scheme ("GS is always
+//     fast, nevertheless of the input being coalesced");
+//   * hub rows (in-degree > kHeavyThreshold) would otherwise be one fp32 atomic chain
+//     of up to ~306k terms (R-MAT), which breaks the tolerance (reading Q12).  Their
+//     edges are routed to slots of at most kCooSlot entries each (a per-hub counter,
+//     warp-aggregated, hands out positions; slot = position / kCooSlot), the slot
+//     partials live in an L2-sized workspace, and hub_combine_kernel sums them in
+//     fp64 -- every fp32 chain stays <= 1024 terms on the atomic strategy too;
 //   * MAX uses 64-bit atomicMax on a packed key (order-preserving value bits in
 //     the high word, 0xffffffff - edge id in the low word), so the result is
 //     deterministic and ties go to the lowest edge id (Q4) without a second pass
 //     over the edges; the keys live in the caller's arg_out buffer and are
-//     decoded in place.
+//     decoded in place.  A key is only sent to the L2 atomic unit when it beats the
+//     key currently stored (keys only grow, so a stale read is never too high):
+//     after the first few edges of a segment almost every element is a plain read,
+//     which saves the dirty-line write-back of the atomic.
 #include "kernels.cuh"
 
 namespace pyg {
 
 namespace {
+
+constexpr int kCooSlot = 1024;  // entries per hub slot (fp32 chain bound of the atomic path)
 
 template <int NCH>
 struct Unroll { static constexpr int U = NCH <= 2 ? 4 : (NCH <= 5 ? 2 : 1); };
@@ -40,11 +52,27 @@ __device__ __forceinline__ void flush(const CooArgs& a, int64_t cur, int l, int 
         const int nv = min(V, a.ncols - col);
         if (RED == PYG_MAX) {
             unsigned long long* kp = a.keys + cur * a.ldk + col;
+            unsigned long long have[V];
+            if (V >= 2 && nv == V && (reinterpret_cast<uintptr_t>(kp) & 15) == 0) {
 #pragma unroll
-            for (int q = 0; q < V; ++q)
-                if (q < nv && bi[ch][q] >= 0) atomicMax(kp + q, max_key(acc[ch][q], (uint32_t)bi[ch][q]));
+                for (int q = 0; q < V; q += 2) {
+                    const ulonglong2 t = __ldcg(reinterpret_cast<const ulonglong2*>(kp + q));
+                    have[q] = t.x;
+                    if (q + 1 < V) have[q + 1] = t.y;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < V; ++q) have[q] = q < nv ? __ldcg(kp + q) : ~0ull;
+            }
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                if (q < nv && bi[ch][q] >= 0) {
+                    const unsigned long long k = max_key(acc[ch][q], (uint32_t)bi[ch][q]);
+                    if (k > have[q]) atomicMax(kp + q, k);
+                }
+            }
         } else {
-            float* op = a.out + cur * a.ldo + col;
+            float* op = cur < a.n_out ? a.out + cur * a.ldo + col : a.part + (cur - a.n_out) * a.ldp + col;
             if (out_vec_ok) redv<V>(op, acc[ch], nv);
             else {
 #pragma unroll
@@ -60,6 +88,7 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
     const int groups = blockDim.x / lpr;
     const int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / lpr;
     const int l = threadIdx.x & (lpr - 1);
+    const int gbase = (threadIdx.x & 31) & ~(lpr - 1);  // first lane of the group in its warp
     const int c0 = blockIdx.y * (lpr * NCH * V);
     const unsigned mask = group_mask(lpr);
     const int64_t e0 = gid * epg;
@@ -102,7 +131,7 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
 
     for (int64_t base = e0; base < e1; base += lpr) {
         const int n = (int)min((int64_t)lpr, e1 - base);
-        long long mi = 0, mg = 0;
+        long long mi = -1 - (long long)l, mg = 0;  // unique keys for lanes without an edge
         float ms = 1.0f;
         if (l < n) {
             const int64_t p = base + l;
@@ -111,16 +140,52 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
             if (a.w) ms = __ldg(a.w + p);
             if (a.gdeg) ms = ms / (float)__ldg(a.gdeg + mg);
         }
+        // hub rows: entry position from the hub's counter (one atomic per hub and batch),
+        // target -> the slot's virtual row n_out + slot
+        if (RED != PYG_MAX && a.hub_base) {
+            const int hb = l < n ? __ldg(a.hub_base + mi) : -1;
+            if (__any_sync(mask, hb >= 0)) {
+                const unsigned hm = __match_any_sync(mask, hb >= 0 ? mi : -1 - (long long)l);
+                const int lead = __ffs(hm) - 1;  // absolute lane of the group's first member
+                const int rank = __popc(hm & ((1u << (threadIdx.x & 31)) - 1u));
+                int b = 0;
+                if (hb >= 0 && (int)(threadIdx.x & 31) == lead)
+                    b = atomicAdd(a.hub_cursor + (int64_t)hb * gridDim.y + blockIdx.y, __popc(hm));
+                b = __shfl_sync(mask, b, lead - gbase, lpr);
+                if (hb >= 0) mi = a.n_out + hb + (b + rank) / kCooSlot;
+            }
+        }
+        // warp-aggregated atomics: visit the batch grouped by target (first-occurrence order)
+        const unsigned gm = __match_any_sync(mask, mi) >> gbase;  // group-relative member mask
+        const int lo = __ffs(gm) - 1;
+        const bool contiguous = (((gm >> lo) & ((gm >> lo) + 1u)) == 0u);
+        const bool permute = !__all_sync(mask, contiguous);
+        int pos = l;
+        if (permute) {
+            int v = (lo == l) ? __popc(gm) : 0;
+            for (int d = 1; d < lpr; d <<= 1) {
+                const int t = __shfl_up_sync(mask, v, d, lpr);
+                if (l >= d) v += t;
+            }
+            const int incl = __shfl_sync(mask, v, lo, lpr);
+            pos = incl - __popc(gm) + __popc(gm & ((1u << l) - 1u));
+        }
+        auto src_of = [&](int t) -> int {
+            return permute ? (__ffs(__ballot_sync(mask, pos == t)) - 1 - gbase) : t;
+        };
         int t = 0;
         for (; t + U <= n; t += U) {
             float v[U][NCH][V];
             float sv[U];
             long long iv[U];
+            int ev[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const long long g = __shfl_sync(mask, mg, t + u, lpr);
-                sv[u] = __shfl_sync(mask, ms, t + u, lpr);
-                iv[u] = __shfl_sync(mask, mi, t + u, lpr);
+                const int sl = src_of(t + u);
+                const long long g = __shfl_sync(mask, mg, sl, lpr);
+                sv[u] = __shfl_sync(mask, ms, sl, lpr);
+                iv[u] = __shfl_sync(mask, mi, sl, lpr);
+                ev[u] = (int)(base + sl);
                 const float* row = a.X + g * a.ldx + c0;
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
@@ -132,12 +197,13 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
                 }
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) consume(iv[u], (int)(base + t + u), sv[u], v[u]);
+            for (int u = 0; u < U; ++u) consume(iv[u], ev[u], sv[u], v[u]);
         }
         for (; t < n; ++t) {
-            const long long g = __shfl_sync(mask, mg, t, lpr);
-            const float sc = __shfl_sync(mask, ms, t, lpr);
-            const long long i = __shfl_sync(mask, mi, t, lpr);
+            const int sl = src_of(t);
+            const long long g = __shfl_sync(mask, mg, sl, lpr);
+            const float sc = __shfl_sync(mask, ms, sl, lpr);
+            const long long i = __shfl_sync(mask, mi, sl, lpr);
             float v[NCH][V];
             const float* row = a.X + g * a.ldx + c0;
 #pragma unroll
@@ -148,7 +214,7 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
                     for (int q = 0; q < V; ++q) v[ch][q] = 0.0f;
                 }
             }
-            consume(i, (int)(base + t), sc, v);
+            consume(i, (int)(base + sl), sc, v);
         }
     }
     if (cur >= 0) flush<V, NCH, RED>(a, cur, l, lpr, c0, cv, acc, bi, out_vec_ok);
@@ -194,6 +260,50 @@ __global__ void degree_kernel(const int64_t* __restrict__ sidx, int64_t E, int32
     }
 }
 
+// hub rows: deg > threshold -> ceil(deg / kCooSlot) consecutive slots, their counters zeroed
+// (one per column tile); counters[0] = hubs, counters[1] = slots handed out
+__global__ void hub_assign_kernel(const int32_t* __restrict__ deg, int64_t n, int threshold, int tiles,
+                                  int32_t* hub_base, int32_t* hub_rows, int32_t* counters, int32_t* cursor) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = deg[i];
+        int hb = -1;
+        if (d > threshold) {
+            const int ns = (d + kCooSlot - 1) / kCooSlot;
+            hb = atomicAdd(counters + 1, ns);
+            hub_rows[atomicAdd(counters, 1)] = (int32_t)i;
+            for (int t = 0; t < tiles; ++t) cursor[(int64_t)hb * tiles + t] = 0;
+        }
+        hub_base[i] = hb;
+    }
+}
+
+__global__ void zero_slots_kernel(float* part, int64_t ldp, const int32_t* __restrict__ counters) {
+    const int64_t total = (int64_t)counters[1] * ldp;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
+        part[t] = 0.0f;
+}
+
+// out[hub] = fp64 sum of the hub's slot partials in slot order (/ deg for mean): Q12 on the
+// atomic path
+template <int RED>
+__global__ void hub_combine_kernel(float* out, int64_t ldo, int ncols, const float* __restrict__ part, int64_t ldp,
+                                   const int32_t* __restrict__ hub_rows, const int32_t* __restrict__ hub_base,
+                                   const int32_t* __restrict__ deg, const int32_t* __restrict__ counters) {
+    const int nh = counters[0];
+    for (int h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int64_t r = hub_rows[h];
+        const int d = deg[r];
+        const int64_t b = hub_base[r];
+        const int ns = (d + kCooSlot - 1) / kCooSlot;
+        for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
+            double s = 0.0;
+            for (int k = 0; k < ns; ++k) s += (double)part[(b + k) * ldp + c];
+            if (RED == PYG_MEAN) s = d > 0 ? s / (double)d : 0.0;
+            out[r * ldo + c] = (float)s;
+        }
+    }
+}
+
 __global__ void mean_div_kernel(float* out, int64_t ldo, int ncols, int64_t n, const int32_t* __restrict__ deg) {
     const int64_t total = n * ncols;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
@@ -228,9 +338,56 @@ int grid_for(int64_t work, int threads = 256) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
 }
 
+struct CooGeom {
+    int V, lpr, nch, tiles, ovk;
+};
+
+CooGeom coo_geometry(const CooArgs& a, int reduce) {
+    CooGeom g{1, 4, 1, 1, 0};
+    for (int cand : {4, 2}) {
+        const bool cols_ok = (a.ncols % cand == 0) || (a.allow_pad_read && cand == 4 &&
+                                                       a.ldx >= (int64_t)align_up(a.ncols, 4));
+        if (cols_ok && a.ldx % cand == 0 && aligned(a.X, 4 * cand)) { g.V = cand; break; }
+    }
+    g.ovk = (reduce != PYG_MAX) && (a.ldo % g.V == 0) && aligned(a.out, 4 * g.V) &&
+            (!a.part || (a.ldp % g.V == 0 && aligned(a.part, 4 * g.V)));
+    const int64_t nvec = cdiv(a.ncols, g.V);
+    if (nvec <= 32) {
+        while (g.lpr < nvec) g.lpr <<= 1;
+    } else {
+        g.lpr = 32;
+        int64_t need = cdiv(nvec, 32);
+        g.tiles = (int)cdiv(need, 16);
+        need = cdiv(nvec, 32 * (int64_t)g.tiles);
+        g.nch = 16;
+        for (int c : kNch) if (c >= need) { g.nch = c; break; }
+    }
+    return g;
+}
+
+// hub workspace capacity: at most E / (threshold + 1) hubs, and sum ceil(d / slot) <= E / slot + hubs
+int64_t hub_cap(int64_t E) { return E / (kHeavyThreshold + 1) + 1; }
+int64_t slot_cap(int64_t E) { return E / kCooSlot + hub_cap(E); }
+int64_t max_tiles(int64_t ncols) { return std::max<int64_t>(1, cdiv(ncols, 32 * 16)); }  // V = 1 worst case
+
 }  // namespace
 
-pyg_status_t coo_reduce(const CooArgs& a, int reduce, cudaStream_t s) {
+size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce) {
+    if (reduce == PYG_MAX || E <= 0) return 0;
+    Carver cv(nullptr, 0);
+    cv.take<int32_t>((size_t)std::max<int64_t>(n_out, 1));  // deg
+    if (E > kHeavyThreshold) {
+        cv.take<int32_t>((size_t)n_out);                             // hub_base
+        cv.take<int32_t>((size_t)hub_cap(E));                        // hub_rows
+        cv.take<int32_t>(4);                                         // counters
+        cv.take<int32_t>((size_t)(slot_cap(E) * max_tiles(ncols)));  // cursors
+        cv.take<float>((size_t)slot_cap(E) * align_up((size_t)ncols, 4));  // slot partials
+    }
+    return cv.off + 256;
+}
+
+pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes, cudaStream_t s) {
+    CooArgs a = a0;
     if (a.n_out <= 0 || a.ncols <= 0) return PYG_OK;
     // zero the accumulation target (outputs are overwritten, Q14)
     if (reduce == PYG_MAX) {
@@ -238,35 +395,63 @@ pyg_status_t coo_reduce(const CooArgs& a, int reduce, cudaStream_t s) {
     } else {
         PYG_CUDA(cudaMemset2DAsync(a.out, a.ldo * 4, 0, (size_t)a.ncols * 4, (size_t)a.n_out, s));
     }
-    if (a.E <= 0) return PYG_OK;
-    int V = 1;
-    for (int cand : {4, 2}) {
-        const bool cols_ok = (a.ncols % cand == 0) || (a.allow_pad_read && cand == 4 &&
-                                                       a.ldx >= (int64_t)align_up(a.ncols, 4));
-        if (cols_ok && a.ldx % cand == 0 && aligned(a.X, 4 * cand)) { V = cand; break; }
+    if (a.E <= 0) {
+        if (reduce == PYG_MAX) PYG_TRY(max_decode(a.keys, a.ldk, a.out, a.ldo, a.ncols, a.n_out, a.E, s));
+        return PYG_OK;
     }
-    const int ovk = (reduce != PYG_MAX) && (a.ldo % V == 0) && aligned(a.out, 4 * V);
-    const int64_t nvec = cdiv(a.ncols, V);
-    int lpr, nch, tiles;
-    if (nvec <= 32) {
-        lpr = 4;
-        while (lpr < nvec) lpr <<= 1;
-        nch = 1;
-        tiles = 1;
-    } else {
-        lpr = 32;
-        int64_t need = cdiv(nvec, 32);
-        tiles = (int)cdiv(need, 16);
-        need = cdiv(nvec, 32 * (int64_t)tiles);
-        nch = 16;
-        for (int c : kNch) if (c >= need) { nch = c; break; }
+    int32_t* deg = nullptr;
+    int32_t* counters = nullptr;
+    int32_t* hub_rows = nullptr;
+    int32_t* hub_base = nullptr;
+    const bool hubs = reduce != PYG_MAX && a.E > kHeavyThreshold;
+    if (reduce != PYG_MAX) {
+        Carver cv(ws, ws_bytes);
+        deg = cv.take<int32_t>((size_t)std::max<int64_t>(a.n_out, 1));
+        if (hubs) {
+            hub_base = cv.take<int32_t>((size_t)a.n_out);
+            a.hub_base = hub_base;
+            hub_rows = cv.take<int32_t>((size_t)hub_cap(a.E));
+            counters = cv.take<int32_t>(4);
+            a.hub_cursor = cv.take<int32_t>((size_t)(slot_cap(a.E) * max_tiles(a.ncols)));
+            a.ldp = (int64_t)align_up((size_t)a.ncols, 4);
+            a.part = cv.take<float>((size_t)slot_cap(a.E) * a.ldp);
+        }
+        if (!ws || !cv.ok())
+            return fail(PYG_ERR_NO_MEMORY, "atomic scatter: workspace too small (%zu < %zu bytes, see pyg_workspace_size)",
+                        ws_bytes, coo_ws_bytes(a.E, a.n_out, a.ncols, reduce));
+        if (a.deg) deg = const_cast<int32_t*>(a.deg);
+        else PYG_TRY(coo_degree(a.sidx, a.E, a.n_out, deg, nullptr, s));
     }
-    const int epg = lpr * 8;  // 8 batches of lpr edges per group
-    switch (reduce) {
-        case PYG_SUM:
-        case PYG_MEAN: return launch_red<PYG_SUM>(a, V, nch, lpr, tiles, epg, ovk, s);
-        default: return launch_red<PYG_MAX>(a, V, nch, lpr, tiles, epg, ovk, s);
+    const CooGeom g = coo_geometry(a, reduce);
+    if (hubs) {
+        PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
+        hub_assign_kernel<<<grid_for(a.n_out), 256, 0, s>>>(deg, a.n_out, kHeavyThreshold, g.tiles, hub_base,
+                                                              hub_rows, counters, a.hub_cursor);
+        PYG_LAUNCHED();
+        zero_slots_kernel<<<148 * 4, 256, 0, s>>>(a.part, a.ldp, counters);
+        PYG_LAUNCHED();
+        PYG_CUDA(cudaGetLastError());
     }
+    const int epg = g.lpr * 8;  // 8 batches of lpr edges per group
+    if (reduce == PYG_MAX) {
+        PYG_TRY(launch_red<PYG_MAX>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
+        return max_decode(a.keys, a.ldk, a.out, a.ldo, a.ncols, a.n_out, a.E, s);
+    }
+    PYG_TRY(launch_red<PYG_SUM>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
+    if (reduce == PYG_MEAN) PYG_TRY(mean_divide(a.out, a.ldo, a.ncols, a.n_out, deg, s));
+    if (hubs) {
+        const int ct = (int)std::min<int64_t>(256, align_up((size_t)a.ncols, 32));
+        const int blocks = (int)std::min<int64_t>(hub_cap(a.E), 148 * 8);
+        if (reduce == PYG_MEAN)
+            hub_combine_kernel<PYG_MEAN><<<blocks, ct, 0, s>>>(a.out, a.ldo, a.ncols, a.part, a.ldp, hub_rows,
+                                                              a.hub_base, deg, counters);
+        else
+            hub_combine_kernel<PYG_SUM><<<blocks, ct, 0, s>>>(a.out, a.ldo, a.ncols, a.part, a.ldp, hub_rows,
+                                                             a.hub_base, deg, counters);
+        PYG_LAUNCHED();
+        PYG_CUDA(cudaGetLastError());
+    }
+    return PYG_OK;
 }
 
 pyg_status_t coo_degree(const int64_t* sidx, int64_t E, int64_t n, int32_t* deg, int32_t* first,

@@ -115,8 +115,18 @@ struct CooArgs {
     int64_t E = 0;
     int64_t n_out = 0;
     int allow_pad_read = 0;
+    const int32_t* deg = nullptr;   // in-degree of the targets if the caller has it (else computed)
+    // hub routing (SUM / MEAN; set up by coo_reduce): rows with more than kHeavyThreshold entries
+    // spread their edges over slots of <= kCooSlot entries, combined in fp64 (reading Q12)
+    const int32_t* hub_base = nullptr;  // [n_out] first slot of a hub row, -1 otherwise
+    int32_t* hub_cursor = nullptr;      // [slots x column tiles] entry counters (by first slot)
+    float* part = nullptr;              // [slots x ldp] slot partials = virtual rows n_out + slot
+    int64_t ldp = 0;
 };
-pyg_status_t coo_reduce(const CooArgs& a, int reduce, cudaStream_t s);
+// Whole atomic reduce of one column block: zero the target, degrees and hub slots (SUM / MEAN),
+// the COO kernel, then the epilogue (mean divide + fp64 hub combine, or the MAX key decode).
+pyg_status_t coo_reduce(const CooArgs& a, int reduce, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce);
 // counts (and first edge id) per target for the COO path
 pyg_status_t coo_degree(const int64_t* sidx, int64_t E, int64_t n, int32_t* deg, int32_t* first,
                         cudaStream_t s);

@@ -347,6 +347,7 @@ pyg_status_t gcn_norm_impl(const int64_t* ei, int64_t E, int64_t N, const float*
 pyg_status_t collate_impl(int64_t G, const int64_t* num_nodes, const int64_t* edge_ptr, const int64_t* local,
                           int64_t Et, int64_t Nt, uint32_t flags, int64_t* ei, int64_t* batch, int64_t* node_ptr,
                           cudaStream_t s) {
+    if (flags & PYG_VALIDATE) validate_begin();
     int* flag = (flags & PYG_VALIDATE) ? validate_flag_dev() : nullptr;
     scan_ptr_kernel<<<1, 1024, 0, s>>>(num_nodes, G, node_ptr, flag);
     LAUNCH_CHECK();

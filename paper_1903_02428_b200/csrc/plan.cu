@@ -68,6 +68,14 @@ __global__ void col_gather(const int64_t* __restrict__ col, const int32_t* __res
     }
 }
 
+__global__ void block_deg_kernel(const int64_t* __restrict__ rowptr, int64_t nb, int64_t n_rows, int32_t* deg) {
+    GRID_STRIDE(r, n_rows) {
+        int64_t d = 0;
+        for (int64_t b = 0; b < nb; ++b) d += rowptr[b * n_rows + r + 1] - rowptr[b * n_rows + r];
+        deg[r] = (int32_t)d;
+    }
+}
+
 __global__ void heavy_flags(const int64_t* __restrict__ rowptr, int64_t n_rows, int thr, int32_t* flag_heavy) {
     GRID_STRIDE(r, n_rows) flag_heavy[r] = (rowptr[r + 1] - rowptr[r]) > thr ? 1 : 0;
 }
@@ -143,7 +151,7 @@ static size_t plan_layout(void* ws, size_t bytes, int64_t E, int64_t n_rows, int
     L.heavy_rows = cv.take<int32_t>(v);
     L.item_ptr = cv.take<int64_t>(v + 1);
     L.deg = n_blocks > 1 ? cv.take<int32_t>((size_t)std::max<int64_t>(n_rows, 1)) : nullptr;
-    L.flags2 = cv.take<int>(2);
+    L.flags2 = cv.take<int>(3);  // [0] perm not identity, [1] empty rows, [2] index out of range
     // scratch
     L.keys = cv.take<int32_t>(e);
     L.vals = cv.take<int32_t>(e);
@@ -212,8 +220,9 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
     int64_t thr = 0, chunk = 0;
     split_params(E, V, nb, &thr, &chunk);
     if (!ws || need > bytes) return fail(PYG_ERR_NO_MEMORY, "plan workspace too small (%zu < %zu)", bytes, need);
-    int* flag = validate_flag_dev();
-    PYG_CUDA(cudaMemsetAsync(L.flags2, 0, 2 * sizeof(int), s));
+    // the out-of-range flag lives in the plan's own workspace (no process-wide state)
+    int* flag = L.flags2 + 2;
+    PYG_CUDA(cudaMemsetAsync(L.flags2, 0, 3 * sizeof(int), s));
     if (E > 0) {
         keys_init<<<grid_for(E), 256, 0, s>>>(row, col, E, n_rows, n_cols, nb > 1 ? col_block : 0, L.keys, L.vals,
                                               flag);
@@ -230,7 +239,10 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
         col_gather<<<grid_for(E), 256, 0, s>>>(col, L.perm, E, L.col, L.flags2);
         LAUNCH_CHECK();
     }
-    if (nb > 1) PYG_TRY(coo_degree(row, E, n_rows, L.deg, nullptr, s));
+    if (nb > 1) {  // total in-degree = sum of the row's lengths over the blocks (clamped keys: in bounds)
+        block_deg_kernel<<<grid_for(n_rows), 256, 0, s>>>(L.rowptr, nb, n_rows, L.deg);
+        LAUNCH_CHECK();
+    }
     std::vector<int64_t> h_rowptr;
     if (nb == 1 && V > 0) {
         order_keys<<<grid_for(V), 256, 0, s>>>(L.rowptr, V, L.okeys, L.ovals, L.flags2 + 1);
@@ -319,10 +331,10 @@ pyg_status_t plan_build_impl(const int64_t* row, const int64_t* col, int64_t E, 
         }
         PYG_CUDA(cudaStreamSynchronize(s));  // tp / ti are locals
     }
-    int flags2[2] = {0, 0};
+    int flags2[3] = {0, 0, 0};
     PYG_CUDA(cudaMemcpyAsync(flags2, L.flags2, sizeof(flags2), cudaMemcpyDeviceToHost, s));
-    pyg_status_t st = validate_flag_check(s, "plan_build: index out of range");
-    if (st != PYG_OK) return st;
+    PYG_CUDA(cudaStreamSynchronize(s));
+    if (flags2[2]) return fail(PYG_ERR_INDEX_OUT_OF_BOUNDS, "plan_build: index out of range");
 
     pyg_plan root;
     root.n_rows = V;

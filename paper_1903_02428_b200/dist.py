@@ -78,6 +78,9 @@ class OverlappedGather:
                 works[q].wait()  # the compute stream waits for owner q's rows (host not blocked)
             if v is not None:
                 compute(v)
+        # the rank's own broadcast (issued last for rank world-1) must finish reading the shard before
+        # the caller rewrites it for the next step: order the current stream after it too
+        works[self.rank].wait()
 
 
 def gather_x(x_shard: torch.Tensor, world: int, group=None, out: Optional[torch.Tensor] = None) -> torch.Tensor:

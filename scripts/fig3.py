@@ -67,7 +67,7 @@ def main():
             planT = pg.pyg_plan_build(ei[0], ei[1], N, N)
             out = torch.empty((N, F), device=dev)
             gx = torch.empty((N, F), device=dev)
-            ws = torch.empty(max(1, pg.pyg_workspace_size(None, N, F, "sum")), dtype=torch.uint8, device=dev)
+            ws = torch.empty(max(1, pg.pyg_workspace_size(None, N, F, "sum", E=ei.shape[1])), dtype=torch.uint8, device=dev)
             wsp = torch.empty(max(1, pg.pyg_workspace_size(plan, N, F, "sum")), dtype=torch.uint8, device=dev)
             row = {"degree": d, "layout": layout, "N": N, "E": E, "F": F, "runs": a.runs}
             row["gs_atomic_fwd_ms"] = timed(lambda: pg.pyg_propagate(x, ei, reduce="sum", out=out, workspace=ws),

@@ -240,3 +240,80 @@ def test_config5_rmat_sampled(pg, rmat, red):
         check_exact(H(arg[trows]), map_arg(ref[1], eid, E))
     else:
         check_close(H(out[trows]), ref)
+
+
+# ------------------------------------------------- config 4 in bench's launch configuration
+# bench.py times the SOURCE-BLOCKED plan (pyg_plan_suggest_col_block: 11 L2-resident passes of
+# seg_kernel with accum / finalize); these tests run exactly that plan at full size.
+
+@pytest.fixture(scope="module")
+def reddit_blocked(pg, reddit):
+    ei, x, _ = reddit
+    N = x.shape[0]
+    E = ei.shape[1]
+    cb = pg.pyg_plan_suggest_col_block(E, N, N, 608 * 4)
+    assert cb > 0, "bench's Reddit plan is source-blocked on a B200 (126 MB L2)"
+    plan = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb)
+    assert plan.view()["n_col_blocks"] >= 2
+    yield plan, cb
+    del plan
+
+
+def _blocked_rows(N, cb, n, seed):
+    """random rows + the first / last rows + the rows on both sides of every source-block edge"""
+    edges = [k * cb + d for k in range(1, (N + cb - 1) // cb) for d in (-1, 0)]
+    extra = [0, 1] + list(range(N - 16, N)) + [r for r in edges if 0 <= r < N]
+    return _sampled_rows(N, n, seed, extra=extra)
+
+
+@pytest.mark.parametrize("red", ["mean", "sum", "max"])
+def test_config4_reddit_blocked_bench_plan(pg, reddit, reddit_blocked, red):
+    ei, x, _ = reddit
+    plan, cb = reddit_blocked
+    N, F = x.shape
+    E = ei.shape[1]
+    if red == "max":  # signed features: sign and ties matter for max (SURVEY 8(d))
+        gen = torch.Generator(DEV).manual_seed(414)
+        buf = torch.zeros((N, 608), dtype=torch.float32, device=DEV)
+        buf[:, :F] = torch.rand((N, F), generator=gen, device=DEV) * 2 - 1
+        x = buf[:, :F]
+    out = torch.empty((N, 608), dtype=torch.float32, device=DEV)[:, :F]
+    arg = torch.empty((N, 608), dtype=torch.int64, device=DEV)[:, :F] if red == "max" else None
+    pg.pyg_propagate(x, None, reduce=red, plan=plan, out=out, arg_out=arg, E=E)
+    rows = _blocked_rows(N, cb, 1200, 40)
+    trows = T(rows)
+    sub, eid = sub_problem(ei, trows, N)
+    ref = oracle.propagate(H(x), sub, n_dst=rows.size, reduce=red)
+    if red == "max":
+        check_exact(H(out[trows]), ref[0])
+        check_exact(H(arg[trows]), map_arg(ref[1], eid, E))
+    else:
+        check_close(H(out[trows]), ref)
+
+
+# ------------------------------------------------- config 5, atomic strategy (hub rows included)
+
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_config5_rmat_atomic_sampled(pg, rmat, red):
+    """The atomic COO strategy on the shuffled R-MAT edge list (no plan): the top-12 hubs
+    (in-degree up to ~306k) must meet the same tolerance as every other row (reading Q12)."""
+    ei, _ = rmat
+    N, F, E = synth.RMAT["N"], synth.RMAT["F"], ei.shape[1]
+    gen = torch.Generator(DEV).manual_seed(515)
+    x = torch.rand((N, F), generator=gen, device=DEV)
+    if red == "max":
+        x = x * 2 - 1
+    res = pg.pyg_propagate(x, ei, reduce=red)
+    out, arg = (res if red == "max" else (res, None))
+    deg = pg.pyg_degree(ei[1], N)
+    hubs = H(torch.topk(deg, 12).indices)
+    empty = H(torch.nonzero(deg == 0).flatten()[:20])
+    rows = _sampled_rows(N, 1000, 7, extra=np.concatenate([hubs, empty]))
+    trows = T(rows)
+    sub, eid = sub_problem(ei, trows, N)
+    ref = oracle.propagate(H(x), sub, n_dst=rows.size, reduce=red)
+    if red == "max":
+        check_exact(H(out[trows]), ref[0])
+        check_exact(H(arg[trows]), map_arg(ref[1], eid, E))
+    else:
+        check_close(H(out[trows]), ref)
