@@ -74,6 +74,11 @@ def parse():
                          "with several ranks on one GPU (tests); nccl is the measured backend")
     ap.add_argument("--no-overlap", action="store_true",
                     help="N > 1 with a source-blocked plan: one all-gather, then the propagate (no per-owner overlap)")
+    ap.add_argument("--dist-capi", action="store_true",
+                    help="run the propagate through the library's multi-GPU layer (pyg_dist_*: NCCL inside "
+                         "libpygs) also at N = 1 (at N > 1 with NCCL it is the default)")
+    ap.add_argument("--dist-python", action="store_true",
+                    help="N > 1 with NCCL: the torch.distributed exchange in dist.py instead of pyg_dist_*")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
@@ -488,12 +493,30 @@ def main():
     # dst-range partition (N > 1): rank owns targets [lo, hi) and their in-edges; X is sharded by
     # the same ranges and all-gathered every step (NCCL over NVLink).
     ranges, per = partition_rows(N, world)
+    # the library's multi-GPU layer (pyg_dist_plan_build / pyg_dist_propagate, NCCL inside libpygs):
+    # the product path at N > 1; --dist-capi runs it at N = 1 too
+    use_capi = (a.strategy == "segment" and a.op == "propagate" and a.exchange != "push" and
+                ((world > 1 and a.dist_backend == "nccl" and not a.dist_python) or a.dist_capi))
+    dplan = None
 
     t0 = time.perf_counter()
     plan_full = None
     col_block = 0
     overlap = False
-    if a.strategy == "segment":
+    if use_capi:
+        col_block = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4) if a.col_block == "auto" else int(a.col_block)
+        ids = [pg.pyg_dist_unique_id() if rank == 0 else None]
+        if dist:
+            dist.broadcast_object_list(ids, src=0)
+        comm = pg.pyg_dist_init(ids[0], rank, world)
+        dplan = pg.pyg_dist_plan_build(comm, ei, N, F, ld, col_block, a.exchange)
+        torch.cuda.synchronize()
+        col_block = dplan.col_block
+        per = dplan.per
+        ranges = [(min(q * per, N), min((q + 1) * per, N)) for q in range(world)]
+        if world == 1:  # the single-GPU extras below (e2e leg, variants, collate) use a plain plan
+            plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=col_block)
+    elif a.strategy == "segment":
         if a.col_block == "auto":
             col_block = pg.pyg_plan_suggest_col_block(E, N, N, ld * 4)
         else:
@@ -552,6 +575,11 @@ def main():
         shard[:n_loc] = x.as_strided((N, ld), (x.stride(0), 1))[lo:hi]
         x_full = xbuf[:, :F]
         plan = halo["plan"]
+    elif use_capi:
+        exchange = "capi-" + dplan.exchange + ("-overlap" if (dplan.col_block and world > 1) else "")
+        halo = dict(n=dplan.n_halo) if dplan.exchange == "halo" else None
+        x_full = dplan.x_shard()  # this rank's rows inside the library's exchange buffer
+        x_full.copy_(x.as_strided((N, ld), (x.stride(0), 1))[lo:hi, :F])
     elif world > 1 and overlap:
         from paper_1903_02428_b200.dist import OverlappedGather
 
@@ -589,8 +617,8 @@ def main():
     out = torch.empty((n_loc, ((F + 7) // 8 * 8) if a.config == "reddit" else F), dtype=torch.float32,
                       device=dev)[:, :F]
     arg = torch.empty((n_loc, out.stride(0)), dtype=torch.int64, device=dev)[:, :F] if red == "max" else None
-    ws = torch.empty(max(1, pg.pyg_workspace_size(plan, n_loc, F, red, E=ei_loc.shape[1])), dtype=torch.uint8,
-                     device=dev)
+    ws = None if use_capi else torch.empty(max(1, pg.pyg_workspace_size(plan, n_loc, F, red, E=ei_loc.shape[1])),
+                                           dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     passes, weighted, prep_ms = 1, False, 0.0
@@ -602,7 +630,9 @@ def main():
                          arg_out=arg, E=E if p is not None else None, workspace=ws)
 
     def compute():
-        if exchange == "allgather-overlap":  # the broadcasts and the per-owner passes interleave
+        if use_capi:  # exchange (all-gather / per-owner broadcasts / halo) + propagate, all in the library
+            pg.pyg_dist_propagate(dplan, x_full, red, out=out, arg_out=arg)
+        elif exchange == "allgather-overlap":  # the broadcasts and the per-owner passes interleave
             ovg.step(one)
         else:
             one(cur["plan"])
@@ -765,7 +795,8 @@ def main():
     # microseconds per call, so host launch overhead would otherwise dominate the device timeline
     # (all K timed steps are captured into ONE graph and replayed once, so the device runs them back
     # to back; per-step time = total / K)
-    use_graph = (a.graph == "on" or (a.graph == "auto" and a.config in ("cora", "pubmed", "clouds"))) and world == 1
+    use_graph = ((a.graph == "on" or (a.graph == "auto" and a.config in ("cora", "pubmed", "clouds"))) and world == 1
+                 and not use_capi)
     launches_per_replay = 0
     if use_graph:
         l0 = pg.launch_count()
@@ -860,7 +891,8 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": CONFIGS[a.config]["name"], "N": N, "E": E, "F": F, "ldx": ld, "reduce": red,
                    "strategy": a.strategy, "col_block": col_block,
-                   "col_blocks": plan_full.view()["n_col_blocks"] if plan_full is not None else 0,
+                   "col_blocks": plan_full.view()["n_col_blocks"] if plan_full is not None else (
+                       (-(-N // col_block) if col_block else 1) if dplan is not None else 0),
                    "parallelism": f"dst-range x{world}" if world > 1 else "single",
                    "exchange": exchange,
                    "cuda_graph": bool(use_graph),
@@ -973,7 +1005,9 @@ def main():
         def e2e_dist_step():
             dei.copy_(e2e_host["hei"], non_blocking=True)
             dxs.copy_(e2e_host["hx"], non_blocking=True)
-            da = DistAggregation(dei, N, world, rank, col_block=cb_e)
+            da = DistAggregation(dei, N, world, rank, col_block=cb_e, F=F, ld=ld,
+                                 comm=comm if dplan is not None else None,
+                                 exchange=a.exchange if dplan is not None else "allgather")
             shard_e = torch.zeros((da.per, ld), dtype=torch.float32, device=dev)
             shard_e[: da.hi - da.lo] = dxs
             r = da.forward(shard_e[:, :F], reduce=red)
@@ -996,8 +1030,9 @@ def main():
         result["e2e"] = {"value": units / (e_ms * 1e-3), "unit": "edges*F/s",
                          "h2d_bytes_per_step": int(e2e_host["hx"].numel() * 4 + e2e_host["hei"].numel() * 8),
                          "d2h_bytes_per_step": int(hout_e.numel() * 4), "ms_per_step": e_ms, "steps": k2,
-                         "includes": "per rank: H2D(edge list, own X rows) + global plan build + slice + NCCL "
-                                     "all-gather of X + propagate + D2H(own out rows); max over ranks"}
+                         "includes": "per rank: H2D(edge list, own X rows) + the dist plan build (global plan, "
+                                     "slice, halo / transposed local plan) + NCCL exchange of X + propagate + "
+                                     "D2H(own out rows); max over ranks"}
 
     # ---- e2e through the C ABI with host buffers (N = 1) ----
     if world == 1 and not a.no_e2e and passes == 1 and gat is None and appnp is None and gcn is None and gatl is None:

@@ -62,7 +62,7 @@ typedef enum {
     PYG_ERR_ALIGNMENT = 4,          /* a forced vector path on unaligned data */
     PYG_ERR_UNSUPPORTED = 5,        /* sizes beyond the int32-internal limits */
     PYG_ERR_CUDA = 6,               /* a CUDA runtime error (message in pyg_last_error) */
-    PYG_ERR_NCCL = 7,               /* reserved for the multi-GPU layer */
+    PYG_ERR_NCCL = 7,               /* NCCL missing or an NCCL call failed (pyg_dist_*) */
     PYG_ERR_NO_MEMORY = 8           /* workspace smaller than the size query returned */
 } pyg_status_t;
 
@@ -271,8 +271,13 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
  * optional (NULL to skip), overwritten:
  *   grad_x_src [n_src x F] stride ldgx:  sum_k w_k * dL/dm_k  over k with src_k = j
  *       (mean: dL/dm_k = g[dst_k] / deg[dst_k]; max: g routed to arg_out).
- *       With plan_T (row_index = edge_index[0], col_index = edge_index[1]) this
- *       is a deterministic segment-reduce over sources; else atomic COO.
+ *       SUM / MEAN with plan_T (row_index = edge_index[0], col_index =
+ *       edge_index[1]): a deterministic segment-reduce over sources; else atomic
+ *       COO.  MAX always routes g[i][c] to source src[arg[i][c]] with fp32
+ *       atomicAdd (plan_T unused): each (i, c) contributes to exactly one
+ *       source, so only sources that are the argmax of several (target, column)
+ *       pairs sum more than one term, in an unspecified (non-deterministic)
+ *       order -- within the summation bound, not bitwise reproducible.
  *   grad_x_dst [n_dst x F] stride ldgxd (CONCAT_XI block): deg*g (sum),
  *       g if deg > 0 (mean, max).
  *   grad_edge_attr [E x D] stride ldge: the e block of dL/dm_k.
@@ -439,6 +444,78 @@ pyg_status_t pyg_gat_transform(const float* X, int64_t M, int64_t K, int64_t ldx
                                int64_t H, int64_t C, int64_t ldw, const float* att_src,
                                const float* att_dst, float* Z, int64_t ldz, float* s_src, float* s_dst,
                                void* stream);
+
+/* ---- multi-GPU: dst-range partitioned propagate over NCCL ------------------------------------
+ * north_star (3), SURVEY 8(b) pyg_dist_init / pyg_dist_propagate and 8(e); the paper's own system
+ * is single-GPU (P:26 names multi-GPU support as PyG's, without a scheme).  One process per GPU.
+ * Rank p owns the targets -- and the X rows -- [lo_p, hi_p) = [p*per, min((p+1)*per, n)) with
+ * per = ceil(n / world) (rounded up to a multiple of the source block for source-blocked plans), and
+ * every in-edge of them, so the reduction is local and results equal the single-GPU call's (max /
+ * argmax bitwise; arg ids stay GLOBAL edge ids).  The exchange moves only source rows:
+ *   PYG_EXCHANGE_ALLGATHER  ncclAllGather of the X shards (dense graphs); with a source-blocked plan
+ *                           one ncclBroadcast per owner on a side stream, each owner's source blocks
+ *                           computed as soon as its rows land (compute / transfer overlap);
+ *   PYG_EXCHANGE_HALO       only the referenced remote rows (the halo, ascending global id), packed
+ *                           by the owner and delivered with grouped ncclSend / ncclRecv;
+ *   PYG_EXCHANGE_AUTO       halo if the largest halo is < half the all-gather rows, else all-gather
+ *                           (always all-gather for source-blocked plans).
+ * Backward: the local edges transposed give partial dL/dX for every referenced source, then
+ * ncclReduceScatter to the owners (all-gather) or the reverse halo (partials of the halo rows sent
+ * back, added per own row in rank order: deterministic for SUM / MEAN).
+ * NCCL is loaded at run time (dlopen libnccl.so.2, or $PYG_NCCL_LIB); if it is missing or an NCCL
+ * call fails the call returns PYG_ERR_NCCL.  All calls taking a comm or a dist plan are
+ * COLLECTIVE: every rank makes the same sequence of them.  Dist plans OWN their device buffers
+ * (cudaMalloc at build, freed by pyg_dist_plan_destroy) -- the exception to "the library never
+ * allocates" above; the communicator is released by pyg_dist_finalize. */
+typedef struct pyg_dist pyg_dist_t;
+typedef struct pyg_dist_plan pyg_dist_plan_t;
+#define PYG_EXCHANGE_AUTO 0
+#define PYG_EXCHANGE_ALLGATHER 1
+#define PYG_EXCHANGE_HALO 2
+typedef struct {
+    int64_t lo, hi, per;      /* own target / X rows [lo, hi); shard capacity per rank */
+    int exchange;             /* PYG_EXCHANGE_ALLGATHER or PYG_EXCHANGE_HALO (resolved) */
+    int64_t n_halo;           /* halo rows received per call (halo) */
+    int64_t n_send;           /* rows sent per call (halo) */
+    int64_t n_local_edges;    /* in-edges of the own targets */
+    int64_t col_block;        /* source rows per block (0: unblocked plan) */
+    float* x_shard;           /* (device) where this rank's X rows live inside the exchange buffer:
+                                 writing them here saves pyg_dist_propagate's copy */
+    int64_t ldx;              /* its row stride */
+    const pyg_plan_t* plan;   /* the rank's slice of the global forward plan */
+} pyg_dist_plan_info_t;
+
+/* 128-byte ncclUniqueId (host) for rank 0 to broadcast over its process group.  Synchronous. */
+pyg_status_t pyg_dist_unique_id(void* nccl_unique_id);
+/* Communicator over `world` ranks (call with the rank's GPU current).  Synchronous, collective. */
+pyg_status_t pyg_dist_init(const void* nccl_unique_id, int rank, int world, pyg_dist_t** comm);
+void pyg_dist_finalize(pyg_dist_t* comm);
+/* One rank's share of a graph: edge_index [2 x E] (device; the FULL graph, identical on every rank,
+ * read during the build only), n nodes, feature width F whose exchange buffers have row stride ld
+ * (ld >= F, ld % 4 == 0), col_block as pyg_plan_build (0: unblocked; see
+ * pyg_plan_suggest_col_block), exchange PYG_EXCHANGE_*.  Builds the global plan and its slice, the
+ * halo and its request lists (exchanged over NCCL), and the transposed plan of the local edges.
+ * SYNCHRONOUS, collective.  PYG_ERR_UNSUPPORTED for the halo with col_block > 0. */
+pyg_status_t pyg_dist_plan_build(pyg_dist_t* comm, const int64_t* edge_index, int64_t E, int64_t n, int64_t F,
+                                 int64_t ld, int64_t col_block, int exchange, pyg_dist_plan_t** plan,
+                                 void* stream);
+pyg_status_t pyg_dist_plan_info(const pyg_dist_plan_t* plan, pyg_dist_plan_info_t* info);
+void pyg_dist_plan_destroy(pyg_dist_plan_t* plan);
+/* out [hi - lo x F] stride ldo (+ arg_out int64, same stride, GLOBAL edge ids, for MAX) = the rows
+ * [lo, hi) of pyg_propagate over the whole graph (Eq. 1).  x_shard [hi - lo x F] stride ldx: this
+ * rank's X rows (may be info.x_shard itself); edge_weight [E] by GLOBAL edge id or NULL.  flags:
+ * PYG_NO_TMA (PYG_PHI_CONCAT_XI unsupported).  Asynchronous on `stream` (NCCL enqueues there too),
+ * collective. */
+pyg_status_t pyg_dist_propagate(pyg_dist_plan_t* plan, const float* x_shard, int64_t ldx, const float* edge_weight,
+                                pyg_reduce_t reduce, uint32_t flags, float* out, int64_t ldo, int64_t* arg_out,
+                                void* stream);
+/* grad_x_shard [hi - lo x F] stride ldgx (overwritten) = the rows [lo, hi) of pyg_propagate_backward's
+ * grad_x_src over the whole graph, from this rank's grad_out [hi - lo x F] (stride ldg) and, for MAX,
+ * its arg_out (stride lda) from pyg_dist_propagate.  MEAN divides by the in-degree; MAX routes
+ * through argmax with fp32 atomics (see pyg_propagate_backward).  Asynchronous, collective. */
+pyg_status_t pyg_dist_propagate_backward(pyg_dist_plan_t* plan, const float* grad_out, int64_t ldg,
+                                         const float* edge_weight, pyg_reduce_t reduce, const int64_t* arg_out,
+                                         int64_t lda, float* grad_x_shard, int64_t ldgx, void* stream);
 
 #ifdef __cplusplus
 }

@@ -24,7 +24,8 @@ __all__ = [
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
     "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
-    "FORCE_SEGMENT", "version",
+    "FORCE_SEGMENT", "version", "DistComm", "DistPlan", "pyg_dist_unique_id", "pyg_dist_init", "pyg_dist_plan_build",
+    "pyg_dist_propagate", "pyg_dist_propagate_backward",
 ]
 
 
@@ -526,3 +527,131 @@ def pyg_gat_transform(x: torch.Tensor, weight: torch.Tensor, att_src: torch.Tens
                                 _ptr(att_dst.contiguous()), _ptr(z), N, _ptr(ss), _ptr(sd), _stream(dev)),
           "pyg_gat_transform")
     return z, ss, sd
+
+
+# ---- multi-GPU layer (include/pyg_gs.h "multi-GPU"; north_star (3)) ----------------
+
+def pyg_dist_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 makes it; broadcast it over the process group)."""
+    buf = ctypes.create_string_buffer(128)
+    check(lib.pyg_dist_unique_id(buf), "pyg_dist_unique_id")
+    return buf.raw
+
+
+class DistComm:
+    """The library's NCCL communicator (pyg_dist_init / pyg_dist_finalize)."""
+
+    def __init__(self, handle, rank: int, world: int):
+        self._h, self.rank, self.world = handle, rank, world
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            lib.pyg_dist_finalize(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def pyg_dist_init(unique_id: bytes, rank: int, world: int) -> DistComm:
+    """Collective: every rank calls it with the same id, its GPU current."""
+    h = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(unique_id, 128)
+    check(lib.pyg_dist_init(buf, rank, world, ctypes.byref(h)), "pyg_dist_init")
+    return DistComm(h, rank, world)
+
+
+class DistPlan:
+    """One rank's share of a dst-range partitioned graph (pyg_dist_plan_build); owns its buffers."""
+
+    def __init__(self, handle, comm: DistComm, F: int):
+        self._h, self.comm, self.F = handle, comm, F
+        info = _abi.DistPlanInfo()
+        check(lib.pyg_dist_plan_info(handle, ctypes.byref(info)), "pyg_dist_plan_info")
+        self.lo, self.hi, self.per = info.lo, info.hi, info.per
+        self.exchange = {1: "allgather", 2: "halo"}[info.exchange]
+        self.n_halo, self.n_send, self.n_local_edges = info.n_halo, info.n_send, info.n_local_edges
+        self.col_block, self.ldx = info.col_block, info.ldx
+        self._x_ptr = info.x_shard
+
+    @property
+    def handle(self):
+        return self._h
+
+    def x_shard(self) -> torch.Tensor:
+        """[hi - lo, F] view of this rank's rows inside the exchange buffer (write X here)."""
+        n = self.hi - self.lo
+        if n == 0:
+            return torch.empty((0, self.F), dtype=torch.float32, device="cuda")
+        # borrow the library's buffer (valid while this DistPlan lives): a strided view over (n, ldx)
+        size = (n - 1) * self.ldx + self.F
+        return torch.as_strided(_device_view(self._x_ptr, size), (n, self.F), (self.ldx, 1))
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib.pyg_dist_plan_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+
+def _device_view(ptr: int, numel: int) -> torch.Tensor:
+    """A torch float32 tensor aliasing library-owned device memory (no copy, no ownership)."""
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (int(ptr), False), "version": 3,
+                                    "strides": None, "stream": None}
+    return torch.as_tensor(_CAI(), device="cuda")
+
+
+def pyg_dist_plan_build(comm: DistComm, edge_index: torch.Tensor, n: int, F: int, ld: Optional[int] = None,
+                        col_block: int = 0, exchange: str = "auto") -> DistPlan:
+    """Collective, synchronous (see the header).  edge_index: the full graph on every rank."""
+    edge_index = _i64(edge_index, "edge_index")
+    ld = ld or (F + 3) // 4 * 4
+    h = ctypes.c_void_p()
+    check(lib.pyg_dist_plan_build(comm.handle, _ptr(edge_index), edge_index.shape[1], n, F, ld, col_block,
+                                  _abi.EXCHANGE[exchange], ctypes.byref(h), _stream(edge_index.device)),
+          "pyg_dist_plan_build")
+    return DistPlan(h, comm, F)
+
+
+def pyg_dist_propagate(plan: DistPlan, x_shard: torch.Tensor, reduce="sum", edge_weight: Optional[torch.Tensor] = None,
+                       out: Optional[torch.Tensor] = None, arg_out: Optional[torch.Tensor] = None, flags: int = 0):
+    """Rows [lo, hi) of pyg_propagate over the whole graph; returns out (or (out, arg) for max)."""
+    n, F, ldx = _rows(x_shard, "x_shard") if x_shard.shape[0] > 0 else (0, plan.F, plan.F)
+    r = _red(reduce)
+    dev = x_shard.device
+    n_own = plan.hi - plan.lo
+    if out is None:
+        out = torch.empty((n_own, plan.F), dtype=torch.float32, device=dev)
+    if r == MAX and arg_out is None:
+        arg_out = torch.empty((n_own, plan.F), dtype=torch.int64, device=dev)
+    ldo = out.stride(0) if n_own > 0 else plan.F
+    check(lib.pyg_dist_propagate(plan.handle, _ptr(x_shard), max(ldx, plan.F), _ptr(edge_weight), r, flags, _ptr(out),
+                                 ldo, _ptr(arg_out), _stream(dev)), "pyg_dist_propagate")
+    return (out, arg_out) if r == MAX else out
+
+
+def pyg_dist_propagate_backward(plan: DistPlan, grad_out: torch.Tensor, reduce="sum",
+                                edge_weight: Optional[torch.Tensor] = None, arg_out: Optional[torch.Tensor] = None,
+                                grad_x: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Rows [lo, hi) of dL/dX (pyg_propagate_backward's grad_x_src over the whole graph)."""
+    r = _red(reduce)
+    dev = grad_out.device
+    n_own = plan.hi - plan.lo
+    ldg = grad_out.stride(0) if n_own > 0 else plan.F
+    if grad_x is None:
+        grad_x = torch.empty((n_own, plan.F), dtype=torch.float32, device=dev)
+    lda = arg_out.stride(0) if (arg_out is not None and n_own > 0) else plan.F
+    check(lib.pyg_dist_propagate_backward(plan.handle, _ptr(grad_out), ldg, _ptr(edge_weight), r, _ptr(arg_out), lda,
+                                          _ptr(grad_x), grad_x.stride(0) if n_own > 0 else plan.F, _stream(dev)),
+          "pyg_dist_propagate_backward")
+    return grad_x

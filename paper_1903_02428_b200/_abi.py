@@ -45,6 +45,17 @@ class PlanView(ctypes.Structure):
     ]
 
 
+class DistPlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("lo", ctypes.c_int64), ("hi", ctypes.c_int64), ("per", ctypes.c_int64), ("exchange", ctypes.c_int),
+        ("n_halo", ctypes.c_int64), ("n_send", ctypes.c_int64), ("n_local_edges", ctypes.c_int64),
+        ("col_block", ctypes.c_int64), ("x_shard", ctypes.c_void_p), ("ldx", ctypes.c_int64),
+        ("plan", ctypes.c_void_p),
+    ]
+
+
+EXCHANGE = {"auto": 0, "allgather": 1, "halo": 2}
+
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
 U32 = ctypes.c_uint32
@@ -92,6 +103,14 @@ SIGNATURES = {
     "pyg_gat_propagate": ([P, I64, I64, I64, I64, P, P, I64, I64, ctypes.c_float, P, P, I64, P, P, SZ, P], C),
     "pyg_gat_backward": ([P, I64, I64, I64, I64, P, P, I64, I64, ctypes.c_float, P, P, I64, P, P, P, I64, P, P, P, P,
                           SZ, P], C),
+    "pyg_dist_unique_id": ([P], C),
+    "pyg_dist_init": ([P, C, C, PP], C),
+    "pyg_dist_finalize": ([P], None),
+    "pyg_dist_plan_build": ([P, P, I64, I64, I64, I64, I64, C, PP, P], C),
+    "pyg_dist_plan_info": ([P, ctypes.POINTER(DistPlanInfo)], C),
+    "pyg_dist_plan_destroy": ([P], None),
+    "pyg_dist_propagate": ([P, P, I64, P, C, U32, P, I64, P, P], C),
+    "pyg_dist_propagate_backward": ([P, P, I64, P, C, P, I64, P, I64, P], C),
 }
 
 

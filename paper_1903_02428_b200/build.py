@@ -29,6 +29,23 @@ NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "-I",
               "--expt-relaxed-constexpr", "-Xptxas", "-O3"] + ARCH
 
 
+def nccl_include() -> list:
+    """nccl.h for the multi-GPU layer's types (NCCL itself is dlopen'ed at run time): the copy
+    torch's NCCL wheel ships, else the system one."""
+    try:
+        import nvidia.nccl as _n  # the torch-bundled NCCL 2.28
+
+        inc = os.path.join(list(_n.__path__)[0], "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return ["-I", inc]
+    except Exception:
+        pass
+    return []
+
+
+NVCC_FLAGS += nccl_include()
+
+
 def nvcc() -> str:
     p = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     if not os.path.exists(p):
@@ -80,7 +97,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), variant: str = "
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(compile_one, _sources()))
     tmp = lib + ".tmp"
-    cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static"]
+    cmd = [cc, "-shared", "-o", tmp] + objs + ARCH + ["-cudart", "static", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

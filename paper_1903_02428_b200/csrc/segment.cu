@@ -39,12 +39,19 @@ __global__ void combine_kernel(SegArgs a, seg::HeavyArgs h) {
             }
             float* o = a.out + r * a.ldo + col;
             int64_t* ap = a.arg + r * a.lda + col;
-            if (!a.accum) {
+            if (!a.accum && a.finalize) {
                 *o = b >= 0 ? best : 0.0f;
                 *ap = b >= 0 ? (int64_t)b : a.E_sentinel;
-            } else if (b >= 0 && (*ap == a.E_sentinel || best > *o || (best == *o && b < *ap))) {
-                *o = best;
-                *ap = b;
+            } else {  // multi-pass: packed keys in the arg buffer (see seg_kernel)
+                unsigned long long* kp = reinterpret_cast<unsigned long long*>(ap);
+                const unsigned long long nk = b >= 0 ? max_key(best, (uint32_t)b) : 0ull;
+                const unsigned long long k = a.accum ? (*kp > nk ? *kp : nk) : nk;
+                if (a.finalize) {
+                    *o = k ? ord2f((uint32_t)(k >> 32)) : 0.0f;
+                    *ap = k ? (int64_t)(0xffffffffu - (uint32_t)(k & 0xffffffffu)) : a.E_sentinel;
+                } else {
+                    *kp = k;
+                }
             }
         } else {
             double s = 0.0;

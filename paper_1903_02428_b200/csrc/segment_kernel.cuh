@@ -260,7 +260,11 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
         // the GCN / APPNP epilogue extras exist only in the kRedSumEpi instantiation, so the plain
         // SUM / MEAN kernels keep their register budget
         constexpr bool EPI = RED == kRedSumEpi;
-        if (a.accum && dseg == 0 && !((RED == PYG_MEAN || (EPI && (a.blend || a.col_bias))) && a.finalize)) return;
+        // MAX over several passes keeps packed (value, edge id) keys in `arg` until the last pass decodes
+        // them, so the final pass visits every row too
+        if (a.accum && dseg == 0 &&
+            !((RED == PYG_MEAN || RED == PYG_MAX || (EPI && (a.blend || a.col_bias))) && a.finalize))
+            return;
         const float rsc = (EPI && a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
         const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
 #pragma unroll
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
                 st<V>(o, r, nv, out_vec_ok);
             } else {
                 int64_t* ap = a.arg + row * a.lda + col;
-                if (!a.accum) {
+                if (!a.accum && a.finalize) {  // one pass: write (value, arg)
                     float r[V];
 #pragma unroll
                     for (int q = 0; q < V; ++q) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
@@ -306,15 +310,26 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
                     for (int q = 0; q < V; ++q)
                         if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
                 } else {
-                    // merge with earlier blocks: larger value wins, IEEE-equal -> lower edge id (Q4)
+                    // several passes (source-blocked plans): the arg buffer holds the packed key
+                    // (ord(value) << 32 | ~edge id; 0 = no edge yet) so each pass merges with ONE 8-byte
+                    // read-modify-write -- larger value wins, IEEE-equal -> lower edge id (Q4) -- and the
+                    // last pass decodes it into (value, arg)
+                    unsigned long long* kp = reinterpret_cast<unsigned long long*>(ap);
 #pragma unroll
                     for (int q = 0; q < V; ++q) {
-                        if (q >= nv || bi[ch][q] < 0) continue;
-                        const int64_t oa = ap[q];
-                        const float ov = o[q];
-                        if (oa == a.E_sentinel || acc[ch][q] > ov || (acc[ch][q] == ov && bi[ch][q] < oa)) {
-                            o[q] = acc[ch][q];
-                            ap[q] = bi[ch][q];
+                        if (q >= nv) continue;
+                        const unsigned long long nk = bi[ch][q] >= 0 ? max_key(acc[ch][q], (uint32_t)bi[ch][q]) : 0ull;
+                        unsigned long long k = nk;
+                        if (a.accum) {
+                            const unsigned long long old = kp[q];
+                            k = old > nk ? old : nk;
+                            if (!a.finalize && k == old) continue;
+                        }
+                        if (a.finalize) {
+                            o[q] = k ? ord2f((uint32_t)(k >> 32)) : 0.0f;
+                            ap[q] = k ? (int64_t)(0xffffffffu - (uint32_t)(k & 0xffffffffu)) : a.E_sentinel;
+                        } else {
+                            kp[q] = k;
                         }
                     }
                 }

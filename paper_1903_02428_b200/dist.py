@@ -224,33 +224,70 @@ def local_edges(edge_index: torch.Tensor, lo: int, hi: int) -> torch.Tensor:
     return torch.stack([sub[0], sub[1] - lo])
 
 
-class DistAggregation:
-    """dst-range partitioned propagate (segment strategy) for one graph shared by all ranks.
+def all_to_all_rows(send: torch.Tensor, send_counts, recv: torch.Tensor, recv_counts, group=None):
+    """Rows send[soff[q] : soff[q] + send_counts[q]] go to rank q; rows from rank q land in recv in rank
+    order (host-staged under gloo)."""
+    if _staged(group, send, recv):
+        h = torch.empty(recv.shape, dtype=recv.dtype)
+        dist.all_to_all_single(h, send.contiguous().cpu(), recv_counts, send_counts, group=group)
+        recv.copy_(h)
+        return recv
+    dist.all_to_all_single(recv, send.contiguous(), recv_counts, send_counts, group=group)
+    return recv
 
-    Every rank holds the full edge_index (it is needed once, to build the plan), builds the global
-    plan and keeps the slice of its rows; X arrives as this rank's padded shard.
-    exchange="allgather": every rank receives every shard (dense graphs: Reddit references
-    essentially every row from every partition).  exchange="halo": only the referenced remote rows
-    travel (power-law / sparse cross-partition edges); the local buffer is [own shard ; halo rows]
-    and the plan's gathered ids are rank-local (pyg_halo_build).
+
+class DistAggregation:
+    """dst-range partitioned propagate + backward for one graph shared by all ranks.
+
+    backend "nccl" (production): a thin shim over the library's multi-GPU layer -- pyg_dist_init /
+    pyg_dist_plan_build / pyg_dist_propagate / pyg_dist_propagate_backward, NCCL inside libpygs
+    (include/pyg_gs.h "multi-GPU").  backend "gloo" (test emulation: several ranks on one GPU, or CPU
+    collectives): the same algorithm with torch.distributed collectives, host-staged, around the
+    library's local kernels.
+
+    Every rank holds the full edge_index (needed once, to build the plans); X arrives as this rank's
+    shard of rows [lo, hi).  exchange="allgather": every rank receives every shard (dense graphs);
+    "halo": only the referenced remote rows travel and the local buffer is [own shard ; halo rows]
+    with rank-local gathered ids (pyg_halo_build); "auto" (nccl) picks per the header's rule.
+    Backward: partial dL/dX over every source the local edges reference, then a reduce-scatter
+    (all-gather mode) or the reverse halo (halo mode).
     """
 
     def __init__(self, edge_index: torch.Tensor, n: int, world: int, rank: int, group=None,
-                 col_block: Optional[int] = None, ld: Optional[int] = None, exchange: str = "allgather"):
+                 col_block: Optional[int] = None, ld: Optional[int] = None, exchange: str = "allgather",
+                 F: Optional[int] = None, backend: Optional[str] = None, comm=None):
         import paper_1903_02428_b200 as pg
 
         self.pg = pg
         self.n, self.world, self.rank, self.group = n, world, rank, group
-        self.ranges, self.per = partition_rows(n, world)
-        self.lo, self.hi = self.ranges[rank]
         self.E = edge_index.shape[1]
+        self.edge_index = edge_index
+        self.backend = backend or (dist.get_backend(group) if dist.is_initialized() else "nccl")
         if col_block is None:
             col_block = pg.pyg_plan_suggest_col_block(self.E, n, n, (ld or 1) * 4) if ld else 0
+        self.col_block, self.ld, self.F = col_block, ld, F
+        self.exchange = exchange
+        self._xbuf = None
+        self._loc = None
+        if self.backend == "nccl":
+            if comm is None:  # the library's own NCCL communicator, id from rank 0 over the process group
+                ids = [pg.pyg_dist_unique_id() if rank == 0 else None]
+                if world > 1:
+                    dist.broadcast_object_list(ids, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                               group=group)
+                comm = pg.pyg_dist_init(ids[0], rank, world)
+            self.comm = comm
+            self.dplan = None
+            if F is not None:
+                self._build_dist(F)
+            return
+        if exchange == "auto":
+            exchange = self.exchange = "allgather"
+        self.ranges, self.per = partition_rows(n, world)
+        self.lo, self.hi = self.ranges[rank]
         self.plan_full = pg.pyg_plan_build(edge_index[1], edge_index[0], n, n, col_block=col_block)
         self.plan = self.plan_full.slice(self.lo, self.hi)
-        self.edge_index = edge_index
-        self._xbuf = None
-        self.exchange = exchange
+        self.n_halo = 0
         if exchange == "halo":
             self.halo_plan, self.halo_ids = pg.pyg_halo_build(self.plan, n, self.lo, self.hi, self.per)
             self.n_halo = self.halo_ids.numel()
@@ -258,9 +295,24 @@ class DistAggregation:
                                                                             group)
             self._sendbuf = None
 
+    # ------------------------------------------------------------------ nccl: the library's layer
+    def _build_dist(self, F: int):
+        ld = self.ld or (F + 3) // 4 * 4
+        self.dplan = self.pg.pyg_dist_plan_build(self.comm, self.edge_index, self.n, F, ld, self.col_block,
+                                                 self.exchange)
+        self.F, self.ld = F, ld
+        self.lo, self.hi, self.per = self.dplan.lo, self.dplan.hi, self.dplan.per
+        self.exchange = self.dplan.exchange
+        self.n_halo = self.dplan.n_halo
+
+    def x_shard(self, F: Optional[int] = None) -> torch.Tensor:
+        """(nccl) this rank's rows inside the library's exchange buffer: writing X there saves a copy."""
+        if self.dplan is None:
+            self._build_dist(F or self.F)
+        return self.dplan.x_shard()
+
     def local_buffer(self, ld: int, dtype=torch.float32) -> torch.Tensor:
-        """[per + n_halo, ld] buffer whose first `per` rows are this rank's shard (halo exchange):
-        writing the shard there saves a copy per call."""
+        """(gloo, halo) [per + n_halo, ld] buffer whose first `per` rows are this rank's shard."""
         rows = self.per + self.n_halo
         if self._xbuf is None or tuple(self._xbuf.shape) != (rows, ld):
             self._xbuf = torch.empty((rows, ld), dtype=dtype, device=self.edge_index.device)
@@ -285,7 +337,12 @@ class DistAggregation:
 
     def forward(self, x_shard: torch.Tensor, reduce="sum", out: Optional[torch.Tensor] = None,
                 arg_out: Optional[torch.Tensor] = None, edge_weight=None):
-        """x_shard: [per, F] (row-strided allowed) -> out [hi - lo, F] (+ global-id arg for max)."""
+        """x_shard: [hi - lo, F] (row-strided allowed) -> out [hi - lo, F] (+ global-id arg for max)."""
+        if self.backend == "nccl":
+            if self.dplan is None:
+                self._build_dist(x_shard.shape[1])
+            return self.pg.pyg_dist_propagate(self.dplan, x_shard, reduce, edge_weight=edge_weight, out=out,
+                                              arg_out=arg_out)
         if self.exchange == "halo":
             return self._forward_halo(x_shard, reduce, out, arg_out, edge_weight)
         F = x_shard.shape[1]
@@ -297,3 +354,51 @@ class DistAggregation:
         x_full = self._xbuf[: self.n, :F]
         return self.pg.pyg_propagate(x_full, None, n_dst=self.hi - self.lo, reduce=reduce, plan=self.plan,
                                      out=out, arg_out=arg_out, E=self.E, edge_weight=edge_weight)
+
+    # ------------------------------------------------------------------ backward
+    def _local_edges(self):
+        """(gloo) the in-edges of own targets, ascending global id, with sources in the rank's source
+        space (global ids padded to per * world, or own-then-halo local ids) and their transposed plan."""
+        if self._loc is None:
+            pg, ei = self.pg, self.edge_index
+            n_own = self.hi - self.lo
+            eid = torch.nonzero((ei[1] >= self.lo) & (ei[1] < self.hi)).flatten()
+            src, dst = ei[0, eid], ei[1, eid] - self.lo
+            if self.exchange == "halo":
+                own = (src >= self.lo) & (src < self.hi)
+                src = torch.where(own, src - self.lo, self.per + torch.searchsorted(self.halo_ids, src))
+                n_src = self.per + self.n_halo
+            else:
+                n_src = self.per * self.world
+            lei = torch.stack([src, dst]).contiguous()
+            plan_t = pg.pyg_plan_build(lei[0], lei[1], n_src, n_own)
+            deg = pg.pyg_degree(lei[1], n_own)
+            self._loc = (eid, lei, n_src, plan_t, deg)
+        return self._loc
+
+    def backward(self, grad_out: torch.Tensor, reduce="sum", arg_out: Optional[torch.Tensor] = None,
+                 edge_weight=None) -> torch.Tensor:
+        """grad_out [hi - lo, F] -> dL/dX rows [hi - lo, F] of this rank (SURVEY 8(e) Backward)."""
+        if self.backend == "nccl":
+            return self.pg.pyg_dist_propagate_backward(self.dplan, grad_out, reduce, edge_weight=edge_weight,
+                                                       arg_out=arg_out)
+        pg = self.pg
+        eid, lei, n_src, plan_t, deg = self._local_edges()
+        n_own, F = grad_out.shape
+        w = edge_weight[eid] if edge_weight is not None else None
+        arg_l = None
+        if reduce == "max":  # global edge ids -> local edge indices (sentinel E -> E_loc)
+            j = torch.searchsorted(eid, arg_out.clamp(max=max(self.E - 1, 0)).contiguous())
+            arg_l = torch.where(arg_out >= self.E, eid.numel(), j)
+        part = pg.pyg_propagate_backward(None, lei, grad_out, n_src=n_src, F=F, reduce=reduce, edge_weight=w,
+                                         arg_out=arg_l, deg_dst=deg, plan_T=plan_t)["x_src"]
+        if self.exchange != "halo":
+            return reduce_scatter_rows(part, self.world, self.group)[:n_own]
+        # reverse halo: my halo rows' partials back to their owners; theirs for my rows come back
+        rbuf = torch.empty((self.send_rows.numel(), F), dtype=part.dtype, device=part.device)
+        all_to_all_rows(part[self.per:], self.recv_counts, rbuf, self.send_counts, self.group)
+        add = pg.pyg_scatter(rbuf, self.send_rows, n_own, "sum") if rbuf.shape[0] else None
+        g = part[:n_own].clone()
+        if add is not None:
+            g += add
+        return g

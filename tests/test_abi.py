@@ -50,7 +50,30 @@ def test_host_validation_without_gpu():
     nb2 = ctypes.c_size_t()
     assert lib.pyg_plan_workspace_size(1000, 100, 100, 10, ctypes.byref(nb2)) == 0 and nb2.value > nb.value
     assert lib.pyg_plan_workspace_size(1000, 100, 100, -1, ctypes.byref(nb2)) == 1
-    assert "collate" in lib.pyg_last_error().decode() or True
+    assert "plan_workspace_size" in lib.pyg_last_error().decode()  # the message of the last failing call
+    assert lib.pyg_collate(0, None, None, None, 0, 0, 0, None, None, None, None) == 1
+    assert "collate" in lib.pyg_last_error().decode()
+    # the atomic path's workspace grows with E (hub slots, reading Q12); a MAX call needs no slots
+    small, big, mx = ctypes.c_size_t(), ctypes.c_size_t(), ctypes.c_size_t()
+    assert lib.pyg_workspace_size(None, 1000, 100, 16, 0, 0, ctypes.byref(small)) == 0
+    assert lib.pyg_workspace_size(None, 10_000_000, 100, 16, 0, 0, ctypes.byref(big)) == 0
+    assert lib.pyg_workspace_size(None, 10_000_000, 100, 16, 2, 0, ctypes.byref(mx)) == 0
+    assert big.value > small.value + (10_000_000 // 1024) * 16 * 4 and mx.value < big.value
+    assert lib.pyg_workspace_size(None, -1, 100, 16, 0, 0, ctypes.byref(mx)) == 1
+
+
+def test_nccl_missing_is_reported_as_pyg_err_nccl():
+    """The multi-GPU layer loads NCCL at run time; without it every pyg_dist_* call returns
+    PYG_ERR_NCCL (the library itself still loads)."""
+    import subprocess
+    import sys
+
+    code = ("import paper_1903_02428_b200 as pg\n"
+            "try:\n    pg.pyg_dist_unique_id()\nexcept pg.PygError as e:\n    print(e.status)\n"
+            "try:\n    pg.pyg_dist_init(bytes(128), 0, 1)\nexcept pg.PygError as e:\n    print(e.status)\n")
+    env = dict(os.environ, PYG_NCCL_LIB="/nonexistent/libnccl.so.2")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=ROOT, timeout=300)
+    assert r.stdout.split() == ["PYG_ERR_NCCL", "PYG_ERR_NCCL"], r.stdout + r.stderr
 
 
 def test_product_does_not_use_the_oracle():

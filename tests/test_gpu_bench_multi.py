@@ -47,3 +47,19 @@ def test_bench_two_ranks(cfg, exchange, reduce, extra):
     for k in ("roofline", "clocks", "steps", "warmup", "metric", "unit"):
         assert k in d
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0  # the N > 1 end-to-end leg
+
+
+@pytest.mark.parametrize("cfg,reduce,extra", [("cora", "sum", []), ("cora", "max", ["--col-block", "500"]),
+                                              ("clouds", "max", [])])
+def test_bench_dist_capi_world1(cfg, reduce, extra):
+    """bench.py's multi-GPU product path (the library's pyg_dist_* layer, NCCL inside libpygs) at N = 1:
+    the same JSON contract, and the oracle pre-check on the sampled rows passes."""
+    cmd = [sys.executable, "bench.py", "--config", cfg, "--reduce", reduce, "--steps", "3", "--warmup", "3",
+           "--dist-capi", "--cpu-seconds", "1", "--no-variants"] + extra
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    d = json.loads(lines[-1])
+    assert d["config"]["exchange"].startswith("capi-allgather"), d["config"]
+    assert d["cpu_baseline"]["parity_on_sample"] is True
+    assert d["value"] > 0 and d["gpu_launches"] > 0

@@ -434,9 +434,20 @@ def test_validate_flag_reports_out_of_bounds(pg):
     with pytest.raises(pg.PygError) as e:
         pg.pyg_plan_build(bad[1], bad[0], 4, 4)
     assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
-    # after an error the library keeps working
+    # source-blocked plans check the same way (and never write outside their arrays: ADVICE r1)
+    big = T(np.array([[0, 1, 2, 3], [0, 1, 2, 1 << 20]], np.int64))
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_plan_build(big[1], big[0], 4, 4, col_block=2)
+    assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_plan_build(bad[1], bad[0], 4, 4, col_block=2)
+    assert e.value.status == "PYG_ERR_INDEX_OUT_OF_BOUNDS"
+    # after an error the library keeps working, and a validated call is not charged with an
+    # earlier call's error
     ok = pg.pyg_propagate(x, T(np.array([[0, 3], [0, 1]], np.int64)), reduce="sum", flags=pg.VALIDATE)
     assert H(ok)[1].tolist() == [1.0, 1.0]
+    p2 = pg.pyg_plan_build(T(np.array([1, 1], np.int64)), T(np.array([0, 3], np.int64)), 4, 4, col_block=2)
+    assert p2.view()["n_col_blocks"] == 2
 
 
 def test_global_pool(pg):
