@@ -286,6 +286,17 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def l2_gather_peak():
+    """Measured L2 -> SM row-gather bandwidth (scripts/l2peak.cu, committed as profiles/l2_peak.json):
+    the roof of a kernel whose gathered matrix (or source block) is L2-resident."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_peak.json")) as f:
+            d = json.load(f)
+        return float(d["l2_row_gather_gbs"]), "measured (profiles/l2_peak.json l2_row_gather_gbs, scripts/l2peak.cu)"
+    except Exception:
+        return None, None
+
+
 def _profile_lookup(fname, workload_key):
     """Entry of profiles/<fname> for this workload; the col_block part of the key may differ between
     boxes (it follows the L2 size), so fall back to the same config / reduce / strategy / N."""
@@ -308,6 +319,59 @@ def traffic_for(workload_key):
 
 
 # --------------------------------------------------------------------------- CPU oracle leg
+
+# The CPU baseline's sample: the in-edges of the first R target rows, R a FIXED fraction of the rows
+# per config (the same rows for bench's cpu_baseline and for the --impl reference arm, so both time
+# the same work); ~10-15 s of single-threaded oracle work on the large graphs, the whole graph on
+# the small ones.  (A full Reddit pass, ~150 s, is timed once by scripts/cpu_full_pass.py and
+# reported from profiles/cpu_full_pass.json.)
+CPU_SAMPLE_FRAC = {"reddit": 0.05, "rmat": 0.08, "pubmed": 1.0, "clouds": 1.0, "cora": 1.0}
+
+
+def cpu_sample_rows(cfg, n_rows):
+    return max(1, min(n_rows, int(round(n_rows * CPU_SAMPLE_FRAC.get(cfg, 1.0)))))
+
+
+def host_info():
+    """The host cores the oracle ran on (nproc, affinity, CPU model)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    try:
+        aff = len(os.sched_getaffinity(0))
+    except Exception:
+        aff = None
+    return {"nproc": os.cpu_count(), "affinity": aff, "cpu_model": model}
+
+
+def full_pass_record(cfg, reduce):
+    """The committed full-pass oracle timing for this workload (scripts/cpu_full_pass.py), if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "cpu_full_pass.json")) as f:
+            return json.load(f).get(f"{cfg}-{reduce}")
+    except Exception:
+        return None
+
+
+def oracle_rows(ei_cpu, x_cpu, R, reduce, F, w=None):
+    """Time the oracle (as it stands, single-threaded C) on the in-edges of the first R target rows.
+    Returns (edges*F/s, seconds, E_s, R, out)."""
+    import oracle
+
+    m = ei_cpu[1] < R
+    sub = ei_cpu[:, m]
+    ws = w[m] if w is not None else None
+    t0 = time.perf_counter()
+    out = oracle.propagate(x_cpu, sub, n_dst=R, reduce=reduce, edge_weight=ws)
+    dt = time.perf_counter() - t0
+    return sub.shape[1] * F / dt, dt, sub.shape[1], R, out
+
 
 def oracle_sample(ei_cpu, x_cpu, n_rows, reduce, target_s, F, w=None):
     """Time the oracle (as it stands) on the edges of the first R target rows, R sized for
@@ -412,9 +476,12 @@ def run_reference(a):
 
     oracle.build()
     cfg = a.config
-    # build the same workload on the CPU (smaller generators use numpy; the big ones use torch CPU)
-    dev = torch.device("cpu")
+    # the same workload: the big generators draw on the GPU when there is one (torch's CUDA generator,
+    # so the edges are identical to our arm's) and the arrays are copied to the host; smaller ones
+    # use numpy.  Nothing of our library runs on this path.
+    dev = torch.device("cuda" if (torch.cuda.is_available() and cfg in ("reddit", "rmat")) else "cpu")
     w = make_workload(cfg, dev, a.ld)
+    w["ei"], w["x"] = w["ei"].cpu(), w["x"].cpu()
     ei = w["ei"].numpy()
     x = np.ascontiguousarray(w["x"].numpy())
     F, N, E = w["F"], w["N"], w["E"]
@@ -441,8 +508,15 @@ def run_reference(a):
             return oracle_gcn_sample(ei, x, W, b, N, per_step)
         what = f"oracle GCN layer (dense_transform + gcn_norm-weighted propagate), hidden {a.hidden}"
     else:
+        R_fix = cpu_sample_rows(cfg, N)
+        # the same rows as bench's cpu_baseline; if K + W steps of it would overrun ~150 s, every step
+        # takes a proportionally shorter prefix (calibrated once)
+        rate0, dt0, _, _, _ = oracle_rows(ei, x, R_fix, a.reduce, F)
+        if dt0 * (a.steps + a.warmup) > 150.0:
+            R_fix = max(1, int(R_fix * per_step / dt0))
+
         def one():
-            return oracle_sample(ei, x, N, a.reduce, per_step, F)
+            return oracle_rows(ei, x, R_fix, a.reduce, F)
         what = f"oracle.propagate {a.reduce}" + (" (one pass of the K-step APPNP recurrence)" if a.op == "appnp" else "")
     for i in range(a.warmup + a.steps):
         rate, dt, Es, R, _ = one()
@@ -452,13 +526,17 @@ def run_reference(a):
     v = float(np.mean(rates))
     Es, R, dt = info
     sample = f"{what}: {Es} edges of the first {R} target rows of {N} ({Es / E:.3%} of E), one pass per step"
+    Fu = a.hidden if a.op == "gcn" else F
     line = {
         "impl": "reference", "metric": "aggregation edges*F/s", "value": v, "unit": "edges*F/s",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": dt * 1e3,
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        # one whole pass of the workload at the sampled rate (the sample itself took sample_ms)
+        "ms_per_step": E * Fu / v * 1e3, "sample_ms": dt * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64-accumulate/f32-io",
         "data": "synthetic", "config": {"workload": CONFIGS[cfg]["name"], "N": N, "E": E, "F": F,
                                         "reduce": a.reduce, "op": a.op},
-        "cpu_baseline": {"value": v, "unit": "edges*F/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "edges*F/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "host": host_info(), "full_pass": full_pass_record(cfg, a.reduce)},
         "e2e": {"value": v, "unit": "edges*F/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -750,8 +828,11 @@ def main():
         if a.config != "pubmed":
             ei, _ = pg.pyg_gcn_norm(ei, N)
             E = ei.shape[1]
-        plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
-        col_block = 0
+        # the aggregation gathers the transformed rows (hidden wide): block the plan for THAT row size
+        ldh = (a.hidden + 7) // 8 * 8
+        col_block = (pg.pyg_plan_suggest_col_block(E, N, N, ldh * 4) if a.col_block == "auto"
+                     else int(a.col_block))
+        plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=col_block)
         torch.cuda.synchronize()
         prep_ms = (time.perf_counter() - t1) * 1e3
         gg = torch.Generator(device=dev)
@@ -843,6 +924,8 @@ def main():
     else:
         kern_ms = float(np.mean([s.elapsed_time(e) for s, e in kev]))
         step_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    # per-step distribution (median and min beside the mean); one value under a CUDA graph
+    per_step = [s.elapsed_time(e) for s, e in ev] if not use_graph else [total_ms / a.steps]
     if dist:
         tt = torch.tensor([total_ms, kern_ms, step_ms - kern_ms], device=dev if a.dist_backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -881,9 +964,26 @@ def main():
             "traffic": (tr / lpc) if tr else None, "peak_source": peak_src,
             "alg_bytes_per_launch": B / lpc, "launches_per_call": lpc, "kernel_ms_per_launch": kern_ms / lpc,
             "alg_bytes_per_call": B, "call_ms": kern_ms, "traffic_per_call": tr,
-            "note": "achieved counts every gathered x_j row (north_star byte model); source-blocked passes serve "
-                    "repeats from L2, so achieved can exceed the HBM copy peak while DRAM traffic stays below it",
+            "note": "achieved = algorithmic bytes (north_star byte model: every gathered x_j row, indices, out) / "
+                    "device time of the call",
             "ncu": _profile_lookup("ncu_summary.json", wk)}
+    # Which roof binds: when the matrix one pass gathers from fits in L2 (a source block of a blocked plan,
+    # or the whole X / transformed H) the x_j rows come from L2, so the physical roof is the L2 -> SM
+    # gather bandwidth, measured by scripts/l2peak.cu (profiles/l2_peak.json); the HBM-model number stays
+    # as modeled_frac.  The atomic strategy is bound by the DRAM read-modify-write of `out` (HBM).
+    l2pk, l2src = l2_gather_peak()
+    l2_size = torch.cuda.get_device_properties(dev).L2_cache_size
+    Fg = a.hidden if gcn is not None else (gatl["H"] * gatl["C"] if gatl else F)
+    x_pass = (col_block if col_block else N) * (Fg if (gcn is not None or gatl) else ld) * 4
+    if (l2pk and a.strategy == "segment" and gat is None and x_pass <= l2_size):
+        l2_bytes = units * 4 + 4 * passes * (E_loc if world > 1 else E)  # x_j rows + col indices, from L2
+        l2_ach = l2_bytes / (kern_ms * 1e-3) / 1e9
+        roof = dict(roof, bound="l2", achieved=l2_ach, peak=l2pk, frac=l2_ach / l2pk, peak_source=l2src,
+                    l2_bytes_per_call=l2_bytes, gathered_matrix_bytes_per_pass=x_pass, l2_size=l2_size,
+                    modeled_achieved=achieved, modeled_peak=peak, modeled_frac=achieved / peak,
+                    note="x_j rows (+ col indices) are served from L2 (the gathered matrix of a pass <= L2): "
+                         "achieved = those bytes / call time against the measured L2 row-gather peak; "
+                         "modeled_* = the north_star HBM byte model against the HBM copy peak")
 
     result = {
         "metric": "aggregation edges*F/s", "value": value, "unit": "edges*F/s", "n_gpus": world,
@@ -901,6 +1001,8 @@ def main():
                    else "L2-resident inputs (warm, back-to-back as in Fig. 3's 1000 runs)"},
         "roofline": roof, "gpu_launches": int(launches), "clocks": clk, "plan_build_ms": plan_ms,
         "exchange_ms": xchg_ms, "compute_ms": kern_ms,
+        "ms_per_step_median": float(np.median(per_step)), "ms_per_step_min": float(np.min(per_step)),
+        "ms_per_step_max": float(np.max(per_step)),
         "gen_s": gen_s,
     }
     if w.get("extra"):
@@ -963,6 +1065,9 @@ def main():
             rate, dt, Es, R, ref = oracle_gat_sample(ei_cpu, zc.cpu().numpy(), s_src.cpu().numpy(), s_dst.cpu().numpy(),
                                                      gat["H"], N, a.cpu_seconds, F)
             got = gat["out"][:R].cpu().numpy()
+        elif passes == 1:
+            rate, dt, Es, R, ref = oracle_rows(ei_cpu, x_cpu, cpu_sample_rows(a.config, N), red, F, w=w_cpu)
+            got = out[:R].cpu().numpy()
         else:
             rate, dt, Es, R, ref = oracle_sample(ei_cpu, x_cpu, N, red, a.cpu_seconds, F, w=w_cpu)
             got = out[:R].cpu().numpy()
@@ -987,7 +1092,8 @@ def main():
             sample = (f"{Es} edges of the first {R} target rows ({Es / E:.2%} of E), {dt:.1f} s single-threaded C, "
                       f"fp64 accumulate")
         result["cpu_baseline"] = {"value": rate, "unit": "edges*F/s", "cores": 1, "kind": "oracle",
-                                  "sample": sample, "parity_on_sample": ok}
+                                  "sample": sample, "parity_on_sample": ok, "host": host_info(),
+                                  "full_pass": full_pass_record(a.config, red) if a.op == "propagate" else None}
         if not ok:
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 

@@ -100,6 +100,10 @@ const char* pyg_last_error(void);           /* thread-local, never NULL */
 /* Number of kernels this library has launched since it was loaded (monotonic,
  * process-wide).  Used by bench.py to report gpu_launches. */
 uint64_t pyg_launch_count(void);
+/* Re-read the tuning / test knobs (PYG_SEG_TMA, PYG_TMA_HUBS, PYG_TMA_WARP_KB, PYG_TMA_WARPS; DESIGN.md
+ * "knobs") from the environment.  They are read once when the library loads; tests that change them
+ * call this.  Not thread-safe against concurrent calls. */
+void pyg_refresh_env(void);
 
 /* ---- degree ------------------------------------------------- */
 /* deg[i] = #{k : index[k] == i}, i in [0, n); multi-edges and self-loops count
@@ -209,10 +213,10 @@ pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, 
  *   plan path: the fp32 partials of split hub rows, combined in fp64 (reading Q12).
  *   atomic path (plan NULL or PYG_FORCE_ATOMIC): the in-degree array and, for
  *   SUM / MEAN, the hub slots -- rows with more than 2048 entries spread their
- *   edges over slots of <= 1024 entries (one atomic counter per hub hands out
+ *   edges over slots of <= 2048 entries (one atomic counter per hub hands out
  *   positions) whose fp32 partials are combined in fp64, so no fp32 atomic chain
- *   exceeds 1024 terms (Q12).  The size is the worst case for E edges
- *   (E/1024 + E/2049 slots x F_out floats); a MAX call needs none of it.
+ *   exceeds 2048 terms (Q12).  The size is the worst case for E edges
+ *   (E/2048 + E/2049 slots x F_out floats); a MAX call needs none of it.
  * For pyg_propagate_backward pass (plan_T, E, n_src, F).  Host-only. */
 pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t E, int64_t n_out, int64_t F_out,
                                 pyg_reduce_t reduce, uint32_t flags, size_t* bytes);
@@ -423,7 +427,9 @@ pyg_status_t pyg_dense_transform(const float* X, int64_t M, int64_t K, int64_t l
  * width F_out), then an UNWEIGHTED segment sum over the plan whose epilogue scales rows by
  * D^-1/2 and adds the bias: no per-edge weights or edge ids are read.
  *   X [n x K] stride ldx, W [F_out x K] stride ldw (alignment as pyg_dense_transform),
- *   bias [F_out] or NULL, out [n x F_out] stride ldo.  plan: unblocked forward plan, n x n.
+ *   bias [F_out] or NULL, out [n x F_out] stride ldo.  plan: forward plan, n x n -- unblocked, or
+ *   source-blocked (pyg_plan_suggest_col_block with row_bytes = 4 * F_out: the transformed rows are
+ *   then aggregated one L2-resident block at a time, D^-1/2 and the bias applied in the last pass).
  *   workspace: pyg_gcn_layer_workspace_size (D^-1/2, the transformed rows, split rows).
  *   Asynchronous. */
 pyg_status_t pyg_gcn_layer_workspace_size(const pyg_plan_t* plan, int64_t n, int64_t F_out,

@@ -67,6 +67,7 @@ SIGNATURES = {
     "pyg_version": ([], ctypes.c_char_p),
     "pyg_last_error": ([], ctypes.c_char_p),
     "pyg_launch_count": ([], ctypes.c_uint64),
+    "pyg_refresh_env": ([], None),
     "pyg_degree": ([P, I64, I64, U32, P, P], C),
     "pyg_plan_workspace_size": ([I64, I64, I64, I64, ctypes.POINTER(SZ)], C),
     "pyg_plan_build": ([P, P, I64, I64, I64, I64, U32, P, SZ, PP, P], C),

@@ -37,6 +37,21 @@ pyg_status_t cuda_check(cudaError_t e, const char* what) {
     return fail(PYG_ERR_CUDA, "CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
 }
 
+static Knobs read_knobs() {
+    Knobs k;
+    auto get = [](const char* name, int dflt) {
+        const char* e = getenv(name);
+        return (e && *e) ? atoi(e) : dflt;
+    };
+    k.seg_tma = get("PYG_SEG_TMA", -1);
+    k.tma_hubs = get("PYG_TMA_HUBS", 1);
+    k.tma_warp_kb = get("PYG_TMA_WARP_KB", 4);
+    k.tma_warps = get("PYG_TMA_WARPS", 8);
+    return k;
+}
+static Knobs g_knobs = read_knobs();
+const Knobs& knobs() { return g_knobs; }
+
 // PYG_VALIDATE flag: one pinned, mapped int per host thread (so concurrent calls on other threads
 // never consume each other's errors).  validate_begin() clears it before a validating call launches
 // its checking kernels (every earlier use on this thread ended with the synchronising check).
@@ -97,7 +112,7 @@ pyg_status_t dense_transform_impl(const float* X, int64_t M, int64_t K, int64_t 
                                   int64_t ldw, const float* bias, const float* row_scale, float* Y, int64_t ldy,
                                   cudaStream_t s, const float* att_src = nullptr, const float* att_dst = nullptr,
                                   float* s_src = nullptr, float* s_dst = nullptr, int heads = 0);
-pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_t s);
+pyg_status_t gcn_dinv(const int64_t* rowptr, const int32_t* deg, int64_t n, float* dinv, cudaStream_t s);
 pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_t* rows, const int64_t* ptr,
                             void* const* dst, const int64_t* dst_row, int64_t ldd, int n_peers, cudaStream_t s);
 pyg_status_t ipc_handle_impl(const void* ptr, void* handle, int64_t* offset);
@@ -130,6 +145,7 @@ extern "C" {
 
 const char* pyg_version(void) { return "pygs 0.1.0 (sm_100a)"; }
 const char* pyg_last_error(void) { return t_err.c_str(); }
+void pyg_refresh_env(void) { g_knobs = read_knobs(); }
 uint64_t pyg_launch_count(void) { return g_launches.load(); }
 
 pyg_status_t pyg_degree(const int64_t* index, int64_t E, int64_t n, uint32_t flags, int32_t* deg, void* stream) {
@@ -787,12 +803,11 @@ pyg_status_t pyg_gcn_layer(const float* X, int64_t n, int64_t K, int64_t ldx, co
     REQUIRE(ws && cv.ok(), PYG_ERR_NO_MEMORY, "gcn_layer: workspace too small (pyg_gcn_layer_workspace_size)");
     if (n == 0 || F_out == 0) return PYG_OK;
     cudaStream_t s = as_stream(stream);
-    // degrees of A+I: the plan's row lengths (all source blocks together for blocked plans)
-    if (plan->parts.empty()) {
-        PYG_TRY(gcn_dinv(plan->rowptr, n, dinv, s));
-    } else {
-        return fail(PYG_ERR_UNSUPPORTED, "gcn_layer: source-blocked plans are not supported (aggregate width F_out is small)");
-    }
+    // degrees of A+I: the plan's row lengths (source-blocked plans: the total in-degree they keep per row;
+    // the aggregation then runs one L2-resident pass per source block and applies D^-1/2 and the bias in
+    // the last pass)
+    REQUIRE(plan->parts.empty() || plan->n_passes == 0, PYG_ERR_UNSUPPORTED, "gcn_layer: needs the whole plan, not a pass view");
+    PYG_TRY(gcn_dinv(plan->rowptr, plan->parts.empty() ? nullptr : plan->deg, n, dinv, s));
     PYG_TRY(pyg_dense_transform(X, n, K, ldx, W, F_out, ldw, nullptr, dinv, H, ldh, stream));
     SegArgs a;
     a.X = H; a.ldx = ldh; a.ncols = (int)F_out;

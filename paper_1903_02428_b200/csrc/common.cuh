@@ -50,6 +50,16 @@ struct Carver {
     size_t rest_bytes() const { return cap > align_up(off, 256) ? cap - align_up(off, 256) : 0; }
 };
 
+// Tuning / test knobs from the environment, read ONCE per process (pyg_refresh_env re-reads them;
+// tests flip PYG_SEG_TMA between cases).  Defaults are the measured best settings.
+struct Knobs {
+    int seg_tma = -1;     // PYG_SEG_TMA: -1 auto, 0 off, 1 whenever eligible
+    int tma_hubs = 1;     // PYG_TMA_HUBS: 0 keeps split hub rows on the LDG kernel
+    int tma_warp_kb = 4;  // PYG_TMA_WARP_KB: ring bytes per warp of the TMA gather4 kernel
+    int tma_warps = 8;    // PYG_TMA_WARPS
+};
+const Knobs& knobs();
+
 // Device-side validation flag (pinned, mapped) -- PYG_VALIDATE paths.
 int* validate_flag_dev();
 void validate_begin();  // clear this thread's flag before launching checking kernels

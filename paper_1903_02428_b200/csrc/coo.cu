@@ -12,10 +12,12 @@
 //     fast, nevertheless of the input being coalesced");
 //   * hub rows (in-degree > kHeavyThreshold) would otherwise be one fp32 atomic chain
 //     of up to ~306k terms (R-MAT), which breaks the tolerance (reading Q12).  Their
-//     edges are routed to slots of at most kCooSlot entries each (a per-hub counter,
+//     edges are routed to slots of at most kCooSlot = 2048 entries each (a per-hub counter,
 //     warp-aggregated, hands out positions; slot = position / kCooSlot), the slot
 //     partials live in an L2-sized workspace, and hub_combine_kernel sums them in
-//     fp64 -- every fp32 chain stays <= 1024 terms on the atomic strategy too;
+//     fp64 -- every fp32 chain stays <= 2048 terms on the atomic strategy too (the same bound as the
+//     plan path); a 1-bit-per-row hub bitmap (1.25 MB for 10M rows, L2-resident) keeps the
+//     per-edge hub test off DRAM;
 //   * MAX uses 64-bit atomicMax on a packed key (order-preserving value bits in
 //     the high word, 0xffffffff - edge id in the low word), so the result is
 //     deterministic and ties go to the lowest edge id (Q4) without a second pass
@@ -30,7 +32,8 @@ namespace pyg {
 
 namespace {
 
-constexpr int kCooSlot = 1024;  // entries per hub slot (fp32 chain bound of the atomic path)
+constexpr int kBatches = 8;   // batches of lpr edges per group (epg = kBatches * lpr)
+constexpr int kCooSlot = 2048;  // entries per hub slot (fp32 chain bound of the atomic path, = Q12's 2048)
 
 template <int NCH>
 struct Unroll { static constexpr int U = NCH <= 2 ? 4 : (NCH <= 5 ? 2 : 1); };
@@ -129,31 +132,52 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
             }
     };
 
+    // hub rows: each hub edge's entry position comes from the hub's counter (warp-aggregated: one atomic
+    // per hub and batch) and its target becomes the slot's virtual row n_out + slot.  The counters of
+    // ALL the group's batches are fetched up front, so their L2 round trips overlap instead of stalling
+    // every batch; the resulting targets wait in shared memory.
+    __shared__ long long s_tgt[kBatches][256];
+    if (RED != PYG_MAX && a.hub_base) {
+        int hb[kBatches], got[kBatches];
+        unsigned hm[kBatches];
+#pragma unroll
+        for (int j = 0; j < kBatches; ++j) {
+            const int64_t p = e0 + (int64_t)j * lpr + l;
+            long long t = -1 - (long long)l;
+            hb[j] = -1;
+            if (p < e1) {
+                t = __ldg(a.sidx + p);
+                if ((__ldg(a.hub_bits + (t >> 5)) >> (t & 31)) & 1u) hb[j] = __ldg(a.hub_base + t);
+            }
+            s_tgt[j][threadIdx.x] = t;
+            hm[j] = 0u;
+            got[j] = 0;
+            if (__any_sync(mask, hb[j] >= 0)) {
+                hm[j] = __match_any_sync(mask, hb[j] >= 0 ? t : -1 - (long long)l);
+                if (hb[j] >= 0 && (int)(threadIdx.x & 31) == __ffs(hm[j]) - 1)
+                    got[j] = atomicAdd(a.hub_cursor + (int64_t)hb[j] * gridDim.y + blockIdx.y, __popc(hm[j]));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < kBatches; ++j) {
+            if (hm[j] == 0u) continue;  // group-uniform: no hub in this batch
+            const int lead = __ffs(hm[j]) - 1;  // absolute lane of the member group's first lane
+            const int b = __shfl_sync(mask, got[j], lead - gbase, lpr);
+            const int rank = __popc(hm[j] & ((1u << (threadIdx.x & 31)) - 1u));
+            if (hb[j] >= 0) s_tgt[j][threadIdx.x] = a.n_out + hb[j] + (b + rank) / kCooSlot;
+        }
+    }
+
     for (int64_t base = e0; base < e1; base += lpr) {
         const int n = (int)min((int64_t)lpr, e1 - base);
         long long mi = -1 - (long long)l, mg = 0;  // unique keys for lanes without an edge
         float ms = 1.0f;
         if (l < n) {
             const int64_t p = base + l;
-            mi = __ldg(a.sidx + p);
+            mi = (RED != PYG_MAX && a.hub_base) ? s_tgt[(base - e0) / lpr][threadIdx.x] : __ldg(a.sidx + p);
             mg = a.gidx ? __ldg(a.gidx + p) : p;
             if (a.w) ms = __ldg(a.w + p);
             if (a.gdeg) ms = ms / (float)__ldg(a.gdeg + mg);
-        }
-        // hub rows: entry position from the hub's counter (one atomic per hub and batch),
-        // target -> the slot's virtual row n_out + slot
-        if (RED != PYG_MAX && a.hub_base) {
-            const int hb = l < n ? __ldg(a.hub_base + mi) : -1;
-            if (__any_sync(mask, hb >= 0)) {
-                const unsigned hm = __match_any_sync(mask, hb >= 0 ? mi : -1 - (long long)l);
-                const int lead = __ffs(hm) - 1;  // absolute lane of the group's first member
-                const int rank = __popc(hm & ((1u << (threadIdx.x & 31)) - 1u));
-                int b = 0;
-                if (hb >= 0 && (int)(threadIdx.x & 31) == lead)
-                    b = atomicAdd(a.hub_cursor + (int64_t)hb * gridDim.y + blockIdx.y, __popc(hm));
-                b = __shfl_sync(mask, b, lead - gbase, lpr);
-                if (hb >= 0) mi = a.n_out + hb + (b + rank) / kCooSlot;
-            }
         }
         // warp-aggregated atomics: visit the batch grouped by target (first-occurrence order)
         const unsigned gm = __match_any_sync(mask, mi) >> gbase;  // group-relative member mask
@@ -263,17 +287,22 @@ __global__ void degree_kernel(const int64_t* __restrict__ sidx, int64_t E, int32
 // hub rows: deg > threshold -> ceil(deg / kCooSlot) consecutive slots, their counters zeroed
 // (one per column tile); counters[0] = hubs, counters[1] = slots handed out
 __global__ void hub_assign_kernel(const int32_t* __restrict__ deg, int64_t n, int threshold, int tiles,
-                                  int32_t* hub_base, int32_t* hub_rows, int32_t* counters, int32_t* cursor) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int d = deg[i];
-        int hb = -1;
-        if (d > threshold) {
+                                  int32_t* hub_base, uint32_t* hub_bits, int32_t* hub_rows, int32_t* counters,
+                                  int32_t* cursor) {
+    // whole warps walk 32 consecutive rows so each bitmap word is one ballot
+    const int64_t n32 = (n + 31) & ~(int64_t)31;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += (int64_t)gridDim.x * blockDim.x) {
+        const int d = i < n ? deg[i] : 0;
+        const bool hub = d > threshold;
+        if (hub) {
             const int ns = (d + kCooSlot - 1) / kCooSlot;
-            hb = atomicAdd(counters + 1, ns);
+            const int hb = atomicAdd(counters + 1, ns);
             hub_rows[atomicAdd(counters, 1)] = (int32_t)i;
             for (int t = 0; t < tiles; ++t) cursor[(int64_t)hb * tiles + t] = 0;
+            hub_base[i] = hb;
         }
-        hub_base[i] = hb;
+        const unsigned word = __ballot_sync(0xffffffffu, hub);
+        if ((threadIdx.x & 31) == 0) hub_bits[i >> 5] = word;
     }
 }
 
@@ -377,7 +406,8 @@ size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce) {
     Carver cv(nullptr, 0);
     cv.take<int32_t>((size_t)std::max<int64_t>(n_out, 1));  // deg
     if (E > kHeavyThreshold) {
-        cv.take<int32_t>((size_t)n_out);                             // hub_base
+        cv.take<int32_t>((size_t)n_out);                             // hub_base (valid for hubs only)
+        cv.take<uint32_t>((size_t)cdiv(n_out, 32));                  // hub bitmap
         cv.take<int32_t>((size_t)hub_cap(E));                        // hub_rows
         cv.take<int32_t>(4);                                         // counters
         cv.take<int32_t>((size_t)(slot_cap(E) * max_tiles(ncols)));  // cursors
@@ -410,6 +440,7 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
         if (hubs) {
             hub_base = cv.take<int32_t>((size_t)a.n_out);
             a.hub_base = hub_base;
+            a.hub_bits = cv.take<uint32_t>((size_t)cdiv(a.n_out, 32));
             hub_rows = cv.take<int32_t>((size_t)hub_cap(a.E));
             counters = cv.take<int32_t>(4);
             a.hub_cursor = cv.take<int32_t>((size_t)(slot_cap(a.E) * max_tiles(a.ncols)));
@@ -426,13 +457,14 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
     if (hubs) {
         PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
         hub_assign_kernel<<<grid_for(a.n_out), 256, 0, s>>>(deg, a.n_out, kHeavyThreshold, g.tiles, hub_base,
-                                                              hub_rows, counters, a.hub_cursor);
+                                                              const_cast<uint32_t*>(a.hub_bits), hub_rows, counters,
+                                                              a.hub_cursor);
         PYG_LAUNCHED();
         zero_slots_kernel<<<148 * 4, 256, 0, s>>>(a.part, a.ldp, counters);
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
     }
-    const int epg = g.lpr * 8;  // 8 batches of lpr edges per group
+    const int epg = g.lpr * kBatches;
     if (reduce == PYG_MAX) {
         PYG_TRY(launch_red<PYG_MAX>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
         return max_decode(a.keys, a.ldk, a.out, a.ldo, a.ncols, a.n_out, a.E, s);

@@ -118,7 +118,8 @@ struct CooArgs {
     const int32_t* deg = nullptr;   // in-degree of the targets if the caller has it (else computed)
     // hub routing (SUM / MEAN; set up by coo_reduce): rows with more than kHeavyThreshold entries
     // spread their edges over slots of <= kCooSlot entries, combined in fp64 (reading Q12)
-    const int32_t* hub_base = nullptr;  // [n_out] first slot of a hub row, -1 otherwise
+    const int32_t* hub_base = nullptr;  // [n_out] first slot of a hub row (read for hubs only)
+    const uint32_t* hub_bits = nullptr; // [n_out / 32] 1 bit per row: is a hub
     int32_t* hub_cursor = nullptr;      // [slots x column tiles] entry counters (by first slot)
     float* part = nullptr;              // [slots x ldp] slot partials = virtual rows n_out + slot
     int64_t ldp = 0;

@@ -160,12 +160,12 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
     const bool extras = a.row_scale || a.blend || a.col_bias;
     if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: epilogue extras need SUM");
-    const int red_k = extras ? kRedSumEpi : reduce;  // LDG / combine instantiation
+    // LDG / combine instantiation: weighted MAX multiplies, plain MAX compares x_j directly
+    const int red_k = extras ? kRedSumEpi : (reduce == PYG_MAX && (a.w || a.gdeg)) ? kRedMaxW : reduce;
     const bool tma = ws && cv.ok() && tma_eligible(a, plan);
     // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
     // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel
-    const char* hub_env = getenv("PYG_TMA_HUBS");
-    const bool tma_hubs = tma && split && !(hub_env && atoi(hub_env) == 0);
+    const bool tma_hubs = tma && split && knobs().tma_hubs != 0;
     // light rows: TMA gather4 pipeline or the LDG kernel
     if (tma && !tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, nullptr, nullptr, 0, s));
     else if (!tma) PYG_TRY(launch(a, red_k, g, 0, h, ovk, s));
@@ -196,7 +196,7 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
         case kRedSumEpi: combine_kernel<kRedSumEpi><<<grid, ct, 0, s>>>(a, h); break;
         case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, ct, 0, s>>>(a, h); break;
         case kRedHeadW: combine_kernel<kRedHeadW><<<grid, ct, 0, s>>>(a, h); break;
-        default: combine_kernel<PYG_MAX><<<grid, ct, 0, s>>>(a, h); break;
+        default: combine_kernel<PYG_MAX><<<grid, ct, 0, s>>>(a, h); break;  // PYG_MAX, kRedMaxW
     }
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());

@@ -78,7 +78,11 @@ __device__ __forceinline__ unsigned group_mask() {
 template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                            float (&acc)[NCH][V], int (&bi)[NCH][V]) {
-    constexpr int U = Unroll<V, NCH, LPR>::U;
+    // MAX keeps an edge id per element besides the value: for 17-20 floats per lane one edge in flight per
+    // lane keeps the kernel at the SUM instantiation's resident CTAs (wider shapes would spill) (Reddit max: 29.8 -> 23.8 ms, gpurun_out/r2e;
+    // occupancy beats per-warp memory-level parallelism for this L2-latency-bound gather)
+    constexpr bool IS_MAX = RED == PYG_MAX || RED == kRedMaxW;
+    constexpr int U = (IS_MAX && V * NCH > 16 && V * NCH <= 20) ? 1 : Unroll<V, NCH, LPR>::U;
     const unsigned mask = group_mask<LPR>();
     const float* __restrict__ X = a.X;
     const int64_t ldx = a.ldx;
@@ -88,12 +92,12 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
     const int32_t* __restrict__ gdeg = a.gdeg;
     const bool scaled = (w != nullptr) || (gdeg != nullptr);
     // the edge id is only needed for weights, argmax or edge-space rows
-    const bool need_e = (RED == PYG_MAX) || (RED == kRedHeadW) || (w != nullptr) || (gidx == nullptr);
+    const bool need_e = IS_MAX || (RED == kRedHeadW) || (w != nullptr) || (gidx == nullptr);
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
 #pragma unroll
         for (int q = 0; q < V; ++q) {
-            acc[ch][q] = (RED == PYG_MAX) ? -INFINITY : 0.0f;
+            acc[ch][q] = IS_MAX ? -INFINITY : 0.0f;
             bi[ch][q] = -1;
         }
     const int lane_off = c0 + l * V;
@@ -139,7 +143,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
             for (int u = 0; u < U; ++u) {
                 const int g = __shfl_sync(mask, mg, t + u, LPR);
                 sv[u] = scaled ? __shfl_sync(mask, ms, t + u, LPR) : 1.0f;
-                ev[u] = (RED == PYG_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t + u, LPR) : 0;
+                ev[u] = (IS_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t + u, LPR) : 0;
                 const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
@@ -152,8 +156,9 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
                     const float hwv = (RED == kRedHeadW) ? __ldg(hw + (int64_t)ev[u] * hH + hch[ch]) : 1.0f;
 #pragma unroll
                     for (int q = 0; q < V; ++q) {
-                        if (RED == PYG_MAX) {
-                            const float m = __fmul_rn(sv[u], v[u][ch][q]);  // s = 1 -> exact
+                        if (IS_MAX) {
+                            // plain MAX: the message is x_j itself (no multiply); kRedMaxW: w * x_j
+                            const float m = RED == kRedMaxW ? __fmul_rn(sv[u], v[u][ch][q]) : v[u][ch][q];
                             if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }  // acc starts at -inf (Q5: finite inputs)
                         } else if (RED == kRedHeadW) {
                             acc[ch][q] = fmaf(hwv, v[u][ch][q], acc[ch][q]);
@@ -166,7 +171,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
         for (; t < n; ++t) {
             const int g = __shfl_sync(mask, mg, t, LPR);
             const float sc = scaled ? __shfl_sync(mask, ms, t, LPR) : 1.0f;
-            const int e = (RED == PYG_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t, LPR) : 0;
+            const int e = (IS_MAX || RED == kRedHeadW) ? __shfl_sync(mask, me, t, LPR) : 0;
             const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
@@ -176,8 +181,8 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
                 const float hwv = (RED == kRedHeadW) ? __ldg(hw + (int64_t)e * hH + hch[ch]) : 1.0f;
 #pragma unroll
                 for (int q = 0; q < V; ++q) {
-                    if (RED == PYG_MAX) {
-                        const float m = __fmul_rn(sc, v[0][ch][q]);
+                    if (IS_MAX) {
+                        const float m = RED == kRedMaxW ? __fmul_rn(sc, v[0][ch][q]) : v[0][ch][q];
                         if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
                     } else if (RED == kRedHeadW) {
                         acc[ch][q] = fmaf(hwv, v[0][ch][q], acc[ch][q]);
@@ -210,8 +215,11 @@ struct HeavyArgs {
 template <int V, int NCH, int RED>
 struct MinBlocks {
     static constexpr int base = V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1);
-    // MAX also keeps arg ids, the head-weighted sum a head index per chunk: one CTA fewer
-    static constexpr int value = ((RED == PYG_MAX || RED == kRedHeadW) && base > 1) ? base - 1 : base;
+    // the head-weighted sum keeps a head index per chunk, narrow MAX an arg id per element: one CTA fewer
+    static constexpr int value =
+        ((RED == kRedHeadW || ((RED == PYG_MAX || RED == kRedMaxW) && !(V * NCH > 16 && V * NCH <= 20))) && base > 1)
+            ? base - 1
+            : base;
 };
 template <int V, int NCH, int RED, int LPR>
 __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kernel(SegArgs a, int mode, HeavyArgs h,
@@ -250,6 +258,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
         end = min(beg + h.chunk, re);
     }
 
+    constexpr bool IS_MAX = RED == PYG_MAX || RED == kRedMaxW;
     float acc[NCH][V];
     int bi[NCH][V];
     accumulate<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
@@ -263,7 +272,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
         // MAX over several passes keeps packed (value, edge id) keys in `arg` until the last pass decodes
         // them, so the final pass visits every row too
         if (a.accum && dseg == 0 &&
-            !((RED == PYG_MEAN || RED == PYG_MAX || (EPI && (a.blend || a.col_bias))) && a.finalize))
+            !((RED == PYG_MEAN || IS_MAX || (EPI && (a.blend || a.col_bias))) && a.finalize))
             return;
         const float rsc = (EPI && a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
         const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
             if (col >= a.ncols) continue;
             const int nv = min(V, a.ncols - col);
             float* o = a.out + row * a.ldo + col;
-            if (RED != PYG_MAX) {
+            if (!IS_MAX) {
                 float r[V];
 #pragma unroll
                 for (int q = 0; q < V; ++q) r[q] = acc[ch][q];
@@ -347,7 +356,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
             for (int q = 0; q < V; ++q)
                 if (q < nv) {
                     pp[col + q] = acc[ch][q];
-                    if (RED == PYG_MAX) pa[col + q] = bi[ch][q];
+                    if (IS_MAX) pa[col + q] = bi[ch][q];
                 }
         }
     }
@@ -399,6 +408,7 @@ pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, i
         case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedHeadW: return launch_red<V, kRedHeadW>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedSumEpi: return launch_red<V, kRedSumEpi>(a, nch, lpr, tiles, mode, h, ovk, s);
+        case kRedMaxW: return launch_red<V, kRedMaxW>(a, nch, lpr, tiles, mode, h, ovk, s);
         default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
     }
 }

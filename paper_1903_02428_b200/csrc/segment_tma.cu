@@ -57,8 +57,7 @@ EncodeFn encode_fn() {
 
 // Whether the TMA path applies: unblocked propagate plan with tasks, 16-byte rows, F in [64, 1024].
 bool tma_eligible(const SegArgs& a, const pyg_plan* plan) {
-    const char* env = getenv("PYG_SEG_TMA");  // unset: auto, 0: off, 1: whenever possible (tests)
-    const int mode = env ? atoi(env) : -1;
+    const int mode = knobs().seg_tma;  // PYG_SEG_TMA unset: auto, 0: off, 1: whenever possible (tests)
     if (mode == 0 || (a.flags & PYG_NO_TMA) || !plan || !plan->parts.empty() || plan->n_tasks <= 0 ||
         !plan->task_pos || !plan->pos_row)
         return false;
@@ -83,12 +82,11 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     const int box_w = (int)align_up((size_t)((F + nb - 1) / nb), 8);  // 128-byte aligned box destinations
     const int nch = (int)cdiv(nb * box_w, 128);
     const int stage_bytes = 16 * nb * box_w;
-    const char* kb_env = getenv("PYG_TMA_WARP_KB");
+
     // ring budget per warp: 4 KB (R-MAT F=128 -> S = 2 stages of 2 KB) measured best (sum 10.6 ms
     // vs 12.9 ms at 8 KB and 22 ms at 12 KB): more resident warps beat deeper rings
-    const int budget = (kb_env ? atoi(kb_env) : 4) * 1024;
-    const char* w_env = getenv("PYG_TMA_WARPS");
-    int warps = w_env ? atoi(w_env) : 8;
+    const int budget = knobs().tma_warp_kb * 1024;
+    int warps = knobs().tma_warps;
     if (warps != 2 && warps != 4 && warps != 8) warps = 8;
     int S = std::max(2, std::min(8, budget / stage_bytes));
     if (S == 5) S = 4;

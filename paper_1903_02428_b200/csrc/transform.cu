@@ -253,18 +253,20 @@ EncodeFn encode_fn() {
 namespace {
 // dinv[i] = deg_i^-1/2 with deg_i = the row length of the plan (in-degree incl. self-loops, Q7),
 // computed in fp64 and rounded once; 0 for empty rows
-__global__ void deg_rsqrt_kernel(const int64_t* __restrict__ rowptr, int64_t n, float* dinv) {
+// (source-blocked plans: deg = the total in-degree the plan keeps per row)
+__global__ void deg_rsqrt_kernel(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ deg, int64_t n,
+                                 float* dinv) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t d = rowptr[i + 1] - rowptr[i];
+        const int64_t d = deg ? (int64_t)deg[i] : rowptr[i + 1] - rowptr[i];
         dinv[i] = d > 0 ? (float)(1.0 / sqrt((double)d)) : 0.0f;
     }
 }
 }  // namespace
 
-pyg_status_t gcn_dinv(const int64_t* rowptr, int64_t n, float* dinv, cudaStream_t s) {
+pyg_status_t gcn_dinv(const int64_t* rowptr, const int32_t* deg, int64_t n, float* dinv, cudaStream_t s) {
     if (n <= 0) return PYG_OK;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 256), 148 * 16));
-    deg_rsqrt_kernel<<<blocks, 256, 0, s>>>(rowptr, n, dinv);
+    deg_rsqrt_kernel<<<blocks, 256, 0, s>>>(rowptr, deg, n, dinv);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;

@@ -3,10 +3,10 @@
 //
 //   stream : every warp reads consecutive 512-byte pieces of an L2-resident buffer (float4),
 //            the plain L2 read bandwidth;
-//   gather : the gather pattern of seg_kernel<8, 3, *, 32> on Reddit rows -- a warp reads one random
-//            row of `row_floats` floats (row stride ld) with 256-bit loads (lane l: chunks l, l+32, l+64
-//            of 8 floats), rows drawn by a hash of the position from a table of `rows` rows that fits
-//            in L2 (no index traffic); bytes = useful row bytes.
+//   gather : the gather pattern of seg_kernel on Reddit rows -- a warp reads U random rows of
+//            `row_floats` floats (row stride ld) with V-float loads (lane l: chunks l, l+32, ...);
+//            rows are drawn by a hash of the position from a table of `rows` rows that fits in L2
+//            (no index traffic); bytes = useful row bytes.  Variants U x V are swept too.
 // Each kernel sweeps the resident CTAs per SM; the best is reported.  Prints one JSON line.
 //   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o l2peak l2peak.cu && ./l2peak
 #include <cuda_runtime.h>
@@ -45,33 +45,50 @@ __device__ __forceinline__ void ld8(float (&r)[8], const float* p) {
                  : "l"(p));
 }
 
+// U rows in flight per warp, V-float vectors (V = 8: 256-bit LDG.E.ENL2.256, V = 4: LDG.E.128)
+template <int U, int V>
 __global__ void gather_kernel(const float* __restrict__ X, int64_t ld, int row_floats, uint32_t rows,
                               int64_t n_gathers, float* sink) {
+    constexpr int NCH = (608 / V + 31) / 32;  // chunks per lane for rows up to 608 floats
     const int lane = threadIdx.x & 31;
     const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int nchunk = (row_floats + 7) / 8;
-    float acc[3][8] = {};
-    for (int64_t k = w; k < n_gathers; k += nw) {
-        const uint32_t r = hash32((uint32_t)k * 2654435761u + 12345u) % rows;
-        const float* row = X + (int64_t)r * ld;
-        float v[3][8];
+    const int nchunk = (row_floats + V - 1) / V;
+    float acc[NCH][V] = {};
+    for (int64_t k0 = w * U; k0 < n_gathers; k0 += nw * U) {
+        float v[U][NCH][V];
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-            if (lane + 32 * c < nchunk) ld8(v[c], row + 8 * (lane + 32 * c));
+        for (int u = 0; u < U; ++u) {
+            const uint32_t r = hash32((uint32_t)(k0 + u) * 2654435761u + 12345u) % rows;
+            const float* row = X + (int64_t)r * ld;
 #pragma unroll
-        for (int c = 0; c < 3; ++c)
-            if (lane + 32 * c < nchunk)
+            for (int c = 0; c < NCH; ++c) {
+                if (lane + 32 * c < nchunk) {
+                    if constexpr (V == 8) ld8(v[u][c], row + 8 * (lane + 32 * c));
+                    else {
+                        const float4 t = __ldg(reinterpret_cast<const float4*>(row) + lane + 32 * c);
+                        v[u][c][0] = t.x; v[u][c][1] = t.y; v[u][c][2] = t.z; v[u][c][3] = t.w;
+                    }
+                }
+            }
+        }
 #pragma unroll
-                for (int q = 0; q < 8; ++q) acc[c][q] += v[c][q];
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int c = 0; c < NCH; ++c)
+                if (lane + 32 * c < nchunk)
+#pragma unroll
+                    for (int q = 0; q < V; ++q) acc[c][q] += v[u][c][q];
     }
     float s = 0.f;
 #pragma unroll
-    for (int c = 0; c < 3; ++c)
+    for (int c = 0; c < NCH; ++c)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) s += acc[c][q];
+        for (int q = 0; q < V; ++q) s += acc[c][q];
     if (s == 123.456f) sink[w] = s;
 }
+
+typedef void (*gather_fn)(const float*, int64_t, int, uint32_t, int64_t, float*);
 
 int main() {
     int dev = 0, sms = 0, l2 = 0;
@@ -93,6 +110,7 @@ int main() {
     CK(cudaEventCreate(&e1));
     double best_stream = 0, best_gather = 0;
     int best_stream_b = 0, best_gather_b = 0;
+    const char* best_variant = "";
     const int64_t n4 = (int64_t)(bytes / 16);
     const int64_t reps = 200;
     const int64_t n_gathers = 40LL * 1000 * 1000;
@@ -108,22 +126,26 @@ int main() {
             const double gbs = (double)bytes * reps / (ms * 1e-3) / 1e9;
             if (it && gbs > best_stream) { best_stream = gbs; best_stream_b = b; }
         }
-        for (int it = 0; it < 2; ++it) {
-            CK(cudaEventRecord(e0));
-            gather_kernel<<<grid, 256>>>(X, ld, row_floats, rows, n_gathers, sink);
-            CK(cudaEventRecord(e1));
-            CK(cudaEventSynchronize(e1));
-            float ms = 0;
-            CK(cudaEventElapsedTime(&ms, e0, e1));
-            const double gbs = (double)n_gathers * row_floats * 4 / (ms * 1e-3) / 1e9;
-            if (it && gbs > best_gather) { best_gather = gbs; best_gather_b = b; }
-        }
+        const gather_fn fns[] = {gather_kernel<1, 8>, gather_kernel<2, 8>, gather_kernel<1, 4>, gather_kernel<2, 4>,
+                                 gather_kernel<4, 4>};
+        const char* names[] = {"U1V8", "U2V8", "U1V4", "U2V4", "U4V4"};
+        for (int f = 0; f < 5; ++f)
+            for (int it = 0; it < 2; ++it) {
+                CK(cudaEventRecord(e0));
+                fns[f]<<<grid, 256>>>(X, ld, row_floats, rows, n_gathers, sink);
+                CK(cudaEventRecord(e1));
+                CK(cudaEventSynchronize(e1));
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, e0, e1));
+                const double gbs = (double)n_gathers * row_floats * 4 / (ms * 1e-3) / 1e9;
+                if (it && gbs > best_gather) { best_gather = gbs; best_gather_b = b; best_variant = names[f]; }
+            }
     }
     CK(cudaGetLastError());
     printf("{\"gpu\": \"%s\", \"sms\": %d, \"l2_bytes\": %d, \"table_bytes\": %zu, \"row_bytes\": %d, "
            "\"l2_stream_gbs\": %.1f, \"l2_stream_ctas_per_sm\": %d, \"l2_row_gather_gbs\": %.1f, "
-           "\"l2_row_gather_ctas_per_sm\": %d, \"n_gathers\": %lld}\n",
+           "\"l2_row_gather_ctas_per_sm\": %d, \"l2_row_gather_variant\": \"%s\", \"n_gathers\": %lld}\n",
            prop.name, sms, l2, bytes, row_floats * 4, best_stream, best_stream_b, best_gather, best_gather_b,
-           (long long)n_gathers);
+           best_variant, (long long)n_gathers);
     return 0;
 }

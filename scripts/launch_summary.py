@@ -29,7 +29,10 @@ for r in rows:
         v *= 1e6
     launch[i][r[M]] = v
 n_last = int(sys.argv[2]) if len(sys.argv) > 2 else 0
-ours = [i for i in order if "pyg" in launch[i]["name"] or "seg::" in launch[i]["name"]]
+OURS = ("pyg", "seg::", "seg_kernel", "seg_tma", "coo_kernel", "combine", "degree_kernel", "hub_", "zero_slots",
+        "mean_div", "max_decode", "softmax", "gat_", "tf32_gemm", "pool_kernel", "gather_rows", "halo_", "empty_rows",
+        "dist_", "xi_kernel", "edge_", "fill_")
+ours = [i for i in order if any(k in launch[i]["name"] for k in OURS)]
 sel = ours[-n_last:] if n_last else ours
 tot_t = sum(launch[i].get("gpu__time_duration.sum", 0) for i in sel)
 tot_b = sum(launch[i].get("dram__bytes_read.sum", 0) + launch[i].get("dram__bytes_write.sum", 0) for i in sel)

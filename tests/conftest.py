@@ -26,3 +26,24 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+@pytest.fixture(autouse=True)
+def _refresh_library_knobs(monkeypatch):
+    """libpygs reads its PYG_* tuning knobs once; tests that monkeypatch them get them re-read
+    (monkeypatch.setenv wrapped) and restored after the test."""
+    mod = sys.modules.get("paper_1903_02428_b200._abi")
+    orig = monkeypatch.setenv
+
+    def setenv(name, value, prepend=None):
+        orig(name, value, prepend)
+        m = sys.modules.get("paper_1903_02428_b200._abi")
+        if m is not None and name.startswith("PYG_"):
+            m.lib.pyg_refresh_env()
+
+    monkeypatch.setenv = setenv
+    yield
+    monkeypatch.undo()
+    m = sys.modules.get("paper_1903_02428_b200._abi") or mod
+    if m is not None:
+        m.lib.pyg_refresh_env()

@@ -58,7 +58,7 @@ def test_host_validation_without_gpu():
     assert lib.pyg_workspace_size(None, 1000, 100, 16, 0, 0, ctypes.byref(small)) == 0
     assert lib.pyg_workspace_size(None, 10_000_000, 100, 16, 0, 0, ctypes.byref(big)) == 0
     assert lib.pyg_workspace_size(None, 10_000_000, 100, 16, 2, 0, ctypes.byref(mx)) == 0
-    assert big.value > small.value + (10_000_000 // 1024) * 16 * 4 and mx.value < big.value
+    assert big.value > small.value + (10_000_000 // 2048) * 16 * 4 and mx.value < big.value
     assert lib.pyg_workspace_size(None, -1, 100, 16, 0, 0, ctypes.byref(mx)) == 1
 
 

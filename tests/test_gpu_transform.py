@@ -77,11 +77,13 @@ def test_dense_transform_errors():
         pg.pyg_dense_transform(torch.zeros((10, 9), device=DEV)[:, 1:], torch.zeros((4, 8), device=DEV))  # unaligned
 
 
+@pytest.mark.parametrize("blocked", [False, True])
 @pytest.mark.parametrize("cfg", ["cora", "pubmed", "rmat_hubs"])
-def test_gcn_layer_fused_normalisation(cfg, monkeypatch):
+def test_gcn_layer_fused_normalisation(cfg, blocked, monkeypatch):
     """pyg_gcn_layer (transform with D^-1/2 rows on the tensor cores, unweighted aggregation over A+I
     with a D^-1/2 row scale and the bias in the epilogue) against the oracle's gcn_norm-weighted
-    propagate of its fp64 transform, plus bias."""
+    propagate of its fp64 transform, plus bias.  blocked: a source-blocked plan (several
+    L2-resident passes; D^-1/2 from the plan's total degree, epilogue in the last pass)."""
     import paper_1903_02428_b200 as pg
 
     if cfg == "cora":
@@ -99,7 +101,9 @@ def test_gcn_layer_fused_normalisation(cfg, monkeypatch):
     w = (rng.standard_normal((F_out, K)) / np.sqrt(K)).astype(np.float32)
     b = rng.standard_normal(F_out).astype(np.float32)
     ei2, _ = pg.pyg_gcn_norm(_t(ei_np), N)
-    plan = pg.pyg_plan_build(ei2[1], ei2[0], N, N)
+    plan = pg.pyg_plan_build(ei2[1], ei2[0], N, N, col_block=(N // 5 + 1) if blocked else 0)
+    if blocked:
+        assert plan.view()["n_col_blocks"] >= 5
     ldk = (K + 3) // 4 * 4
     xb = torch.zeros((N, ldk), device=DEV)
     xb[:, :K] = _t(x_np)
