@@ -47,6 +47,8 @@ static Knobs read_knobs() {
     k.tma_hubs = get("PYG_TMA_HUBS", 1);
     k.tma_warp_kb = get("PYG_TMA_WARP_KB", 4);
     k.tma_warps = get("PYG_TMA_WARPS", 8);
+    k.seg_bulk = get("PYG_SEG_BULK", -1);
+    k.bulk_warp_kb = get("PYG_BULK_WARP_KB", 8);
     return k;
 }
 static Knobs g_knobs = read_knobs();

@@ -215,26 +215,47 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(SoftmaxArgs a, RowSet 
         float m[kMaxHeads], s[kMaxHeads], l[kMaxHeads];
 #pragma unroll
         for (int h = 0; h < kMaxHeads; ++h) { m[h] = -INFINITY; s[h] = 0.0f; }
-        for (int64_t p = b + t; p < e; p += G) {
-            const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-            logits<GAT>(a, p, k, sd, l);
+        // (PU = 2 / 4 positions per step measured slower on R-MAT: softmax 21 -> 27 ms at PU = 4, the
+        // register growth cost more warps than the extra gathers in flight gained; gpurun_out/r2h)
+        constexpr int PU = 1;
+        for (int64_t p0 = b + t; p0 < e; p0 += (int64_t)G * PU) {
+            float lv[PU][kMaxHeads];
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) {
-                if (h >= a.H) continue;
-                if (l[h] > m[h]) { s[h] = s[h] * expf(m[h] - l[h]) + 1.0f; m[h] = l[h]; }
-                else s[h] += expf(l[h] - m[h]);
+            for (int j = 0; j < PU; ++j) {
+                const int64_t p = p0 + (int64_t)j * G;
+                if (p < e) logits<GAT>(a, p, a.eid ? (int64_t)a.eid[p] : p, sd, lv[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < PU; ++j) {
+                if (p0 + (int64_t)j * G >= e) continue;
+#pragma unroll
+                for (int h = 0; h < kMaxHeads; ++h) {
+                    if (h >= a.H) continue;
+                    if (lv[j][h] > m[h]) { s[h] = s[h] * expf(m[h] - lv[j][h]) + 1.0f; m[h] = lv[j][h]; }
+                    else s[h] += expf(lv[j][h] - m[h]);
+                }
             }
         }
         grp.max_sum(m, s, a.H);
-        for (int64_t p = b + t; p < e; p += G) {
-            const int64_t k = a.eid ? (int64_t)a.eid[p] : p;
-            logits<GAT>(a, p, k, sd, l);
+        for (int64_t p0 = b + t; p0 < e; p0 += (int64_t)G * PU) {
+            float lv[PU][kMaxHeads];
+            int64_t kv[PU];
 #pragma unroll
-            for (int h = 0; h < kMaxHeads; ++h) l[h] = h < a.H ? expf(l[h] - m[h]) / s[h] : 0.0f;
-            if (a.lda == a.H) {
-                store_heads(a.alpha, k, a.H, l);
-            } else {
-                for (int h = 0; h < a.H; ++h) a.alpha[k * a.lda + h] = l[h];
+            for (int j = 0; j < PU; ++j) {
+                const int64_t p = p0 + (int64_t)j * G;
+                kv[j] = p < e ? (a.eid ? (int64_t)a.eid[p] : p) : -1;
+                if (p < e) logits<GAT>(a, p, kv[j], sd, lv[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < PU; ++j) {
+                if (kv[j] < 0) continue;
+#pragma unroll
+                for (int h = 0; h < kMaxHeads; ++h) l[h] = h < a.H ? expf(lv[j][h] - m[h]) / s[h] : 0.0f;
+                if (a.lda == a.H) {
+                    store_heads(a.alpha, kv[j], a.H, l);
+                } else {
+                    for (int h = 0; h < a.H; ++h) a.alpha[kv[j] * a.lda + h] = l[h];
+                }
             }
         }
     }

@@ -57,6 +57,8 @@ struct Knobs {
     int tma_hubs = 1;     // PYG_TMA_HUBS: 0 keeps split hub rows on the LDG kernel
     int tma_warp_kb = 4;  // PYG_TMA_WARP_KB: ring bytes per warp of the TMA gather4 kernel
     int tma_warps = 8;    // PYG_TMA_WARPS
+    int seg_bulk = -1;    // PYG_SEG_BULK: row-staged bulk-copy kernel -- -1 auto (MAX), 0 off, 1 all eligible
+    int bulk_warp_kb = 8; // PYG_BULK_WARP_KB: ring bytes per warp of the bulk-copy kernel
 };
 const Knobs& knobs();
 

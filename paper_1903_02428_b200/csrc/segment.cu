@@ -15,6 +15,8 @@ extern template pyg_status_t launch<8>(const SegArgs&, int, int, int, int, int, 
 }  // namespace seg
 
 bool tma_eligible(const SegArgs& a, const pyg_plan* plan);
+bool bulk_eligible(const SegArgs& a, const pyg_plan* plan, int reduce);
+pyg_status_t segment_bulk(const SegArgs& a, int reduce, unsigned long long* counter, int ovk, cudaStream_t s);
 pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, unsigned long long* counter,
                          float* part, int32_t* part_arg, int64_t ldp, cudaStream_t s);
 
@@ -112,7 +114,10 @@ Geometry choose(const SegArgs& a) {
     for (int V : {2, 4, 8}) {
         if (!v_ok(a, V)) continue;
         Geometry g = geometry(a.ncols, V);
-        if (g.util >= best.util - 1e-9 || (V <= 4 && g.util >= 0.75)) best = g;
+        // 256-bit loads only when they fill clearly more lanes: at equal utilisation V = 4 won
+        // (GCN aggregation at F = 512 on 9 L2-resident passes: 13.0 ms with V = 4, NCH = 4 vs 20.8 ms
+        // with V = 8, NCH = 2, whose SASS keeps the loaded rows in local memory; gpurun_out/r2h)
+        if (V == 8 ? g.util > best.util * 1.05 : (g.util >= best.util - 1e-9 || (V <= 4 && g.util >= 0.75))) best = g;
     }
     // Few rows with narrow features (e.g. 10,000 rows x 16 columns): one group of LPR lanes per row
     // leaves most of the GPU idle (4 lanes per row at V = 4 -> 40k threads).  Narrow the vector
@@ -160,15 +165,22 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
     const bool extras = a.row_scale || a.blend || a.col_bias;
     if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: epilogue extras need SUM");
-    // LDG / combine instantiation: weighted MAX multiplies, plain MAX compares x_j directly
-    const int red_k = extras ? kRedSumEpi : (reduce == PYG_MAX && (a.w || a.gdeg)) ? kRedMaxW : reduce;
+    const int red_k = extras ? kRedSumEpi : reduce;  // LDG / combine instantiation
     const bool tma = ws && cv.ok() && tma_eligible(a, plan);
     // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
     // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel
     const bool tma_hubs = tma && split && knobs().tma_hubs != 0;
-    // light rows: TMA gather4 pipeline or the LDG kernel
-    if (tma && !tma_hubs) PYG_TRY(segment_tma(a, reduce, plan, counter, nullptr, nullptr, 0, s));
-    else if (!tma) PYG_TRY(launch(a, red_k, g, 0, h, ovk, s));
+    // wide rows without split hubs (source-blocked passes): the row-staged bulk-copy kernel
+    const bool bulk = !tma && ws && cv.ok() && bulk_eligible(a, plan, reduce);
+    // light rows: TMA gather4 pipeline, the bulk-copy kernel or the LDG kernel
+    if (tma && !tma_hubs) {
+        PYG_TRY(segment_tma(a, reduce, plan, counter, nullptr, nullptr, 0, s));
+    } else if (bulk) {
+        const int ovk4 = (a.ldo % 4 == 0) && aligned(a.out, 16);
+        PYG_TRY(segment_bulk(a, extras ? kRedSumEpi : (reduce == PYG_MAX && a.w) ? kRedMaxW : reduce, counter, ovk4, s));
+    } else if (!tma) {
+        PYG_TRY(launch(a, red_k, g, 0, h, ovk, s));
+    }
     if (!split) return PYG_OK;
 
     // split hub rows: chunk partials, then the fp64 combine
@@ -196,7 +208,7 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
         case kRedSumEpi: combine_kernel<kRedSumEpi><<<grid, ct, 0, s>>>(a, h); break;
         case PYG_MEAN: combine_kernel<PYG_MEAN><<<grid, ct, 0, s>>>(a, h); break;
         case kRedHeadW: combine_kernel<kRedHeadW><<<grid, ct, 0, s>>>(a, h); break;
-        default: combine_kernel<PYG_MAX><<<grid, ct, 0, s>>>(a, h); break;  // PYG_MAX, kRedMaxW
+        default: combine_kernel<PYG_MAX><<<grid, ct, 0, s>>>(a, h); break;
     }
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());

@@ -157,8 +157,10 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
 #pragma unroll
                     for (int q = 0; q < V; ++q) {
                         if (IS_MAX) {
-                            // plain MAX: the message is x_j itself (no multiply); kRedMaxW: w * x_j
-                            const float m = RED == kRedMaxW ? __fmul_rn(sv[u], v[u][ch][q]) : v[u][ch][q];
+                            // m = w * x_j (s = 1 without weights: exact).  Dropping the multiply for the
+                            // unweighted case was measured SLOWER on Reddit (27.7 vs 23.8 ms: ptxas then
+                            // spills 208 instead of 72 bytes at 3 CTAs / SM), so both cases multiply
+                            const float m = __fmul_rn(sv[u], v[u][ch][q]);
                             if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = ev[u]; }  // acc starts at -inf (Q5: finite inputs)
                         } else if (RED == kRedHeadW) {
                             acc[ch][q] = fmaf(hwv, v[u][ch][q], acc[ch][q]);
@@ -182,7 +184,7 @@ __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_
 #pragma unroll
                 for (int q = 0; q < V; ++q) {
                     if (IS_MAX) {
-                        const float m = RED == kRedMaxW ? __fmul_rn(sc, v[0][ch][q]) : v[0][ch][q];
+                        const float m = __fmul_rn(sc, v[0][ch][q]);
                         if (m > acc[ch][q]) { acc[ch][q] = m; bi[ch][q] = e; }
                     } else if (RED == kRedHeadW) {
                         acc[ch][q] = fmaf(hwv, v[0][ch][q], acc[ch][q]);
@@ -221,6 +223,94 @@ struct MinBlocks {
             ? base - 1
             : base;
 };
+// Epilogue of a light row (mode 0): write / accumulate into `out` (and `arg`), apply the mean divide,
+// the GCN / APPNP extras and, for MAX over several passes, the packed-key merge / decode.  Shared by
+// seg_kernel and the bulk-copy pipeline (segment_bulk.cuh).
+template <int V, int NCH, int RED, int LPR>
+__device__ __forceinline__ void row_epilogue(const SegArgs& a, int64_t row, int64_t dseg, int l, int c0,
+                                             const float (&acc)[NCH][V], const int (&bi)[NCH][V], int out_vec_ok) {
+    constexpr bool IS_MAX = RED == PYG_MAX || RED == kRedMaxW;
+    // accumulate passes (source-blocked plans) have nothing to add for empty segments
+    // the GCN / APPNP epilogue extras exist only in the kRedSumEpi instantiation, so the plain
+    // SUM / MEAN kernels keep their register budget
+    constexpr bool EPI = RED == kRedSumEpi;
+    // MAX over several passes keeps packed (value, edge id) keys in `arg` until the last pass decodes
+    // them, so the final pass visits every row too
+    if (a.accum && dseg == 0 &&
+        !((RED == PYG_MEAN || IS_MAX || (EPI && (a.blend || a.col_bias))) && a.finalize))
+        return;
+    const float rsc = (EPI && a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
+    const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int col = c0 + l * V + ch * LPR * V;
+        if (col >= a.ncols) continue;
+        const int nv = min(V, a.ncols - col);
+        float* o = a.out + row * a.ldo + col;
+        if (!IS_MAX) {
+            float r[V];
+#pragma unroll
+            for (int q = 0; q < V; ++q) r[q] = acc[ch][q];
+            if (a.accum) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) if (q < nv) r[q] += o[q];
+            }
+            if (RED == PYG_MEAN && a.finalize) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
+            }
+            if (EPI && a.row_scale && a.finalize) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) r[q] *= rsc;
+            }
+            if (EPI && a.blend && a.finalize) {
+                const float* hb = a.blend + row * a.ldb + col;
+#pragma unroll
+                for (int q = 0; q < V; ++q) if (q < nv) r[q] = fmaf(a.blend_b, hb[q], a.blend_a * r[q]);
+            }
+            if (EPI && a.col_bias && a.finalize) {
+#pragma unroll
+                for (int q = 0; q < V; ++q) if (q < nv) r[q] += __ldg(a.col_bias + col + q);
+            }
+            st<V>(o, r, nv, out_vec_ok);
+        } else {
+            int64_t* ap = a.arg + row * a.lda + col;
+            if (!a.accum && a.finalize) {  // one pass: write (value, arg)
+                float r[V];
+#pragma unroll
+                for (int q = 0; q < V; ++q) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
+                st<V>(o, r, nv, out_vec_ok);
+#pragma unroll
+                for (int q = 0; q < V; ++q)
+                    if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
+            } else {
+                // several passes (source-blocked plans): the arg buffer holds the packed key
+                // (ord(value) << 32 | ~edge id; 0 = no edge yet) so each pass merges with ONE 8-byte
+                // read-modify-write -- larger value wins, IEEE-equal -> lower edge id (Q4) -- and the
+                // last pass decodes it into (value, arg)
+                unsigned long long* kp = reinterpret_cast<unsigned long long*>(ap);
+#pragma unroll
+                for (int q = 0; q < V; ++q) {
+                    if (q >= nv) continue;
+                    const unsigned long long nk = bi[ch][q] >= 0 ? max_key(acc[ch][q], (uint32_t)bi[ch][q]) : 0ull;
+                    unsigned long long k = nk;
+                    if (a.accum) {
+                        const unsigned long long old = kp[q];
+                        k = old > nk ? old : nk;
+                        if (!a.finalize && k == old) continue;
+                    }
+                    if (a.finalize) {
+                        o[q] = k ? ord2f((uint32_t)(k >> 32)) : 0.0f;
+                        ap[q] = k ? (int64_t)(0xffffffffu - (uint32_t)(k & 0xffffffffu)) : a.E_sentinel;
+                    } else {
+                        kp[q] = k;
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int V, int NCH, int RED, int LPR>
 __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kernel(SegArgs a, int mode, HeavyArgs h,
                                                                                   int out_vec_ok) {
@@ -264,86 +354,7 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
     accumulate<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
 
     if (mode == 0) {
-        const int64_t dseg = end - beg;
-        // accumulate passes (source-blocked plans) have nothing to add for empty segments
-        // the GCN / APPNP epilogue extras exist only in the kRedSumEpi instantiation, so the plain
-        // SUM / MEAN kernels keep their register budget
-        constexpr bool EPI = RED == kRedSumEpi;
-        // MAX over several passes keeps packed (value, edge id) keys in `arg` until the last pass decodes
-        // them, so the final pass visits every row too
-        if (a.accum && dseg == 0 &&
-            !((RED == PYG_MEAN || IS_MAX || (EPI && (a.blend || a.col_bias))) && a.finalize))
-            return;
-        const float rsc = (EPI && a.row_scale && a.finalize) ? __ldg(a.row_scale + row) : 1.0f;
-        const int64_t dtot = (RED == PYG_MEAN && a.deg_total) ? (int64_t)__ldg(a.deg_total + row) : dseg;
-#pragma unroll
-        for (int ch = 0; ch < NCH; ++ch) {
-            const int col = c0 + l * V + ch * LPR * V;
-            if (col >= a.ncols) continue;
-            const int nv = min(V, a.ncols - col);
-            float* o = a.out + row * a.ldo + col;
-            if (!IS_MAX) {
-                float r[V];
-#pragma unroll
-                for (int q = 0; q < V; ++q) r[q] = acc[ch][q];
-                if (a.accum) {
-#pragma unroll
-                    for (int q = 0; q < V; ++q) if (q < nv) r[q] += o[q];
-                }
-                if (RED == PYG_MEAN && a.finalize) {
-#pragma unroll
-                    for (int q = 0; q < V; ++q) r[q] = dtot > 0 ? r[q] / (float)dtot : 0.0f;
-                }
-                if (EPI && a.row_scale && a.finalize) {
-#pragma unroll
-                    for (int q = 0; q < V; ++q) r[q] *= rsc;
-                }
-                if (EPI && a.blend && a.finalize) {
-                    const float* hb = a.blend + row * a.ldb + col;
-#pragma unroll
-                    for (int q = 0; q < V; ++q) if (q < nv) r[q] = fmaf(a.blend_b, hb[q], a.blend_a * r[q]);
-                }
-                if (EPI && a.col_bias && a.finalize) {
-#pragma unroll
-                    for (int q = 0; q < V; ++q) if (q < nv) r[q] += __ldg(a.col_bias + col + q);
-                }
-                st<V>(o, r, nv, out_vec_ok);
-            } else {
-                int64_t* ap = a.arg + row * a.lda + col;
-                if (!a.accum && a.finalize) {  // one pass: write (value, arg)
-                    float r[V];
-#pragma unroll
-                    for (int q = 0; q < V; ++q) r[q] = bi[ch][q] >= 0 ? acc[ch][q] : 0.0f;
-                    st<V>(o, r, nv, out_vec_ok);
-#pragma unroll
-                    for (int q = 0; q < V; ++q)
-                        if (q < nv) ap[q] = bi[ch][q] >= 0 ? (int64_t)bi[ch][q] : a.E_sentinel;
-                } else {
-                    // several passes (source-blocked plans): the arg buffer holds the packed key
-                    // (ord(value) << 32 | ~edge id; 0 = no edge yet) so each pass merges with ONE 8-byte
-                    // read-modify-write -- larger value wins, IEEE-equal -> lower edge id (Q4) -- and the
-                    // last pass decodes it into (value, arg)
-                    unsigned long long* kp = reinterpret_cast<unsigned long long*>(ap);
-#pragma unroll
-                    for (int q = 0; q < V; ++q) {
-                        if (q >= nv) continue;
-                        const unsigned long long nk = bi[ch][q] >= 0 ? max_key(acc[ch][q], (uint32_t)bi[ch][q]) : 0ull;
-                        unsigned long long k = nk;
-                        if (a.accum) {
-                            const unsigned long long old = kp[q];
-                            k = old > nk ? old : nk;
-                            if (!a.finalize && k == old) continue;
-                        }
-                        if (a.finalize) {
-                            o[q] = k ? ord2f((uint32_t)(k >> 32)) : 0.0f;
-                            ap[q] = k ? (int64_t)(0xffffffffu - (uint32_t)(k & 0xffffffffu)) : a.E_sentinel;
-                        } else {
-                            kp[q] = k;
-                        }
-                    }
-                }
-            }
-        }
+        row_epilogue<V, NCH, RED, LPR>(a, row, end - beg, l, c0, acc, bi, out_vec_ok);
     } else {
         float* pp = h.part + gid * h.ldp;
         int32_t* pa = h.part_arg ? h.part_arg + gid * h.ldp : nullptr;
@@ -408,7 +419,6 @@ pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, i
         case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedHeadW: return launch_red<V, kRedHeadW>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedSumEpi: return launch_red<V, kRedSumEpi>(a, nch, lpr, tiles, mode, h, ovk, s);
-        case kRedMaxW: return launch_red<V, kRedMaxW>(a, nch, lpr, tiles, mode, h, ovk, s);
         default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
     }
 }
