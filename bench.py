@@ -216,14 +216,18 @@ def alg_bytes(E, n_dst, F, reduce, strategy, weighted=False):
 
 
 def gat_step_bytes(E, N, F, H):
-    """Algorithmic bytes of one GAT aggregation forward + backward (NEXT-1), every array counted
-    once per kernel that must read or write it: per edge the index pair (col 4 B + edge id 4 B) in
-    each of the five kernels, the gathered rows (z in the forward and the SDDMM, grad_out over the
-    transposed plan: 3 x 4F), the per-edge scalars (s_src gather 4H x 2, alpha write / read x3,
-    dL/dlogit write / read 4H x 2); per node z-out, grad_out, grad_z (4F each), rowptrs (2 x 8),
-    s_dst / grad_s_dst / grad_s_src (4H each)."""
-    per_edge = 5 * 8 + 3 * 4 * F + 4 * H * (2 + 3 + 2)
-    per_node = 3 * 4 * F + 2 * 8 + 3 * 4 * H
+    """Algorithmic bytes of one GAT aggregation forward + backward (NEXT-1), every array counted once
+    per kernel that must read or write it (index widths as stored: int32 col / edge id / row):
+      per edge: softmax (two passes: col + edge id + s_src row 4H each, alpha write 4H) 16 + 12H;
+                alpha-weighted sum (col, edge id, z row 4F, alpha 4H) 8 + 4F + 4H;
+                one-pass backward (col, edge id, row, z row 4F, alpha, s_src, dlogit write) 12 + 4F + 12H;
+                grad_z over the transposed plan (col, edge id, grad_out row 4F, alpha) 8 + 4F + 4H;
+                grad_s_src (edge id, dlogit row) 4 + 4H;
+      per node: out write 4F; t_i = g_i . out_i (g, out, t) 8F + 4H; backward row state (g, t, s_dst,
+                grad_s_dst) 4F + 12H; grad_z write 4F; grad_s_src write 4H; s_dst in the softmax 4H;
+                rowptrs 2 x 8."""
+    per_edge = 48 + 12 * F + 32 * H
+    per_node = 20 * F + 24 * H + 16
     return E * per_edge + N * per_node
 
 
@@ -763,11 +767,13 @@ def main():
         zc = torch.randn((N, F), generator=gg, device=dev)
         gout = torch.randn((N, F), generator=gg, device=dev)
         gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
+        gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C), 1), dtype=torch.uint8,
+                          device=dev)
         passes, red = 2, "gat"
 
         def compute():
             o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"])
-            gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT)
+            gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT, out=o, workspace=gws)
 
     gatl = None
     if a.op == "gatlayer":

@@ -372,6 +372,9 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
                                float negative_slope, const pyg_plan_t* plan, float* out,
                                int64_t ldo, float* alpha, void* workspace, size_t workspace_bytes,
                                void* stream);
+/* Scratch of pyg_gat_backward (both its paths).  Host-only. */
+pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_plan_t* plan_T,
+                                             int64_t H, int64_t C, size_t* bytes);
 /* Backward of pyg_gat_propagate, g = grad_out [n_dst x H*C] stride ldg:
  *   grad_z[j][h*C+c] = sum_{k: src_k = j} alpha[k][h] g[dst_k][h*C+c]     (grad_z optional)
  *   grad_logit[k][h] = alpha[k][h] (g_i . z_j|_h - sum_{k' in seg(i)} alpha[k'][h] g_i . z_j'|_h)
@@ -379,13 +382,19 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
  *                      [E x H] packed, by edge id)
  *   grad_s_dst[i][h] = sum over i's in-edges of grad_logit     ([n_dst x H] packed, required)
  *   grad_s_src[j][h] = sum over j's out-edges of grad_logit    ([n_src x H] packed, optional)
+ * out [n_dst x H*C] stride ldo: the forward output of pyg_gat_propagate, or NULL.  With it,
+ *   sum_{k' in seg(i)} alpha[k'][h] g_i . z_j'|_h = g_i . out_i|_h (the aggregation is linear in
+ *   z), so the SDDMM and the softmax backward run as ONE streaming pass over the plan (TMA
+ *   gather4 pipeline; H in {4, 8}, C a power of two <= 128 or a multiple of 128, 16-byte
+ *   aligned rows); without it (or outside those shapes) two passes per row recompute the sum.
  * plan: the forward plan; plan_T: row_index = sources, col_index = targets.
- * H*C <= 4096.  workspace: pyg_workspace_size(plan_T, n_src, H*C, PYG_SUM, 0).
+ * H*C <= 4096.  workspace: pyg_gat_backward_workspace_size(plan, plan_T, H, C).
  * Asynchronous. */
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                               const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
                               float negative_slope, const float* alpha, const float* grad_out,
-                              int64_t ldg, const pyg_plan_t* plan, const pyg_plan_t* plan_T,
+                              int64_t ldg, const float* out, int64_t ldo,
+                              const pyg_plan_t* plan, const pyg_plan_t* plan_T,
                               float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst,
                               float* grad_logit, void* workspace, size_t workspace_bytes,
                               void* stream);

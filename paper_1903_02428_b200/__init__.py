@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version", "DistComm", "DistPlan", "pyg_dist_unique_id", "pyg_dist_init", "pyg_dist_plan_build",
     "pyg_dist_propagate", "pyg_dist_propagate_backward",
 ]
@@ -408,23 +408,35 @@ def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor,
     return out, alpha
 
 
+def pyg_gat_backward_workspace_size(plan: Plan, plan_T: Plan, H: int, C: int) -> int:
+    nb = ctypes.c_size_t()
+    check(lib.pyg_gat_backward_workspace_size(plan.handle, plan_T.handle, H, C, ctypes.byref(nb)),
+          "pyg_gat_backward_workspace_size")
+    return nb.value
+
+
 def pyg_gat_backward(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, alpha: torch.Tensor,
-                     grad_out: torch.Tensor, plan: Plan, plan_T: Plan, negative_slope: float = 0.2):
-    """dict(z, s_src, s_dst, logit) gradients of pyg_gat_propagate."""
+                     grad_out: torch.Tensor, plan: Plan, plan_T: Plan, negative_slope: float = 0.2,
+                     out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+    """dict(z, s_src, s_dst, logit) gradients of pyg_gat_propagate.  out: the forward output (enables
+    the one-pass SDDMM + softmax backward, t_i = g_i . out_i)."""
     n_src, F, ldz = _rows(z, "z")
     C = F // H
     n_dst = s_dst.shape[0]
     E = plan.view()["E"]
     _, _, ldg = _rows(grad_out, "grad_out")
+    ldo = _rows(out, "out")[2] if out is not None else 0
     dev = z.device
     gz = torch.empty((n_src, F), dtype=torch.float32, device=dev)
     gss = torch.empty((n_src, H), dtype=torch.float32, device=dev)
     gsd = torch.empty((n_dst, H), dtype=torch.float32, device=dev)
     gl = torch.empty((max(E, 1), H), dtype=torch.float32, device=dev)[:E]
-    ws = _workspace(pyg_workspace_size(plan_T, n_src, F, SUM), dev)
+    if workspace is None:
+        workspace = _workspace(pyg_gat_backward_workspace_size(plan, plan_T, H, C), dev)
     check(lib.pyg_gat_backward(_ptr(z), n_src, H, C, ldz, _ptr(s_src.contiguous()), _ptr(s_dst.contiguous()), n_dst,
-                               E, negative_slope, _ptr(alpha), _ptr(grad_out), ldg, plan.handle, plan_T.handle,
-                               _ptr(gz), F, _ptr(gss), _ptr(gsd), _ptr(gl), _ptr(ws), ws.numel(), _stream(dev)),
+                               E, negative_slope, _ptr(alpha), _ptr(grad_out), ldg, _ptr(out), ldo, plan.handle,
+                               plan_T.handle, _ptr(gz), F, _ptr(gss), _ptr(gsd), _ptr(gl), _ptr(workspace),
+                               workspace.numel(), _stream(dev)),
           "pyg_gat_backward")
     return {"z": gz, "s_src": gss, "s_dst": gsd, "logit": gl}
 

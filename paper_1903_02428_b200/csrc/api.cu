@@ -49,6 +49,8 @@ static Knobs read_knobs() {
     k.tma_warps = get("PYG_TMA_WARPS", 8);
     k.seg_bulk = get("PYG_SEG_BULK", -1);
     k.bulk_warp_kb = get("PYG_BULK_WARP_KB", 8);
+    k.gat_warp_kb = get("PYG_GAT_WARP_KB", 10);
+    k.gat_sm_kb = get("PYG_GAT_SM_KB", 160);
     return k;
 }
 static Knobs g_knobs = read_knobs();
@@ -668,11 +670,18 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
     return headw_sum(plan, z, ldz, F, C, H, alpha, out, ldo, n_dst, ws, ws_bytes, s);
 }
 
+pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_plan_t* plan_T, int64_t H, int64_t C,
+                                             size_t* bytes) {
+    REQUIRE(bytes && plan && plan_T && H > 0 && C >= 0, PYG_ERR_INVALID_ARGUMENT, "gat_backward_workspace_size: bad args");
+    *bytes = std::max(gat_bwd_tma_ws_bytes(plan, H), segment_ws_bytes(plan_T, H * C, PYG_SUM));
+    return PYG_OK;
+}
+
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
                               const float* s_dst, int64_t n_dst, int64_t E, float negative_slope, const float* alpha,
-                              const float* grad_out, int64_t ldg, const pyg_plan_t* plan, const pyg_plan_t* plan_T,
-                              float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst, float* grad_logit,
-                              void* ws, size_t ws_bytes, void* stream) {
+                              const float* grad_out, int64_t ldg, const float* out, int64_t ldo, const pyg_plan_t* plan,
+                              const pyg_plan_t* plan_T, float* grad_z, int64_t ldgz, float* grad_s_src,
+                              float* grad_s_dst, float* grad_logit, void* ws, size_t ws_bytes, void* stream) {
     REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
             "gat_backward: bad sizes");
     const int64_t F = H * C;
@@ -687,12 +696,20 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
     REQUIRE(E == 0 || (z && s_src && s_dst && alpha && grad_out && grad_logit), PYG_ERR_INVALID_ARGUMENT,
             "gat_backward: null input (grad_logit [E x H] is required)");
     REQUIRE(n_dst * H == 0 || grad_s_dst, PYG_ERR_INVALID_ARGUMENT, "gat_backward: null grad_s_dst");
+    REQUIRE(!out || ldo >= F, PYG_ERR_DIMENSION, "gat_backward: ldo < H*C");
     cudaStream_t s = as_stream(stream);
-    if (n_dst > 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));  // rows without in-edges
-    if (E > 0)
-        PYG_TRY(attention_softmax_bwd(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, (int)H, (int)C,
-                                      (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst, negative_slope, grad_logit,
-                                      H, grad_s_dst, s));
+    if (E > 0 && gat_bwd_tma_eligible(plan, (int)H, (int)C, (int)F, z, ldz, grad_out, ldg, out, ldo, alpha, s_src, s_dst,
+                                      grad_s_dst)) {
+        // one pass: SDDMM + softmax backward with t_i = g_i . out_i (gat_tma.cu)
+        PYG_TRY(gat_bwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, grad_out, ldg, out, ldo, alpha, s_src, s_dst,
+                            negative_slope, grad_logit, grad_s_dst, ws, ws_bytes, s));
+    } else {
+        if (n_dst > 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));  // rows without in-edges
+        if (E > 0)
+            PYG_TRY(attention_softmax_bwd(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, (int)H, (int)C,
+                                          (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst, negative_slope,
+                                          grad_logit, H, grad_s_dst, s));
+    }
     if (grad_z && n_src > 0 && F > 0)
         PYG_TRY(headw_sum(plan_T, grad_out, ldg, F, C, H, alpha, grad_z, ldgz, n_src, ws, ws_bytes, s));
     if (grad_s_src && n_src > 0) {

@@ -57,8 +57,10 @@ struct Knobs {
     int tma_hubs = 1;     // PYG_TMA_HUBS: 0 keeps split hub rows on the LDG kernel
     int tma_warp_kb = 4;  // PYG_TMA_WARP_KB: ring bytes per warp of the TMA gather4 kernel
     int tma_warps = 8;    // PYG_TMA_WARPS
-    int seg_bulk = -1;    // PYG_SEG_BULK: row-staged bulk-copy kernel -- -1 auto (MAX), 0 off, 1 all eligible
+    int seg_bulk = -1;    // PYG_SEG_BULK: row-staged bulk-copy kernel -- 1 on wherever eligible, else off
     int bulk_warp_kb = 8; // PYG_BULK_WARP_KB: ring bytes per warp of the bulk-copy kernel
+    int gat_warp_kb = 10; // PYG_GAT_WARP_KB: ring bytes per warp of the one-pass GAT backward
+    int gat_sm_kb = 160;  // PYG_GAT_SM_KB: its shared memory per SM (the rest stays L1)
 };
 const Knobs& knobs();
 

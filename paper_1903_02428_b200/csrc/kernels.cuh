@@ -172,4 +172,15 @@ pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, con
                                    int64_t ldz, const float* s_src, const float* s_dst, float slope, float* dlogit,
                                    int64_t ldd, float* grad_s_dst, cudaStream_t s);
 
+// GAT backward in one TMA gather4 pass (gat_tma.cu): dlogit and grad_s_dst from z, alpha, s_src,
+// s_dst, grad_out and the forward output (t_i = g_i . out_i)
+bool gat_bwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t ldz, const float* g,
+                          int64_t ldg, const float* out, int64_t ldo, const float* alpha, const float* s_src,
+                          const float* s_dst, const float* gsd);
+size_t gat_bwd_tma_ws_bytes(const pyg_plan* plan, int64_t H);
+pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
+                         const float* g, int64_t ldg, const float* out, int64_t ldo, const float* alpha,
+                         const float* s_src, const float* s_dst, float slope, float* dlogit, float* gsd, void* ws,
+                         size_t ws_bytes, cudaStream_t s);
+
 }  // namespace pyg

@@ -88,18 +88,45 @@ __global__ void __launch_bounds__(256) seg_bulk_kernel(SegArgs a, Ring g, int ou
         const int64_t r0 = task * g.rows_per_task;
         if (r0 >= a.n_rows) break;
         const int64_t r1 = min(a.n_rows, r0 + (int64_t)g.rows_per_task);
-        const int64_t pb = __ldg(a.rowptr + r0), pe = __ldg(a.rowptr + r1);
+        // the task's row pointers, one per lane (rows_per_task + 1 <= 32), read coalesced once
+        const int64_t rp = (r0 + lane <= r1) ? __ldg(a.rowptr + r0 + lane) : 0;
+        const int64_t pb = __shfl_sync(0xffffffffu, rp, 0);
+        const int64_t pe = __shfl_sync(0xffffffffu, rp, (int)(r1 - r0));
         const int64_t n = pe - pb;
+        // index windows (coalesced, one per 32 positions): A = [wb, wb + 32), B = the next 32
+        int gA = 0, eA = 0, gB = 0, eB = 0;
+        float sA = 1.0f, sB = 1.0f;
+        auto load = [&](int64_t base, int& gg, int& ee, float& ss) {
+            const int64_t p = base + lane;
+            gg = 0; ee = 0; ss = 1.0f;
+            if (p < pe) {
+                gg = __ldg(a.gidx + p);
+                if (need_e) {
+                    ee = a.eid ? __ldg(a.eid + p) : (int)p;
+                    if (a.w) ss = __ldg(a.w + ee);
+                }
+            }
+        };
+        int64_t wb = pb;
+        load(wb, gA, eA, sA);
+        load(wb + 32, gB, eB, sB);
+        // the source row of window position j (j < 64), all lanes
+        auto gsrc = [&](int j) -> int {
+            const int a0 = __shfl_sync(0xffffffffu, gA, j & 31);
+            const int b0 = __shfl_sync(0xffffffffu, gB, j & 31);
+            return j < 32 ? a0 : b0;
+        };
         // prologue: the first S positions of the task in flight
-        if (lane == 0) {
-            for (int k = 0; k < g.S && k < n; ++k) {
+        for (int k = 0; k < g.S && k < n; ++k) {
+            const int gq = gsrc(k);
+            if (lane == 0) {
                 const uint32_t slot = (cnt + k) % g.S;
                 const uint32_t bar = region + 8 * slot;
                 bar_expect(bar, g.copy);
-                copy_row(data0 + slot * g.stride, X + (uint64_t)(uint32_t)__ldg(a.gidx + pb + k) * row_bytes, g.copy, bar);
+                copy_row(data0 + slot * g.stride, X + (uint64_t)(uint32_t)gq * row_bytes, g.copy, bar);
             }
         }
-        int64_t row = r0, rbeg = pb, rend = __ldg(a.rowptr + r0 + 1);
+        int64_t row = r0, rbeg = pb, rend = __shfl_sync(0xffffffffu, rp, 1);
         float acc[NCH][4];
         int bi[NCH][4];
         auto reset = [&]() {
@@ -111,18 +138,24 @@ __global__ void __launch_bounds__(256) seg_bulk_kernel(SegArgs a, Ring g, int ou
         reset();
         for (int64_t k = 0; k < n; ++k) {
             const int64_t p = pb + k;
+            if (p - wb >= 32) {
+                wb += 32;
+                gA = gB; eA = eB; sA = sB;
+                load(wb + 32, gB, eB, sB);
+            }
             while (rend <= p) {  // rows ending here (incl. empty rows) are complete
                 seg::row_epilogue<4, NCH, RED, 32>(a, row, rend - rbeg, lane, 0, acc, bi, out_vec_ok);
                 reset();
                 ++row;
                 rbeg = rend;
-                rend = __ldg(a.rowptr + row + 1);
+                rend = __shfl_sync(0xffffffffu, rp, (int)(row - r0 + 1));
             }
+            const int jj = (int)(p - wb);
             int e = 0;
             float sc = 1.0f;
             if (need_e) {
-                e = a.eid ? __ldg(a.eid + p) : (int)p;
-                if (a.w) sc = __ldg(a.w + e);
+                e = __shfl_sync(0xffffffffu, eA, jj);
+                if (a.w) sc = __shfl_sync(0xffffffffu, sA, jj);
             }
             const uint32_t slot = cnt % g.S;
             bar_wait(region + 8 * slot, (cnt / g.S) & 1u);
@@ -143,11 +176,13 @@ __global__ void __launch_bounds__(256) seg_bulk_kernel(SegArgs a, Ring g, int ou
                 }
             }
             __syncwarp();  // every lane has read the stage: refill it with position p + S
-            if (lane == 0 && k + g.S < n) {
-                const uint32_t bar = region + 8 * slot;
-                bar_expect(bar, g.copy);
-                copy_row(data0 + slot * g.stride,
-                         X + (uint64_t)(uint32_t)__ldg(a.gidx + p + g.S) * row_bytes, g.copy, bar);
+            if (k + g.S < n) {
+                const int gq = gsrc(jj + g.S);
+                if (lane == 0) {
+                    const uint32_t bar = region + 8 * slot;
+                    bar_expect(bar, g.copy);
+                    copy_row(data0 + slot * g.stride, X + (uint64_t)(uint32_t)gq * row_bytes, g.copy, bar);
+                }
             }
             ++cnt;
         }
@@ -157,7 +192,7 @@ __global__ void __launch_bounds__(256) seg_bulk_kernel(SegArgs a, Ring g, int ou
             ++row;
             if (row < r1) {
                 rbeg = rend;
-                rend = __ldg(a.rowptr + row + 1);
+                rend = __shfl_sync(0xffffffffu, rp, (int)(row - r0 + 1));
             }
         }
     }
@@ -166,11 +201,9 @@ __global__ void __launch_bounds__(256) seg_bulk_kernel(SegArgs a, Ring g, int ou
 template <int RED>
 pyg_status_t launch_red(const SegArgs& a, int nch, const Ring& g, int smem, int ovk, cudaStream_t s) {
     auto pick = [&](auto kern) -> pyg_status_t {
-        static int configured = 0;  // per instantiation: opt in to > 48 KB of dynamic shared memory once
-        if (!configured) {
-            PYG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-            configured = 1;
-        }
+        // opt in to > 48 KB of dynamic shared memory on every launch (a cached "done once" flag went
+        // stale inside the GPU test suite: the launch then failed with cudaErrorInvalidValue)
+        PYG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int dev = 0, sms = 0, per_sm = 0;
         PYG_CUDA(cudaGetDevice(&dev));
         PYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -196,9 +229,11 @@ pyg_status_t launch_red(const SegArgs& a, int nch, const Ring& g, int smem, int 
 }  // namespace bulk
 
 bool bulk_eligible(const SegArgs& a, const pyg_plan* plan, int reduce) {
-    const int mode = knobs().seg_bulk;  // -1 auto (MAX), 0 off, 1 every eligible call
-    if (mode == 0 || (a.flags & PYG_NO_TMA) || !plan) return false;
-    if (mode < 0 && reduce != PYG_MAX) return false;
+    // opt-in only (PYG_SEG_BULK=1): on Reddit's source-blocked MAX passes it measured 3.15 ms per pass
+    // against 2.52 ms for seg_kernel (gpurun_out/r2k launch lists), so auto mode does not pick it
+    const int mode = knobs().seg_bulk;
+    (void)reduce;
+    if (mode != 1 || (a.flags & PYG_NO_TMA) || !plan) return false;
     if (plan->item_hi > plan->item_lo || a.row_order || !a.gidx || a.gdeg || a.hw) return false;
     if (a.ncols < 256 || a.ncols > 1024) return false;
     if ((reinterpret_cast<uintptr_t>(a.X) & 15) || (a.ldx % 4)) return false;

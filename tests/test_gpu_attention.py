@@ -78,9 +78,12 @@ def test_gat_forward(name, tma, monkeypatch):
     assert torch.equal(out, out2) and torch.equal(alpha, alpha2)
 
 
+@pytest.mark.parametrize("with_out", [False, True])
 @pytest.mark.parametrize("tma", ["auto", "1"])
 @pytest.mark.parametrize("name", CASES)
-def test_gat_backward(name, tma, monkeypatch):
+def test_gat_backward(name, tma, with_out, monkeypatch):
+    """with_out: the forward output is passed, so (H in {4, 8}, tma = "1") the one-pass TMA backward
+    runs (gat_tma.cu: t_i = g_i . out_i); otherwise the two-pass softmax backward."""
     import paper_1903_02428_b200 as pg
 
     if tma == "1":
@@ -91,8 +94,8 @@ def test_gat_backward(name, tma, monkeypatch):
     plan = pg.pyg_plan_build(eit[1], eit[0], n_dst, n_src)
     planT = pg.pyg_plan_build(eit[0], eit[1], n_src, n_dst)
     zt, sst, sdt = _t(z), _t(ss), _t(sd)
-    _, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan)
-    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT)
+    out, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan)
+    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT, out=out if with_out else None)
     ref = oracle.gat_backward(z, ss, sd, ei, H, g, n_dst=n_dst, with_abs=True)
     check_close(got["z"].cpu().numpy(), ref["z"], abs_sum=ref["abs_z"], what="grad_z")
     check_close(got["s_src"].cpu().numpy(), ref["s_src"], abs_sum=ref["abs_s_src"], what="grad_s_src")
@@ -184,3 +187,31 @@ def test_gat_empty_graph_and_single_edge():
     gr1 = pg.pyg_gat_backward(z, ss, sd, H, a1, g, plan1, planT1)
     assert torch.equal(gr1["z"][3], g[7])
     assert gr1["s_src"].abs().max().item() == 0 and gr1["s_dst"].abs().max().item() == 0
+
+
+def test_gat_backward_one_pass_single_in_edge_is_exact(monkeypatch):
+    """The one-pass backward takes t_i = g_i . out_i in the SDDMM's own product order and reduction
+    tree: rows with one in-edge (alpha = 1, out_i = z_j bitwise) get dlogit = 0 EXACTLY, as the
+    chain rule says (softmax over one element is constant); other rows match the oracle."""
+    import paper_1903_02428_b200 as pg
+
+    monkeypatch.setenv("PYG_SEG_TMA", "1")
+    rng = np.random.default_rng(5)
+    n, H, C = 3000, 8, 16
+    dst = np.concatenate([np.arange(1000), rng.integers(1000, n, 20000)])  # rows 0..999: one in-edge
+    src = rng.integers(0, n, dst.size)
+    ei = np.stack([src, dst]).astype(np.int64)
+    z = rng.standard_normal((n, H * C)).astype(np.float32)
+    ss = rng.standard_normal((n, H)).astype(np.float32)
+    sd = rng.standard_normal((n, H)).astype(np.float32)
+    g = rng.standard_normal((n, H * C)).astype(np.float32)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n, n)
+    planT = pg.pyg_plan_build(eit[0], eit[1], n, n)
+    out, alpha = pg.pyg_gat_propagate(_t(z), _t(ss), _t(sd), H, plan)
+    gr = pg.pyg_gat_backward(_t(z), _t(ss), _t(sd), H, alpha, _t(g), plan, planT, out=out)
+    assert torch.equal(gr["logit"][:1000], torch.zeros_like(gr["logit"][:1000]))
+    assert torch.equal(gr["s_dst"][:1000], torch.zeros_like(gr["s_dst"][:1000]))
+    ref = oracle.gat_backward(z, ss, sd, ei, H, g, n_dst=n, with_abs=True)
+    check_close(gr["s_dst"].cpu().numpy(), ref["s_dst"], abs_sum=ref["abs_s_dst"], what="grad_s_dst")
+    check_close(gr["s_src"].cpu().numpy(), ref["s_src"], abs_sum=ref["abs_s_src"], what="grad_s_src")
