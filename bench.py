@@ -769,10 +769,11 @@ def main():
         gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
         gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C), 1), dtype=torch.uint8,
                           device=dev)
+        gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 2, "gat"
 
         def compute():
-            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"])
+            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"], workspace=gfw)
             gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT, out=o, workspace=gws)
 
     gatl = None
@@ -795,11 +796,12 @@ def main():
         go = torch.empty((N, H * C), device=dev)
         gal = torch.empty((E, H), device=dev)
         gatl = dict(H=H, C=C, out=go)
+        glw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 1, "gatlayer"
 
         def compute():
             z, ss, sd = pg.pyg_gat_transform(x_full, Wg[:, :F], a_s, a_d, H)
-            pg.pyg_gat_propagate(z, ss, sd, H, plan, out=go, alpha=gal)
+            pg.pyg_gat_propagate(z, ss, sd, H, plan, out=go, alpha=gal, workspace=glw)
 
     appnp = None
     if a.op == "appnp":

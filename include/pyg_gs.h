@@ -356,6 +356,8 @@ pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const f
                                           int64_t ldg, int64_t E, int64_t H, int64_t dim_size,
                                           const pyg_plan_t* plan, float* grad_src, int64_t lds,
                                           void* stream);
+/* Scratch of pyg_gat_propagate.  Host-only. */
+pyg_status_t pyg_gat_propagate_workspace_size(const pyg_plan_t* plan, int64_t H, int64_t C, size_t* bytes);
 /* GAT aggregation with H heads of C channels: for edge k = (j -> i),
  *   alpha[k][h] = softmax over the in-edges of i of
  *                 leaky_relu(s_src[j][h] + s_dst[i][h], negative_slope),
@@ -365,8 +367,12 @@ pyg_status_t pyg_segment_softmax_backward(const float* out, int64_t ldo, const f
  * projections a_src . z_j and a_dst . z_i per head, computed by the caller);
  * out [n_dst x H*C] stride ldo; alpha [E x H] packed, OUTPUT (by original edge
  * id; needed by the backward).  plan: unblocked forward plan (row = target,
- * col = source).  H <= 8.  workspace: pyg_workspace_size(plan, n_dst, H*C,
- * PYG_SUM, 0) (split hub rows).  Asynchronous. */
+ * col = source).  H <= 8.  workspace: pyg_gat_propagate_workspace_size(plan, H, C).
+ * Large graphs (H in {4, 8}, 16-byte aligned rows) take ONE streaming pass: softmax is
+ * shift-invariant, and c_i[h] = leaky_relu(max_j s_src[j][h] + s_dst[i][h]) bounds every
+ * logit of row i (leaky_relu is monotone), so the weights exp(l - c_i) <= 1 are accumulated
+ * with z_j as they are gathered and divided by their row sum at the row's end; rows whose sum
+ * underflows (< 1e-30) are recomputed with their own max.  Asynchronous. */
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                                const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
                                float negative_slope, const pyg_plan_t* plan, float* out,

@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_gat_propagate_workspace_size", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version", "DistComm", "DistPlan", "pyg_dist_unique_id", "pyg_dist_init", "pyg_dist_plan_build",
     "pyg_dist_propagate", "pyg_dist_propagate_backward",
 ]
@@ -401,11 +401,17 @@ def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor,
         alpha = torch.empty((E, H), dtype=torch.float32, device=z.device)
     _, _, ldo = _rows(out, "out")
     if workspace is None:
-        workspace = _workspace(pyg_workspace_size(plan, n_dst, F, SUM), z.device)
+        workspace = _workspace(pyg_gat_propagate_workspace_size(plan, H, C), z.device)
     check(lib.pyg_gat_propagate(_ptr(z), n_src, H, C, ldz, _ptr(s_src), _ptr(s_dst), n_dst, E, negative_slope,
                                 plan.handle, _ptr(out), ldo, _ptr(alpha), _ptr(workspace), workspace.numel(),
                                 _stream(z.device)), "pyg_gat_propagate")
     return out, alpha
+
+
+def pyg_gat_propagate_workspace_size(plan: Plan, H: int, C: int) -> int:
+    nb = ctypes.c_size_t()
+    check(lib.pyg_gat_propagate_workspace_size(plan.handle, H, C, ctypes.byref(nb)), "pyg_gat_propagate_workspace_size")
+    return nb.value
 
 
 def pyg_gat_backward_workspace_size(plan: Plan, plan_T: Plan, H: int, C: int) -> int:

@@ -51,6 +51,9 @@ static Knobs read_knobs() {
     k.bulk_warp_kb = get("PYG_BULK_WARP_KB", 8);
     k.gat_warp_kb = get("PYG_GAT_WARP_KB", 10);
     k.gat_sm_kb = get("PYG_GAT_SM_KB", 160);
+    k.gat_fused = get("PYG_GAT_FUSED", 1);
+    k.gat_fwd_warp_kb = get("PYG_GAT_FWD_WARP_KB", 5);
+    k.gat_fwd_sm_kb = get("PYG_GAT_FWD_SM_KB", 160);
     return k;
 }
 static Knobs g_knobs = read_knobs();
@@ -648,6 +651,12 @@ static pyg_status_t headw_sum(const pyg_plan* p, const float* X, int64_t ldx, in
     return segment_reduce(a, kRedHeadW, p, ws, ws_bytes, s);
 }
 
+pyg_status_t pyg_gat_propagate_workspace_size(const pyg_plan_t* plan, int64_t H, int64_t C, size_t* bytes) {
+    REQUIRE(bytes && plan && H > 0 && C >= 0, PYG_ERR_INVALID_ARGUMENT, "gat_propagate_workspace_size: bad args");
+    *bytes = std::max(gat_fwd_tma_ws_bytes(plan, H, H * C), segment_ws_bytes(plan, H * C, PYG_SUM));
+    return PYG_OK;
+}
+
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
                                const float* s_dst, int64_t n_dst, int64_t E, float negative_slope,
                                const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, void* ws,
@@ -663,6 +672,10 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
     REQUIRE(n_dst * F == 0 || out, PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null out");
     REQUIRE(E == 0 || (z && s_src && s_dst && alpha), PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null input");
     cudaStream_t s = as_stream(stream);
+    if (E > 0 && n_dst > 0 && gat_fwd_tma_eligible(plan, (int)H, (int)C, (int)F, z, ldz, out, ldo, alpha, s_src, s_dst))
+        // softmax with a per-row shift bounded from the global max of s_src + the weighted sum, one pass
+        return gat_fwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, s_src, s_dst, negative_slope, out, ldo, alpha,
+                           ws, ws_bytes, s);
     if (E > 0)
         PYG_TRY(attention_softmax(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, nullptr, 0, s_src, s_dst,
                                   (int)H, negative_slope, alpha, H, s));

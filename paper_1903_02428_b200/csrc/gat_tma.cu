@@ -50,7 +50,21 @@ __device__ __forceinline__ void sts32f(uint32_t addr, float v) {
     asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
-constexpr int kMeta = 48;  // per stage: int keys[4] | int rows[4] | int eids[4]
+// predicated shared-memory loads: the destination keeps its value when p is false (no branch, so
+// the shuffles around them need no divergence handling)
+__device__ __forceinline__ void lds128f_if(bool p, float4& v, uint32_t addr) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n}\n"
+        : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+        : "r"(addr), "r"((unsigned)p));
+}
+__device__ __forceinline__ void lds32f_if(bool p, float& v, uint32_t addr) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q ld.shared.f32 %0, [%1];\n}\n"
+                 : "+f"(v)
+                 : "r"(addr), "r"((unsigned)p));
+}
+
+constexpr int kMeta = 64;  // per stage: int keys[4] | int rows[4] | int eids[4] | int cols[4]
 
 struct BwdArgs {
     const int64_t* rowptr;   // ROOT rowptr
@@ -62,9 +76,6 @@ struct BwdArgs {
     int64_t E_root;
     const int32_t* gidx;     // source j per position
     const int32_t* eid;      // edge id per position (null: identity)
-    const float* g;          // grad_out [n x F] stride ldg (rows 16-byte aligned)
-    int64_t ldg;
-    const float* s_dst;      // [n x H] packed
     float* gsd;              // grad_s_dst [n x H]: t_i on entry, the row sums on exit
     float* dlogit;           // [E x H] packed, by edge id
     float* part;             // hub chunk partials [items x H]
@@ -73,22 +84,55 @@ struct BwdArgs {
     int F, H, C, box_w, nb;
     float slope;
     int warp_bytes, data_off;
-    int zbytes, off_a, off_s, off_g, off_t, off_d, stage_bytes;
+    int zbytes, off_g, off_a, off_s, off_t, off_d, stage_bytes;
 };
 
-template <int NCH, int S>
-__global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant__ CUtensorMap tz,
-                                                          const __grid_constant__ CUtensorMap ta,
-                                                          const __grid_constant__ CUtensorMap ts, BwdArgs a) {
+// The chunk visiting order of head h (C = 4 CPH columns = CPH float4 chunks): j-th chunk visited is
+// (j + rot(h)) mod CPH.  rot spreads the 8 heads of a staged row over distinct 16-byte bank groups
+// (a row's heads are CPH * 16 bytes apart), so the 8 lanes reading one row are conflict-free.  The
+// SDDMM (gat_bwd_tma_kernel) and t_i (gat_t_row_head_kernel) both add the chunk dots sequentially in
+// this order, each chunk as x0 y0 then fma of y, z, w: t_i of a row whose output equals one source
+// row bitwise equals that edge's d_alpha bitwise.
+template <int CPH>
+__device__ __forceinline__ int head_rot(int h) { return CPH >= 8 ? h % CPH : h / (8 / CPH); }
+
+template <int CPH>
+__device__ __forceinline__ float head_dot(uint32_t zb, uint32_t gb, int rot) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < CPH; ++j) {
+        const uint32_t off = 16u * (uint32_t)((j + rot) % CPH);
+        const float4 x = lds128f(gb + off);
+        const float4 y = lds128f(zb + off);
+        float q = x.x * y.x;
+        q = fmaf(x.y, y.y, q);
+        q = fmaf(x.z, y.z, q);
+        q = fmaf(x.w, y.w, q);
+        acc = j == 0 ? q : acc + q;
+    }
+    return acc;
+}
+
+// One pass per stage of 4 positions: lane (i, h) = (lane / 8, lane % 8) owns slot i, head h.  Lane 0
+// gathers (TMA gather4, all completing on the stage's mbarrier): the 4 z_j rows and the 4 g_i rows
+// (by target), and the 4 rows of alpha (by edge id), s_src (by source), t and s_dst (by target).
+// Each lane then needs no shuffles for its d_alpha and dlogit; the per-row head sums are a 4-step
+// segmented scan over the slots.
+template <int CPH, int NB, int S>
+__global__ void __launch_bounds__(256, 2) gat_bwd_tma_kernel(const __grid_constant__ CUtensorMap tz,
+                                                             const __grid_constant__ CUtensorMap tg,
+                                                             const __grid_constant__ CUtensorMap ta,
+                                                             const __grid_constant__ CUtensorMap ts,
+                                                             const __grid_constant__ CUtensorMap tt,
+                                                             const __grid_constant__ CUtensorMap td, BwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const uint32_t region = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)(warp * a.warp_bytes);
-    const uint32_t bar0 = region;                     // S barriers
-    const uint32_t meta0 = region + 128;              // S x kMeta
-    const uint32_t scr = meta0 + (uint32_t)(S * kMeta);  // 4 slots x 8 heads of d_alpha (128 B)
+    const uint32_t bar0 = region;
+    const uint32_t meta0 = region + 128;
     const uint32_t data0 = region + (uint32_t)a.data_off;
-    const int H = a.H, F = a.F;
+    const int H = a.H;
     const uint32_t stage_bytes = (uint32_t)a.stage_bytes;
     const uint32_t row_bytes = (uint32_t)(4 * a.box_w);
 
@@ -99,7 +143,313 @@ __global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant_
     }
     __syncwarp();
 
-    // lane chunk layout: float4 chunk (lane + 32 ch) = columns 4 (lane + 32 ch) .. + 3
+    const int my_i = lane >> 3, my_h = lane & 7;
+    const bool hv = my_h < H;
+    // this lane's head inside a staged row: column my_h * C lives in box (my_h * C) / box_w
+    const int hc0 = hv ? my_h * a.C : 0;
+    const uint32_t hoff = (uint32_t)(4 * ((hc0 / a.box_w) * 4 * a.box_w + hc0 % a.box_w)) + (uint32_t)my_i * row_bytes;
+    const int rot = head_rot<CPH>(my_h);
+    const int64_t plo = __ldg(a.rowptr + a.row_lo), phi = __ldg(a.rowptr + a.row_hi);
+
+    // ---------------- producer (warp-uniform) ----------------
+    int64_t pp = 0, pe = 0, iwb = 0, nwb = -1, task = 0;
+    bool done = false;
+    int wg = 0, wr = 0, we = 0, ng = 0, nr = 0, ne = 0;
+    int citem = -1;
+    auto load_window = [&](int64_t base, int& gg, int& rr, int& ee) {
+        const int64_t p = base + lane;
+        gg = 0; rr = -1; ee = 0;
+        if (p < a.E_root) {
+            gg = __ldg(a.gidx + p);
+            rr = __ldg(a.pos_row + p);
+            ee = a.eid ? __ldg(a.eid + p) : (int)p;
+        }
+    };
+    auto set_window = [&](int64_t base) {
+        if (base == nwb) {
+            wg = ng; wr = nr; we = ne;
+        } else {
+            load_window(base, wg, wr, we);
+        }
+        iwb = base;
+        nwb = base + 32;
+        load_window(nwb, ng, nr, ne);
+    };
+    auto next_task = [&]() -> bool {
+        for (;;) {
+            unsigned long long t = 0;
+            if (lane == 0) t = atomicAdd(a.next, 1ull);
+            task = (int64_t)__shfl_sync(0xffffffffu, t, 0);
+            if (task >= a.n_tasks) return false;
+            const int64_t t0 = max(__ldg(a.task_pos + 2 * task), plo);
+            const int64_t t1 = min(__ldg(a.task_pos + 2 * task + 1), phi);
+            const int it = a.task_item ? __ldg(a.task_item + task) : -1;
+            if (t0 < t1) {
+                pp = t0;
+                pe = t1;
+                citem = it;
+                return true;
+            }
+        }
+    };
+    if (next_task()) set_window(pp); else done = true;
+
+    auto fill = [&](int s) {
+        const uint32_t m = meta0 + (uint32_t)(s * kMeta) + 4u * (uint32_t)lane;
+        if (done) {
+            if (lane < 4) sts32(m, -1);
+            return;
+        }
+        if (pp - iwb >= 32) set_window(pp);
+        const int j = (int)(pp - iwb);
+        const int cnt = (int)min((int64_t)4, pe - pp);
+        const int src = j + (lane & 3);
+        const int gj = __shfl_sync(0xffffffffu, wg, src);
+        const int row = __shfl_sync(0xffffffffu, wr, src);
+        const int e = __shfl_sync(0xffffffffu, we, src);
+        if (lane < 4) {
+            sts32(m, lane < cnt ? (citem >= 0 ? -(citem + 2) : row) : -1);
+            sts32(m + 16, row);
+            sts32(m + 32, e);
+            sts32(m + 48, gj);
+        }
+        __syncwarp();
+        if (lane == 0) {  // the stage's slots back from shared memory (missing slots repeat slot 0)
+            const uint32_t ms = meta0 + (uint32_t)(s * kMeta);
+            const int4 r4 = lds128(ms + 16), e4 = lds128(ms + 32), g4 = lds128(ms + 48);
+            const int lo = (int)a.row_lo;
+            const int r0 = r4.x - lo, r1 = (cnt > 1 ? r4.y : r4.x) - lo, r2 = (cnt > 2 ? r4.z : r4.x) - lo,
+                      r3 = (cnt > 3 ? r4.w : r4.x) - lo;
+            const int gs1 = cnt > 1 ? g4.y : g4.x, gs2 = cnt > 2 ? g4.z : g4.x, gs3 = cnt > 3 ? g4.w : g4.x;
+            const int es1 = cnt > 1 ? e4.y : e4.x, es2 = cnt > 2 ? e4.z : e4.x, es3 = cnt > 3 ? e4.w : e4.x;
+            const uint32_t bar = bar0 + 8 * s;
+            const uint32_t st = data0 + (uint32_t)s * stage_bytes;
+            bar_expect(bar, 2u * (uint32_t)a.zbytes + 64u * (uint32_t)H);
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                gather4(st + (uint32_t)b * 4u * row_bytes, &tz, b * a.box_w, g4.x, gs1, gs2, gs3, bar);
+                gather4(st + (uint32_t)a.off_g + (uint32_t)b * 4u * row_bytes, &tg, b * a.box_w, r0, r1, r2, r3, bar);
+            }
+            gather4(st + (uint32_t)a.off_a, &ta, 0, e4.x, es1, es2, es3, bar);
+            gather4(st + (uint32_t)a.off_s, &ts, 0, g4.x, gs1, gs2, gs3, bar);
+            gather4(st + (uint32_t)a.off_t, &tt, 0, r0, r1, r2, r3, bar);
+            gather4(st + (uint32_t)a.off_d, &td, 0, r0, r1, r2, r3, bar);
+        }
+        pp += cnt;
+        if (pp >= pe) {
+            if (next_task()) {
+                if (pp != iwb + 32 && (pp < iwb || pp - iwb >= 32 || ((pp - iwb) & 3))) set_window(pp);
+            } else {
+                done = true;
+            }
+        }
+    };
+
+    // ---------------- consumer ----------------
+    int gkey = -1, grow = 0;  // key / root row of the head sums being accumulated
+    float gs = 0.0f;          // lanes < H: running head sum of dlogit
+
+#pragma unroll 1
+    for (int s = 0; s < S; ++s) fill(s);
+    __syncwarp();
+    uint32_t phase = 0;
+#pragma unroll 1
+    for (int s = 0;; s = (s + 1 == S) ? 0 : s + 1) {
+        const uint32_t m = meta0 + (uint32_t)(s * kMeta);
+        const int4 keys = lds128(m);
+        const int c = (keys.x != -1) + (keys.y != -1) + (keys.z != -1) + (keys.w != -1);
+        if (c == 0) break;
+        const int4 rows = lds128(m + 16);
+        const int4 eids = lds128(m + 32);
+        bar_wait(bar0 + 8 * s, (phase >> s) & 1u);
+        phase ^= 1u << s;
+        const uint32_t st = data0 + (uint32_t)s * stage_bytes;
+        // (slot my_i, head my_h): d_alpha, then dlogit
+        const bool mine = my_i < c && hv;
+        float dl = 0.0f;
+        if (mine) {
+            const float d = head_dot<CPH>(st + hoff, st + (uint32_t)a.off_g + hoff, rot);
+            const uint32_t q = 4u * (uint32_t)(my_i * H + my_h);
+            const float al = lds32f(st + (uint32_t)a.off_a + q);
+            const float ss = lds32f(st + (uint32_t)a.off_s + q);
+            const float t = lds32f(st + (uint32_t)a.off_t + q);
+            const float sd = lds32f(st + (uint32_t)a.off_d + q);
+            dl = al * (d - t);
+            if (!(ss + sd > 0.0f)) dl *= a.slope;
+            const int e = my_i == 0 ? eids.x : my_i == 1 ? eids.y : my_i == 2 ? eids.z : eids.w;
+            a.dlogit[(int64_t)e * H + my_h] = dl;
+        }
+        // head sums per row, in position order (lanes < H hold head `lane`)
+        const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
+        const int rr[4] = {rows.x, rows.y, rows.z, rows.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float v = __shfl_sync(0xffffffffu, dl, i * 8 + my_h);
+            const bool vi = i < c;
+            const bool nk = vi && kk[i] != gkey;
+            float* dst = gkey < -1 ? a.part + ((int64_t)(-gkey - 2) - a.item_lo) * H
+                                   : a.gsd + ((int64_t)grow - a.row_lo) * H;
+            if (nk && gkey != -1 && lane < H) dst[lane] = gs;
+            gkey = nk ? kk[i] : gkey;
+            grow = nk ? rr[i] : grow;
+            gs = nk ? 0.0f : gs;
+            gs = vi ? gs + v : gs;
+        }
+        __syncwarp();  // every lane is done with stage s before it is refilled
+        fill(s);
+    }
+    if (gkey != -1 && lane < H) {
+        if (gkey < -1) a.part[((int64_t)(-gkey - 2) - a.item_lo) * H + lane] = gs;
+        else a.gsd[((int64_t)grow - a.row_lo) * H + lane] = gs;
+    }
+}
+
+// t_i[h] = g_i . out_i |_h (0 for rows without in-edges), written into grad_s_dst (the backward
+// kernel reads it per slot, then overwrites the row with its head sums).  A thread per (row, head),
+// the chunks in head_dot's order (rotation, product order, sequential sum), so a row whose forward
+// output equals one source row bitwise (one in-edge, alpha = 1) gets t_i equal to that edge's
+// d_alpha bitwise; every thread keeps 2 CPH vector loads in flight.
+template <int CPH>
+__global__ void gat_t_row_head_kernel(const float* __restrict__ g, int64_t ldg, const float* __restrict__ out,
+                                      int64_t ldo, const int64_t* __restrict__ rowptr, int64_t n, int H, float* gsd) {
+    const int64_t total = n * H;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t r = t / H;
+        const int h = (int)(t - r * H);
+        float v = 0.0f;
+        if (__ldg(rowptr + r + 1) > __ldg(rowptr + r)) {
+            const float4* gr = reinterpret_cast<const float4*>(g + r * ldg) + h * CPH;
+            const float4* orr = reinterpret_cast<const float4*>(out + r * ldo) + h * CPH;
+            const int rot = head_rot<CPH>(h);
+#pragma unroll
+            for (int j = 0; j < CPH; ++j) {
+                const int k = (j + rot) % CPH;
+                const float4 x = __ldg(gr + k), y = __ldg(orr + k);
+                float q = x.x * y.x;
+                q = fmaf(x.y, y.y, q);
+                q = fmaf(x.z, y.z, q);
+                q = fmaf(x.w, y.w, q);
+                v = j == 0 ? q : v + q;
+            }
+        }
+        gsd[t] = v;
+    }
+}
+
+// grad_s_dst of a split hub row = its chunk partials added in fp64 in chunk order
+__global__ void gat_combine_kernel(const int32_t* heavy_rows, const int64_t* item_ptr, int64_t h_lo, int64_t h_hi,
+                                   int64_t item_lo, int64_t row_offset, const float* part, int H, float* gsd) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t hr = h_lo + t / H;
+    const int h = (int)(t % H);
+    if (hr >= h_hi) return;
+    double s = 0.0;
+    for (int64_t it = item_ptr[hr]; it < item_ptr[hr + 1]; ++it) s += (double)part[(it - item_lo) * H + h];
+    gsd[((int64_t)heavy_rows[hr] - row_offset) * H + h] = (float)s;
+}
+
+template <int CPH, int NB>
+pyg_status_t launch(int S, int64_t want, int warps, int smem, cudaStream_t s, const CUtensorMap (&tm)[6],
+                    const BwdArgs& a) {
+    void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
+              const CUtensorMap, BwdArgs) = S >= 3 ? gat_bwd_tma_kernel<CPH, NB, 3> : gat_bwd_tma_kernel<CPH, NB, 2>;
+    PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int kSmemPerSm = std::min(227, std::max(32, knobs().gat_sm_kb)) * 1024;
+    int dev = 0, sms = 148, per_sm = 1;
+    PYG_CUDA(cudaGetDevice(&dev));
+    PYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int cap = std::max(1, kSmemPerSm / (smem + 1024));
+    const int carve = std::min(100, (int)cdiv((int64_t)cap * (smem + 1024) * 100, 228 * 1024));
+    PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+    PYG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * warps, smem));
+    per_sm = std::min(per_sm, cap);
+    const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1))));
+    k<<<grid, 32 * warps, smem, s>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], a);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+bool encode_rows(CUtensorMap* tm, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_w) {
+    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {(cuuint32_t)box_w, 1};
+    cuuint32_t es[2] = {1, 1};
+    return tma::encode_fn()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+
+// ============================================================================================
+// Forward: softmax + alpha-weighted aggregation in ONE streaming pass.
+//
+// Softmax is shift-invariant: alpha[k][h] = exp(l_k - c_i) / sum_{k' in seg(i)} exp(l_k' - c_i) for
+// ANY per-row shift c_i.  The usual c_i = max_k l_k needs a pass over the row before the first
+// weight.  Because leaky_relu is monotone, c_i[h] = leaky_relu(S_h + s_dst[i][h]) with S_h = max_j
+// s_src[j][h] (one tiny reduction over s_src) bounds every logit of row i from above (in fp32 too:
+// rounding is monotone), so every weight p = exp(l - c_i) lies in (0, 1] -- no overflow -- and the
+// row is aggregated as out_i = (sum p z_j) / (sum p) in the same pass that gathers z_j.  The
+// weights p are stored by edge id and divided by the row sum afterwards (gat_alpha_norm_kernel).
+// If a row's sum underflows (its logits all sit ~80 below the global bound -- far outside GAT's
+// range), the row is listed and recomputed exactly with its own max (gat_fwd_fix_kernel).
+// ============================================================================================
+
+struct FwdArgs {
+    const int64_t* rowptr;   // ROOT rowptr
+    const int32_t* pos_row;
+    const int64_t* task_pos;
+    const int32_t* task_item;
+    int64_t n_tasks;
+    unsigned long long* next;
+    int64_t E_root;
+    const int32_t* gidx;
+    const int32_t* eid;
+    const float* s_dst;      // [n x H]
+    const unsigned* smax;    // [H] ordered-int max of s_src per head
+    float* alpha;            // [E x H]: the weights p on exit (normalised later)
+    float* out;
+    int64_t ldo;
+    float* rs;               // [n x H] row sums of p
+    float* part;             // hub chunk partial sums of p z [items x ldp]
+    float* part_s;           // hub chunk partial sums of p [items x H]
+    int64_t ldp, item_lo;
+    int* bad;                // [0]: count, [1..]: local rows whose sum underflowed
+    int64_t row_lo, row_hi;
+    int F, H, C, box_w, nb;
+    float slope;
+    int warp_bytes, data_off;
+    int zbytes, off_s, off_d, stage_bytes;
+};
+
+constexpr float kTinySum = 1e-30f;  // a row sum below this is recomputed with the row's own max
+
+template <int NCH, int S>
+__global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_constant__ CUtensorMap tz,
+                                                             const __grid_constant__ CUtensorMap ts, FwdArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t region = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)(warp * a.warp_bytes);
+    const uint32_t bar0 = region;
+    const uint32_t meta0 = region + 128;
+    const uint32_t scr = meta0 + (uint32_t)(S * kMeta);  // 4 slots x 8 heads of p (128 B)
+    const uint32_t data0 = region + (uint32_t)a.data_off;
+    const int H = a.H, F = a.F;
+    const uint32_t stage_bytes = (uint32_t)a.stage_bytes;
+    const uint32_t row_bytes = (uint32_t)(4 * a.box_w);
+    const float slope = a.slope;
+
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) bar_init(bar0 + 8 * s);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
     uint32_t coff[NCH];
     int hch[NCH];
     bool cval[NCH];
@@ -111,17 +461,15 @@ __global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant_
         coff[ch] = cval[ch] ? (uint32_t)(4 * (b * 4 * a.box_w + cc)) : 0u;
         hch[ch] = cval[ch] ? c / a.C : 0;
     }
-    const int CL = a.C >= 128 ? 32 : a.C / 4;  // lanes sharing a head inside one chunk row
-    const bool leader = (lane % CL) == 0;
+    const float smax_h = lane < H ? ord2f(__ldg(a.smax + lane)) : 0.0f;
     const int64_t plo = __ldg(a.rowptr + a.row_lo), phi = __ldg(a.rowptr + a.row_hi);
 
-    // ---------------- producer state (warp-uniform) ----------------
+    // ---------------- producer (as gat_bwd_tma_kernel: z rows, s_src rows, s_dst of new rows) -----
     int64_t pp = 0, pe = 0, iwb = 0, nwb = -1, task = 0;
     bool done = false;
     int wg = 0, wr = 0, we = 0, ng = 0, nr = 0, ne = 0;
     int citem = -1;
-    int pkey = -1;  // key of the last position issued (row starts are detected against it)
-
+    int pkey = -1;
     auto load_window = [&](int64_t base, int& gg, int& rr, int& ee) {
         const int64_t p = base + lane;
         gg = 0; rr = -1; ee = 0;
@@ -182,32 +530,26 @@ __global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant_
             sts32(m, lane < cnt ? key : -1);
             sts32(m + 16, row);
             sts32(m + 32, e);
+            sts32(m + 48, gj);
         }
-        int gs4[4], es4[4], rs4[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int sl = cnt > i ? i : 0;
-            gs4[i] = __shfl_sync(0xffffffffu, gj, sl);
-            es4[i] = __shfl_sync(0xffffffffu, e, sl);
-            rs4[i] = __shfl_sync(0xffffffffu, row, sl);
-        }
+        __syncwarp();
         if (lane == 0) {
+            const uint32_t ms = meta0 + (uint32_t)(s * kMeta);
+            const int4 r4 = lds128(ms + 16), g4 = lds128(ms + 48);
+            const int gs1 = cnt > 1 ? g4.y : g4.x, gs2 = cnt > 2 ? g4.z : g4.x, gs3 = cnt > 3 ? g4.w : g4.x;
+            const int rs4[4] = {r4.x, r4.y, r4.z, r4.w};
             const uint32_t bar = bar0 + 8 * s;
             const uint32_t st = data0 + (uint32_t)s * stage_bytes;
             const uint32_t nnew = (uint32_t)__popc(newm);
-            bar_expect(bar, (uint32_t)a.zbytes + 32u * (uint32_t)H + nnew * (uint32_t)(4 * F + 8 * H));
+            bar_expect(bar, (uint32_t)a.zbytes + 16u * (uint32_t)H + nnew * (uint32_t)(4 * H));
 #pragma unroll
             for (int b = 0; b < 4; ++b)
-                if (b < a.nb)
-                    gather4(st + (uint32_t)b * 4u * row_bytes, &tz, b * a.box_w, gs4[0], gs4[1], gs4[2], gs4[3], bar);
-            gather4(st + (uint32_t)a.off_a, &ta, 0, es4[0], es4[1], es4[2], es4[3], bar);
-            gather4(st + (uint32_t)a.off_s, &ts, 0, gs4[0], gs4[1], gs4[2], gs4[3], bar);
+                if (b < a.nb) gather4(st + (uint32_t)b * 4u * row_bytes, &tz, b * a.box_w, g4.x, gs1, gs2, gs3, bar);
+            gather4(st + (uint32_t)a.off_s, &ts, 0, g4.x, gs1, gs2, gs3, bar);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 if (!((newm >> i) & 1u)) continue;
                 const int64_t lr = (int64_t)rs4[i] - a.row_lo;
-                bulk_copy(st + (uint32_t)a.off_g + (uint32_t)(i * 4 * F), a.g + lr * a.ldg, (uint32_t)(4 * F), bar);
-                bulk_copy(st + (uint32_t)a.off_t + (uint32_t)(i * 4 * H), a.gsd + lr * H, (uint32_t)(4 * H), bar);
                 bulk_copy(st + (uint32_t)a.off_d + (uint32_t)(i * 4 * H), a.s_dst + lr * H, (uint32_t)(4 * H), bar);
             }
         }
@@ -222,20 +564,44 @@ __global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant_
     };
 
     // ---------------- consumer ----------------
-    float4 gv[NCH];
-#pragma unroll
-    for (int ch = 0; ch < NCH; ++ch) gv[ch] = make_float4(0.f, 0.f, 0.f, 0.f);
-    float treg = 0.0f, sdreg = 0.0f;  // lanes < H: t_i[h], s_dst[i][h] of the current row
-    int crow = -1;                    // key of the row whose g_i is in gv
-    int gkey = -1, grow = 0;          // key / root row of the head sums being accumulated
-    float gs = 0.0f;                  // lanes < H: running head sum of dlogit
+    float sdreg = 0.0f;               // lanes < H: s_dst[i][h] of the capture row
+    int crow = -1;
+    int arow = -1, agrow = 0;         // key / root row being aggregated
+    float acc[NCH][4];
+    float ssum[NCH];                  // running sum of p of each chunk's head (replicated per lane)
     const int my_i = lane >> 3, my_h = lane & 7;
-
-    auto flush = [&]() {
-        if (lane < H) {
-            if (gkey < -1) a.part[((int64_t)(-gkey - 2) - a.item_lo) * H + lane] = gs;
-            else a.gsd[((int64_t)grow - a.row_lo) * H + lane] = gs;
+    const int CLh = a.C >= 128 ? 32 : a.C / 4;
+    const bool leader = (lane % CLh) == 0;  // writes its chunk's head sum
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        ssum[ch] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[ch][q] = 0.0f;
+    }
+    auto flush = [&]() {  // no warp-synchronous operations: called under a (uniform) branch
+        if (arow < -1) {  // hub chunk: raw partials for gat_fwd_combine_kernel
+            const int64_t it = (int64_t)(-arow - 2) - a.item_lo;
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (cval[ch]) {
+                    *reinterpret_cast<float4*>(a.part + it * a.ldp + 4 * (lane + 32 * ch)) =
+                        make_float4(acc[ch][0], acc[ch][1], acc[ch][2], acc[ch][3]);
+                    if (leader) a.part_s[it * H + hch[ch]] = ssum[ch];
+                }
+            return;
         }
+        const int64_t r = (int64_t)agrow - a.row_lo;
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+            if (cval[ch]) {
+                const float sh = ssum[ch];
+                *reinterpret_cast<float4*>(a.out + r * a.ldo + 4 * (lane + 32 * ch)) =
+                    make_float4(acc[ch][0] / sh, acc[ch][1] / sh, acc[ch][2] / sh, acc[ch][3] / sh);
+                if (leader) {
+                    a.rs[r * H + hch[ch]] = sh;
+                    if (!(sh >= kTinySum)) a.bad[1 + atomicAdd(a.bad, 1)] = (int)r;  // rare; may repeat a row
+                }
+            }
     };
 
 #pragma unroll 1
@@ -250,158 +616,185 @@ __global__ void __launch_bounds__(256) gat_bwd_tma_kernel(const __grid_constant_
         if (c == 0) break;
         const int4 rows = lds128(m + 16);
         const int4 eids = lds128(m + 32);
-        sts32f(scr + 4u * (uint32_t)lane, 0.0f);
         bar_wait(bar0 + 8 * s, (phase >> s) & 1u);
         phase ^= 1u << s;
-        __syncwarp();
         const uint32_t st = data0 + (uint32_t)s * stage_bytes;
         const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
-        float tme = 0.0f, sme = 0.0f;
+        const int rr[4] = {rows.x, rows.y, rows.z, rows.w};
+        // (1) s_dst of each slot's row for the (slot, head) lanes (branch-free)
+        float sme = 0.0f;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            if (i >= c) break;
-            if (kk[i] != crow) {  // a row starts at slot i: its g_i / t_i / s_dst[i] are in this stage
-                crow = kk[i];
-                const uint32_t gb = st + (uint32_t)a.off_g + (uint32_t)(i * 4 * F) + 16u * (uint32_t)lane;
+            const bool nr = i < c && kk[i] != crow;
+            crow = nr ? kk[i] : crow;
+            lds32f_if(nr && lane < H, sdreg, st + (uint32_t)a.off_d + (uint32_t)(i * 4 * H) + 4u * (uint32_t)lane);
+            const float tv = __shfl_sync(0xffffffffu, sdreg, my_h);
+            sme = my_i == i ? tv : sme;
+        }
+        const float smx = __shfl_sync(0xffffffffu, smax_h, my_h);
+        // (2) the weight of (slot my_i, head my_h): one exp per lane per stage
+        const bool mine = my_i < c && my_h < H;
+        float ss = 0.0f;
+        lds32f_if(mine, ss, st + (uint32_t)a.off_s + 4u * (uint32_t)(my_i * H + my_h));
+        const float pre = ss + sme, cpre = smx + sme;
+        const float l = pre > 0.0f ? pre : slope * pre;
+        const float cs = cpre > 0.0f ? cpre : slope * cpre;  // the row's shift c_i (>= every logit)
+        const float p = mine ? expf(l - cs) : 0.0f;
+        const int e = my_i == 0 ? eids.x : my_i == 1 ? eids.y : my_i == 2 ? eids.z : eids.w;
+        if (mine) a.alpha[(int64_t)e * H + my_h] = p;
+        sts32f(scr + 4u * (uint32_t)lane, p);
+        __syncwarp();
+        // (3) aggregation in position order
 #pragma unroll
-                for (int ch = 0; ch < NCH; ++ch)
-                    gv[ch] = cval[ch] ? lds128f(gb + 512u * (uint32_t)ch) : make_float4(0.f, 0.f, 0.f, 0.f);
-                if (lane < H) {
-                    treg = lds32f(st + (uint32_t)a.off_t + (uint32_t)(i * 4 * H) + 4u * (uint32_t)lane);
-                    sdreg = lds32f(st + (uint32_t)a.off_d + (uint32_t)(i * 4 * H) + 4u * (uint32_t)lane);
+        for (int i = 0; i < 4; ++i) {
+            const bool vi = i < c;
+            if (vi && kk[i] != arow) {
+                if (arow != -1) flush();
+                arow = kk[i];
+                agrow = rr[i];
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) {
+                    ssum[ch] = 0.0f;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[ch][q] = 0.0f;
                 }
             }
-            const float tv = __shfl_sync(0xffffffffu, treg, my_h);
-            const float sv = __shfl_sync(0xffffffffu, sdreg, my_h);
-            if (my_i == i) { tme = tv; sme = sv; }
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
-                const float4 zv = cval[ch] ? lds128f(st + coff[ch] + (uint32_t)i * row_bytes)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-                float d = gv[ch].x * zv.x;
-                d = fmaf(gv[ch].y, zv.y, d);
-                d = fmaf(gv[ch].z, zv.z, d);
-                d = fmaf(gv[ch].w, zv.w, d);
-                for (int o = 1; o < CL; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                if (leader && cval[ch]) {
-                    const uint32_t q = scr + 4u * (uint32_t)(i * 8 + hch[ch]);
-                    sts32f(q, lds32f(q) + d);
-                }
+                float w = 0.0f;
+                float4 zv = make_float4(0.f, 0.f, 0.f, 0.f);
+                lds32f_if(vi, w, scr + 4u * (uint32_t)(i * 8 + hch[ch]));
+                lds128f_if(vi && cval[ch], zv, st + coff[ch] + (uint32_t)i * row_bytes);
+                acc[ch][0] = fmaf(w, zv.x, acc[ch][0]);
+                acc[ch][1] = fmaf(w, zv.y, acc[ch][1]);
+                acc[ch][2] = fmaf(w, zv.z, acc[ch][2]);
+                acc[ch][3] = fmaf(w, zv.w, acc[ch][3]);
+                ssum[ch] += w;
             }
         }
         __syncwarp();
-        // 32 lanes = 4 slots x 8 heads: dlogit of (slot my_i, head my_h)
-        float dl = 0.0f;
-        if (my_i < c && my_h < H) {
-            const float d = lds32f(scr + 4u * (uint32_t)lane);
-            const float al = lds32f(st + (uint32_t)a.off_a + 4u * (uint32_t)(my_i * H + my_h));
-            const float ss = lds32f(st + (uint32_t)a.off_s + 4u * (uint32_t)(my_i * H + my_h));
-            const int e = my_i == 0 ? eids.x : my_i == 1 ? eids.y : my_i == 2 ? eids.z : eids.w;
-            dl = al * (d - tme);
-            if (!(ss + sme > 0.0f)) dl *= a.slope;
-            a.dlogit[(int64_t)e * H + my_h] = dl;
-        }
-        // head sums per row, in position order
-        const int rr[4] = {rows.x, rows.y, rows.z, rows.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            if (i >= c) break;
-            const float v = __shfl_sync(0xffffffffu, dl, i * 8 + my_h);
-            if (kk[i] != gkey) {
-                if (gkey != -1) flush();
-                gkey = kk[i];
-                grow = rr[i];
-                gs = 0.0f;
-            }
-            gs += v;
-        }
-        __syncwarp();  // every lane is done with stage s (data, scratch) before it is refilled
         fill(s);
     }
-    if (gkey != -1) flush();
+    if (arow != -1) flush();
 }
 
-// t_i[h] = g_i . out_i |_h (0 for rows without in-edges), written into grad_s_dst.  Same lane
-// layout, product order and reduction tree as the SDDMM in gat_bwd_tma_kernel, so a row whose
-// forward output equals one source row bitwise (a single in-edge: alpha = 1) gets t_i equal to its
-// d_alpha bitwise and dlogit exactly 0.  A warp takes RU rows per step (their loads in flight
-// together).
-template <int NCH, int RU>
-__global__ void gat_t_kernel(const float* __restrict__ g, int64_t ldg, const float* __restrict__ out, int64_t ldo,
-                             const int64_t* __restrict__ rowptr, int64_t n, int F, int H, int C, float* gsd) {
-    const int lane = threadIdx.x & 31;
-    const int CL = C >= 128 ? 32 : C / 4;
-    const bool leader = (lane % CL) == 0;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * RU; r0 < n; r0 += warps * RU) {
-        // rowptr[r0 .. r0 + RU] in lanes 0..RU
-        const int64_t rp = (lane <= RU && r0 + lane <= n) ? rowptr[r0 + lane] : 0;
-        float4 x[RU][NCH], y[RU][NCH];
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-            const int64_t r = r0 + u;
-            const bool ok = r < n;
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-                const bool cv = ok && 4 * (lane + 32 * ch) < F;
-                x[u][ch] = cv ? __ldg(reinterpret_cast<const float4*>(g + r * ldg) + lane + 32 * ch) : make_float4(0.f, 0.f, 0.f, 0.f);
-                y[u][ch] = cv ? __ldg(reinterpret_cast<const float4*>(out + r * ldo) + lane + 32 * ch) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-            const int64_t r = r0 + u;
-            const int64_t b = __shfl_sync(0xffffffffu, rp, u), e = __shfl_sync(0xffffffffu, rp, u + 1);
-            if (r >= n) break;
-            float acc[8];
-#pragma unroll
-            for (int h = 0; h < 8; ++h) acc[h] = 0.0f;
-#pragma unroll
-            for (int ch = 0; ch < NCH; ++ch) {
-                const int c = 4 * (lane + 32 * ch);
-                float d = x[u][ch].x * y[u][ch].x;
-                d = fmaf(x[u][ch].y, y[u][ch].y, d);
-                d = fmaf(x[u][ch].z, y[u][ch].z, d);
-                d = fmaf(x[u][ch].w, y[u][ch].w, d);
-                for (int o = 1; o < CL; o <<= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-                if (leader && c < F) {
-                    const int hh = c / C;
-#pragma unroll
-                    for (int h = 0; h < 8; ++h)
-                        if (h == hh) acc[h] += d;
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 8; ++h) {
-                if (h >= H) break;
-                const int owner = C >= 128 ? 0 : (h * (C / 4)) % 32;  // the leader lane of head h's chunk
-                if (lane == owner) gsd[r * H + h] = e > b ? acc[h] : 0.0f;
-            }
-        }
+__global__ void gat_smax_kernel(const float* __restrict__ s_src, int64_t total, int H, unsigned* smax) {
+    // stride is a multiple of 32, so each thread always reads the same head (tid % H)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    float m = -INFINITY;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) m = fmaxf(m, __ldg(s_src + i));
+    for (int o = 16; o >= H; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) < H) atomicMax(smax + (threadIdx.x & 31), f2ord(m));
+}
+
+// a split hub row: out = (sum of chunk partials of p z) / (sum of chunk partials of p), fp64 in chunk order
+__global__ void gat_fwd_combine_kernel(const int32_t* heavy_rows, const int64_t* item_ptr, int64_t h_lo,
+                                       int64_t item_lo, int64_t row_offset, const float* part, int64_t ldp,
+                                       const float* part_s, int H, int C, int F, float* out, int64_t ldo, float* rs,
+                                       int* bad) {
+    const int64_t hr = h_lo + blockIdx.x;
+    const int64_t r = (int64_t)heavy_rows[hr] - row_offset;
+    const int64_t i0 = item_ptr[hr] - item_lo, i1 = item_ptr[hr + 1] - item_lo;
+    __shared__ double sh[8];
+    __shared__ int tiny;
+    if (threadIdx.x == 0) tiny = 0;
+    __syncthreads();
+    if (threadIdx.x < H) {
+        double t = 0.0;
+        for (int64_t it = i0; it < i1; ++it) t += (double)part_s[it * H + threadIdx.x];
+        sh[threadIdx.x] = t;
+        rs[r * H + threadIdx.x] = (float)t;
+        if (!(t >= (double)kTinySum)) tiny = 1;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < F; c += blockDim.x) {
+        double t = 0.0;
+        for (int64_t it = i0; it < i1; ++it) t += (double)part[it * ldp + c];
+        out[r * ldo + c] = (float)(t / sh[c / C]);
+    }
+    if (threadIdx.x == 0 && tiny) bad[1 + atomicAdd(bad, 1)] = (int)r;
+}
+
+// alpha[k][h] = p[k][h] / rs[row(k)][h] over this plan's positions (thread per (position, head))
+__global__ void gat_alpha_norm_kernel(const int32_t* __restrict__ pos_row, const int32_t* __restrict__ eid,
+                                      const int64_t* __restrict__ rowptr, int64_t n, int64_t row_lo, int H,
+                                      const float* __restrict__ rs, float* alpha) {
+    const int64_t plo = rowptr[0], phi = rowptr[n];  // this plan's positions (slices: a sub-range)
+    const int64_t total = (phi - plo) * H;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t p = plo + t / H;
+        const int h = (int)(t % H);
+        const int64_t k = eid ? (int64_t)__ldg(eid + p) : p;
+        const int64_t r = (int64_t)__ldg(pos_row + p) - row_lo;
+        alpha[k * H + h] = alpha[k * H + h] / __ldg(rs + r * H + h);
     }
 }
 
-// grad_s_dst of a split hub row = its chunk partials added in fp64 in chunk order
-__global__ void gat_combine_kernel(const int32_t* heavy_rows, const int64_t* item_ptr, int64_t h_lo, int64_t h_hi,
-                                   int64_t item_lo, int64_t row_offset, const float* part, int H, float* gsd) {
-    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t hr = h_lo + t / H;
-    const int h = (int)(t % H);
-    if (hr >= h_hi) return;
-    double s = 0.0;
-    for (int64_t it = item_ptr[hr]; it < item_ptr[hr + 1]; ++it) s += (double)part[(it - item_lo) * H + h];
-    gsd[((int64_t)heavy_rows[hr] - row_offset) * H + h] = (float)s;
+// rows without in-edges: out = 0 (the plan's empty-row list)
+__global__ void gat_empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
+                                      int64_t row_hi, int F, float* out, int64_t ldo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t k = begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < end; k += warps) {
+        const int64_t r = (int64_t)order[k];
+        if (r < row_lo || r >= row_hi) continue;
+        for (int c = lane; c < F; c += 32) out[(r - row_lo) * ldo + c] = 0.0f;
+    }
+}
+
+// the listed rows (sum underflow), exactly: the row's own max, then exp / sum, then the
+// alpha-weighted sum (warp per row; a fallback far outside GAT's logit range, kept simple)
+__global__ void gat_fwd_fix_kernel(const int* __restrict__ bad, const int64_t* __restrict__ rowptr,
+                                   const int32_t* __restrict__ col, const int32_t* __restrict__ eid,
+                                   const float* __restrict__ z, int64_t ldz, const float* __restrict__ s_src,
+                                   const float* __restrict__ s_dst, int H, int C, int F, float slope, float* alpha,
+                                   float* out, int64_t ldo) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int count = bad[0];
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
+        const int64_t r = bad[1 + w];
+        const int64_t b = rowptr[r], e = rowptr[r + 1];
+        for (int h = 0; h < H; ++h) {
+            const float sd = s_dst[r * H + h];
+            float m = -INFINITY;
+            for (int64_t p = b + lane; p < e; p += 32) {
+                const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                m = fmaxf(m, pre > 0.0f ? pre : slope * pre);
+            }
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            float sum = 0.0f;
+            for (int64_t p = b + lane; p < e; p += 32) {
+                const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                sum += expf((pre > 0.0f ? pre : slope * pre) - m);
+            }
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            for (int64_t p = b + lane; p < e; p += 32) {
+                const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                const int64_t k = eid ? (int64_t)eid[p] : p;
+                alpha[k * H + h] = expf((pre > 0.0f ? pre : slope * pre) - m) / sum;
+            }
+        }
+        __syncwarp();
+        for (int c = lane; c < F; c += 32) {
+            float acc = 0.0f;
+            for (int64_t p = b; p < e; ++p) {
+                const int64_t k = eid ? (int64_t)eid[p] : p;
+                acc = fmaf(alpha[k * H + c / C], z[(int64_t)col[p] * ldz + c], acc);
+            }
+            out[r * ldo + c] = acc;
+        }
+    }
 }
 
 template <int NCH>
-pyg_status_t launch(int S, int64_t want, int warps, int smem, cudaStream_t s, const CUtensorMap& tz,
-                    const CUtensorMap& ta, const CUtensorMap& tsrc, const BwdArgs& a) {
-    void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, BwdArgs) =
-        S >= 4 ? gat_bwd_tma_kernel<NCH, 4> : S == 3 ? gat_bwd_tma_kernel<NCH, 3> : gat_bwd_tma_kernel<NCH, 2>;
+pyg_status_t launch_fwd(int S, int64_t want, int warps, int smem, int sm_kb, cudaStream_t s, const CUtensorMap& tz,
+                        const CUtensorMap& tsrc, const FwdArgs& a) {
+    void (*k)(const CUtensorMap, const CUtensorMap, FwdArgs) =
+        S >= 3 ? gat_fwd_tma_kernel<NCH, 3> : gat_fwd_tma_kernel<NCH, 2>;
     PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    // as seg_tma, keep part of the SM's unified array as L1 for the index windows (two 77 KB CTAs
-    // at F = 128 leave ~100 KB)
-    const int kSmemPerSm = std::min(227, std::max(32, knobs().gat_sm_kb)) * 1024;
+    const int kSmemPerSm = std::min(227, std::max(32, sm_kb)) * 1024;
     int dev = 0, sms = 148, per_sm = 1;
     PYG_CUDA(cudaGetDevice(&dev));
     PYG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -411,23 +804,11 @@ pyg_status_t launch(int S, int64_t want, int warps, int smem, cudaStream_t s, co
     PYG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * warps, smem));
     per_sm = std::min(per_sm, cap);
     const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1))));
-    k<<<grid, 32 * warps, smem, s>>>(tz, ta, tsrc, a);
+    k<<<grid, 32 * warps, smem, s>>>(tz, tsrc, a);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;
 }
-
-bool encode_rows(CUtensorMap* tm, const float* base, int64_t cols, int64_t rows, int64_t ld, int box_w) {
-    cuuint64_t gdim[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t gstr[1] = {(cuuint64_t)ld * 4};
-    cuuint32_t box[2] = {(cuuint32_t)box_w, 1};
-    cuuint32_t es[2] = {1, 1};
-    return tma::encode_fn()(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace gat
 
@@ -445,7 +826,7 @@ bool gat_bwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
         return false;
     if (!(H == 4 || H == 8) || F % 4 || F > 1024 || F < 16) return false;
     const bool pow2 = C > 0 && (C & (C - 1)) == 0;
-    if (!((pow2 && C >= 4 && C <= 128) || C % 128 == 0)) return false;
+    if (!(pow2 && C >= 4 && C <= 128)) return false;  // a head = 1..32 float4 chunks of one staged row
     if (mode != 1 && plan->n_light_tasks < 1024) return false;
     if (!al16(z) || ldz % 4 || !al16(g) || ldg % 4 || !al16(out) || ldo % 4) return false;
     if (!al16(alpha) || !al16(s_src) || !al16(s_dst) || !al16(gsd)) return false;
@@ -466,21 +847,20 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     PYG_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s));
     // t_i = g_i . out_i per head, parked in grad_s_dst (0 for rows without in-edges)
     {
-        const int nch_t = (int)cdiv(F, 128);
-        auto go = [&](auto k, int ru) {
-            const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8 * ru), 148 * 8));
-            k<<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, F, H, C, gsd);
-        };
-        if (nch_t == 1) go(gat_t_kernel<1, 4>, 4);
-        else if (nch_t == 2) go(gat_t_kernel<2, 2>, 2);
-        else if (nch_t <= 4) go(gat_t_kernel<4, 1>, 1);
-        else go(gat_t_kernel<8, 1>, 1);
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * H, 256), 148 * 16));
+        switch (C / 4) {
+            case 1: gat_t_row_head_kernel<1><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            case 2: gat_t_row_head_kernel<2><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            case 4: gat_t_row_head_kernel<4><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            case 8: gat_t_row_head_kernel<8><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            case 16: gat_t_row_head_kernel<16><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            default: gat_t_row_head_kernel<32><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+        }
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
     }
     const int nb = (F + 255) / 256;
     const int box_w = (int)align_up((size_t)((F + nb - 1) / nb), 8);
-    const int nch = (int)cdiv(nb * box_w, 128);
     BwdArgs a;
     a.rowptr = plan->rowptr - plan->row_offset;
     a.pos_row = plan->pos_row;
@@ -491,9 +871,6 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     a.E_root = plan->E;
     a.gidx = plan->col;
     a.eid = plan->perm_identity ? nullptr : plan->perm;
-    a.g = g;
-    a.ldg = ldg;
-    a.s_dst = s_dst;
     a.gsd = gsd;
     a.dlogit = dlogit;
     a.part = part;
@@ -502,36 +879,44 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     a.row_hi = plan->row_offset + n;
     a.F = F; a.H = H; a.C = C; a.box_w = box_w; a.nb = nb;
     a.slope = slope;
-    // stage: z boxes | alpha rows | s_src rows | g rows | t rows | s_dst rows (TMA destinations 128 B aligned)
+    // stage: z boxes | g boxes | alpha rows | s_src rows | t rows | s_dst rows (TMA destinations 128 B aligned)
     a.zbytes = 16 * nb * box_w;
-    a.off_a = (int)align_up((size_t)a.zbytes, 128);
+    a.off_g = (int)align_up((size_t)a.zbytes, 128);
+    a.off_a = a.off_g + (int)align_up((size_t)a.zbytes, 128);
     a.off_s = a.off_a + (int)align_up((size_t)16 * H, 128);
-    a.off_g = a.off_s + (int)align_up((size_t)16 * H, 128);
-    a.off_t = a.off_g + 16 * F;
-    a.off_d = a.off_t + 16 * H;
+    a.off_t = a.off_s + (int)align_up((size_t)16 * H, 128);
+    a.off_d = a.off_t + (int)align_up((size_t)16 * H, 128);
     a.stage_bytes = (int)align_up((size_t)(a.off_d + 16 * H), 128);
-    const int S = std::max(2, std::min(4, (knobs().gat_warp_kb * 1024) / a.stage_bytes));
-    a.data_off = (int)align_up((size_t)(128 + S * kMeta + 128), 128);
+    const int S = std::max(2, std::min(3, (knobs().gat_warp_kb * 1024) / a.stage_bytes));
+    a.data_off = (int)align_up((size_t)(128 + S * kMeta), 128);
     a.warp_bytes = (int)align_up((size_t)(a.data_off + S * a.stage_bytes), 128);
-    // 8 warps per CTA while two CTAs still fit an SM (F = 128: 8 x 9.6 KB); wide rows take fewer
+    // 8 warps per CTA while two CTAs still fit an SM (F = 128: 8 x 9.9 KB); wide rows take fewer
     int warps = 8;
     while (warps > 1 && warps * a.warp_bytes > 112 * 1024) warps >>= 1;
     const int smem = warps * a.warp_bytes;
     if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_backward: stage ring does not fit shared memory");
 
-    CUtensorMap tz, ta, tsrc;
-    if (!encode_rows(&tz, z, F, n_src, ldz, box_w) || !encode_rows(&ta, alpha, H, plan->E, H, H) ||
-        !encode_rows(&tsrc, s_src, H, n_src, H, H))
+    CUtensorMap tm[6];
+    if (!encode_rows(&tm[0], z, F, n_src, ldz, box_w) || !encode_rows(&tm[1], g, F, n, ldg, box_w) ||
+        !encode_rows(&tm[2], alpha, H, plan->E, H, H) || !encode_rows(&tm[3], s_src, H, n_src, H, H) ||
+        !encode_rows(&tm[4], gsd, H, n, H, H) || !encode_rows(&tm[5], s_dst, H, n, H, H))
         return fail(PYG_ERR_CUDA, "gat_backward: cuTensorMapEncodeTiled failed");
     const int64_t want = cdiv(a.n_tasks, warps);
-    switch (nch) {
-        case 1: PYG_TRY(launch<1>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-        case 2: PYG_TRY(launch<2>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-        case 3: PYG_TRY(launch<3>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-        case 4: PYG_TRY(launch<4>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-        case 5: case 6: PYG_TRY(launch<6>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-        default: PYG_TRY(launch<8>(S, want, warps, smem, s, tz, ta, tsrc, a)); break;
-    }
+    // C = 4 CPH <= 128: F <= 1024 -> NB = 1 (F <= 256), 2 (<= 512) or 4 column boxes
+    auto go = [&](auto nbc) -> pyg_status_t {
+        constexpr int NBc = decltype(nbc)::value;
+        switch (C / 4) {
+            case 1: return launch<1, NBc>(S, want, warps, smem, s, tm, a);
+            case 2: return launch<2, NBc>(S, want, warps, smem, s, tm, a);
+            case 4: return launch<4, NBc>(S, want, warps, smem, s, tm, a);
+            case 8: return launch<8, NBc>(S, want, warps, smem, s, tm, a);
+            case 16: return launch<16, NBc>(S, want, warps, smem, s, tm, a);
+            default: return launch<32, NBc>(S, want, warps, smem, s, tm, a);
+        }
+    };
+    if (nb == 1) PYG_TRY(go(std::integral_constant<int, 1>()));
+    else if (nb == 2) PYG_TRY(go(std::integral_constant<int, 2>()));
+    else PYG_TRY(go(std::integral_constant<int, 4>()));
     if (items > 0) {
         const int64_t nt = (plan->h_hi - plan->h_lo) * H;
         gat_combine_kernel<<<(unsigned)cdiv(nt, 256), 256, 0, s>>>(plan->heavy_rows, plan->heavy_item_ptr, plan->h_lo,
@@ -540,6 +925,134 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
     }
+    return PYG_OK;
+}
+
+
+// ---- forward host side ----
+
+size_t gat_fwd_tma_ws_bytes(const pyg_plan* plan, int64_t H, int64_t F) {
+    if (!plan) return 0;
+    const size_t items = (size_t)std::max<int64_t>(0, plan->item_hi - plan->item_lo);
+    const size_t ldp = align_up((size_t)F, 4);
+    return 256 + 256 + align_up((size_t)plan->n_rows * H * 4, 256) + align_up(items * ldp * 4, 256) +
+           align_up(items * H * 4, 256) + align_up(((size_t)plan->n_rows + 1) * 4, 256);
+}
+
+bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t ldz, float* out,
+                          int64_t ldo, const float* alpha, const float* s_src, const float* s_dst) {
+    using namespace gat;
+    const int mode = knobs().seg_tma;
+    if (mode == 0 || knobs().gat_fused == 0 || !plan || !plan->parts.empty() || plan->n_tasks <= 0 ||
+        !plan->task_pos || !plan->pos_row)
+        return false;
+    if (plan->n_empty > 0 && !plan->row_order) return false;
+    if (!(H == 4 || H == 8) || F % 4 || F > 1024 || F < 16 || C <= 0) return false;
+    if (mode != 1 && plan->n_light_tasks < 1024) return false;
+    if (!al16(z) || ldz % 4 || !al16(out) || ldo % 4) return false;
+    if (!al16(alpha) || !al16(s_src) || !al16(s_dst)) return false;
+    return tma::encode_fn() != nullptr;
+}
+
+pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
+                         const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
+                         void* ws, size_t ws_bytes, cudaStream_t s) {
+    using namespace gat;
+    const int64_t n = plan->n_rows;
+    const int64_t items = plan->item_hi - plan->item_lo;
+    const int64_t ldp = (int64_t)align_up((size_t)F, 4);
+    Carver cv(ws, ws_bytes);
+    unsigned long long* counter = cv.take<unsigned long long>(1);
+    unsigned* smax = cv.take<unsigned>(8);
+    float* rs = cv.take<float>((size_t)n * H);
+    float* part = cv.take<float>((size_t)std::max<int64_t>(items, 0) * ldp);
+    float* part_s = cv.take<float>((size_t)std::max<int64_t>(items, 0) * H);
+    int* bad = cv.take<int>((size_t)n + 1);
+    if (!ws || !cv.ok()) return fail(PYG_ERR_NO_MEMORY, "gat_propagate: workspace too small (pyg_gat_propagate_workspace_size)");
+    PYG_CUDA(cudaMemsetAsync(counter, 0, 256 + 256, s));  // counter and smax (adjacent carves)
+    PYG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    {
+        const int64_t total = n_src * H;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 4));
+        gat_smax_kernel<<<blocks, 256, 0, s>>>(s_src, total, H, smax);
+        PYG_LAUNCHED();
+    }
+    const int nb = (F + 255) / 256;
+    const int box_w = (int)align_up((size_t)((F + nb - 1) / nb), 8);
+    const int nch = (int)cdiv(nb * box_w, 128);
+    FwdArgs a;
+    a.rowptr = plan->rowptr - plan->row_offset;
+    a.pos_row = plan->pos_row;
+    a.task_pos = plan->task_pos;
+    a.task_item = plan->task_item;
+    a.n_tasks = items > 0 ? plan->n_tasks : plan->n_light_tasks;
+    a.next = counter;
+    a.E_root = plan->E;
+    a.gidx = plan->col;
+    a.eid = plan->perm_identity ? nullptr : plan->perm;
+    a.s_dst = s_dst;
+    a.smax = smax;
+    a.alpha = alpha;
+    a.out = out;
+    a.ldo = ldo;
+    a.rs = rs;
+    a.part = part;
+    a.part_s = part_s;
+    a.ldp = ldp;
+    a.item_lo = plan->item_lo;
+    a.bad = bad;
+    a.row_lo = plan->row_offset;
+    a.row_hi = plan->row_offset + n;
+    a.F = F; a.H = H; a.C = C; a.box_w = box_w; a.nb = nb;
+    a.slope = slope;
+    a.zbytes = 16 * nb * box_w;
+    a.off_s = (int)align_up((size_t)a.zbytes, 128);
+    a.off_d = a.off_s + (int)align_up((size_t)16 * H, 128);
+    a.stage_bytes = (int)align_up((size_t)(a.off_d + 16 * H), 128);
+    const int S = std::max(2, std::min(3, (knobs().gat_fwd_warp_kb * 1024) / a.stage_bytes));
+    a.data_off = (int)align_up((size_t)(128 + S * kMeta + 128), 128);
+    a.warp_bytes = (int)align_up((size_t)(a.data_off + S * a.stage_bytes), 128);
+    int warps = 8;
+    while (warps > 1 && warps * a.warp_bytes > 112 * 1024) warps >>= 1;
+    const int smem = warps * a.warp_bytes;
+    if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_propagate: stage ring does not fit shared memory");
+    CUtensorMap tz, tsrc;
+    if (!encode_rows(&tz, z, F, n_src, ldz, box_w) || !encode_rows(&tsrc, s_src, H, n_src, H, H))
+        return fail(PYG_ERR_CUDA, "gat_propagate: cuTensorMapEncodeTiled failed");
+    const int64_t want = cdiv(a.n_tasks, warps);
+    const int sm_kb = knobs().gat_fwd_sm_kb;
+    switch (nch) {
+        case 1: PYG_TRY(launch_fwd<1>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        case 2: PYG_TRY(launch_fwd<2>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        case 3: PYG_TRY(launch_fwd<3>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        case 4: PYG_TRY(launch_fwd<4>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        case 5: case 6: PYG_TRY(launch_fwd<6>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        default: PYG_TRY(launch_fwd<8>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+    }
+    if (items > 0) {
+        gat_fwd_combine_kernel<<<(unsigned)(plan->h_hi - plan->h_lo), 128, 0, s>>>(
+            plan->heavy_rows, plan->heavy_item_ptr, plan->h_lo, plan->item_lo, plan->row_offset, part, ldp, part_s, H,
+            C, F, out, ldo, rs, bad);
+        PYG_LAUNCHED();
+    }
+    if (plan->n_empty > 0) {
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(plan->n_empty, 8), 148 * 16));
+        gat_empty_rows_kernel<<<blocks, 256, 0, s>>>(plan->row_order, plan->empty_begin,
+                                                     plan->empty_begin + plan->n_empty, plan->row_offset,
+                                                     plan->row_offset + n, F, out, ldo);
+        PYG_LAUNCHED();
+    }
+    {
+        const int64_t total_max = plan->E * H;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total_max, 256), 148 * 16));
+        gat_alpha_norm_kernel<<<blocks, 256, 0, s>>>(plan->pos_row, a.eid, plan->rowptr, n, plan->row_offset, H, rs,
+                                                     alpha);
+        PYG_LAUNCHED();
+    }
+    gat_fwd_fix_kernel<<<148, 256, 0, s>>>(bad, plan->rowptr, plan->col, a.eid, z, ldz, s_src, s_dst, H, C, F, slope,
+                                           alpha, out, ldo);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
     return PYG_OK;
 }
 

@@ -178,6 +178,13 @@ bool gat_bwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
                           int64_t ldg, const float* out, int64_t ldo, const float* alpha, const float* s_src,
                           const float* s_dst, const float* gsd);
 size_t gat_bwd_tma_ws_bytes(const pyg_plan* plan, int64_t H);
+// GAT forward in one TMA gather4 pass (softmax shift bounded by max s_src; gat_tma.cu)
+bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t ldz, float* out,
+                          int64_t ldo, const float* alpha, const float* s_src, const float* s_dst);
+size_t gat_fwd_tma_ws_bytes(const pyg_plan* plan, int64_t H, int64_t F);
+pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
+                         const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
+                         void* ws, size_t ws_bytes, cudaStream_t s);
 pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* g, int64_t ldg, const float* out, int64_t ldo, const float* alpha,
                          const float* s_src, const float* s_dst, float slope, float* dlogit, float* gsd, void* ws,
