@@ -767,14 +767,19 @@ def main():
         zc = torch.randn((N, F), generator=gg, device=dev)
         gout = torch.randn((N, F), generator=gg, device=dev)
         gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
-        gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C), 1), dtype=torch.uint8,
+        # the training step keeps the attention in factored form (alpha = p / row_sums[dst]): the forward's
+        # consumer is the backward, which divides where it reads alpha (no E x H normalisation pass)
+        gat["row_sums"] = torch.empty((N, H), device=dev)
+        gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C, True), 1), dtype=torch.uint8,
                           device=dev)
         gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 2, "gat"
 
         def compute():
-            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"], workspace=gfw)
-            gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT, out=o, workspace=gws)
+            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"], workspace=gfw,
+                                         row_sums=gat["row_sums"])
+            gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT, out=o, workspace=gws,
+                                               row_sums=gat["row_sums"])
 
     gatl = None
     if a.op == "gatlayer":
@@ -797,11 +802,12 @@ def main():
         gal = torch.empty((E, H), device=dev)
         gatl = dict(H=H, C=C, out=go)
         glw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
+        grs = torch.empty((N, H), device=dev)  # attention in factored form (alpha = p / row_sums[dst])
         passes, red = 1, "gatlayer"
 
         def compute():
             z, ss, sd = pg.pyg_gat_transform(x_full, Wg[:, :F], a_s, a_d, H)
-            pg.pyg_gat_propagate(z, ss, sd, H, plan, out=go, alpha=gal, workspace=glw)
+            pg.pyg_gat_propagate(z, ss, sd, H, plan, out=go, alpha=gal, workspace=glw, row_sums=grs)
 
     appnp = None
     if a.op == "appnp":

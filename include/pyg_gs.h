@@ -372,15 +372,20 @@ pyg_status_t pyg_gat_propagate_workspace_size(const pyg_plan_t* plan, int64_t H,
  * shift-invariant, and c_i[h] = leaky_relu(max_j s_src[j][h] + s_dst[i][h]) bounds every
  * logit of row i (leaky_relu is monotone), so the weights exp(l - c_i) <= 1 are accumulated
  * with z_j as they are gathered and divided by their row sum at the row's end; rows whose sum
- * underflows (< 1e-30) are recomputed with their own max.  Asynchronous. */
+ * underflows (< 1e-30) are recomputed with their own max.
+ * row_sums [n_dst x H] packed, OPTIONAL OUTPUT: the attention in factored form -- alpha then holds
+ * weights p with alpha_true[k][h] = alpha[k][h] / row_sums[dst_k][h] (on the one-pass path the
+ * division over all E x H entries, a random read-modify-write, is skipped; pyg_gat_backward takes
+ * the pair).  NULL -> alpha is normalised.  Asynchronous. */
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                                const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
                                float negative_slope, const pyg_plan_t* plan, float* out,
-                               int64_t ldo, float* alpha, void* workspace, size_t workspace_bytes,
-                               void* stream);
-/* Scratch of pyg_gat_backward (both its paths).  Host-only. */
+                               int64_t ldo, float* alpha, float* row_sums, void* workspace,
+                               size_t workspace_bytes, void* stream);
+/* Scratch of pyg_gat_backward (both its paths; with_row_sums: alpha passed in factored form,
+ * + n_dst x H*C floats).  Host-only. */
 pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_plan_t* plan_T,
-                                             int64_t H, int64_t C, size_t* bytes);
+                                             int64_t H, int64_t C, int with_row_sums, size_t* bytes);
 /* Backward of pyg_gat_propagate, g = grad_out [n_dst x H*C] stride ldg:
  *   grad_z[j][h*C+c] = sum_{k: src_k = j} alpha[k][h] g[dst_k][h*C+c]     (grad_z optional)
  *   grad_logit[k][h] = alpha[k][h] (g_i . z_j|_h - sum_{k' in seg(i)} alpha[k'][h] g_i . z_j'|_h)
@@ -393,12 +398,14 @@ pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_p
  *   z), so the SDDMM and the softmax backward run as ONE streaming pass over the plan (TMA
  *   gather4 pipeline; H in {4, 8}, C a power of two <= 128 or a multiple of 128, 16-byte
  *   aligned rows); without it (or outside those shapes) two passes per row recompute the sum.
+ * row_sums: NULL (alpha normalised) or the forward's row_sums (alpha in factored form).
  * plan: the forward plan; plan_T: row_index = sources, col_index = targets.
- * H*C <= 4096.  workspace: pyg_gat_backward_workspace_size(plan, plan_T, H, C).
+ * H*C <= 4096.  workspace: pyg_gat_backward_workspace_size(plan, plan_T, H, C, row_sums != NULL).
  * Asynchronous. */
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
                               const float* s_src, const float* s_dst, int64_t n_dst, int64_t E,
-                              float negative_slope, const float* alpha, const float* grad_out,
+                              float negative_slope, const float* alpha, const float* row_sums,
+                              const float* grad_out,
                               int64_t ldg, const float* out, int64_t ldo,
                               const pyg_plan_t* plan, const pyg_plan_t* plan_T,
                               float* grad_z, int64_t ldgz, float* grad_s_src, float* grad_s_dst,

@@ -386,8 +386,10 @@ def pyg_segment_softmax_backward(out: torch.Tensor, grad_out: torch.Tensor, plan
 
 def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, plan: Plan,
                       negative_slope: float = 0.2, out: Optional[torch.Tensor] = None,
-                      alpha: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
-    """GAT attention aggregation: (out [n_dst x H*C], alpha [E x H])."""
+                      alpha: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                      row_sums: Optional[torch.Tensor] = None):
+    """GAT attention aggregation: (out [n_dst x H*C], alpha [E x H]).
+    row_sums [n_dst x H] (optional output): alpha in factored form, alpha / row_sums[dst]."""
     n_src, F, ldz = _rows(z, "z")
     C = F // H
     assert C * H == F
@@ -403,8 +405,8 @@ def pyg_gat_propagate(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor,
     if workspace is None:
         workspace = _workspace(pyg_gat_propagate_workspace_size(plan, H, C), z.device)
     check(lib.pyg_gat_propagate(_ptr(z), n_src, H, C, ldz, _ptr(s_src), _ptr(s_dst), n_dst, E, negative_slope,
-                                plan.handle, _ptr(out), ldo, _ptr(alpha), _ptr(workspace), workspace.numel(),
-                                _stream(z.device)), "pyg_gat_propagate")
+                                plan.handle, _ptr(out), ldo, _ptr(alpha), _ptr(row_sums), _ptr(workspace),
+                                workspace.numel(), _stream(z.device)), "pyg_gat_propagate")
     return out, alpha
 
 
@@ -414,16 +416,17 @@ def pyg_gat_propagate_workspace_size(plan: Plan, H: int, C: int) -> int:
     return nb.value
 
 
-def pyg_gat_backward_workspace_size(plan: Plan, plan_T: Plan, H: int, C: int) -> int:
+def pyg_gat_backward_workspace_size(plan: Plan, plan_T: Plan, H: int, C: int, row_sums: bool = False) -> int:
     nb = ctypes.c_size_t()
-    check(lib.pyg_gat_backward_workspace_size(plan.handle, plan_T.handle, H, C, ctypes.byref(nb)),
+    check(lib.pyg_gat_backward_workspace_size(plan.handle, plan_T.handle, H, C, int(row_sums), ctypes.byref(nb)),
           "pyg_gat_backward_workspace_size")
     return nb.value
 
 
 def pyg_gat_backward(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, H: int, alpha: torch.Tensor,
                      grad_out: torch.Tensor, plan: Plan, plan_T: Plan, negative_slope: float = 0.2,
-                     out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None):
+                     out: Optional[torch.Tensor] = None, workspace: Optional[torch.Tensor] = None,
+                     row_sums: Optional[torch.Tensor] = None):
     """dict(z, s_src, s_dst, logit) gradients of pyg_gat_propagate.  out: the forward output (enables
     the one-pass SDDMM + softmax backward, t_i = g_i . out_i)."""
     n_src, F, ldz = _rows(z, "z")
@@ -438,9 +441,10 @@ def pyg_gat_backward(z: torch.Tensor, s_src: torch.Tensor, s_dst: torch.Tensor, 
     gsd = torch.empty((n_dst, H), dtype=torch.float32, device=dev)
     gl = torch.empty((max(E, 1), H), dtype=torch.float32, device=dev)[:E]
     if workspace is None:
-        workspace = _workspace(pyg_gat_backward_workspace_size(plan, plan_T, H, C), dev)
+        workspace = _workspace(pyg_gat_backward_workspace_size(plan, plan_T, H, C, row_sums is not None), dev)
     check(lib.pyg_gat_backward(_ptr(z), n_src, H, C, ldz, _ptr(s_src.contiguous()), _ptr(s_dst.contiguous()), n_dst,
-                               E, negative_slope, _ptr(alpha), _ptr(grad_out), ldg, _ptr(out), ldo, plan.handle,
+                               E, negative_slope, _ptr(alpha), _ptr(row_sums), _ptr(grad_out), ldg, _ptr(out), ldo,
+                               plan.handle,
                                plan_T.handle, _ptr(gz), F, _ptr(gss), _ptr(gsd), _ptr(gl), _ptr(workspace),
                                workspace.numel(), _stream(dev)),
           "pyg_gat_backward")

@@ -659,8 +659,8 @@ pyg_status_t pyg_gat_propagate_workspace_size(const pyg_plan_t* plan, int64_t H,
 
 pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
                                const float* s_dst, int64_t n_dst, int64_t E, float negative_slope,
-                               const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, void* ws,
-                               size_t ws_bytes, void* stream) {
+                               const pyg_plan_t* plan, float* out, int64_t ldo, float* alpha, float* row_sums,
+                               void* ws, size_t ws_bytes, void* stream) {
     REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
             "gat_propagate: bad sizes");
     const int64_t F = H * C;
@@ -675,24 +675,31 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
     if (E > 0 && n_dst > 0 && gat_fwd_tma_eligible(plan, (int)H, (int)C, (int)F, z, ldz, out, ldo, alpha, s_src, s_dst))
         // softmax with a per-row shift bounded from the global max of s_src + the weighted sum, one pass
         return gat_fwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, s_src, s_dst, negative_slope, out, ldo, alpha,
-                           ws, ws_bytes, s);
+                           row_sums, ws, ws_bytes, s);
     if (E > 0)
         PYG_TRY(attention_softmax(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, nullptr, 0, s_src, s_dst,
                                   (int)H, negative_slope, alpha, H, s));
+    if (row_sums && n_dst > 0) PYG_TRY(fill_const(row_sums, n_dst * H, 1.0f, s));  // alpha is normalised here
     if (n_dst == 0 || F == 0) return PYG_OK;
     return headw_sum(plan, z, ldz, F, C, H, alpha, out, ldo, n_dst, ws, ws_bytes, s);
 }
 
+static size_t gat_bwd_ws_main(const pyg_plan* plan, const pyg_plan* plan_T, int64_t H, int64_t C) {
+    return align_up(std::max(gat_bwd_tma_ws_bytes(plan, H), segment_ws_bytes(plan_T, H * C, PYG_SUM)), 256);
+}
+
 pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_plan_t* plan_T, int64_t H, int64_t C,
-                                             size_t* bytes) {
+                                             int with_row_sums, size_t* bytes) {
     REQUIRE(bytes && plan && plan_T && H > 0 && C >= 0, PYG_ERR_INVALID_ARGUMENT, "gat_backward_workspace_size: bad args");
-    *bytes = std::max(gat_bwd_tma_ws_bytes(plan, H), segment_ws_bytes(plan_T, H * C, PYG_SUM));
+    // + grad_out scaled by 1 / row_sums per head (the alpha-weighted grad_z with unnormalised alpha)
+    *bytes = gat_bwd_ws_main(plan, plan_T, H, C) + (with_row_sums ? (size_t)plan->n_rows * H * C * 4 : 0);
     return PYG_OK;
 }
 
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz, const float* s_src,
                               const float* s_dst, int64_t n_dst, int64_t E, float negative_slope, const float* alpha,
-                              const float* grad_out, int64_t ldg, const float* out, int64_t ldo, const pyg_plan_t* plan,
+                              const float* row_sums, const float* grad_out, int64_t ldg, const float* out, int64_t ldo,
+                              const pyg_plan_t* plan,
                               const pyg_plan_t* plan_T, float* grad_z, int64_t ldgz, float* grad_s_src,
                               float* grad_s_dst, float* grad_logit, void* ws, size_t ws_bytes, void* stream) {
     REQUIRE(n_src >= 0 && H > 0 && C >= 0 && n_dst >= 0 && E >= 0, PYG_ERR_INVALID_ARGUMENT,
@@ -711,20 +718,32 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
     REQUIRE(n_dst * H == 0 || grad_s_dst, PYG_ERR_INVALID_ARGUMENT, "gat_backward: null grad_s_dst");
     REQUIRE(!out || ldo >= F, PYG_ERR_DIMENSION, "gat_backward: ldo < H*C");
     cudaStream_t s = as_stream(stream);
+    // row_sums (the forward's factored alpha): grad_z = sum_i p_ij g_i / row_sums_i takes grad_out
+    // scaled per row and head, kept behind the main workspace
+    float* gsc = nullptr;
+    const size_t main_ws = gat_bwd_ws_main(plan, plan_T, H, C);
+    if (row_sums && n_dst > 0 && F > 0) {
+        REQUIRE(ws && ws_bytes >= main_ws + (size_t)n_dst * F * 4, PYG_ERR_NO_MEMORY,
+                "gat_backward: workspace too small (pyg_gat_backward_workspace_size with row_sums)");
+        gsc = reinterpret_cast<float*>(static_cast<char*>(ws) + main_ws);
+    }
     if (E > 0 && gat_bwd_tma_eligible(plan, (int)H, (int)C, (int)F, z, ldz, grad_out, ldg, out, ldo, alpha, s_src, s_dst,
                                       grad_s_dst)) {
         // one pass: SDDMM + softmax backward with t_i = g_i . out_i (gat_tma.cu)
-        PYG_TRY(gat_bwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, grad_out, ldg, out, ldo, alpha, s_src, s_dst,
-                            negative_slope, grad_logit, grad_s_dst, ws, ws_bytes, s));
+        PYG_TRY(gat_bwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, grad_out, ldg, out, ldo, alpha, row_sums, s_src,
+                            s_dst, negative_slope, grad_logit, grad_s_dst, gsc, ws, main_ws, s));
     } else {
         if (n_dst > 0) PYG_TRY(fill_rows(grad_s_dst, H, (int)H, n_dst, s));  // rows without in-edges
         if (E > 0)
             PYG_TRY(attention_softmax_bwd(plan, plan->col, plan->perm_identity ? nullptr : plan->perm, (int)H, (int)C,
                                           (int)F, alpha, H, grad_out, ldg, z, ldz, s_src, s_dst, negative_slope,
-                                          grad_logit, H, grad_s_dst, s));
+                                          grad_logit, H, grad_s_dst, s, row_sums));
+        if (gsc) PYG_TRY(gat_scale_rows(grad_out, ldg, n_dst, (int)H, (int)C, row_sums, gsc, s));
     }
-    if (grad_z && n_src > 0 && F > 0)
-        PYG_TRY(headw_sum(plan_T, grad_out, ldg, F, C, H, alpha, grad_z, ldgz, n_src, ws, ws_bytes, s));
+    if (grad_z && n_src > 0 && F > 0) {
+        if (gsc) PYG_TRY(headw_sum(plan_T, gsc, F, F, C, H, alpha, grad_z, ldgz, n_src, ws, main_ws, s));
+        else PYG_TRY(headw_sum(plan_T, grad_out, ldg, F, C, H, alpha, grad_z, ldgz, n_src, ws, ws_bytes, s));
+    }
     if (grad_s_src && n_src > 0) {
         SegArgs a;
         a.X = grad_logit; a.ldx = H; a.ncols = (int)H;

@@ -278,7 +278,20 @@ struct SoftmaxBwdArgs {
     float* dlogit;          // [E x H] stride ldd (GAT: also the d_alpha scratch of pass A)
     int64_t ldd;
     float* grad_s_dst;      // GAT: [n_rows x H]
+    const float* rs;        // GAT with factored alpha: alpha[k][h] / rs[row][h] is the coefficient (or null)
 };
+
+// the row's 1 / rs factors (all 1 when alpha is normalised), applied to every alpha load of the row
+__device__ __forceinline__ void row_scale(float (&inv)[kMaxHeads], const float* rs, int64_t r, int H) {
+    if (rs) {
+        load_heads(inv, rs, r, H);
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) inv[h] = h < H ? 1.0f / inv[h] : 1.0f;
+    } else {
+#pragma unroll
+        for (int h = 0; h < kMaxHeads; ++h) inv[h] = 1.0f;
+    }
+}
 
 template <int G, bool GAT>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowSet rs) {
@@ -294,7 +307,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowS
         if (r == -2) break;
         if (r < 0) continue;
         const int64_t b = rs.rowptr[r], e = rs.rowptr[r + 1];
-        float sd[kMaxHeads];
+        float sd[kMaxHeads], inv[kMaxHeads];
+        row_scale(inv, GAT ? a.rs : nullptr, r, a.H);
         if (GAT) {
             load_heads(sd, a.s_dst, r, a.H);
             if (G == 32) __syncwarp(); else __syncthreads();
@@ -344,6 +358,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowS
                 for (int h = 0; h < kMaxHeads; ++h) al[h] = h < a.H ? __ldg(a.alpha + k * a.lda + h) : 0.0f;
             }
 #pragma unroll
+            for (int h = 0; h < kMaxHeads; ++h) al[h] *= inv[h];
+#pragma unroll
             for (int h = 0; h < kMaxHeads; ++h) tp[h] = fmaf(al[h], da[h], tp[h]);
         }
         grp.sum(tp, a.H);
@@ -360,7 +376,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(SoftmaxBwdArgs a, RowS
                 load_heads(ss, a.s_src, a.col[p], a.H);
 #pragma unroll
                 for (int h = 0; h < kMaxHeads; ++h) {
-                    float d = al[h] * (da[h] - tp[h]);
+                    float d = al[h] * inv[h] * (da[h] - tp[h]);
                     if (!(ss[h] + sd[h] > 0.0f)) d *= a.slope;
                     da[h] = d;
                     gs[h] += d;
@@ -426,8 +442,9 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
         }
         const bool rok = r >= 0;
         const int64_t b = rok ? rs.rowptr[r] : 0, e = rok ? rs.rowptr[r + 1] : 0;
-        float sd[kMaxHeads];
+        float sd[kMaxHeads], inv[kMaxHeads];
         if (rok) load_heads(sd, a.s_dst, r, a.H);
+        row_scale(inv, rok ? a.rs : nullptr, r, a.H);
         float4 gv[NCH];
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
@@ -484,7 +501,7 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
                 store_heads(a.dlogit, k, a.H, da);  // scratch, re-read by this thread in pass B
                 load_heads(al, a.alpha, k, a.H);
 #pragma unroll
-                for (int h = 0; h < kMaxHeads; ++h) tp[h] = fmaf(al[h], da[h], tp[h]);
+                for (int h = 0; h < kMaxHeads; ++h) tp[h] = fmaf(al[h] * inv[h], da[h], tp[h]);
             }
             __syncwarp();
         }
@@ -502,7 +519,7 @@ __global__ void __launch_bounds__(256) gat_bwd_coop_kernel(SoftmaxBwdArgs a, Row
             load_heads(ss, a.s_src, a.col[p], a.H);
 #pragma unroll
             for (int h = 0; h < kMaxHeads; ++h) {
-                float d = al[h] * (da[h] - tp[h]);
+                float d = al[h] * inv[h] * (da[h] - tp[h]);
                 if (!(ss[h] + sd[h] > 0.0f)) d *= a.slope;
                 da[h] = d;
                 gs[h] += d;
@@ -569,10 +586,11 @@ pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const i
 pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, const int32_t* eid, int H, int C, int F,
                                    const float* alpha, int64_t lda, const float* grad, int64_t ldg, const float* z,
                                    int64_t ldz, const float* s_src, const float* s_dst, float slope, float* dlogit,
-                                   int64_t ldd, float* grad_s_dst, cudaStream_t s) {
+                                   int64_t ldd, float* grad_s_dst, cudaStream_t s, const float* row_sums) {
     if (plan->n_rows <= 0 || H <= 0) return PYG_OK;
     if (H > kMaxHeads) return fail(PYG_ERR_UNSUPPORTED, "softmax backward: at most %d heads / columns", kMaxHeads);
     SoftmaxBwdArgs a;
+    a.rs = row_sums;
     a.col = col; a.eid = eid;
     a.H = H; a.C = C; a.F = F; a.alpha = alpha; a.lda = lda; a.grad = grad; a.ldg = ldg;
     a.z = z; a.ldz = ldz; a.s_src = s_src; a.s_dst = s_dst; a.slope = slope;

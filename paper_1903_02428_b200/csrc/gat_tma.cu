@@ -311,7 +311,8 @@ __global__ void __launch_bounds__(256, 2) gat_bwd_tma_kernel(const __grid_consta
 // d_alpha bitwise; every thread keeps 2 CPH vector loads in flight.
 template <int CPH>
 __global__ void gat_t_row_head_kernel(const float* __restrict__ g, int64_t ldg, const float* __restrict__ out,
-                                      int64_t ldo, const int64_t* __restrict__ rowptr, int64_t n, int H, float* gsd) {
+                                      int64_t ldo, const int64_t* __restrict__ rowptr, int64_t n, int H, float* gsd,
+                                      const float* __restrict__ rs, float* gsc) {
     const int64_t total = n * H;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
@@ -322,10 +323,18 @@ __global__ void gat_t_row_head_kernel(const float* __restrict__ g, int64_t ldg, 
             const float4* gr = reinterpret_cast<const float4*>(g + r * ldg) + h * CPH;
             const float4* orr = reinterpret_cast<const float4*>(out + r * ldo) + h * CPH;
             const int rot = head_rot<CPH>(h);
+            // factored alpha: this head's grad_out / row sum for the alpha-weighted grad_z
+            const float inv = gsc ? 1.0f / __ldg(rs + t) : 0.0f;
+            float4* gs = gsc ? reinterpret_cast<float4*>(gsc + r * (int64_t)H * 4 * CPH) + h * CPH : nullptr;
 #pragma unroll
             for (int j = 0; j < CPH; ++j) {
                 const int k = (j + rot) % CPH;
-                const float4 x = __ldg(gr + k), y = __ldg(orr + k);
+                float4 x = __ldg(gr + k);
+                const float4 y = __ldg(orr + k);
+                if (gs) {  // factored alpha: t and the SDDMM both use g / row_sum (see gat_bwd_tma)
+                    x = make_float4(x.x * inv, x.y * inv, x.z * inv, x.w * inv);
+                    gs[k] = x;
+                }
                 float q = x.x * y.x;
                 q = fmaf(x.y, y.y, q);
                 q = fmaf(x.z, y.z, q);
@@ -353,7 +362,8 @@ template <int CPH, int NB>
 pyg_status_t launch(int S, int64_t want, int warps, int smem, cudaStream_t s, const CUtensorMap (&tm)[6],
                     const BwdArgs& a) {
     void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap, const CUtensorMap,
-              const CUtensorMap, BwdArgs) = S >= 3 ? gat_bwd_tma_kernel<CPH, NB, 3> : gat_bwd_tma_kernel<CPH, NB, 2>;
+              const CUtensorMap, BwdArgs) =
+        S >= 3 ? gat_bwd_tma_kernel<CPH, NB, 3> : gat_bwd_tma_kernel<CPH, NB, 2>;
     PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int kSmemPerSm = std::min(227, std::max(32, knobs().gat_sm_kb)) * 1024;
     int dev = 0, sms = 148, per_sm = 1;
@@ -749,7 +759,7 @@ __global__ void gat_fwd_fix_kernel(const int* __restrict__ bad, const int64_t* _
                                    const int32_t* __restrict__ col, const int32_t* __restrict__ eid,
                                    const float* __restrict__ z, int64_t ldz, const float* __restrict__ s_src,
                                    const float* __restrict__ s_dst, int H, int C, int F, float slope, float* alpha,
-                                   float* out, int64_t ldo) {
+                                   float* out, int64_t ldo, float* row_sums) {
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
     const int count = bad[0];
@@ -775,6 +785,7 @@ __global__ void gat_fwd_fix_kernel(const int* __restrict__ bad, const int64_t* _
                 const int64_t k = eid ? (int64_t)eid[p] : p;
                 alpha[k * H + h] = expf((pre > 0.0f ? pre : slope * pre) - m) / sum;
             }
+            if (row_sums && lane == 0) row_sums[r * H + h] = 1.0f;  // this row's alpha is normalised
         }
         __syncwarp();
         for (int c = lane; c < F; c += 32) {
@@ -835,8 +846,8 @@ bool gat_bwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
 
 pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* g, int64_t ldg, const float* out, int64_t ldo, const float* alpha,
-                         const float* s_src, const float* s_dst, float slope, float* dlogit, float* gsd, void* ws,
-                         size_t ws_bytes, cudaStream_t s) {
+                         const float* row_sums, const float* s_src, const float* s_dst, float slope, float* dlogit,
+                         float* gsd, float* gsc, void* ws, size_t ws_bytes, cudaStream_t s) {
     using namespace gat;
     const int64_t n = plan->n_rows;
     Carver cv(ws, ws_bytes);
@@ -849,12 +860,12 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     {
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n * H, 256), 148 * 16));
         switch (C / 4) {
-            case 1: gat_t_row_head_kernel<1><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
-            case 2: gat_t_row_head_kernel<2><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
-            case 4: gat_t_row_head_kernel<4><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
-            case 8: gat_t_row_head_kernel<8><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
-            case 16: gat_t_row_head_kernel<16><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
-            default: gat_t_row_head_kernel<32><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd); break;
+            case 1: gat_t_row_head_kernel<1><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
+            case 2: gat_t_row_head_kernel<2><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
+            case 4: gat_t_row_head_kernel<4><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
+            case 8: gat_t_row_head_kernel<8><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
+            case 16: gat_t_row_head_kernel<16><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
+            default: gat_t_row_head_kernel<32><<<blocks, 256, 0, s>>>(g, ldg, out, ldo, plan->rowptr, n, H, gsd, row_sums, gsc); break;
         }
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
@@ -886,6 +897,9 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     a.off_s = a.off_a + (int)align_up((size_t)16 * H, 128);
     a.off_t = a.off_s + (int)align_up((size_t)16 * H, 128);
     a.off_d = a.off_t + (int)align_up((size_t)16 * H, 128);
+    // factored alpha (alpha = p / rs_i): with g' = g_i / rs_i (written by the t kernel, also grad_z's
+    // input), d' = g' . z_j = d / rs_i and t' = g' . out_i = t / rs_i, so p (d' - t') = alpha (d - t):
+    // the SDDMM gathers g' and needs no row-sum gather or division
     a.stage_bytes = (int)align_up((size_t)(a.off_d + 16 * H), 128);
     const int S = std::max(2, std::min(3, (knobs().gat_warp_kb * 1024) / a.stage_bytes));
     a.data_off = (int)align_up((size_t)(128 + S * kMeta), 128);
@@ -897,7 +911,9 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_backward: stage ring does not fit shared memory");
 
     CUtensorMap tm[6];
-    if (!encode_rows(&tm[0], z, F, n_src, ldz, box_w) || !encode_rows(&tm[1], g, F, n, ldg, box_w) ||
+    if (row_sums && !gsc) return fail(PYG_ERR_INVALID_ARGUMENT, "internal: factored alpha without g' scratch");
+    if (!encode_rows(&tm[0], z, F, n_src, ldz, box_w) ||
+        !(row_sums ? encode_rows(&tm[1], gsc, F, n, F, box_w) : encode_rows(&tm[1], g, F, n, ldg, box_w)) ||
         !encode_rows(&tm[2], alpha, H, plan->E, H, H) || !encode_rows(&tm[3], s_src, H, n_src, H, H) ||
         !encode_rows(&tm[4], gsd, H, n, H, H) || !encode_rows(&tm[5], s_dst, H, n, H, H))
         return fail(PYG_ERR_CUDA, "gat_backward: cuTensorMapEncodeTiled failed");
@@ -929,6 +945,43 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
 }
 
 
+// ---- helpers ----
+
+namespace gat {
+__global__ void scale_rows_kernel(const float* __restrict__ g, int64_t ldg, int64_t n, int H, int C,
+                                  const float* __restrict__ rs, float* gsc) {
+    const int64_t F = (int64_t)H * C, total = n * F;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t r = t / F, c = t - r * F;
+        gsc[t] = g[r * ldg + c] / rs[r * H + c / C];
+    }
+}
+__global__ void fill_kernel(float* p, int64_t n, float v) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) p[t] = v;
+}
+}  // namespace gat
+
+pyg_status_t gat_scale_rows(const float* g, int64_t ldg, int64_t n, int H, int C, const float* row_sums, float* gsc,
+                            cudaStream_t s) {
+    const int64_t total = n * H * C;
+    if (total <= 0) return PYG_OK;
+    gat::scale_rows_kernel<<<(unsigned)std::min<int64_t>(cdiv(total, 256), 148 * 16), 256, 0, s>>>(g, ldg, n, H, C,
+                                                                                                   row_sums, gsc);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+pyg_status_t fill_const(float* p, int64_t n, float v, cudaStream_t s) {
+    if (n <= 0) return PYG_OK;
+    gat::fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 16), 256, 0, s>>>(p, n, v);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
 // ---- forward host side ----
 
 size_t gat_fwd_tma_ws_bytes(const pyg_plan* plan, int64_t H, int64_t F) {
@@ -956,7 +1009,7 @@ bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
 
 pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
-                         void* ws, size_t ws_bytes, cudaStream_t s) {
+                         float* row_sums, void* ws, size_t ws_bytes, cudaStream_t s) {
     using namespace gat;
     const int64_t n = plan->n_rows;
     const int64_t items = plan->item_hi - plan->item_lo;
@@ -968,6 +1021,7 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     float* part = cv.take<float>((size_t)std::max<int64_t>(items, 0) * ldp);
     float* part_s = cv.take<float>((size_t)std::max<int64_t>(items, 0) * H);
     int* bad = cv.take<int>((size_t)n + 1);
+    if (row_sums) rs = row_sums;  // factored alpha: the caller keeps the row sums, alpha stays p
     if (!ws || !cv.ok()) return fail(PYG_ERR_NO_MEMORY, "gat_propagate: workspace too small (pyg_gat_propagate_workspace_size)");
     PYG_CUDA(cudaMemsetAsync(counter, 0, 256 + 256, s));  // counter and smax (adjacent carves)
     PYG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
@@ -1042,7 +1096,7 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
                                                      plan->row_offset + n, F, out, ldo);
         PYG_LAUNCHED();
     }
-    {
+    if (!row_sums) {
         const int64_t total_max = plan->E * H;
         const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total_max, 256), 148 * 16));
         gat_alpha_norm_kernel<<<blocks, 256, 0, s>>>(plan->pos_row, a.eid, plan->rowptr, n, plan->row_offset, H, rs,
@@ -1050,7 +1104,7 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
         PYG_LAUNCHED();
     }
     gat_fwd_fix_kernel<<<148, 256, 0, s>>>(bad, plan->rowptr, plan->col, a.eid, z, ldz, s_src, s_dst, H, C, F, slope,
-                                           alpha, out, ldo);
+                                           alpha, out, ldo, row_sums);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;

@@ -170,7 +170,7 @@ pyg_status_t attention_softmax(const pyg_plan* plan, const int32_t* col, const i
 pyg_status_t attention_softmax_bwd(const pyg_plan* plan, const int32_t* col, const int32_t* eid, int H, int C, int F,
                                    const float* alpha, int64_t lda, const float* grad, int64_t ldg, const float* z,
                                    int64_t ldz, const float* s_src, const float* s_dst, float slope, float* dlogit,
-                                   int64_t ldd, float* grad_s_dst, cudaStream_t s);
+                                   int64_t ldd, float* grad_s_dst, cudaStream_t s, const float* row_sums = nullptr);
 
 // GAT backward in one TMA gather4 pass (gat_tma.cu): dlogit and grad_s_dst from z, alpha, s_src,
 // s_dst, grad_out and the forward output (t_i = g_i . out_i)
@@ -184,10 +184,14 @@ bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
 size_t gat_fwd_tma_ws_bytes(const pyg_plan* plan, int64_t H, int64_t F);
 pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
-                         void* ws, size_t ws_bytes, cudaStream_t s);
+                         float* row_sums, void* ws, size_t ws_bytes, cudaStream_t s);
 pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* g, int64_t ldg, const float* out, int64_t ldo, const float* alpha,
-                         const float* s_src, const float* s_dst, float slope, float* dlogit, float* gsd, void* ws,
-                         size_t ws_bytes, cudaStream_t s);
+                         const float* row_sums, const float* s_src, const float* s_dst, float slope, float* dlogit,
+                         float* gsd, float* gsc, void* ws, size_t ws_bytes, cudaStream_t s);
+// gsc[r][c] = g[r][c] / row_sums[r][c / C] (grad_out for the factored alpha, packed ld H*C)
+pyg_status_t gat_scale_rows(const float* g, int64_t ldg, int64_t n, int H, int C, const float* row_sums, float* gsc,
+                            cudaStream_t s);
+pyg_status_t fill_const(float* p, int64_t n, float v, cudaStream_t s);
 
 }  // namespace pyg

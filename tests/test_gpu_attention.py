@@ -78,12 +78,34 @@ def test_gat_forward(name, tma, monkeypatch):
     assert torch.equal(out, out2) and torch.equal(alpha, alpha2)
 
 
-@pytest.mark.parametrize("with_out", [False, True])
+@pytest.mark.parametrize("factored", [False, True])
 @pytest.mark.parametrize("tma", ["auto", "1"])
 @pytest.mark.parametrize("name", CASES)
-def test_gat_backward(name, tma, with_out, monkeypatch):
-    """with_out: the forward output is passed, so (H in {4, 8}, tma = "1") the one-pass TMA backward
-    runs (gat_tma.cu: t_i = g_i . out_i); otherwise the two-pass softmax backward."""
+def test_gat_forward_factored(name, tma, factored, monkeypatch):
+    """row_sums given: alpha comes back in factored form, alpha / row_sums[dst] = the oracle's alpha;
+    out is the same either way."""
+    import paper_1903_02428_b200 as pg
+
+    if tma == "1":
+        monkeypatch.setenv("PYG_SEG_TMA", "1")
+    ei, n_src, n_dst, H, C, z, ss, sd, _ = _inputs(name)
+    ref, ralpha, ab = oracle.gat(z, ss, sd, ei, H, n_dst=n_dst, with_abs=True)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n_dst, n_src)
+    rs = torch.full((n_dst, H), float("nan"), device=DEV) if factored else None
+    out, alpha = pg.pyg_gat_propagate(_t(z), _t(ss), _t(sd), H, plan, row_sums=rs)
+    a = alpha / rs[eit[1]] if factored else alpha
+    check_close(a.cpu().numpy(), ralpha, what="alpha")
+    check_close(out.cpu().numpy(), ref, abs_sum=ab, what="out")
+
+
+@pytest.mark.parametrize("mode", ["plain", "out", "factored"])
+@pytest.mark.parametrize("tma", ["auto", "1"])
+@pytest.mark.parametrize("name", CASES)
+def test_gat_backward(name, tma, mode, monkeypatch):
+    """mode "out"/"factored": the forward output is passed, so (H in {4, 8}, tma = "1") the one-pass TMA
+    backward runs (gat_tma.cu: t_i = g_i . out_i); "factored" also keeps alpha in factored form
+    (row_sums) through forward and backward; "plain": the two-pass softmax backward."""
     import paper_1903_02428_b200 as pg
 
     if tma == "1":
@@ -94,8 +116,10 @@ def test_gat_backward(name, tma, with_out, monkeypatch):
     plan = pg.pyg_plan_build(eit[1], eit[0], n_dst, n_src)
     planT = pg.pyg_plan_build(eit[0], eit[1], n_src, n_dst)
     zt, sst, sdt = _t(z), _t(ss), _t(sd)
-    out, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan)
-    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT, out=out if with_out else None)
+    rs = torch.empty((n_dst, H), device=DEV) if mode == "factored" else None
+    out, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan, row_sums=rs)
+    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT, out=out if mode != "plain" else None,
+                              row_sums=rs)
     ref = oracle.gat_backward(z, ss, sd, ei, H, g, n_dst=n_dst, with_abs=True)
     check_close(got["z"].cpu().numpy(), ref["z"], abs_sum=ref["abs_z"], what="grad_z")
     check_close(got["s_src"].cpu().numpy(), ref["s_src"], abs_sum=ref["abs_s_src"], what="grad_s_src")
