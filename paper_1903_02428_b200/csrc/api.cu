@@ -59,6 +59,7 @@ static Knobs read_knobs() {
 static Knobs g_knobs = read_knobs();
 const Knobs& knobs() { return g_knobs; }
 
+
 // PYG_VALIDATE flag: one pinned, mapped int per host thread (so concurrent calls on other threads
 // never consume each other's errors).  validate_begin() clears it before a validating call launches
 // its checking kernels (every earlier use on this thread ended with the synchronising check).

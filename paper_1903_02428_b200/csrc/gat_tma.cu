@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(256, 2) gat_bwd_tma_kernel(const __grid_consta
     };
 
     // ---------------- consumer ----------------
-    int gkey = -1, grow = 0;  // key / root row of the head sums being accumulated
+    int gkey = -1;            // key of the row whose head sums are being accumulated
+    float* gdst = nullptr;    // where they go (grad_s_dst row, or a hub chunk's partial)
     float gs = 0.0f;          // lanes < H: running head sum of dlogit
 
 #pragma unroll 1
@@ -279,29 +280,28 @@ __global__ void __launch_bounds__(256, 2) gat_bwd_tma_kernel(const __grid_consta
             const int e = my_i == 0 ? eids.x : my_i == 1 ? eids.y : my_i == 2 ? eids.z : eids.w;
             a.dlogit[(int64_t)e * H + my_h] = dl;
         }
-        // head sums per row, in position order (lanes < H hold head `lane`)
+        // head sums per row, in position order (lanes < H hold head `lane`): the four slot values first
+        // (shuffles outside any branch), then the rare row changes store through a pointer kept per row
         const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
         const int rr[4] = {rows.x, rows.y, rows.z, rows.w};
+        float vs[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) vs[i] = __shfl_sync(0xffffffffu, dl, i * 8 + my_h);
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float v = __shfl_sync(0xffffffffu, dl, i * 8 + my_h);
-            const bool vi = i < c;
-            const bool nk = vi && kk[i] != gkey;
-            float* dst = gkey < -1 ? a.part + ((int64_t)(-gkey - 2) - a.item_lo) * H
-                                   : a.gsd + ((int64_t)grow - a.row_lo) * H;
-            if (nk && gkey != -1 && lane < H) dst[lane] = gs;
-            gkey = nk ? kk[i] : gkey;
-            grow = nk ? rr[i] : grow;
-            gs = nk ? 0.0f : gs;
-            gs = vi ? gs + v : gs;
+            if (i < c && kk[i] != gkey) {
+                if (gdst && lane < H) gdst[lane] = gs;
+                gkey = kk[i];
+                gdst = kk[i] < -1 ? a.part + ((int64_t)(-kk[i] - 2) - a.item_lo) * H
+                                  : a.gsd + ((int64_t)rr[i] - a.row_lo) * H;
+                gs = 0.0f;
+            }
+            gs = i < c ? gs + vs[i] : gs;
         }
         __syncwarp();  // every lane is done with stage s before it is refilled
         fill(s);
     }
-    if (gkey != -1 && lane < H) {
-        if (gkey < -1) a.part[((int64_t)(-gkey - 2) - a.item_lo) * H + lane] = gs;
-        else a.gsd[((int64_t)grow - a.row_lo) * H + lane] = gs;
-    }
+    if (gdst && lane < H) gdst[lane] = gs;
 }
 
 // t_i[h] = g_i . out_i |_h (0 for rows without in-edges), written into grad_s_dst (the backward

@@ -149,6 +149,10 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
                                 cudaStream_t s) {
     SegArgs a = a0;
     if (a.n_rows <= 0 || a.ncols <= 0) return PYG_OK;
+    // MAX keeps 16-bit argmax positions per segment on the LDG kernel: segments come from plans,
+    // whose rows above kHeavyThreshold are split
+    if ((reduce == PYG_MAX) && (!plan || plan->heavy_threshold > 0xfffe))
+        return fail(PYG_ERR_UNSUPPORTED, "internal: MAX segment-reduce needs a plan with split rows");
     if (plan && plan->row_order) {
         a.row_order = plan->row_order;
         a.order_len = plan->order_len;
@@ -165,7 +169,8 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
     unsigned long long* counter = cv.take<unsigned long long>(1);  // TMA dynamic task counter
     const bool extras = a.row_scale || a.blend || a.col_bias;
     if (extras && reduce != PYG_SUM) return fail(PYG_ERR_UNSUPPORTED, "internal: epilogue extras need SUM");
-    const int red_k = extras ? kRedSumEpi : reduce;  // LDG / combine instantiation
+    // LDG / combine instantiation (weighted max has its own: the plain MAX one skips the multiply)
+    const int red_k = extras ? kRedSumEpi : (reduce == PYG_MAX && a.w) ? kRedMaxW : reduce;
     const bool tma = ws && cv.ok() && tma_eligible(a, plan);
     // hub chunks through the TMA pipeline too (as partial tasks after the light tasks), unless
     // PYG_TMA_HUBS=0 keeps them on the LDG chunk kernel

@@ -74,10 +74,123 @@ __device__ __forceinline__ unsigned group_mask() {
     }
 }
 
+#ifndef PYG_MAX_PACK
+#define PYG_MAX_PACK 1
+#endif
+#ifndef PYG_SEG_PERSIST
+#define PYG_SEG_PERSIST 0
+#endif
+#ifndef PYG_MAX_U
+#define PYG_MAX_U 1
+#endif
+
+// MAX of a wide segment (17-20 floats per lane, e.g. Reddit's 602 columns) with the argmax kept as a
+// 16-bit position inside the segment, two per register (segments are <= 2048 positions: light rows
+// and 512-position hub chunks), so U edges can be in flight per lane at the SUM instantiation's
+// occupancy; the positions become edge ids once, at the end.  With 10 registers freed the plain
+// (unweighted) MAX instantiation also drops the x1 multiply without spilling (Reddit max, 11 passes:
+// 23.8 -> 22.6 ms, gpurun_out/r2u; more edges in flight per lane measured slower: U = 2 at 2 CTAs/SM
+// 27.3 ms, U = 3 37.2 ms).
+template <int V, int NCH, int RED, int LPR>
+__device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
+                                                      float (&acc)[NCH][V], int (&bi)[NCH][V]) {
+    static_assert(V % 2 == 0, "packed positions pair up vector elements");
+    constexpr int U = PYG_MAX_U;
+    const unsigned mask = group_mask<LPR>();
+    const int32_t* __restrict__ gidx = a.gidx;
+    const int32_t* __restrict__ eid = a.eid;
+    const float* __restrict__ w = a.w;
+    uint32_t bp[NCH][V / 2];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+#pragma unroll
+        for (int q = 0; q < V; ++q) acc[ch][q] = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < V / 2; ++q) bp[ch][q] = 0xffffffffu;
+    }
+    const int lane_off = c0 + l * V;
+    bool cv[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) cv[ch] = lane_off + ch * LPR * V < a.ncols;
+    const char* __restrict__ Xl = reinterpret_cast<const char*>(a.X + lane_off);
+    const uint32_t row_bytes = (uint32_t)(a.ldx * 4);
+    float v[U][NCH][V];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int q = 0; q < V; ++q) v[u][ch][q] = 0.0f;
+    auto take = [&](const float (&vv)[NCH][V], float sc, uint32_t pos) {
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int q = 0; q < V; ++q) {
+                const float m = RED == kRedMaxW ? __fmul_rn(sc, vv[ch][q]) : vv[ch][q];
+                if (m > acc[ch][q]) {  // acc starts at -inf (Q5: finite inputs); strict > keeps the lowest id
+                    acc[ch][q] = m;
+                    // one byte permute (PRMT) inserts pos into the element's 16-bit half
+                    bp[ch][q / 2] = __byte_perm(bp[ch][q / 2], pos, (q & 1) ? 0x5410u : 0x3254u);
+                }
+            }
+    };
+    for (int64_t base = beg; base < end; base += LPR) {
+        const int n = (int)min((int64_t)LPR, end - base);
+        int mg = 0;
+        float ms = 1.0f;
+        if (l < n) {
+            const int64_t p = base + l;
+            mg = __ldg(gidx + p);
+            if (RED == kRedMaxW) ms = __ldg(w + (eid ? (int64_t)__ldg(eid + p) : p));
+        }
+        const uint32_t pos0 = (uint32_t)(base - beg);
+        int t = 0;
+        for (; t + U <= n; t += U) {
+            float sv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int g = __shfl_sync(mask, mg, t + u, LPR);
+                sv[u] = RED == kRedMaxW ? __shfl_sync(mask, ms, t + u, LPR) : 1.0f;
+                const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch)
+                    if (cv[ch]) ld<V>(v[u][ch], row + ch * LPR * V);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) take(v[u], sv[u], pos0 + (uint32_t)(t + u));
+        }
+        for (; t < n; ++t) {
+            const int g = __shfl_sync(mask, mg, t, LPR);
+            const float sc = RED == kRedMaxW ? __shfl_sync(mask, ms, t, LPR) : 1.0f;
+            const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
+#pragma unroll
+            for (int ch = 0; ch < NCH; ++ch)
+                if (cv[ch]) ld<V>(v[0][ch], row + ch * LPR * V);
+            take(v[0], sc, pos0 + (uint32_t)t);
+        }
+    }
+    // positions -> edge ids (0xffff: no edge yet)
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+            const uint32_t pos = (bp[ch][q / 2] >> (16 * (q & 1))) & 0xffffu;
+            const int64_t p = beg + (int64_t)pos;
+            bi[ch][q] = pos == 0xffffu ? -1 : (eid ? __ldg(eid + p) : (int)p);
+        }
+}
+
 // Accumulate positions [beg, end) of one segment into registers.
 template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                            float (&acc)[NCH][V], int (&bi)[NCH][V]) {
+    if constexpr (PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 &&
+                  V * NCH <= 20) {
+        // 16-bit positions (0xffff = none): plans split rows above 2,048 positions (segment_reduce_one
+        // refuses MAX without a plan), so a segment is always shorter
+        accumulate_max_packed<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
+        return;
+    }
     // MAX keeps an edge id per element besides the value: for 17-20 floats per lane one edge in flight per
     // lane keeps the kernel at the SUM instantiation's resident CTAs (wider shapes would spill) (Reddit max: 29.8 -> 23.8 ms, gpurun_out/r2e;
     // occupancy beats per-warp memory-level parallelism for this L2-latency-bound gather)
@@ -214,12 +327,18 @@ struct HeavyArgs {
 #ifndef PYG_SEG_MINB
 #define PYG_SEG_MINB 3
 #endif
+#ifndef PYG_MAX_MINB
+#define PYG_MAX_MINB 3
+#endif
 template <int V, int NCH, int RED>
 struct MinBlocks {
-    static constexpr int base = V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1);
+    static constexpr bool packed_max =
+        PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 && V * NCH <= 20;
+    static constexpr int base = packed_max ? PYG_MAX_MINB : (V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1));
     // the head-weighted sum keeps a head index per chunk, narrow MAX an arg id per element: one CTA fewer
     static constexpr int value =
-        ((RED == kRedHeadW || ((RED == PYG_MAX || RED == kRedMaxW) && !(V * NCH > 16 && V * NCH <= 20))) && base > 1)
+        (!packed_max && (RED == kRedHeadW || ((RED == PYG_MAX || RED == kRedMaxW) && !(V * NCH > 16 && V * NCH <= 20))) &&
+         base > 1)
             ? base - 1
             : base;
 };
@@ -315,23 +434,25 @@ template <int V, int NCH, int RED, int LPR>
 __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kernel(SegArgs a, int mode, HeavyArgs h,
                                                                                   int out_vec_ok) {
     constexpr int groups = 256 / LPR;
-    const int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / LPR;
     const int l = threadIdx.x & (LPR - 1);
     const int c0 = blockIdx.y * (LPR * NCH * V);
-
+    // PYG_SEG_PERSIST: a grid of resident CTAs whose groups stride over the rows (no group idles while
+    // the slowest row of its CTA finishes); else one row per group
+    const int64_t gstride = PYG_SEG_PERSIST ? (int64_t)gridDim.x * groups : INT64_MAX;
+    for (int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / LPR;; gid += gstride) {
     int64_t beg, end, row = -1;
     if (mode == 0) {
         if (a.row_order) {
             if (gid >= a.order_len) return;
             row = (int64_t)__ldg(a.row_order + gid) - a.order_offset;
-            if (row < 0 || row >= a.n_rows) return;  // a slice visits only its own rows
+            if (row < 0 || row >= a.n_rows) { if (PYG_SEG_PERSIST) continue; return; }  // a slice visits only its own rows
         } else {
             if (gid >= a.n_rows) return;
             row = gid;
         }
         beg = __ldg(a.rowptr + row);
         end = __ldg(a.rowptr + row + 1);
-        if (end - beg > a.heavy_threshold) return;  // handled by the split path
+        if (end - beg > a.heavy_threshold) { if (PYG_SEG_PERSIST) continue; return; }  // handled by the split path
     } else {
         if (gid >= h.n_items) return;
         const int64_t item = h.item_lo + gid;
@@ -371,6 +492,8 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
                 }
         }
     }
+    if (!PYG_SEG_PERSIST) return;
+    }
 }
 
 template <int V, int NCH, int RED, int LPR>
@@ -379,7 +502,9 @@ inline pyg_status_t launch_one(const SegArgs& a, int tiles, int mode, const Heav
     constexpr int groups = 256 / LPR;
     const int64_t units = mode == 0 ? (a.row_order ? a.order_len : a.n_rows) : h.n_items;
     if (units <= 0) return PYG_OK;
-    dim3 grid((unsigned)cdiv(units, groups), (unsigned)tiles);
+    int64_t blocks = cdiv(units, groups);
+    if (PYG_SEG_PERSIST) blocks = std::min<int64_t>(blocks, 148LL * MinBlocks<V, NCH, RED>::value * PYG_SEG_PERSIST);
+    dim3 grid((unsigned)blocks, (unsigned)tiles);
     seg_kernel<V, NCH, RED, LPR><<<grid, 256, 0, s>>>(a, mode, h, ovk);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
@@ -419,6 +544,7 @@ pyg_status_t launch(const SegArgs& a, int reduce, int nch, int lpr, int tiles, i
         case PYG_MEAN: return launch_red<V, PYG_MEAN>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedHeadW: return launch_red<V, kRedHeadW>(a, nch, lpr, tiles, mode, h, ovk, s);
         case kRedSumEpi: return launch_red<V, kRedSumEpi>(a, nch, lpr, tiles, mode, h, ovk, s);
+        case kRedMaxW: return launch_red<V, kRedMaxW>(a, nch, lpr, tiles, mode, h, ovk, s);
         default: return launch_red<V, PYG_MAX>(a, nch, lpr, tiles, mode, h, ovk, s);
     }
 }

@@ -13,29 +13,33 @@ extern template pyg_status_t launch_nch<kRedSumEpi>(int, int, int64_t, int, int,
 extern template pyg_status_t launch_nch<kRedHeadW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<kRedMaxW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 
-// one warp per empty row: out = 0 (float4 stores when aligned), arg = E
+// empty rows: out = 0 (or the APPNP teleport term / GCN bias), arg = E.  One thread per float4 (or
+// float) of the flattened [empty rows x F] block, so the stores stream instead of waiting on one
+// row index per warp (R-MAT: 5M empty rows, 2.5 GB of zeros)
 __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
                                   int64_t row_hi, int ncols, float* out, int64_t ldo, int64_t* arg, int64_t lda,
                                   int64_t E, int vec_ok, const float* blend, int64_t ldb, float blend_b,
                                   const float* col_bias) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t k = begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < end; k += warps) {
-        const int64_t r = (int64_t)order[k];
+    const int per = vec_ok && !blend && !col_bias ? ncols / 4 : ncols;  // units per row
+    const int64_t total = (end - begin) * per;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+        const int64_t k = t / per;
+        const int u = (int)(t - k * per);
+        const int64_t r = (int64_t)__ldg(order + begin + k);
         if (r < row_lo || r >= row_hi) continue;
         float* o = out + (r - row_lo) * ldo;
-        if (blend || col_bias) {  // APPNP: an empty row keeps only the teleport term; GCN: the bias
-            const float* hb = blend ? blend + (r - row_lo) * ldb : nullptr;
-            for (int c = lane; c < ncols; c += 32)
-                o[c] = (hb ? fmaf(blend_b, hb[c], 0.0f) : 0.0f) + (col_bias ? __ldg(col_bias + c) : 0.0f);
-        } else if (vec_ok) {
-            for (int c = 4 * lane; c < ncols; c += 128) *reinterpret_cast<float4*>(o + c) = make_float4(0, 0, 0, 0);
+        if (per != ncols) {
+            reinterpret_cast<float4*>(o)[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (arg) {
+                int64_t* ap = arg + (r - row_lo) * lda + 4 * u;
+                ap[0] = E; ap[1] = E; ap[2] = E; ap[3] = E;
+            }
         } else {
-            for (int c = lane; c < ncols; c += 32) o[c] = 0.0f;
-        }
-        if (arg) {
-            int64_t* ap = arg + (r - row_lo) * lda;
-            for (int c = lane; c < ncols; c += 32) ap[c] = E;
+            // APPNP: an empty row keeps only the teleport term; GCN: the bias
+            const float* hb = blend ? blend + (r - row_lo) * ldb : nullptr;
+            o[u] = (hb ? fmaf(blend_b, hb[u], 0.0f) : 0.0f) + (col_bias ? __ldg(col_bias + u) : 0.0f);
+            if (arg) arg[(r - row_lo) * lda + u] = E;
         }
     }
 }
@@ -54,6 +58,25 @@ EncodeFn encode_fn() {
 }
 
 }  // namespace tma
+
+// The empty rows of a plan (tail of row_order from empty_begin), after the gather kernel.  (Filling
+// them on a side stream concurrently with the gather measured no gain for R-MAT sum, 10.68 vs
+// 10.71 ms, and a loss for max, 15.5 vs 13.5 ms: the 7.7 GB of value + arg stores compete with the
+// gather for DRAM; gpurun_out/r2x.)
+pyg_status_t fill_empty(const SegArgs& a, int reduce, const pyg_plan* plan, int F, cudaStream_t s) {
+    const int64_t n_empty = plan->n_empty;
+    if (n_empty <= 0) return PYG_OK;
+    const int vec_ok = (F % 4 == 0) && (a.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
+    const int64_t units = n_empty * (int64_t)F;
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(units, 256 * 4), 148 * 8));
+    tma::empty_rows_kernel<<<blocks, 256, 0, s>>>(
+        plan->row_order, plan->empty_begin, plan->empty_begin + n_empty, plan->row_offset,
+        plan->row_offset + plan->n_rows, F, a.out, a.ldo, reduce == PYG_MAX ? a.arg : nullptr, a.lda, a.E_sentinel,
+        vec_ok, a.blend, a.ldb, a.blend_b, reduce == PYG_MAX ? nullptr : a.col_bias);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
 
 // Whether the TMA path applies: unblocked propagate plan with tasks, 16-byte rows, F in [64, 1024].
 bool tma_eligible(const SegArgs& a, const pyg_plan* plan) {
@@ -157,20 +180,7 @@ pyg_status_t segment_tma(const SegArgs& a, int reduce, const pyg_plan* plan, uns
     }
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
-
-    // zero-fill the empty rows of this plan
-    const int64_t n_empty = plan->n_empty;
-    if (n_empty > 0) {
-        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n_empty, 8), 148 * 16));
-        const int vec_ok = (F % 4 == 0) && (a.ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(a.out) & 15) == 0);
-        empty_rows_kernel<<<blocks, 256, 0, s>>>(plan->row_order, plan->empty_begin, plan->empty_begin + n_empty,
-                                                 plan->row_offset, plan->row_offset + plan->n_rows, F, a.out, a.ldo,
-                                                 reduce == PYG_MAX ? a.arg : nullptr, a.lda, a.E_sentinel, vec_ok,
-                                                 a.blend, a.ldb, a.blend_b, reduce == PYG_MAX ? nullptr : a.col_bias);
-        PYG_LAUNCHED();
-        PYG_CUDA(cudaGetLastError());
-    }
-    return PYG_OK;
+    return fill_empty(a, reduce, plan, F, s);  // zero the empty rows of this plan
 }
 
 }  // namespace pyg

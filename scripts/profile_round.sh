@@ -52,18 +52,26 @@ done
 for cfg in reddit rmat pubmed; do
   timeout 600 python bench.py --config $cfg --op gcn --steps 10 > $O/bench_gcn_$cfg.json 2> $O/bench_gcn_$cfg.err
 done
+timeout 600 python bench.py --op gcn --hidden 512 --steps 10 > $O/bench_gcn512.json 2> $O/bench_gcn512.err
+for cfg in rmat reddit pubmed; do
+  timeout 600 python bench.py --config $cfg --op gatlayer --steps 10 > $O/bench_gatlayer_$cfg.json 2> $O/bench_gatlayer_$cfg.err
+done
+timeout 600 python bench.py --reduce max --steps 10 --no-e2e --no-cpu --no-variants > $O/bench_reddit_max.json 2> $O/bench_reddit_max.err
+timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_reddit_max.csv python bench.py --reduce max $Q > /dev/null 2>&1
+timeout 900 $FULL -k regex:seg_kernel -s 12 -c 1 -o $O/full_reddit_max python bench.py --reduce max $Q > /dev/null 2>&1
+export_rep $O/full_reddit_max
+timeout 900 $FULL -k regex:"gat_(bwd|fwd)_tma" -c 2 -o $O/full_gat_rmat python bench.py --config rmat --op gat $Q > /dev/null 2>&1
+export_rep $O/full_gat_rmat
 timeout 600 ncu --metrics $M --clock-control none -k regex:"softmax|seg_|combine|gat_" --csv --log-file $O/launches_gat_rmat.csv python bench.py --config rmat --op gat $Q > /dev/null 2>&1
-timeout 900 $FULL -k regex:gat_bwd_coop -c 1 -o $O/full_gat_bwd_rmat python bench.py --config rmat --op gat $Q > /dev/null 2>&1
-export_rep $O/full_gat_bwd_rmat
 timeout 600 ncu --metrics $M --clock-control none -k regex:"tf32|seg_|combine|deg_rsqrt" --csv --log-file $O/launches_gcn_reddit.csv python bench.py --config reddit --op gcn $Q > /dev/null 2>&1
 timeout 900 $FULL -k regex:tf32 -s 1 -c 1 -o $O/full_tf32_reddit python bench.py --config reddit --op gcn $Q > /dev/null 2>&1
 export_rep $O/full_tf32_reddit
 timeout 600 python scripts/fig3.py --out $O/fig3.json > $O/fig3.log 2>&1
 # memory-safety evidence: compute-sanitizer memcheck / racecheck on representative small tests
 timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_appnp.py tests/test_gpu_transform.py tests/test_gpu_dist.py -q -x \
-  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward or cora or rmat_h4c16 or softmax or power_law or pubmed_shaped or (transform and 300) or gcn_layer or halo_plan" \
+  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward or cora or rmat_h4c16 or softmax or power_law or pubmed_shaped or (transform and 300) or gcn_layer or halo_plan or far_logits or one_pass or (bulk and 602)" \
   > $O/sanitizer_memcheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck.txt
 timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_transform.py -q -x \
-  -k "(tma_pipeline and 128) or split_hub or rmat_h4c16 or (transform and 1000)" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
+  -k "(tma_pipeline and 128) or split_hub or rmat_h4c16 or (transform and 1000) or far_logits or one_pass or (bulk and 602)" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
 
 gzip -f $O/launches_*.csv
