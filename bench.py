@@ -769,9 +769,11 @@ def main():
         gat = dict(H=H, alpha=torch.empty((E, H), device=dev), out=torch.empty((N, F), device=dev))
         # the training step keeps the attention in factored form (alpha = p / row_sums[dst]): the forward's
         # consumer is the backward, which divides where it reads alpha (no E x H normalisation pass)
-        gat["row_sums"] = torch.empty((N, H), device=dev)
-        gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C, True), 1), dtype=torch.uint8,
-                          device=dev)
+        # (large graphs only: the small ones take the two-pass kernels, where alpha comes out normalised and
+        # the factored form would only add the row-sum fill and the grad_out scaling)
+        gat["row_sums"] = torch.empty((N, H), device=dev) if E >= (1 << 22) else None
+        gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C, gat["row_sums"] is not None), 1),
+                          dtype=torch.uint8, device=dev)
         gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 2, "gat"
 
@@ -789,9 +791,12 @@ def main():
         assert world == 1 and a.strategy == "segment", "--op gatlayer: one GPU, segment strategy"
         H = a.heads or 8
         C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, min(F, 256) // H))
-        if plan_full.view()["n_col_blocks"] > 1:
-            plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
-            col_block = 0
+        # the gathered matrix is z [N x H*C]: source blocks sized for ITS rows (an L2-resident pass per
+        # block when z exceeds L2, e.g. Reddit 232,965 x 256 floats = 238 MB)
+        cb_z = pg.pyg_plan_suggest_col_block(E, N, N, H * C * 4) if a.col_block == "auto" else int(a.col_block)
+        if plan_full.view()["col_block"] != cb_z:
+            plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb_z)
+            col_block = cb_z
         gg = torch.Generator(device=dev)
         gg.manual_seed(109)
         Wg = torch.zeros((H * C, ld), device=dev)
@@ -802,7 +807,8 @@ def main():
         gal = torch.empty((E, H), device=dev)
         gatl = dict(H=H, C=C, out=go)
         glw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
-        grs = torch.empty((N, H), device=dev)  # attention in factored form (alpha = p / row_sums[dst])
+        # attention in factored form (alpha = p / row_sums[dst]) on the large graphs (see --op gat)
+        grs = torch.empty((N, H), device=dev) if E >= (1 << 22) else None
         passes, red = 1, "gatlayer"
 
         def compute():

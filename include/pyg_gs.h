@@ -199,14 +199,25 @@ pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx
  *     send_ptr[q+1]) of x [n_x x F] (stride ldx) are stored to rows dst_row[q] + i of dst[q]
  *     (stride ldd).  send_ptr [n_peers + 1], dst [n_peers] (device pointers, e.g. from
  *     pyg_ipc_open) and dst_row [n_peers] are HOST arrays; send_rows is a device array.
- *     Asynchronous; the caller orders the peers' reads after the pushes (stream sync + a
- *     process-group barrier). */
+ *     Asynchronous; the caller orders the peers' reads after the pushes (pyg_peer_signal /
+ *     pyg_peer_wait below, or a stream sync + a process-group barrier). */
 pyg_status_t pyg_ipc_handle(const void* dev_ptr, void* handle, int64_t* offset);
 pyg_status_t pyg_ipc_open(const void* handle, int64_t offset, void** dev_ptr);
 pyg_status_t pyg_ipc_close(void* dev_ptr, int64_t offset);
 pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* send_rows,
                            const int64_t* send_ptr, void* const* dst, const int64_t* dst_row,
                            int64_t ldd, int n_peers, void* stream);
+/* Device-side step flags between the ranks of a node (replace the host stream-sync + process-group
+ * barrier around a peer-store exchange; P:26 multi-GPU, north_star (3)).  flags: HOST array of n
+ * (<= 16) device addresses of uint32 flags (a peer's, mapped with pyg_ipc_open, or local).
+ *   pyg_peer_signal: enqueue on `stream`: make every earlier write of the stream visible system-wide
+ *     (the peer stores of pyg_halo_push), then release-store `value` into each flag.
+ *   pyg_peer_wait: enqueue on `stream`: spin until each flag reaches `value` (acquire; wrap-safe
+ *     uint32 comparison), so later work on the stream sees the writes made before the matching
+ *     signal.  Deadlock-free use: every rank signals what it owes before it waits (dist.HaloPush).
+ * Asynchronous. */
+pyg_status_t pyg_peer_signal(uint32_t* const* flags, int n, uint32_t value, void* stream);
+pyg_status_t pyg_peer_wait(uint32_t* const* flags, int n, uint32_t value, void* stream);
 
 /* Scratch needed by pyg_scatter / pyg_propagate / pyg_propagate_backward for
  * an output of n_out rows x F_out columns over E edges.

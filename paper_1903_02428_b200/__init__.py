@@ -23,7 +23,7 @@ __all__ = [
     "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
-    "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_gat_propagate_workspace_size", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
+    "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_gat_propagate_workspace_size", "pyg_peer_signal", "pyg_peer_wait", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
     "FORCE_SEGMENT", "version", "DistComm", "DistPlan", "pyg_dist_unique_id", "pyg_dist_init", "pyg_dist_plan_build",
     "pyg_dist_propagate", "pyg_dist_propagate_backward",
 ]
@@ -533,6 +533,22 @@ def pyg_halo_push(x: torch.Tensor, send_rows: torch.Tensor, send_ptr, dst_ptrs, 
     dr = (ctypes.c_int64 * max(n, 1))(*dst_rows)
     check(lib.pyg_halo_push(_ptr(x), n_x, F, ldx, _ptr(send_rows) if send_rows.numel() else None, sp, dp, dr, ldd, n,
                             _stream(x.device)), "pyg_halo_push")
+
+
+def _flag_array(ptrs):
+    return (ctypes.c_void_p * max(len(ptrs), 1))(*[ctypes.c_void_p(p) for p in ptrs])
+
+
+def pyg_peer_signal(flag_ptrs, value: int, device=None):
+    """Release-store value into each device flag (after every earlier write of the stream)."""
+    check(lib.pyg_peer_signal(_flag_array(flag_ptrs), len(flag_ptrs), value & 0xFFFFFFFF, _stream(device)),
+          "pyg_peer_signal")
+
+
+def pyg_peer_wait(flag_ptrs, value: int, device=None):
+    """Make the stream wait until each device flag reaches value."""
+    check(lib.pyg_peer_wait(_flag_array(flag_ptrs), len(flag_ptrs), value & 0xFFFFFFFF, _stream(device)),
+          "pyg_peer_wait")
 
 
 def pyg_gat_transform(x: torch.Tensor, weight: torch.Tensor, att_src: torch.Tensor, att_dst: torch.Tensor, H: int):

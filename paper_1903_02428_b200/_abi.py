@@ -102,6 +102,8 @@ SIGNATURES = {
     "pyg_segment_softmax": ([P, I64, I64, I64, P, I64, P, P, I64, P], C),
     "pyg_segment_softmax_backward": ([P, I64, P, I64, I64, I64, I64, P, P, I64, P], C),
     "pyg_gat_propagate": ([P, I64, I64, I64, I64, P, P, I64, I64, ctypes.c_float, P, P, I64, P, P, P, SZ, P], C),
+    "pyg_peer_signal": ([P, C, U32, P], C),
+    "pyg_peer_wait": ([P, C, U32, P], C),
     "pyg_gat_backward_workspace_size": ([P, P, I64, I64, C, ctypes.POINTER(SZ)], C),
     "pyg_gat_propagate_workspace_size": ([P, I64, I64, ctypes.POINTER(SZ)], C),
     "pyg_gat_backward": ([P, I64, I64, I64, I64, P, P, I64, I64, ctypes.c_float, P, P, P, I64, P, I64, P, P, P, I64, P,

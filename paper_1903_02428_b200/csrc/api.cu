@@ -52,6 +52,7 @@ static Knobs read_knobs() {
     k.gat_warp_kb = get("PYG_GAT_WARP_KB", 10);
     k.gat_sm_kb = get("PYG_GAT_SM_KB", 160);
     k.gat_fused = get("PYG_GAT_FUSED", 1);
+    k.gat_warps = get("PYG_GAT_WARPS", 8);
     k.gat_fwd_warp_kb = get("PYG_GAT_FWD_WARP_KB", 5);
     k.gat_fwd_sm_kb = get("PYG_GAT_FWD_SM_KB", 160);
     return k;
@@ -297,6 +298,18 @@ pyg_status_t pyg_halo_push(const float* x, int64_t n_x, int64_t F, int64_t ldx, 
     REQUIRE(n_peers == 0 || send_ptr[n_peers] == 0 || (x && send_rows), PYG_ERR_INVALID_ARGUMENT,
             "halo_push: null x / send_rows");
     return halo_push_impl(x, ldx, F, send_rows, send_ptr, dst, dst_row, ldd, n_peers, as_stream(stream));
+}
+
+pyg_status_t pyg_peer_signal(uint32_t* const* flags, int n, uint32_t value, void* stream) {
+    REQUIRE(n >= 0 && (n == 0 || flags), PYG_ERR_INVALID_ARGUMENT, "peer_signal: bad flags");
+    for (int i = 0; i < n; ++i) REQUIRE(flags[i], PYG_ERR_INVALID_ARGUMENT, "peer_signal: null flag %d", i);
+    return peer_flags_impl(flags, n, value, 0, as_stream(stream));
+}
+
+pyg_status_t pyg_peer_wait(uint32_t* const* flags, int n, uint32_t value, void* stream) {
+    REQUIRE(n >= 0 && (n == 0 || flags), PYG_ERR_INVALID_ARGUMENT, "peer_wait: bad flags");
+    for (int i = 0; i < n; ++i) REQUIRE(flags[i], PYG_ERR_INVALID_ARGUMENT, "peer_wait: null flag %d", i);
+    return peer_flags_impl(flags, n, value, 1, as_stream(stream));
 }
 
 pyg_status_t pyg_gather_rows(const float* x, int64_t n_x, int64_t F, int64_t ldx, const int64_t* rows, int64_t n,
@@ -654,7 +667,8 @@ static pyg_status_t headw_sum(const pyg_plan* p, const float* X, int64_t ldx, in
 
 pyg_status_t pyg_gat_propagate_workspace_size(const pyg_plan_t* plan, int64_t H, int64_t C, size_t* bytes) {
     REQUIRE(bytes && plan && H > 0 && C >= 0, PYG_ERR_INVALID_ARGUMENT, "gat_propagate_workspace_size: bad args");
-    *bytes = std::max(gat_fwd_tma_ws_bytes(plan, H, H * C), segment_ws_bytes(plan, H * C, PYG_SUM));
+    *bytes = plan->parts.empty() ? std::max(gat_fwd_tma_ws_bytes(plan, H, H * C), segment_ws_bytes(plan, H * C, PYG_SUM))
+                                 : gat_fwd_blocked_ws_bytes(plan, H);
     return PYG_OK;
 }
 
@@ -667,12 +681,18 @@ pyg_status_t pyg_gat_propagate(const float* z, int64_t n_src, int64_t H, int64_t
     const int64_t F = H * C;
     REQUIRE(ldz >= F && ldo >= F, PYG_ERR_DIMENSION, "gat_propagate: leading dimension < H*C");
     REQUIRE(F <= 16384 && H <= kAttnMaxHeads, PYG_ERR_UNSUPPORTED, "gat_propagate: H <= %d", kAttnMaxHeads);
-    REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() &&
-                plan->n_cols <= n_src && plan->E == E,
-            PYG_ERR_DIMENSION, "gat_propagate: needs an unblocked forward plan over n_dst rows and E edges");
+    REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->n_cols <= n_src && plan->E == E,
+            PYG_ERR_DIMENSION, "gat_propagate: needs a forward plan over n_dst rows and E edges");
     REQUIRE(n_dst * F == 0 || out, PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null out");
     REQUIRE(E == 0 || (z && s_src && s_dst && alpha), PYG_ERR_INVALID_ARGUMENT, "gat_propagate: null input");
     cudaStream_t s = as_stream(stream);
+    if (!plan->parts.empty()) {  // source-blocked plan: one L2-resident pass per block of z rows
+        REQUIRE(plan->n_passes == 0 || plan->n_passes == (int64_t)plan->parts.size(), PYG_ERR_UNSUPPORTED,
+                "gat_propagate: needs the whole source-blocked plan, not a pass view");
+        if (n_dst == 0 || F == 0) return PYG_OK;
+        return gat_fwd_blocked(plan, (int)H, (int)C, (int)F, z, n_src, ldz, s_src, s_dst, negative_slope, out, ldo,
+                               alpha, row_sums, ws, ws_bytes, s);
+    }
     if (E > 0 && n_dst > 0 && gat_fwd_tma_eligible(plan, (int)H, (int)C, (int)F, z, ldz, out, ldo, alpha, s_src, s_dst))
         // softmax with a per-row shift bounded from the global max of s_src + the weighted sum, one pass
         return gat_fwd_tma(plan, (int)H, (int)C, (int)F, z, n_src, ldz, s_src, s_dst, negative_slope, out, ldo, alpha,

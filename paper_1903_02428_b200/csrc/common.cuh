@@ -61,6 +61,7 @@ struct Knobs {
     int bulk_warp_kb = 8; // PYG_BULK_WARP_KB: ring bytes per warp of the bulk-copy kernel
     int gat_warp_kb = 10; // PYG_GAT_WARP_KB: ring bytes per warp of the one-pass GAT backward
     int gat_sm_kb = 160;  // PYG_GAT_SM_KB: its shared memory per SM (the rest stays L1)
+    int gat_warps = 8;    // PYG_GAT_WARPS: warps per CTA of the GAT TMA kernels (8, 4 or 2)
     int gat_fused = 1;    // PYG_GAT_FUSED: 0 keeps the GAT forward on softmax + aggregation (two kernels)
     int gat_fwd_warp_kb = 5;   // PYG_GAT_FWD_WARP_KB: ring bytes per warp of the one-pass GAT forward
     int gat_fwd_sm_kb = 160;   // PYG_GAT_FWD_SM_KB

@@ -64,6 +64,8 @@ __device__ __forceinline__ void lds32f_if(bool p, float& v, uint32_t addr) {
                  : "r"(addr), "r"((unsigned)p));
 }
 
+__device__ __forceinline__ int sel4(const int4& v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
 constexpr int kMeta = 64;  // per stage: int keys[4] | int rows[4] | int eids[4] | int cols[4]
 
 struct BwdArgs {
@@ -601,17 +603,20 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
             return;
         }
         const int64_t r = (int64_t)agrow - a.row_lo;
+        bool tiny = false;
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
             if (cval[ch]) {
                 const float sh = ssum[ch];
+                const float inv = 1.0f / sh;  // one IEEE division per chunk (a division per element spilled
+                                              // the registers around its slow-path calls)
                 *reinterpret_cast<float4*>(a.out + r * a.ldo + 4 * (lane + 32 * ch)) =
-                    make_float4(acc[ch][0] / sh, acc[ch][1] / sh, acc[ch][2] / sh, acc[ch][3] / sh);
-                if (leader) {
-                    a.rs[r * H + hch[ch]] = sh;
-                    if (!(sh >= kTinySum)) a.bad[1 + atomicAdd(a.bad, 1)] = (int)r;  // rare; may repeat a row
-                }
+                    make_float4(acc[ch][0] * inv, acc[ch][1] * inv, acc[ch][2] * inv, acc[ch][3] * inv);
+                if (leader) a.rs[r * H + hch[ch]] = sh;
+                tiny |= !(sh >= kTinySum);
             }
+        // a row whose sum underflowed in any head is listed once (flush runs warp-uniformly)
+        if (__ballot_sync(0xffffffffu, tiny) && lane == 0) a.bad[1 + atomicAdd(a.bad, 1)] = (int)r;
     };
 
 #pragma unroll 1
@@ -630,7 +635,6 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         phase ^= 1u << s;
         const uint32_t st = data0 + (uint32_t)s * stage_bytes;
         const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
-        const int rr[4] = {rows.x, rows.y, rows.z, rows.w};
         // (1) s_dst of each slot's row for the (slot, head) lanes (branch-free)
         float sme = 0.0f;
 #pragma unroll
@@ -654,14 +658,16 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         if (mine) a.alpha[(int64_t)e * H + my_h] = p;
         sts32f(scr + 4u * (uint32_t)lane, p);
         __syncwarp();
-        // (3) aggregation in position order
+        // (3) aggregation in position order (unrolled: a rolled loop with one flush path measured slower,
+        // 22.8 vs 21.4 ms on R-MAT, gpurun_out/r2y)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const bool vi = i < c;
-            if (vi && kk[i] != arow) {
+            if (i >= c) break;
+            const int ki = kk[i];
+            if (ki != arow) {
                 if (arow != -1) flush();
-                arow = kk[i];
-                agrow = rr[i];
+                arow = ki;
+                agrow = sel4(rows, i);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) {
                     ssum[ch] = 0.0f;
@@ -671,10 +677,9 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
             }
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
-                float w = 0.0f;
+                const float w = lds32f(scr + 4u * (uint32_t)(i * 8 + hch[ch]));
                 float4 zv = make_float4(0.f, 0.f, 0.f, 0.f);
-                lds32f_if(vi, w, scr + 4u * (uint32_t)(i * 8 + hch[ch]));
-                lds128f_if(vi && cval[ch], zv, st + coff[ch] + (uint32_t)i * row_bytes);
+                lds128f_if(cval[ch], zv, st + coff[ch] + (uint32_t)i * row_bytes);
                 acc[ch][0] = fmaf(w, zv.x, acc[ch][0]);
                 acc[ch][1] = fmaf(w, zv.y, acc[ch][1]);
                 acc[ch][2] = fmaf(w, zv.z, acc[ch][2]);
@@ -905,7 +910,7 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     a.data_off = (int)align_up((size_t)(128 + S * kMeta), 128);
     a.warp_bytes = (int)align_up((size_t)(a.data_off + S * a.stage_bytes), 128);
     // 8 warps per CTA while two CTAs still fit an SM (F = 128: 8 x 9.9 KB); wide rows take fewer
-    int warps = 8;
+    int warps = knobs().gat_warps == 4 || knobs().gat_warps == 2 ? knobs().gat_warps : 8;
     while (warps > 1 && warps * a.warp_bytes > 112 * 1024) warps >>= 1;
     const int smem = warps * a.warp_bytes;
     if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_backward: stage ring does not fit shared memory");
@@ -1066,7 +1071,7 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     const int S = std::max(2, std::min(3, (knobs().gat_fwd_warp_kb * 1024) / a.stage_bytes));
     a.data_off = (int)align_up((size_t)(128 + S * kMeta + 128), 128);
     a.warp_bytes = (int)align_up((size_t)(a.data_off + S * a.stage_bytes), 128);
-    int warps = 8;
+    int warps = knobs().gat_warps == 4 || knobs().gat_warps == 2 ? knobs().gat_warps : 8;
     while (warps > 1 && warps * a.warp_bytes > 112 * 1024) warps >>= 1;
     const int smem = warps * a.warp_bytes;
     if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_propagate: stage ring does not fit shared memory");
@@ -1105,6 +1110,280 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     }
     gat_fwd_fix_kernel<<<148, 256, 0, s>>>(bad, plan->rowptr, plan->col, a.eid, z, ldz, s_src, s_dst, H, C, F, slope,
                                            alpha, out, ldo, row_sums);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
+
+// ============================================================================================
+// Forward on a SOURCE-BLOCKED plan (one pass per L2-resident block of z rows, like the segment-reduce
+// passes): the fixed per-row shift of the one-pass forward (reading A9) makes the softmax additive
+// across passes -- each pass adds sum p z_j into out and sum p into the row sums; the last pass
+// divides.  A warp per row of the pass, the lanes over float4 column chunks; every lane forms the
+// weight of its chunk's head (s_src[j] load, exp) per position.
+// ============================================================================================
+namespace gat {
+
+struct BlockArgs {
+    const int64_t* rowptr;  // this pass's virtual rows (n + 1)
+    int64_t n;
+    const int32_t* col;
+    const int32_t* eid;
+    const float* z;
+    int64_t ldz;
+    const float* s_src;
+    const float* s_dst;
+    const unsigned* smax;
+    const int32_t* deg;     // total in-degree per row (blocked plans)
+    float* out;
+    int64_t ldo;
+    float* rs;              // [n x H] running row sums
+    float* alpha;           // [E x H]: p by edge id
+    int* bad;
+    int H, C, F;
+    float slope;
+    int accum, finalize;
+};
+
+// A warp per row of the pass; positions in groups of 4: lane (i, h) = (lane / 8, lane % 8) forms the
+// weight of position i, head h (one s_src load and one exp per lane per group), the column lanes
+// gather the 4 z_j rows (loads in flight together) and take each weight by a shuffle.
+template <int NCH>
+__global__ void __launch_bounds__(256) gat_fwd_block_kernel(BlockArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int my_i = lane >> 3, my_h = lane & 7;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int H = a.H;
+    const bool hv = my_h < H;
+    int hch[NCH];
+    bool cval[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int c = 4 * (lane + 32 * ch);
+        cval[ch] = c < a.F;
+        hch[ch] = cval[ch] ? c / a.C : 0;
+    }
+    const float smax_h = hv ? ord2f(__ldg(a.smax + my_h)) : 0.0f;
+    for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < a.n; r += nw) {
+        const int64_t beg = a.rowptr[r], end = a.rowptr[r + 1];
+        // this lane's head: s_dst and the row's shift (>= every logit of the row, reading A9)
+        const float sd = hv ? __ldg(a.s_dst + r * H + my_h) : 0.0f;
+        const float cpre = smax_h + sd;
+        const float cs = cpre > 0.0f ? cpre : a.slope * cpre;
+        float ps = 0.0f, acc[NCH][4];
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[ch][q] = 0.0f;
+        for (int64_t base = beg; base < end; base += 32) {
+            const int cnt = (int)min((int64_t)32, end - base);
+            int jl = 0, el = 0;
+            if (lane < cnt) {
+                jl = __ldg(a.col + base + lane);
+                el = a.eid ? __ldg(a.eid + base + lane) : (int)(base + lane);
+            }
+            for (int t0 = 0; t0 < cnt; t0 += 4) {
+                int js[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) js[u] = __shfl_sync(0xffffffffu, jl, (t0 + u) & 31);
+                float4 zv[4][NCH];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch)
+                        zv[u][ch] = (cval[ch] && t0 + u < cnt)
+                                        ? __ldg(reinterpret_cast<const float4*>(a.z + (int64_t)js[u] * a.ldz) + lane + 32 * ch)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                // weight of (position t0 + my_i, head my_h)
+                const int jm = __shfl_sync(0xffffffffu, jl, (t0 + my_i) & 31);
+                const int em = __shfl_sync(0xffffffffu, el, (t0 + my_i) & 31);
+                float p = 0.0f;
+                if (hv && t0 + my_i < cnt) {
+                    const float pre = __ldg(a.s_src + (int64_t)jm * H + my_h) + sd;
+                    const float l = pre > 0.0f ? pre : a.slope * pre;
+                    p = expf(l - cs);
+                    a.alpha[(int64_t)em * H + my_h] = p;
+                }
+                ps += p;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) {
+                        const float w = __shfl_sync(0xffffffffu, p, u * 8 + hch[ch]);
+                        acc[ch][0] = fmaf(w, zv[u][ch].x, acc[ch][0]);
+                        acc[ch][1] = fmaf(w, zv[u][ch].y, acc[ch][1]);
+                        acc[ch][2] = fmaf(w, zv[u][ch].z, acc[ch][2]);
+                        acc[ch][3] = fmaf(w, zv[u][ch].w, acc[ch][3]);
+                    }
+            }
+        }
+        // the row's per-head sum over its position groups (lanes h, h + 8, h + 16, h + 24)
+        ps += __shfl_xor_sync(0xffffffffu, ps, 8);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 16);
+        float tot = ps;
+        if (a.accum && hv && lane < 8) tot += a.rs[r * H + my_h];
+        if (hv && lane < 8) a.rs[r * H + my_h] = tot;
+        // a row whose sum underflowed in any head is listed once (the list holds at most n rows)
+        const bool tiny = a.finalize && hv && lane < 8 && !(tot >= kTinySum) && __ldg(a.deg + r) > 0;
+        if (__ballot_sync(0xffffffffu, tiny) && lane == 0) a.bad[1 + atomicAdd(a.bad, 1)] = (int)r;
+        // epilogue: add the earlier passes, divide in the last
+#pragma unroll
+        for (int ch = 0; ch < NCH; ++ch) {
+            const float th = __shfl_sync(0xffffffffu, tot, hch[ch]);
+            if (!cval[ch]) continue;
+            float4* o = reinterpret_cast<float4*>(a.out + r * a.ldo) + lane + 32 * ch;
+            if (a.accum) {
+                const float4 prev = *o;
+                acc[ch][0] += prev.x; acc[ch][1] += prev.y; acc[ch][2] += prev.z; acc[ch][3] += prev.w;
+            }
+            if (a.finalize) {
+                const float inv = th > 0.0f ? 1.0f / th : 0.0f;
+                *o = make_float4(acc[ch][0] * inv, acc[ch][1] * inv, acc[ch][2] * inv, acc[ch][3] * inv);
+            } else {
+                *o = make_float4(acc[ch][0], acc[ch][1], acc[ch][2], acc[ch][3]);
+            }
+        }
+    }
+}
+
+// alpha[k] /= rs[row] over one pass's rows (non-factored calls on blocked plans): warp per row
+__global__ void gat_alpha_norm_rows_kernel(const int64_t* __restrict__ rowptr, int64_t n, const int32_t* __restrict__ eid,
+                                           int H, const float* __restrict__ rs, float* alpha) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = (((int64_t)blockIdx.x * blockDim.x) >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const int64_t beg = rowptr[r], end = rowptr[r + 1];
+        for (int64_t u = beg * H + lane; u < end * H; u += 32) {
+            const int64_t p = u / H;
+            const int h = (int)(u - p * H);
+            const int64_t k = eid ? (int64_t)eid[p] : p;
+            alpha[k * H + h] = alpha[k * H + h] / rs[r * H + h];
+        }
+    }
+}
+
+constexpr int kMaxParts = 64;
+struct PartPtrs {
+    const int64_t* rp[kMaxParts];
+    int n;
+};
+
+// the listed rows of a blocked plan, exactly (as gat_fwd_fix_kernel, positions spread over the passes)
+__global__ void gat_fwd_fix_blocked_kernel(const int* __restrict__ bad, PartPtrs parts, const int32_t* __restrict__ col,
+                                           const int32_t* __restrict__ eid, const float* __restrict__ z, int64_t ldz,
+                                           const float* __restrict__ s_src, const float* __restrict__ s_dst, int H,
+                                           int C, int F, float slope, float* alpha, float* out, int64_t ldo,
+                                           float* row_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const int count = bad[0];
+    for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < count; w += warps) {
+        const int64_t r = bad[1 + w];
+        for (int h = 0; h < H; ++h) {
+            const float sd = s_dst[r * H + h];
+            float m = -INFINITY, sum = 0.0f;
+            for (int b = 0; b < parts.n; ++b)
+                for (int64_t p = parts.rp[b][r] + lane; p < parts.rp[b][r + 1]; p += 32) {
+                    const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                    m = fmaxf(m, pre > 0.0f ? pre : slope * pre);
+                }
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            for (int b = 0; b < parts.n; ++b)
+                for (int64_t p = parts.rp[b][r] + lane; p < parts.rp[b][r + 1]; p += 32) {
+                    const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                    sum += expf((pre > 0.0f ? pre : slope * pre) - m);
+                }
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            for (int b = 0; b < parts.n; ++b)
+                for (int64_t p = parts.rp[b][r] + lane; p < parts.rp[b][r + 1]; p += 32) {
+                    const float pre = s_src[(int64_t)col[p] * H + h] + sd;
+                    const int64_t k = eid ? (int64_t)eid[p] : p;
+                    alpha[k * H + h] = expf((pre > 0.0f ? pre : slope * pre) - m) / sum;
+                }
+            if (row_sums && lane == 0) row_sums[r * H + h] = 1.0f;
+        }
+        __syncwarp();
+        for (int c = lane; c < F; c += 32) {
+            float acc = 0.0f;
+            for (int b = 0; b < parts.n; ++b)
+                for (int64_t p = parts.rp[b][r]; p < parts.rp[b][r + 1]; ++p) {
+                    const int64_t k = eid ? (int64_t)eid[p] : p;
+                    acc = fmaf(alpha[k * H + c / C], z[(int64_t)col[p] * ldz + c], acc);
+                }
+            out[r * ldo + c] = acc;
+        }
+    }
+}
+
+}  // namespace gat
+
+size_t gat_fwd_blocked_ws_bytes(const pyg_plan* plan, int64_t H) {
+    if (!plan) return 0;
+    return 256 + 256 + align_up((size_t)plan->n_rows * H * 4, 256) + align_up(((size_t)plan->n_rows + 1) * 4, 256);
+}
+
+pyg_status_t gat_fwd_blocked(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
+                             const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
+                             float* row_sums, void* ws, size_t ws_bytes, cudaStream_t s) {
+    using namespace gat;
+    const int64_t n = plan->n_rows;
+    const size_t np = plan->parts.size();
+    if (np > (size_t)kMaxParts) return fail(PYG_ERR_UNSUPPORTED, "gat_propagate: at most %d source blocks", kMaxParts);
+    if (F % 4 || F > 1024 || (reinterpret_cast<uintptr_t>(z) & 15) || ldz % 4 || (reinterpret_cast<uintptr_t>(out) & 15) ||
+        ldo % 4 || !plan->deg)
+        return fail(PYG_ERR_UNSUPPORTED, "gat_propagate on a source-blocked plan: H*C %% 4 == 0, <= 1024, 16-byte rows");
+    Carver cv(ws, ws_bytes);
+    cv.take<unsigned long long>(1);
+    unsigned* smax = cv.take<unsigned>(8);
+    float* rs = cv.take<float>((size_t)n * H);
+    int* bad = cv.take<int>((size_t)n + 1);
+    if (!ws || !cv.ok()) return fail(PYG_ERR_NO_MEMORY, "gat_propagate: workspace too small (pyg_gat_propagate_workspace_size)");
+    if (row_sums) rs = row_sums;
+    PYG_CUDA(cudaMemsetAsync(smax, 0, 8 * sizeof(unsigned), s));
+    PYG_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    {
+        const int64_t total = n_src * H;
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(total, 256), 148 * 4));
+        gat_smax_kernel<<<blocks, 256, 0, s>>>(s_src, total, H, smax);
+        PYG_LAUNCHED();
+    }
+    BlockArgs a;
+    a.n = n;
+    a.col = plan->col;
+    a.eid = plan->perm_identity ? nullptr : plan->perm;
+    a.z = z; a.ldz = ldz; a.s_src = s_src; a.s_dst = s_dst; a.smax = smax; a.deg = plan->deg;
+    a.out = out; a.ldo = ldo; a.rs = rs; a.alpha = alpha; a.bad = bad;
+    a.H = H; a.C = C; a.F = F; a.slope = slope;
+    const int nch = (int)cdiv(F, 128);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(n, 8), 148 * 8));
+    const int64_t total_passes = plan->n_passes > 0 ? plan->n_passes : (int64_t)np;
+    for (size_t b = 0; b < np; ++b) {
+        const int64_t gb = plan->pass_base + (int64_t)b;
+        a.rowptr = plan->parts[b].rowptr;
+        a.accum = gb > 0;
+        a.finalize = gb + 1 == total_passes;
+        switch (nch) {
+            case 1: gat_fwd_block_kernel<1><<<blocks, 256, 0, s>>>(a); break;
+            case 2: gat_fwd_block_kernel<2><<<blocks, 256, 0, s>>>(a); break;
+            case 3: gat_fwd_block_kernel<3><<<blocks, 256, 0, s>>>(a); break;
+            case 4: gat_fwd_block_kernel<4><<<blocks, 256, 0, s>>>(a); break;
+            case 5: case 6: gat_fwd_block_kernel<6><<<blocks, 256, 0, s>>>(a); break;
+            default: gat_fwd_block_kernel<8><<<blocks, 256, 0, s>>>(a); break;
+        }
+        PYG_LAUNCHED();
+        PYG_CUDA(cudaGetLastError());
+    }
+    if (!row_sums)
+        for (size_t b = 0; b < np; ++b) {
+            gat_alpha_norm_rows_kernel<<<blocks, 256, 0, s>>>(plan->parts[b].rowptr, n, a.eid, H, rs, alpha);
+            PYG_LAUNCHED();
+        }
+    PartPtrs pp;
+    pp.n = (int)np;
+    for (size_t b = 0; b < np; ++b) pp.rp[b] = plan->parts[b].rowptr;
+    gat_fwd_fix_blocked_kernel<<<148, 256, 0, s>>>(bad, pp, plan->col, a.eid, z, ldz, s_src, s_dst, H, C, F, slope,
+                                                   alpha, out, ldo, row_sums);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;

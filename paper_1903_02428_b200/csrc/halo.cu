@@ -246,12 +246,60 @@ pyg_status_t halo_push_impl(const float* x, int64_t ldx, int64_t F, const int64_
     return PYG_OK;
 }
 
+namespace {
+struct FlagArgs {
+    uint32_t* f[kMaxPeers];
+    int n;
+    uint32_t value;
+};
+// every earlier write of this stream (the push kernel's peer stores) is made visible system-wide,
+// then each flag (a peer's, mapped over NVLink, or local) is released with `value`
+__global__ void peer_signal_kernel(FlagArgs a) {
+    const int i = threadIdx.x;
+    if (i >= a.n) return;
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.f[i]), "r"(a.value) : "memory");
+}
+// spin (with backoff) until every flag reaches `value` (wrap-safe comparison), acquire semantics
+__global__ void peer_wait_kernel(FlagArgs a) {
+    const int i = threadIdx.x;
+    if (i < a.n) {
+        uint32_t v = 0;
+        unsigned ns = 32;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a.f[i]) : "memory");
+            if ((int32_t)(v - a.value) >= 0) break;
+            __nanosleep(ns);
+            if (ns < 4096) ns <<= 1;
+        }
+    }
+    __syncwarp();
+}
+}  // namespace
+
+pyg_status_t peer_flags_impl(uint32_t* const* flags, int n, uint32_t value, int wait, cudaStream_t s) {
+    if (n <= 0) return PYG_OK;
+    if (n > kMaxPeers) return fail(PYG_ERR_UNSUPPORTED, "peer flags: at most %d", kMaxPeers);
+    FlagArgs a;
+    for (int i = 0; i < n; ++i) a.f[i] = flags[i];
+    a.n = n;
+    a.value = value;
+    if (wait) peer_wait_kernel<<<1, 32, 0, s>>>(a);
+    else peer_signal_kernel<<<1, 32, 0, s>>>(a);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
 }  // namespace pyg
 
 // ---- CUDA IPC for the peer-store halo ---------------------------------------------------------
 #include <cuda.h>
 
+#include <cstring>
+#include <map>
 #include <mutex>
+#include <string>
 
 namespace pyg {
 
@@ -285,17 +333,51 @@ pyg_status_t ipc_handle_impl(const void* ptr, void* handle, int64_t* offset) {
     return PYG_OK;
 }
 
+// A peer allocation can hold several of its buffers (torch's caching allocator packs tensors into
+// one cudaMalloc segment) while CUDA maps an IPC handle once per context: mappings are shared and
+// reference-counted per allocation.
+namespace {
+struct IpcMap {
+    std::mutex mu;
+    std::map<std::string, std::pair<void*, int>> by_handle;  // handle bytes -> (base, refs)
+    std::map<void*, std::string> by_base;
+};
+IpcMap& ipc_map() {
+    static IpcMap m;
+    return m;
+}
+}  // namespace
+
 pyg_status_t ipc_open_impl(const void* handle, int64_t offset, void** ptr) {
-    cudaIpcMemHandle_t h;
-    memcpy(&h, handle, 64);
-    void* base = nullptr;
-    PYG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-    *ptr = static_cast<char*>(base) + offset;
+    IpcMap& m = ipc_map();
+    std::lock_guard<std::mutex> g(m.mu);
+    const std::string key(static_cast<const char*>(handle), 64);
+    auto it = m.by_handle.find(key);
+    if (it == m.by_handle.end()) {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, handle, 64);
+        void* base = nullptr;
+        PYG_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        it = m.by_handle.emplace(key, std::make_pair(base, 0)).first;
+        m.by_base[base] = key;
+    }
+    it->second.second += 1;
+    *ptr = static_cast<char*>(it->second.first) + offset;
     return PYG_OK;
 }
 
 pyg_status_t ipc_close_impl(void* ptr, int64_t offset) {
-    PYG_CUDA(cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset));
+    IpcMap& m = ipc_map();
+    std::lock_guard<std::mutex> g(m.mu);
+    void* base = static_cast<char*>(ptr) - offset;
+    auto b = m.by_base.find(base);
+    if (b == m.by_base.end()) return fail(PYG_ERR_INVALID_ARGUMENT, "ipc_close: not an open mapping");
+    auto it = m.by_handle.find(b->second);
+    if (--it->second.second == 0) {
+        m.by_handle.erase(it);
+        m.by_base.erase(b);
+        PYG_CUDA(cudaIpcCloseMemHandle(base));
+    }
     return PYG_OK;
 }
 

@@ -182,6 +182,11 @@ size_t gat_bwd_tma_ws_bytes(const pyg_plan* plan, int64_t H);
 bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t ldz, float* out,
                           int64_t ldo, const float* alpha, const float* s_src, const float* s_dst);
 size_t gat_fwd_tma_ws_bytes(const pyg_plan* plan, int64_t H, int64_t F);
+// GAT forward on a source-blocked plan: one pass per block, additive thanks to the fixed shift
+size_t gat_fwd_blocked_ws_bytes(const pyg_plan* plan, int64_t H);
+pyg_status_t gat_fwd_blocked(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
+                             const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
+                             float* row_sums, void* ws, size_t ws_bytes, cudaStream_t s);
 pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float* z, int64_t n_src, int64_t ldz,
                          const float* s_src, const float* s_dst, float slope, float* out, int64_t ldo, float* alpha,
                          float* row_sums, void* ws, size_t ws_bytes, cudaStream_t s);
@@ -193,5 +198,8 @@ pyg_status_t gat_bwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
 pyg_status_t gat_scale_rows(const float* g, int64_t ldg, int64_t n, int H, int C, const float* row_sums, float* gsc,
                             cudaStream_t s);
 pyg_status_t fill_const(float* p, int64_t n, float v, cudaStream_t s);
+
+// device-side peer flags (halo.cu): release-store `value` into each flag, or spin until each >= value
+pyg_status_t peer_flags_impl(uint32_t* const* flags, int n, uint32_t value, int wait, cudaStream_t s);
 
 }  // namespace pyg

@@ -80,8 +80,16 @@ __device__ __forceinline__ unsigned group_mask() {
 #ifndef PYG_SEG_PERSIST
 #define PYG_SEG_PERSIST 0
 #endif
+#if PYG_SEG_PERSIST
+#define PYG_SEG_SKIP continue
+#else
+#define PYG_SEG_SKIP return
+#endif
 #ifndef PYG_MAX_U
 #define PYG_MAX_U 1
+#endif
+#ifndef PYG_MAX_PACK_NARROW
+#define PYG_MAX_PACK_NARROW 0  // A/B: also the 8-12 floats-per-lane MAX shapes (column tiles), U = 2
 #endif
 
 // MAX of a wide segment (17-20 floats per lane, e.g. Reddit's 602 columns) with the argmax kept as a
@@ -95,7 +103,7 @@ template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                                       float (&acc)[NCH][V], int (&bi)[NCH][V]) {
     static_assert(V % 2 == 0, "packed positions pair up vector elements");
-    constexpr int U = PYG_MAX_U;
+    constexpr int U = V * NCH <= 12 ? 2 : PYG_MAX_U;
     const unsigned mask = group_mask<LPR>();
     const int32_t* __restrict__ gidx = a.gidx;
     const int32_t* __restrict__ eid = a.eid;
@@ -184,8 +192,8 @@ __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t 
 template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                            float (&acc)[NCH][V], int (&bi)[NCH][V]) {
-    if constexpr (PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 &&
-                  V * NCH <= 20) {
+    if constexpr (PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 &&
+                  ((V * NCH > 16 && V * NCH <= 20) || (PYG_MAX_PACK_NARROW && V * NCH >= 8 && V * NCH <= 12))) {
         // 16-bit positions (0xffff = none): plans split rows above 2,048 positions (segment_reduce_one
         // refuses MAX without a plan), so a segment is always shorter
         accumulate_max_packed<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
@@ -333,7 +341,8 @@ struct HeavyArgs {
 template <int V, int NCH, int RED>
 struct MinBlocks {
     static constexpr bool packed_max =
-        PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 && V * NCH <= 20;
+        PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 &&
+        ((V * NCH > 16 && V * NCH <= 20) || (PYG_MAX_PACK_NARROW && V * NCH >= 8 && V * NCH <= 12));
     static constexpr int base = packed_max ? PYG_MAX_MINB : (V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1));
     // the head-weighted sum keeps a head index per chunk, narrow MAX an arg id per element: one CTA fewer
     static constexpr int value =
@@ -436,23 +445,28 @@ __global__ void __launch_bounds__(256, (MinBlocks<V, NCH, RED>::value)) seg_kern
     constexpr int groups = 256 / LPR;
     const int l = threadIdx.x & (LPR - 1);
     const int c0 = blockIdx.y * (LPR * NCH * V);
-    // PYG_SEG_PERSIST: a grid of resident CTAs whose groups stride over the rows (no group idles while
-    // the slowest row of its CTA finishes); else one row per group
-    const int64_t gstride = PYG_SEG_PERSIST ? (int64_t)gridDim.x * groups : INT64_MAX;
+    // PYG_SEG_PERSIST (A/B builds only; measured no gain on Reddit, gpurun_out/r2v): a grid of resident
+    // CTAs whose groups stride over the rows; the default is one row per group
+#if PYG_SEG_PERSIST
+    const int64_t gstride = (int64_t)gridDim.x * groups;
     for (int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / LPR;; gid += gstride) {
+#else
+    {
+    const int64_t gid = (int64_t)blockIdx.x * groups + threadIdx.x / LPR;
+#endif
     int64_t beg, end, row = -1;
     if (mode == 0) {
         if (a.row_order) {
             if (gid >= a.order_len) return;
             row = (int64_t)__ldg(a.row_order + gid) - a.order_offset;
-            if (row < 0 || row >= a.n_rows) { if (PYG_SEG_PERSIST) continue; return; }  // a slice visits only its own rows
+            if (row < 0 || row >= a.n_rows) { PYG_SEG_SKIP; }  // a slice visits only its own rows
         } else {
             if (gid >= a.n_rows) return;
             row = gid;
         }
         beg = __ldg(a.rowptr + row);
         end = __ldg(a.rowptr + row + 1);
-        if (end - beg > a.heavy_threshold) { if (PYG_SEG_PERSIST) continue; return; }  // handled by the split path
+        if (end - beg > a.heavy_threshold) { PYG_SEG_SKIP; }  // handled by the split path
     } else {
         if (gid >= h.n_items) return;
         const int64_t item = h.item_lo + gid;

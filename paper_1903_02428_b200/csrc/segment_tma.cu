@@ -13,34 +13,43 @@ extern template pyg_status_t launch_nch<kRedSumEpi>(int, int, int64_t, int, int,
 extern template pyg_status_t launch_nch<kRedHeadW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 extern template pyg_status_t launch_nch<kRedMaxW>(int, int, int64_t, int, int, cudaStream_t, const CUtensorMap&, const Args&);
 
-// empty rows: out = 0 (or the APPNP teleport term / GCN bias), arg = E.  One thread per float4 (or
-// float) of the flattened [empty rows x F] block, so the stores stream instead of waiting on one
-// row index per warp (R-MAT: 5M empty rows, 2.5 GB of zeros)
+// empty rows: out = 0 (or the APPNP teleport term / GCN bias), arg = E.  Flattened over the
+// [empty rows x F] block so consecutive threads store consecutive 16 bytes (the stores stream instead of
+// waiting on one row index per warp; R-MAT: 5M empty rows, 2.5 GB of zeros + 5 GB of int64 args)
 __global__ void empty_rows_kernel(const int32_t* __restrict__ order, int64_t begin, int64_t end, int64_t row_lo,
                                   int64_t row_hi, int ncols, float* out, int64_t ldo, int64_t* arg, int64_t lda,
                                   int64_t E, int vec_ok, const float* blend, int64_t ldb, float blend_b,
                                   const float* col_bias) {
-    const int per = vec_ok && !blend && !col_bias ? ncols / 4 : ncols;  // units per row
-    const int64_t total = (end - begin) * per;
+    const bool vec = vec_ok && !blend && !col_bias;
+    const int per = vec ? ncols / 4 : ncols;  // out units per row (float4 or float)
+    const int64_t rows = end - begin;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t t = t0; t < rows * per; t += stride) {
         const int64_t k = t / per;
         const int u = (int)(t - k * per);
         const int64_t r = (int64_t)__ldg(order + begin + k);
         if (r < row_lo || r >= row_hi) continue;
         float* o = out + (r - row_lo) * ldo;
-        if (per != ncols) {
+        if (vec) {
             reinterpret_cast<float4*>(o)[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (arg) {
-                int64_t* ap = arg + (r - row_lo) * lda + 4 * u;
-                ap[0] = E; ap[1] = E; ap[2] = E; ap[3] = E;
-            }
-        } else {
-            // APPNP: an empty row keeps only the teleport term; GCN: the bias
+        } else {  // APPNP: an empty row keeps only the teleport term; GCN: the bias
             const float* hb = blend ? blend + (r - row_lo) * ldb : nullptr;
             o[u] = (hb ? fmaf(blend_b, hb[u], 0.0f) : 0.0f) + (col_bias ? __ldg(col_bias + u) : 0.0f);
-            if (arg) arg[(r - row_lo) * lda + u] = E;
         }
+    }
+    if (!arg) return;
+    // args: pairs of int64 (16-byte stores) when the row is 16-byte aligned, else single values
+    const bool pairs = (ncols % 2 == 0) && (lda % 2 == 0) && !(reinterpret_cast<uintptr_t>(arg) & 15);
+    const int pa = pairs ? ncols / 2 : ncols;
+    for (int64_t t = t0; t < rows * pa; t += stride) {
+        const int64_t k = t / pa;
+        const int u = (int)(t - k * pa);
+        const int64_t r = (int64_t)__ldg(order + begin + k);
+        if (r < row_lo || r >= row_hi) continue;
+        int64_t* ap = arg + (r - row_lo) * lda;
+        if (pairs) reinterpret_cast<longlong2*>(ap)[u] = make_longlong2(E, E);
+        else ap[u] = E;
     }
 }
 

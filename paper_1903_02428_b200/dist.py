@@ -158,10 +158,15 @@ class HaloPush:
     """Peer-store halo exchange (north_star (3)): each owner writes the rows its peers
     requested straight into their X_loc buffers over NVLink with one kernel (pyg_halo_push: gather +
     transfer, no staging buffer, no NCCL), the buffers mapped once with CUDA IPC.  The halo block is
-    double-buffered -- X_loc = [own shard (per rows) ; halo A ; halo B], one halo plan per block --
-    so a step needs a single host barrier: a push of step k+1 can only start after every peer has
-    synchronised step k, whose stream also finished that peer's step k-1 propagate (the last
-    reader of the block being overwritten)."""
+    double-buffered -- X_loc = [own shard (per rows) ; halo A ; halo B], one halo plan per block.
+    The steps are ordered on the DEVICE, with no host synchronisation: every rank owns 2 x world
+    uint32 flags (mapped into its peers) -- ready[q] = k + 1 once peer q's step-k push into me is
+    complete, consumed[q] = k + 1 once peer q finished reading what I pushed at step k -- and
+    exchange(k), all enqueued on the current stream, (1) signals consumed = k to the ranks that push
+    to me (my step k-1 propagate precedes it on the stream), (2) waits until the ranks I push to
+    consumed step k-2 (the last reader of the block being overwritten), (3) pushes, (4) signals
+    ready = k + 1 to them, (5) waits for ready = k + 1 from the ranks that push to me.  Every rank
+    signals before it waits, so the waits cannot form a cycle."""
 
     def __init__(self, slice_plan, n: int, lo: int, hi: int, per: int, ld: int, world: int, rank: int, group=None,
                  dtype=torch.float32):
@@ -191,6 +196,16 @@ class HaloPush:
         self.send_ptr = [0]
         for c in self.send_counts:
             self.send_ptr.append(self.send_ptr[-1] + c)
+        # step flags: [ready[world] | consumed[world]] per rank, mapped into every peer
+        self.flags = torch.zeros(2 * world, dtype=torch.int32, device=dev)
+        fh = [None] * world
+        dist.all_gather_object(fh, pg.pyg_ipc_handle(self.flags), group=group)
+        self.flag_handles = fh
+        self.flag_base = [self.flags.data_ptr() if q == rank else pg.pyg_ipc_open(fh[q]) for q in range(world)]
+        self.recv_from = [q for q in range(world) if q != rank and recv_counts[q] > 0]
+        self.send_to = [q for q in range(world) if q != rank and self.send_counts[q] > 0]
+        torch.cuda.synchronize(dev)
+        dist.barrier(group=group)  # every rank's flags are zero before any signal
         self.step = 0
 
     @property
@@ -198,22 +213,38 @@ class HaloPush:
         """This rank's X rows (write the shard here)."""
         return self.xloc[: self.per]
 
+    def _flag(self, owner: int, kind: int, about: int) -> int:
+        """Address of owner's flag `kind` (0 ready, 1 consumed) about peer `about`."""
+        return self.flag_base[owner] + 4 * (kind * self.world + about)
+
     def exchange(self):
-        """Push this step's halo rows to every peer, then wait for every peer's push into mine.
-        Returns the halo plan to propagate with (X_loc = self.xloc)."""
-        b = self.step & 1
-        self.pg.pyg_halo_push(self.shard, self.send_rows, self.send_ptr, self.dst, self.dst_row[b],
-                              self.xloc.stride(0))
-        torch.cuda.current_stream().synchronize()
-        dist.barrier(group=self.group)
+        """Push this step's halo rows to every peer and make the stream wait for every peer's push
+        into mine, all on the device (see the class notes).  Returns the halo plan to propagate with
+        (X_loc = self.xloc); the propagate must be enqueued on the current stream."""
+        k, b, me, pg = self.step, self.step & 1, self.rank, self.pg
+        dev = self.xloc.device
+        if k >= 1:  # my step k-1 reads of what they pushed are done (stream order)
+            pg.pyg_peer_signal([self._flag(q, 1, me) for q in self.recv_from], k, dev)
+        if k >= 2:  # block b was last read at step k-2 by the ranks I push to
+            pg.pyg_peer_wait([self._flag(me, 1, q) for q in self.send_to], k - 1, dev)
+        pg.pyg_halo_push(self.shard, self.send_rows, self.send_ptr, self.dst, self.dst_row[b], self.xloc.stride(0))
+        pg.pyg_peer_signal([self._flag(q, 0, me) for q in self.send_to], k + 1, dev)
+        pg.pyg_peer_wait([self._flag(me, 0, q) for q in self.recv_from], k + 1, dev)
         self.step += 1
         return self.plans[b]
 
     def close(self):
+        """Wait until the peers are done with my buffers, then unmap theirs."""
+        torch.cuda.synchronize(self.xloc.device)
+        dist.barrier(group=self.group)
         for q, p in enumerate(self.dst):
             if p:
                 self.pg.pyg_ipc_close(p, self.handles[q])
         self.dst = [0] * self.world
+        for q in range(self.world):
+            if q != self.rank and self.flag_base[q]:
+                self.pg.pyg_ipc_close(self.flag_base[q], self.flag_handles[q])
+        self.flag_base = [0] * self.world
 
 
 def local_edges(edge_index: torch.Tensor, lo: int, hi: int) -> torch.Tensor:

@@ -26,12 +26,14 @@ WORKLOADS = {  # capture -> bench workload key
     "full_rmat_max": "rmat-max-segment-cb0-n1",
     "full_rmat_sum_atomic": "rmat-sum-atomic-cb0-n1",
     "full_reddit_mean_atomic": "reddit-mean-atomic-cb0-n1",
+    "full_reddit_max": "reddit-max-segment-cb21179-n1",
+    "full_gat_rmat": "rmat-gat-segment-cb0-n1-gat",
 }
 
 
-def summary(path):
+def summary(path, row=2):
     rows = list(csv.reader(open(path)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[row]
     d = dict(zip(hdr, vals))
     u = dict(zip(hdr, units))
     out = {"kernel": d.get("Kernel Name", "")[:80]}
@@ -56,5 +58,8 @@ if __name__ == "__main__":
         if os.path.exists(p):
             res[key] = summary(p)
             res[key]["source"] = p
+            n_rows = len(list(csv.reader(open(p))))
+            for extra in range(3, n_rows):  # captures of several kernels (GAT: forward, backward)
+                res[f"{key}#{extra - 2}"] = dict(summary(p, extra), source=p)
     json.dump(res, open("profiles/ncu_summary.json", "w"), indent=1)
     print(json.dumps(res, indent=1))

@@ -1,13 +1,16 @@
 """Write profiles/traffic.json from ncu launch lists: DRAM bytes (read + write) summed over the
 launches of ONE propagate call (the last call in the list), keyed like bench.py's roofline key."""
 import csv
+import gzip
+import io
 import json
 import os
 import sys
 
 
 def call_traffic(path, n_last):
-    rows = list(csv.reader(open(path)))
+    f = io.TextIOWrapper(gzip.open(path)) if path.endswith(".gz") else open(path)
+    rows = list(csv.reader(f))
     hdr = [r for r in rows if r and r[0] == "ID"][0]
     K, M, V, U = (hdr.index(c) for c in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit"))
     d = {}
@@ -15,7 +18,8 @@ def call_traffic(path, n_last):
     for r in rows:
         if r and r[0].isdigit():
             d.setdefault(int(r[0]), {"name": r[K]})[r[M]] = float(r[V].replace(",", "")) * scale.get(r[U], 1)
-    ours = [i for i in sorted(d) if "pyg::" in d[i]["name"] or "seg::" in d[i]["name"] or "tma::" in d[i]["name"]]
+    ours = [i for i in sorted(d) if "seg_kernel" in d[i]["name"] or "seg_tma" in d[i]["name"] or
+            "combine_kernel" in d[i]["name"] or "empty_rows" in d[i]["name"]]
     sel = ours[-n_last:]
     b = sum(d[i].get("dram__bytes_read.sum", 0) + d[i].get("dram__bytes_write.sum", 0) for i in sel)
     t = sum(d[i].get("gpu__time_duration.sum", 0) for i in sel)
@@ -28,9 +32,12 @@ if __name__ == "__main__":
                     "propagate call, from the ncu launch lists in profiles/; bench.py divides by launches_per_call."}
     specs = [("reddit-mean-segment-cb21179-n1", f"launches_reddit_mean.csv", 11),
              ("rmat-sum-segment-cb0-n1", "launches_rmat_sum.csv", 3),
-             ("rmat-max-segment-cb0-n1", "launches_rmat_max.csv", 3)]
+             ("rmat-max-segment-cb0-n1", "launches_rmat_max.csv", 3),
+             ("reddit-max-segment-cb21179-n1", "launches_reddit_max.csv", 11)]
     for key, f, n in specs:
         p = os.path.join("profiles", f"{tag}_{f}")
+        if not os.path.exists(p) and os.path.exists(p + ".gz"):
+            p += ".gz"
         if os.path.exists(p):
             b, ms, names = call_traffic(p, n)
             out[key] = b

@@ -153,6 +153,37 @@ def test_gat_forward_far_logits_fall_back_exactly(fused, monkeypatch):
     check_close(out.cpu().numpy(), ref, abs_sum=ab, what="out")
 
 
+@pytest.mark.parametrize("factored", [False, True])
+@pytest.mark.parametrize("outlier", [False, True])
+def test_gat_forward_source_blocked(factored, outlier):
+    """GAT forward on a source-blocked plan (one pass per block of z rows; the fixed per-row shift of
+    reading A9 makes the passes additive) equals the oracle, alpha (normalised, or factored through
+    row_sums) and out; rows without in-edges stay 0.  outlier: an s_src of 400 forces the exact
+    fallback for most rows (their sums underflow against the global bound)."""
+    import paper_1903_02428_b200 as pg
+
+    rng = np.random.default_rng(23)
+    n, H, C = 2000, 8, 16
+    E = 30000
+    ei = np.stack([rng.integers(1, n, E), rng.integers(0, n - 100, E)]).astype(np.int64)  # last 100 rows empty
+    ei[0, :40] = 0
+    z = rng.standard_normal((n, H * C)).astype(np.float32)
+    ss = rng.standard_normal((n, H)).astype(np.float32)
+    if outlier:
+        ss[0] = 400.0
+    sd = rng.standard_normal((n, H)).astype(np.float32)
+    ref, ralpha, ab = oracle.gat(z, ss, sd, ei, H, n_dst=n, with_abs=True)
+    eit = _t(ei)
+    plan = pg.pyg_plan_build(eit[1], eit[0], n, n, col_block=450)
+    assert plan.view()["n_col_blocks"] == 5
+    rs = torch.empty((n, H), device=DEV) if factored else None
+    out, alpha = pg.pyg_gat_propagate(_t(z), _t(ss), _t(sd), H, plan, row_sums=rs)
+    a = alpha / rs[eit[1]] if factored else alpha
+    check_close(a.cpu().numpy(), ralpha, what="alpha")
+    check_close(out.cpu().numpy(), ref, abs_sum=ab, what="out")
+    assert torch.equal(out[n - 100:], torch.zeros_like(out[n - 100:]))
+
+
 def test_gat_zero_attention_equals_mean():
     """S:428 on the GPU: s = 0 -> uniform attention = the mean aggregation kernel's result."""
     import paper_1903_02428_b200 as pg
