@@ -441,7 +441,8 @@ constexpr float kTinySum = 1e-30f;  // a row sum below this is recomputed with t
 
 template <int NCH, int S>
 __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_constant__ CUtensorMap tz,
-                                                             const __grid_constant__ CUtensorMap ts, FwdArgs a) {
+                                                             const __grid_constant__ CUtensorMap ts,
+                                                             const __grid_constant__ CUtensorMap td, FwdArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         coff[ch] = cval[ch] ? (uint32_t)(4 * (b * 4 * a.box_w + cc)) : 0u;
         hch[ch] = cval[ch] ? c / a.C : 0;
     }
-    const float smax_h = lane < H ? ord2f(__ldg(a.smax + lane)) : 0.0f;
+    const float smx = (lane & 7) < H ? ord2f(__ldg(a.smax + (lane & 7))) : 0.0f;  // the max s_src of lane's head
     const int64_t plo = __ldg(a.rowptr + a.row_lo), phi = __ldg(a.rowptr + a.row_hi);
 
     // ---------------- producer (as gat_bwd_tma_kernel: z rows, s_src rows, s_dst of new rows) -----
@@ -481,7 +482,6 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
     bool done = false;
     int wg = 0, wr = 0, we = 0, ng = 0, nr = 0, ne = 0;
     int citem = -1;
-    int pkey = -1;
     auto load_window = [&](int64_t base, int& gg, int& rr, int& ee) {
         const int64_t p = base + lane;
         gg = 0; rr = -1; ee = 0;
@@ -533,37 +533,28 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         const int gj = __shfl_sync(0xffffffffu, wg, src);
         const int row = __shfl_sync(0xffffffffu, wr, src);
         const int e = __shfl_sync(0xffffffffu, we, src);
-        const int key = citem >= 0 ? -(citem + 2) : row;
-        int prev = __shfl_up_sync(0xffffffffu, key, 1);
-        if (lane == 0) prev = pkey;
-        const unsigned newm = __ballot_sync(0xffffffffu, lane < cnt && key != prev) & 0xFu;
-        pkey = __shfl_sync(0xffffffffu, key, cnt - 1);
         if (lane < 4) {
-            sts32(m, lane < cnt ? key : -1);
+            sts32(m, lane < cnt ? (citem >= 0 ? -(citem + 2) : row) : -1);
             sts32(m + 16, row);
             sts32(m + 32, e);
             sts32(m + 48, gj);
         }
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0) {  // z_j and s_src rows by source, s_dst rows by target (missing slots repeat slot 0)
             const uint32_t ms = meta0 + (uint32_t)(s * kMeta);
             const int4 r4 = lds128(ms + 16), g4 = lds128(ms + 48);
             const int gs1 = cnt > 1 ? g4.y : g4.x, gs2 = cnt > 2 ? g4.z : g4.x, gs3 = cnt > 3 ? g4.w : g4.x;
-            const int rs4[4] = {r4.x, r4.y, r4.z, r4.w};
+            const int lo = (int)a.row_lo;
+            const int r0 = r4.x - lo, r1 = (cnt > 1 ? r4.y : r4.x) - lo, r2 = (cnt > 2 ? r4.z : r4.x) - lo,
+                      r3 = (cnt > 3 ? r4.w : r4.x) - lo;
             const uint32_t bar = bar0 + 8 * s;
             const uint32_t st = data0 + (uint32_t)s * stage_bytes;
-            const uint32_t nnew = (uint32_t)__popc(newm);
-            bar_expect(bar, (uint32_t)a.zbytes + 16u * (uint32_t)H + nnew * (uint32_t)(4 * H));
+            bar_expect(bar, (uint32_t)a.zbytes + 32u * (uint32_t)H);
 #pragma unroll
             for (int b = 0; b < 4; ++b)
                 if (b < a.nb) gather4(st + (uint32_t)b * 4u * row_bytes, &tz, b * a.box_w, g4.x, gs1, gs2, gs3, bar);
             gather4(st + (uint32_t)a.off_s, &ts, 0, g4.x, gs1, gs2, gs3, bar);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                if (!((newm >> i) & 1u)) continue;
-                const int64_t lr = (int64_t)rs4[i] - a.row_lo;
-                bulk_copy(st + (uint32_t)a.off_d + (uint32_t)(i * 4 * H), a.s_dst + lr * H, (uint32_t)(4 * H), bar);
-            }
+            gather4(st + (uint32_t)a.off_d, &td, 0, r0, r1, r2, r3, bar);
         }
         pp += cnt;
         if (pp >= pe) {
@@ -576,8 +567,6 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
     };
 
     // ---------------- consumer ----------------
-    float sdreg = 0.0f;               // lanes < H: s_dst[i][h] of the capture row
-    int crow = -1;
     int arow = -1, agrow = 0;         // key / root row being aggregated
     float acc[NCH][4];
     float ssum[NCH];                  // running sum of p of each chunk's head (replicated per lane)
@@ -635,21 +624,11 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         phase ^= 1u << s;
         const uint32_t st = data0 + (uint32_t)s * stage_bytes;
         const int kk[4] = {keys.x, keys.y, keys.z, keys.w};
-        // (1) s_dst of each slot's row for the (slot, head) lanes (branch-free)
-        float sme = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const bool nr = i < c && kk[i] != crow;
-            crow = nr ? kk[i] : crow;
-            lds32f_if(nr && lane < H, sdreg, st + (uint32_t)a.off_d + (uint32_t)(i * 4 * H) + 4u * (uint32_t)lane);
-            const float tv = __shfl_sync(0xffffffffu, sdreg, my_h);
-            sme = my_i == i ? tv : sme;
-        }
-        const float smx = __shfl_sync(0xffffffffu, smax_h, my_h);
-        // (2) the weight of (slot my_i, head my_h): one exp per lane per stage
+        // the weight of (slot my_i, head my_h), from its staged s_src and s_dst: one exp per lane per stage
         const bool mine = my_i < c && my_h < H;
-        float ss = 0.0f;
+        float ss = 0.0f, sme = 0.0f;
         lds32f_if(mine, ss, st + (uint32_t)a.off_s + 4u * (uint32_t)(my_i * H + my_h));
+        lds32f_if(mine, sme, st + (uint32_t)a.off_d + 4u * (uint32_t)(my_i * H + my_h));
         const float pre = ss + sme, cpre = smx + sme;
         const float l = pre > 0.0f ? pre : slope * pre;
         const float cs = cpre > 0.0f ? cpre : slope * cpre;  // the row's shift c_i (>= every logit)
@@ -806,8 +785,8 @@ __global__ void gat_fwd_fix_kernel(const int* __restrict__ bad, const int64_t* _
 
 template <int NCH>
 pyg_status_t launch_fwd(int S, int64_t want, int warps, int smem, int sm_kb, cudaStream_t s, const CUtensorMap& tz,
-                        const CUtensorMap& tsrc, const FwdArgs& a) {
-    void (*k)(const CUtensorMap, const CUtensorMap, FwdArgs) =
+                        const CUtensorMap& tsrc, const CUtensorMap& tdst, const FwdArgs& a) {
+    void (*k)(const CUtensorMap, const CUtensorMap, const CUtensorMap, FwdArgs) =
         S >= 3 ? gat_fwd_tma_kernel<NCH, 3> : gat_fwd_tma_kernel<NCH, 2>;
     PYG_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int kSmemPerSm = std::min(227, std::max(32, sm_kb)) * 1024;
@@ -820,7 +799,7 @@ pyg_status_t launch_fwd(int S, int64_t want, int warps, int smem, int sm_kb, cud
     PYG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * warps, smem));
     per_sm = std::min(per_sm, cap);
     const dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)sms * std::max(per_sm, 1))));
-    k<<<grid, 32 * warps, smem, s>>>(tz, tsrc, a);
+    k<<<grid, 32 * warps, smem, s>>>(tz, tsrc, tdst, a);
     PYG_LAUNCHED();
     PYG_CUDA(cudaGetLastError());
     return PYG_OK;
@@ -1076,17 +1055,19 @@ pyg_status_t gat_fwd_tma(const pyg_plan* plan, int H, int C, int F, const float*
     const int smem = warps * a.warp_bytes;
     if (smem > 227 * 1024) return fail(PYG_ERR_UNSUPPORTED, "gat_propagate: stage ring does not fit shared memory");
     CUtensorMap tz, tsrc;
-    if (!encode_rows(&tz, z, F, n_src, ldz, box_w) || !encode_rows(&tsrc, s_src, H, n_src, H, H))
+    CUtensorMap tdst;
+    if (!encode_rows(&tz, z, F, n_src, ldz, box_w) || !encode_rows(&tsrc, s_src, H, n_src, H, H) ||
+        !encode_rows(&tdst, s_dst, H, n, H, H))
         return fail(PYG_ERR_CUDA, "gat_propagate: cuTensorMapEncodeTiled failed");
     const int64_t want = cdiv(a.n_tasks, warps);
     const int sm_kb = knobs().gat_fwd_sm_kb;
     switch (nch) {
-        case 1: PYG_TRY(launch_fwd<1>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
-        case 2: PYG_TRY(launch_fwd<2>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
-        case 3: PYG_TRY(launch_fwd<3>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
-        case 4: PYG_TRY(launch_fwd<4>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
-        case 5: case 6: PYG_TRY(launch_fwd<6>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
-        default: PYG_TRY(launch_fwd<8>(S, want, warps, smem, sm_kb, s, tz, tsrc, a)); break;
+        case 1: PYG_TRY(launch_fwd<1>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
+        case 2: PYG_TRY(launch_fwd<2>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
+        case 3: PYG_TRY(launch_fwd<3>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
+        case 4: PYG_TRY(launch_fwd<4>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
+        case 5: case 6: PYG_TRY(launch_fwd<6>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
+        default: PYG_TRY(launch_fwd<8>(S, want, warps, smem, sm_kb, s, tz, tsrc, tdst, a)); break;
     }
     if (items > 0) {
         gat_fwd_combine_kernel<<<(unsigned)(plan->h_hi - plan->h_lo), 128, 0, s>>>(

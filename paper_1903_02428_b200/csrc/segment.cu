@@ -103,25 +103,11 @@ bool v_ok(const SegArgs& a, int V) {
 }
 
 // widest vector whose lane utilisation is not worse than the next narrower one
-Geometry choose(const SegArgs& a, int reduce = PYG_SUM) {
+Geometry choose(const SegArgs& a) {
     static const int forced = [] {
         const char* e = getenv("PYG_SEG_VEC");
         return e ? atoi(e) : 0;
     }();
-    // A/B knob: MAX over wide rows split into column tiles (fewer registers per lane, more rows in flight)
-    static const int max_tiles = [] {
-        const char* e = getenv("PYG_MAX_TILES");
-        return e ? atoi(e) : 0;
-    }();
-    if (max_tiles > 1 && (reduce == PYG_MAX || reduce == kRedMaxW) && v_ok(a, 4) && a.ncols > 128 * max_tiles) {
-        Geometry g{4, 32, 1, max_tiles, 0.0};
-        const int64_t per = cdiv(cdiv(a.ncols, max_tiles), 4);  // float4 chunks per tile
-        g.nch = (int)cdiv(per, 32);
-        if (g.nch <= 6 && g.nch != 5) {
-            g.util = (double)cdiv(a.ncols, 4) / (32.0 * g.nch * max_tiles);
-            return g;
-        }
-    }
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8)
         if (v_ok(a, forced)) return geometry(a.ncols, forced);
     Geometry best = geometry(a.ncols, 1);
@@ -172,7 +158,7 @@ pyg_status_t segment_reduce_one(const SegArgs& a0, int reduce, const pyg_plan* p
         a.order_len = plan->order_len;
         a.order_offset = plan->row_offset;
     }
-    const Geometry g = choose(a, reduce);
+    const Geometry g = choose(a);
     const int sv = g.V >= 4 ? 4 : g.V;  // store width
     const int ovk = (a.ldo % sv == 0) && aligned(a.out, 4 * sv);
     const bool split = plan && (plan->item_hi > plan->item_lo);

@@ -88,9 +88,6 @@ __device__ __forceinline__ unsigned group_mask() {
 #ifndef PYG_MAX_U
 #define PYG_MAX_U 1
 #endif
-#ifndef PYG_MAX_PACK_NARROW
-#define PYG_MAX_PACK_NARROW 0  // A/B: also the 8-12 floats-per-lane MAX shapes (column tiles), U = 2
-#endif
 
 // MAX of a wide segment (17-20 floats per lane, e.g. Reddit's 602 columns) with the argmax kept as a
 // 16-bit position inside the segment, two per register (segments are <= 2048 positions: light rows
@@ -98,12 +95,13 @@ __device__ __forceinline__ unsigned group_mask() {
 // occupancy; the positions become edge ids once, at the end.  With 10 registers freed the plain
 // (unweighted) MAX instantiation also drops the x1 multiply without spilling (Reddit max, 11 passes:
 // 23.8 -> 22.6 ms, gpurun_out/r2u; more edges in flight per lane measured slower: U = 2 at 2 CTAs/SM
-// 27.3 ms, U = 3 37.2 ms).
+// 27.3 ms, U = 3 37.2 ms; splitting the 602 columns over 2 / 3 column tiles of 12 / 8 floats per lane
+// with U = 2 measured 27.9 / 32.9 ms, gpurun_out/r2ac).
 template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                                       float (&acc)[NCH][V], int (&bi)[NCH][V]) {
     static_assert(V % 2 == 0, "packed positions pair up vector elements");
-    constexpr int U = V * NCH <= 12 ? 2 : PYG_MAX_U;
+    constexpr int U = PYG_MAX_U;
     const unsigned mask = group_mask<LPR>();
     const int32_t* __restrict__ gidx = a.gidx;
     const int32_t* __restrict__ eid = a.eid;
@@ -192,8 +190,8 @@ __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t 
 template <int V, int NCH, int RED, int LPR>
 __device__ __forceinline__ void accumulate(const SegArgs& a, int64_t beg, int64_t end, int l, int c0,
                                            float (&acc)[NCH][V], int (&bi)[NCH][V]) {
-    if constexpr (PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 &&
-                  ((V * NCH > 16 && V * NCH <= 20) || (PYG_MAX_PACK_NARROW && V * NCH >= 8 && V * NCH <= 12))) {
+    if constexpr (PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 &&
+                  V * NCH <= 20) {
         // 16-bit positions (0xffff = none): plans split rows above 2,048 positions (segment_reduce_one
         // refuses MAX without a plan), so a segment is always shorter
         accumulate_max_packed<V, NCH, RED, LPR>(a, beg, end, l, c0, acc, bi);
@@ -341,8 +339,7 @@ struct HeavyArgs {
 template <int V, int NCH, int RED>
 struct MinBlocks {
     static constexpr bool packed_max =
-        PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 &&
-        ((V * NCH > 16 && V * NCH <= 20) || (PYG_MAX_PACK_NARROW && V * NCH >= 8 && V * NCH <= 12));
+        PYG_MAX_PACK && (RED == PYG_MAX || RED == kRedMaxW) && V % 2 == 0 && V * NCH > 16 && V * NCH <= 20;
     static constexpr int base = packed_max ? PYG_MAX_MINB : (V * NCH <= 24 ? PYG_SEG_MINB : (V * NCH <= 48 ? 2 : 1));
     // the head-weighted sum keeps a head index per chunk, narrow MAX an arg id per element: one CTA fewer
     static constexpr int value =
