@@ -53,6 +53,7 @@ static Knobs read_knobs() {
     k.gat_sm_kb = get("PYG_GAT_SM_KB", 160);
     k.gat_fused = get("PYG_GAT_FUSED", 1);
     k.gat_warps = get("PYG_GAT_WARPS", 8);
+    k.coo_l2_mb = get("PYG_COO_L2_MB", 72);
     k.gat_fwd_warp_kb = get("PYG_GAT_FWD_WARP_KB", 5);
     k.gat_fwd_sm_kb = get("PYG_GAT_FWD_SM_KB", 160);
     return k;
@@ -485,7 +486,7 @@ pyg_status_t pyg_propagate(const float* x_src, int64_t n_src, int64_t F, int64_t
         c.gidx = gidx; c.sidx = edge_index + E; c.w = w;
         c.out = out + off; c.ldo = ldo;
         c.keys = arg_out ? reinterpret_cast<unsigned long long*>(arg_out + off) : nullptr; c.ldk = ldo;
-        c.E = E; c.n_out = n_dst;
+        c.E = E; c.n_out = n_dst; c.n_src = gidx ? n_src : E;
         c.allow_pad_read = (X == x_src);
         c.deg = need_deg ? deg : nullptr;
         return coo_reduce(c, reduce, cv.rest(), cv.rest_bytes(), s);
@@ -553,7 +554,7 @@ pyg_status_t pyg_propagate_backward(const float* x_src, int64_t n_src, int64_t F
             CooArgs c;
             c.X = grad_out + off1; c.ldx = ldg; c.ncols = (int)F;
             c.gidx = dst; c.sidx = src; c.w = edge_weight; c.gdeg = reduce == PYG_MEAN ? deg_dst : nullptr;
-            c.out = grad_x_src; c.ldo = ldgx; c.E = E; c.n_out = n_src;
+            c.out = grad_x_src; c.ldo = ldgx; c.E = E; c.n_out = n_src; c.n_src = n_dst;
             PYG_TRY(coo_reduce(c, PYG_SUM, ws, ws_bytes, s));
         }
     }

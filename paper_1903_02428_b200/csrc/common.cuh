@@ -65,6 +65,7 @@ struct Knobs {
     int gat_fused = 1;    // PYG_GAT_FUSED: 0 keeps the GAT forward on softmax + aggregation (two kernels)
     int gat_fwd_warp_kb = 5;   // PYG_GAT_FWD_WARP_KB: ring bytes per warp of the one-pass GAT forward
     int gat_fwd_sm_kb = 160;   // PYG_GAT_FWD_SM_KB
+    int coo_l2_mb = 72;   // PYG_COO_L2_MB: L2 budget of the atomic path's column tiles (0: no tiling)
 };
 const Knobs& knobs();
 

@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
             long long t = -1 - (long long)l;
             hb[j] = -1;
             if (p < e1) {
-                t = __ldg(a.sidx + p);
+                t = __ldcs(a.sidx + p);
                 if ((__ldg(a.hub_bits + (t >> 5)) >> (t & 31)) & 1u) hb[j] = __ldg(a.hub_base + t);
             }
             s_tgt[j][threadIdx.x] = t;
@@ -174,9 +174,9 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
         float ms = 1.0f;
         if (l < n) {
             const int64_t p = base + l;
-            mi = (RED != PYG_MAX && a.hub_base) ? s_tgt[(base - e0) / lpr][threadIdx.x] : __ldg(a.sidx + p);
-            mg = a.gidx ? __ldg(a.gidx + p) : p;
-            if (a.w) ms = __ldg(a.w + p);
+            mi = (RED != PYG_MAX && a.hub_base) ? s_tgt[(base - e0) / lpr][threadIdx.x] : __ldcs(a.sidx + p);
+            mg = a.gidx ? __ldcs(a.gidx + p) : p;
+            if (a.w) ms = __ldcs(a.w + p);
             if (a.gdeg) ms = ms / (float)__ldg(a.gdeg + mg);
         }
         // warp-aggregated atomics: visit the batch grouped by target (first-occurrence order)
@@ -367,6 +367,20 @@ int grid_for(int64_t work, int threads = 256) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
 }
 
+// Column-tile width that keeps one tile's accumulation target (fp32 out or 64-bit MAX keys) and its
+// gathered source rows inside the L2 budget (PYG_COO_L2_MB): without it a plan-free scatter into an
+// output wider than L2 (Reddit: 561 MB) misses L2 on every red.global and pays a DRAM read-modify-
+// write per element.  0: no tiling (everything fits already, or even 8 columns do not).
+int l2_tile_cols(const CooArgs& a, int reduce) {
+    const int64_t budget = (int64_t)knobs().coo_l2_mb << 20;
+    if (budget <= 0) return 0;
+    const int64_t per_col = a.n_out * (reduce == PYG_MAX ? 8 : 4) + (a.gidx ? a.n_src * 4 : 0);
+    if (per_col * a.ncols <= budget) return 0;
+    for (int W : {64, 32, 16, 8})
+        if (per_col * W <= budget && W < a.ncols) return W;
+    return 0;
+}
+
 struct CooGeom {
     int V, lpr, nch, tiles, ovk;
 };
@@ -381,7 +395,15 @@ CooGeom coo_geometry(const CooArgs& a, int reduce) {
     g.ovk = (reduce != PYG_MAX) && (a.ldo % g.V == 0) && aligned(a.out, 4 * g.V) &&
             (!a.part || (a.ldp % g.V == 0 && aligned(a.part, 4 * g.V)));
     const int64_t nvec = cdiv(a.ncols, g.V);
-    if (nvec <= 32) {
+    const int W = l2_tile_cols(a, reduce);
+    if (W > 0 && W % g.V == 0) {
+        // L2 column tiles: tile y's REDs (and gathers) stay inside an L2-resident slice; grid.y is the
+        // slowest-varying block index, so tiles run one after another
+        const int wv = W / g.V;
+        g.lpr = std::min(32, wv);
+        g.nch = wv / g.lpr;
+        g.tiles = (int)cdiv(a.ncols, W);
+    } else if (nvec <= 32) {
         while (g.lpr < nvec) g.lpr <<= 1;
     } else {
         g.lpr = 32;
@@ -397,7 +419,7 @@ CooGeom coo_geometry(const CooArgs& a, int reduce) {
 // hub workspace capacity: at most E / (threshold + 1) hubs, and sum ceil(d / slot) <= E / slot + hubs
 int64_t hub_cap(int64_t E) { return E / (kHeavyThreshold + 1) + 1; }
 int64_t slot_cap(int64_t E) { return E / kCooSlot + hub_cap(E); }
-int64_t max_tiles(int64_t ncols) { return std::max<int64_t>(1, cdiv(ncols, 32 * 16)); }  // V = 1 worst case
+int64_t max_tiles(int64_t ncols) { return std::max<int64_t>(1, cdiv(ncols, 8)); }  // L2 tiles of >= 8 columns
 
 }  // namespace
 

@@ -114,6 +114,7 @@ struct CooArgs {
     int64_t ldk = 0;
     int64_t E = 0;
     int64_t n_out = 0;
+    int64_t n_src = 0;  // rows gidx gathers from (L2 column-tile sizing; 0 -> E rows streamed once)
     int allow_pad_read = 0;
     const int32_t* deg = nullptr;   // in-degree of the targets if the caller has it (else computed)
     // hub routing (SUM / MEAN; set up by coo_reduce): rows with more than kHeavyThreshold entries

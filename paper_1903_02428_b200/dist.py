@@ -166,7 +166,12 @@ class HaloPush:
     to me (my step k-1 propagate precedes it on the stream), (2) waits until the ranks I push to
     consumed step k-2 (the last reader of the block being overwritten), (3) pushes, (4) signals
     ready = k + 1 to them, (5) waits for ready = k + 1 from the ranks that push to me.  Every rank
-    signals before it waits, so the waits cannot form a cycle."""
+    signals before it waits, so the waits cannot form a cycle.
+
+    Ranks that share one GPU (the one-GPU tests) must not spin on flags another process's kernel
+    writes: nothing makes the two kernels co-resident (B200_PROFILING.md; Xid 109 on this driver).
+    There the steps are ordered on the HOST instead (stream sync + barrier around the push); the
+    flag protocol itself is checked in one process (tests/test_gpu_halo_push.py)."""
 
     def __init__(self, slice_plan, n: int, lo: int, hi: int, per: int, ld: int, world: int, rank: int, group=None,
                  dtype=torch.float32):
@@ -202,6 +207,9 @@ class HaloPush:
         dist.all_gather_object(fh, pg.pyg_ipc_handle(self.flags), group=group)
         self.flag_handles = fh
         self.flag_base = [self.flags.data_ptr() if q == rank else pg.pyg_ipc_open(fh[q]) for q in range(world)]
+        uuids = [None] * world
+        dist.all_gather_object(uuids, str(torch.cuda.get_device_properties(dev).uuid), group=group)
+        self.host_ordered = len(set(uuids)) < world  # ranks share a GPU: no cross-process spin-waits
         self.recv_from = [q for q in range(world) if q != rank and recv_counts[q] > 0]
         self.send_to = [q for q in range(world) if q != rank and self.send_counts[q] > 0]
         torch.cuda.synchronize(dev)
@@ -223,6 +231,14 @@ class HaloPush:
         (X_loc = self.xloc); the propagate must be enqueued on the current stream."""
         k, b, me, pg = self.step, self.step & 1, self.rank, self.pg
         dev = self.xloc.device
+        if self.host_ordered:
+            torch.cuda.current_stream(dev).synchronize()
+            dist.barrier(group=self.group)  # every rank's reads of block b (step k - 2) are done
+            pg.pyg_halo_push(self.shard, self.send_rows, self.send_ptr, self.dst, self.dst_row[b], self.xloc.stride(0))
+            torch.cuda.current_stream(dev).synchronize()
+            dist.barrier(group=self.group)  # every push into my halo block has landed
+            self.step += 1
+            return self.plans[b]
         if k >= 1:  # my step k-1 reads of what they pushed are done (stream order)
             pg.pyg_peer_signal([self._flag(q, 1, me) for q in self.recv_from], k, dev)
         if k >= 2:  # block b was last read at step k-2 by the ranks I push to

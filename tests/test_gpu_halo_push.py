@@ -40,6 +40,7 @@ def _worker(rank, world, port, q):
         lo, hi = ranges[rank]
         sl = plan.slice(lo, hi)
         hp = HaloPush(sl, N, lo, hi, per, F, world, rank)
+        assert hp.host_ordered  # both ranks on cuda:0: steps ordered on the host, no spin-waits
         ok = True
         for step in range(5):
             x = torch.from_numpy(synth.features(N, F, 100 + step, signed=True)).to(dev)
@@ -74,3 +75,26 @@ def test_halo_push_two_ranks_one_gpu():
         assert res[r][0], f"rank {r}: halo-push propagate differs from the full-X slice"
         assert res[r][1] > 0
     assert res[0][1] == res[1][2] and res[1][1] == res[0][2]
+
+
+def test_peer_flags_one_process():
+    """The device-side step flags of the peer-store halo (pyg_peer_signal / pyg_peer_wait) in ONE
+    process on one stream: every wait is enqueued after the signal that satisfies it, so no kernel
+    waits on another that might not be resident (the two-process test above orders its steps on the
+    host because its ranks share the GPU).  Checks the release store and the wrap-safe comparison."""
+    import paper_1903_02428_b200 as pg
+
+    dev = torch.device("cuda:0")
+    flags = torch.zeros(6, dtype=torch.int32, device=dev)
+    ptrs = [flags.data_ptr() + 4 * i for i in range(6)]
+    pg.pyg_peer_signal(ptrs[:3], 7, dev)
+    pg.pyg_peer_wait(ptrs[:3], 7, dev)
+    pg.pyg_peer_wait(ptrs[:3], 5, dev)  # already past 5
+    torch.cuda.synchronize(dev)
+    assert flags.tolist() == [7, 7, 7, 0, 0, 0]
+    # the step counter wraps: flag 1 (= 2^32 + 1) satisfies a wait for 0xffffffff
+    pg.pyg_peer_signal(ptrs[3:], 0xFFFFFFFF, dev)
+    pg.pyg_peer_signal(ptrs[3:], 1, dev)
+    pg.pyg_peer_wait(ptrs[3:], 0xFFFFFFFF, dev)
+    torch.cuda.synchronize(dev)
+    assert flags.tolist()[3:] == [1, 1, 1]
