@@ -54,6 +54,9 @@ static Knobs read_knobs() {
     k.gat_fused = get("PYG_GAT_FUSED", 1);
     k.gat_warps = get("PYG_GAT_WARPS", 8);
     k.coo_l2_mb = get("PYG_COO_L2_MB", 72);
+    k.coo_tile = get("PYG_COO_TILE", 1);
+    k.coo_chunk = get("PYG_COO_CHUNK", 128);
+    k.coo_l2_mb_max = get("PYG_COO_L2_MB_MAX", 96);
     k.gat_fwd_warp_kb = get("PYG_GAT_FWD_WARP_KB", 5);
     k.gat_fwd_sm_kb = get("PYG_GAT_FWD_SM_KB", 160);
     return k;

@@ -244,6 +244,168 @@ __global__ void __launch_bounds__(256) coo_kernel(CooArgs a, int lpr, int epg, i
     if (cur >= 0) flush<V, NCH, RED>(a, cur, l, lpr, c0, cv, acc, bi, out_vec_ok);
 }
 
+// ---------------------------------------------------------------- warp-batched tile kernel
+// coo_tile_kernel<LPR, RED>: the atomic strategy for float4-capable rows whose column tile is
+// W = 4 * LPR floats (LPR in {4, 8, 16}; one tile = the whole row for F <= 64, else the L2 column
+// tiles of l2_tile_cols).  Rows of 65-128 floats that are not L2-tiled (R-MAT: out 5 GB, DRAM read-
+// modify-write bound) stay on coo_kernel, whose up-front hub-counter prefetch measured faster there
+// (R-MAT sum 34.4 vs 36.0 ms, max 63.5 vs 70.5 ms, gpurun_out/r3e).  A WARP takes 32 edges at a time (one coalesced, streaming load of
+// source, target and weight per lane) and its 32 / LPR lane groups split them:
+//   * warp-aggregated atomics with ONE full-warp __match_any_sync per 32 edges: if any target repeats
+//     (sorted input, hubs, small graphs), the batch is visited in grouped order (leaders in lane order,
+//     members after their leader, positions from a shuffle scan, inverted through shared memory), so a
+//     group sums the run of equal targets it holds in registers and sends one red.global.add.v4.f32 per
+//     run; for distinct targets (the common case on large uniform graphs) the identity order costs
+//     nothing;
+//   * U = 8 rows in flight per lane before any is consumed (the generic coo_kernel spends ~26 warp
+//     instructions per edge on per-group matching, 64-bit index arithmetic and runtime lane counts;
+//     ncu on the L2-tiled Reddit pass: 50% issue-busy at 2.0 IPC, MATCH/WARPSYNC the top stalls,
+//     gpurun_out/r3d);
+//   * hub rows (SUM / MEAN) take slot positions from their per-(slot, tile) counter exactly as in
+//     coo_kernel (one atomic per hub and batch) and become the virtual rows n_out + slot;
+//   * MAX: packed 64-bit keys, a group's run keeps the lowest edge id (grouped order is ascending edge
+//     id within a target), atomicMax only when the stored key is smaller.
+template <int LPR, int RED>
+__global__ void __launch_bounds__(256, 3) coo_tile_kernel(CooArgs a, int64_t chunk, int out_vec_ok) {
+    constexpr int G = 32 / LPR;  // lane groups per warp
+    constexpr int PER = LPR;     // grouped positions per group per batch (G * PER = 32)
+    constexpr int U = PER < 8 ? PER : 8;
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31, grp = lane / LPR, l = lane % LPR;
+    const int wib = threadIdx.x >> 5;
+    __shared__ int s_inv[8][32];
+    const int col = blockIdx.y * (4 * LPR) + 4 * l;
+    const int nv = max(0, min(4, a.ncols - col));
+    const bool full_ld = nv == 4 || (nv > 0 && a.allow_pad_read);
+    const int64_t e0 = ((int64_t)blockIdx.x * 8 + wib) * chunk;
+    if (e0 >= a.E) return;
+    const int64_t e1 = min(a.E, e0 + chunk);
+    const bool scaled = (a.w != nullptr) || (a.gdeg != nullptr);
+    const unsigned lt = (1u << lane) - 1u;
+
+    for (int64_t base = e0; base < e1; base += 32) {
+        const int n = (int)min((int64_t)32, e1 - base);
+        const int64_t p = base + lane;
+        const bool valid = lane < n;
+        int t = -1 - lane, g = 0;
+        float s = 1.0f;
+        if (valid) {
+            t = (int)__ldcs(a.sidx + p);
+            g = a.gidx ? (int)__ldcs(a.gidx + p) : (int)p;
+            if (a.w) s = __ldcs(a.w + p);
+            if (a.gdeg) s = s / (float)__ldg(a.gdeg + g);
+        }
+        if (RED != PYG_MAX && a.hub_base) {
+            int hb = -1;
+            if (valid && ((__ldg(a.hub_bits + (t >> 5)) >> (t & 31)) & 1u)) hb = __ldg(a.hub_base + t);
+            if (__any_sync(full, hb >= 0)) {
+                const unsigned hm = __match_any_sync(full, hb >= 0 ? t : -1 - lane);
+                const int lead = __ffs(hm) - 1;
+                int got = 0;
+                if (hb >= 0 && lane == lead)
+                    got = atomicAdd(a.hub_cursor + (int64_t)hb * gridDim.y + blockIdx.y, __popc(hm));
+                got = __shfl_sync(full, got, lead);
+                if (hb >= 0) t = (int)a.n_out + hb + (got + __popc(hm & lt)) / kCooSlot;
+            }
+        }
+        const unsigned m = __match_any_sync(full, t);
+        const bool dup = __any_sync(full, m != (1u << lane));
+        if (dup) {
+            const int lead = __ffs(m) - 1;
+            int v = lane == lead ? __popc(m) : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(full, v, d);
+                if (lane >= d) v += y;
+            }
+            const int incl = __shfl_sync(full, v, lead);
+            s_inv[wib][incl - __popc(m) + __popc(m & lt)] = lane;
+            __syncwarp();
+        }
+        float acc[4];
+        int bi[4];
+        int cur = 0;
+        bool have = false;
+        auto flush = [&]() {
+            if (!have || nv == 0) return;
+            if (RED == PYG_MAX) {
+                unsigned long long* kp = a.keys + (int64_t)cur * a.ldk + col;
+                unsigned long long hv[4];
+                if (nv == 4 && (reinterpret_cast<uintptr_t>(kp) & 15) == 0) {
+                    const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(kp));
+                    const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(kp + 2));
+                    hv[0] = x0.x; hv[1] = x0.y; hv[2] = x1.x; hv[3] = x1.y;
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) hv[q] = q < nv ? __ldcg(kp + q) : ~0ull;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (q < nv) {
+                        const unsigned long long k = max_key(acc[q], (uint32_t)bi[q]);
+                        if (k > hv[q]) atomicMax(kp + q, k);
+                    }
+                }
+            } else {
+                float* op = cur < a.n_out ? a.out + (int64_t)cur * a.ldo + col
+                                          : a.part + (int64_t)(cur - a.n_out) * a.ldp + col;
+                if (out_vec_ok) redv<4>(op, acc, nv);
+                else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) if (q < nv) atomicAdd(op + q, acc[q]);
+                }
+            }
+        };
+#pragma unroll
+        for (int k0 = 0; k0 < PER; k0 += U) {
+            // only the rows and their source lanes live across the loads (target and scale are
+            // re-shuffled when consumed): 8 rows in flight per lane without spilling at 4 CTAs / SM
+            float v[U][4];
+            int slv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = grp * PER + k0 + u;
+                const int sl = dup ? s_inv[wib][q] : q;
+                slv[u] = sl;
+                const int gg = __shfl_sync(full, g, sl);
+                const float* row = a.X + (int64_t)gg * a.ldx + col;
+                if (q < n && full_ld) {
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(row));
+                    v[u][0] = x.x; v[u][1] = x.y; v[u][2] = x.z; v[u][3] = x.w;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) v[u][c] = (q < n && c < nv) ? __ldg(row + c) : 0.0f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int q = grp * PER + k0 + u;
+                const int tu = __shfl_sync(full, t, slv[u]);
+                const float su = scaled ? __shfl_sync(full, s, slv[u]) : 1.0f;
+                if (q >= n) continue;  // (shuffles above stay warp-uniform)
+                if (!have || tu != cur) {
+                    flush();
+                    cur = tu;
+                    have = true;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) { acc[c] = RED == PYG_MAX ? -INFINITY : 0.0f; bi[c] = -1; }
+                }
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (RED == PYG_MAX) {
+                        const float mv = scaled ? __fmul_rn(su, v[u][c]) : v[u][c];
+                        if (bi[c] < 0 || mv > acc[c]) { acc[c] = mv; bi[c] = (int)base + slv[u]; }
+                    } else {
+                        acc[c] = scaled ? fmaf(su, v[u][c], acc[c]) : acc[c] + v[u][c];
+                    }
+                }
+            }
+        }
+        flush();
+        if (dup) __syncwarp();  // s_inv is rewritten by the next batch
+    }
+}
+
 template <int V, int RED>
 pyg_status_t launch_v(const CooArgs& a, int nch, int lpr, int tiles, int epg, int ovk, cudaStream_t s) {
     const int threads = 256;
@@ -367,12 +529,20 @@ int grid_for(int64_t work, int threads = 256) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
 }
 
+// hub workspace capacity: at most E / (threshold + 1) hubs, and sum ceil(d / slot) <= E / slot + hubs
+int64_t hub_cap(int64_t E) { return E / (kHeavyThreshold + 1) + 1; }
+int64_t slot_cap(int64_t E) { return E / kCooSlot + hub_cap(E); }
+
 // Column-tile width that keeps one tile's accumulation target (fp32 out or 64-bit MAX keys) and its
 // gathered source rows inside the L2 budget (PYG_COO_L2_MB): without it a plan-free scatter into an
 // output wider than L2 (Reddit: 561 MB) misses L2 on every red.global and pays a DRAM read-modify-
 // write per element.  0: no tiling (everything fits already, or even 8 columns do not).
 int l2_tile_cols(const CooArgs& a, int reduce) {
-    const int64_t budget = (int64_t)knobs().coo_l2_mb << 20;
+    // MAX: the keys are mostly only read (an atomicMax is sent only when the stored key is smaller), so
+    // wider tiles pay off up to a larger footprint (Reddit max: 32-column tiles, 89 MB, 153 ms against
+    // 16-column tiles 189 ms; SUM / MEAN: 32-column tiles, 60 MB; PubMed sum untiled at 79 MB 0.40 ms
+    // against 64-column tiles 0.16 ms; gpurun_out/r3f)
+    const int64_t budget = (int64_t)(reduce == PYG_MAX ? knobs().coo_l2_mb_max : knobs().coo_l2_mb) << 20;
     if (budget <= 0) return 0;
     const int64_t per_col = a.n_out * (reduce == PYG_MAX ? 8 : 4) + (a.gidx ? a.n_src * 4 : 0);
     if (per_col * a.ncols <= budget) return 0;
@@ -383,10 +553,11 @@ int l2_tile_cols(const CooArgs& a, int reduce) {
 
 struct CooGeom {
     int V, lpr, nch, tiles, ovk;
+    int tile_lpr;  // > 0: coo_tile_kernel<tile_lpr> (float4 rows), else coo_kernel
 };
 
 CooGeom coo_geometry(const CooArgs& a, int reduce) {
-    CooGeom g{1, 4, 1, 1, 0};
+    CooGeom g{1, 4, 1, 1, 0, 0};
     for (int cand : {4, 2}) {
         const bool cols_ok = (a.ncols % cand == 0) || (a.allow_pad_read && cand == 4 &&
                                                        a.ldx >= (int64_t)align_up(a.ncols, 4));
@@ -396,6 +567,14 @@ CooGeom coo_geometry(const CooArgs& a, int reduce) {
             (!a.part || (a.ldp % g.V == 0 && aligned(a.part, 4 * g.V)));
     const int64_t nvec = cdiv(a.ncols, g.V);
     const int W = l2_tile_cols(a, reduce);
+    if (g.V == 4 && knobs().coo_tile && a.E < (1LL << 31) && a.n_out + slot_cap(a.E) < (1LL << 31) &&
+        (W >= 16 || (W == 0 && a.ncols <= 64))) {
+        int lpr = 4;
+        while (4 * lpr < (W ? W : a.ncols)) lpr <<= 1;
+        g.tile_lpr = lpr;
+        g.tiles = (int)cdiv(a.ncols, 4 * lpr);
+        return g;
+    }
     if (W > 0 && W % g.V == 0) {
         // L2 column tiles: tile y's REDs (and gathers) stay inside an L2-resident slice; grid.y is the
         // slowest-varying block index, so tiles run one after another
@@ -416,9 +595,27 @@ CooGeom coo_geometry(const CooArgs& a, int reduce) {
     return g;
 }
 
-// hub workspace capacity: at most E / (threshold + 1) hubs, and sum ceil(d / slot) <= E / slot + hubs
-int64_t hub_cap(int64_t E) { return E / (kHeavyThreshold + 1) + 1; }
-int64_t slot_cap(int64_t E) { return E / kCooSlot + hub_cap(E); }
+// edges per warp of coo_tile_kernel (PYG_COO_CHUNK, a multiple of 32; default 4 batches of 32:
+// Reddit mean 81.8 ms against 83.8 ms at 8 and 86.5 ms at 64, gpurun_out/r3f)
+int64_t tile_chunk() { return std::max<int64_t>(32, (int64_t)knobs().coo_chunk / 32 * 32); }
+
+template <int RED>
+pyg_status_t launch_tile(const CooArgs& a, const CooGeom& g, cudaStream_t s) {
+    const int64_t chunk = tile_chunk();
+    const int64_t blocks = cdiv(a.E, 8 * chunk);
+    if (blocks <= 0) return PYG_OK;
+    dim3 grid((unsigned)blocks, (unsigned)g.tiles);
+    switch (g.tile_lpr) {
+        case 4: coo_tile_kernel<4, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
+        case 8: coo_tile_kernel<8, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
+        case 16: coo_tile_kernel<16, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
+        default: return fail(PYG_ERR_INVALID_ARGUMENT, "internal: bad tile lanes %d", g.tile_lpr);
+    }
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
 int64_t max_tiles(int64_t ncols) { return std::max<int64_t>(1, cdiv(ncols, 8)); }  // L2 tiles of >= 8 columns
 
 }  // namespace
@@ -488,10 +685,12 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
     }
     const int epg = g.lpr * kBatches;
     if (reduce == PYG_MAX) {
-        PYG_TRY(launch_red<PYG_MAX>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
+        if (g.tile_lpr) PYG_TRY(launch_tile<PYG_MAX>(a, g, s));
+        else PYG_TRY(launch_red<PYG_MAX>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
         return max_decode(a.keys, a.ldk, a.out, a.ldo, a.ncols, a.n_out, a.E, s);
     }
-    PYG_TRY(launch_red<PYG_SUM>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
+    if (g.tile_lpr) PYG_TRY(launch_tile<PYG_SUM>(a, g, s));
+    else PYG_TRY(launch_red<PYG_SUM>(a, g.V, g.nch, g.lpr, g.tiles, epg, g.ovk, s));
     if (reduce == PYG_MEAN) PYG_TRY(mean_divide(a.out, a.ldo, a.ncols, a.n_out, deg, s));
     if (hubs) {
         const int ct = (int)std::min<int64_t>(256, align_up((size_t)a.ncols, 32));
