@@ -301,6 +301,17 @@ def l2_gather_peak():
         return None, None
 
 
+def l2_red_peak():
+    """Measured gather + red.global.add.v4 throughput into L2-resident rows (scripts/l2red.cu,
+    profiles/l2_red.json): the roof of the atomic strategy once its column tiles fit L2."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "l2_red.json")) as f:
+            d = json.load(f)
+        return float(d["gather_red_w32_gbs"]), "measured (profiles/l2_red.json gather_red_w32_gbs, scripts/l2red.cu)"
+    except Exception:
+        return None, None
+
+
 def _profile_lookup(fname, workload_key):
     """Entry of profiles/<fname> for this workload; the col_block part of the key may differ between
     boxes (it follows the L2 size), so fall back to the same config / reduce / strategy / N."""
@@ -1004,6 +1015,22 @@ def main():
                     note="x_j rows (+ col indices) are served from L2 (the gathered matrix of a pass <= L2): "
                          "achieved = those bytes / call time against the measured L2 row-gather peak; "
                          "modeled_* = the north_star HBM byte model against the HBM copy peak")
+
+    # The atomic strategy in L2 column tiles (pyg_atomic_tile_cols > 0): the out slice and the gathered
+    # slice of a tile are L2-resident, so each edge costs one row gather + one red.global per tile from /
+    # into L2: the roof is the measured gather + RED rate (scripts/l2red.cu)
+    if a.strategy == "atomic" and a.op == "propagate" and world == 1:
+        tcols = pg.pyg_atomic_tile_cols(N, N, F, red)
+        rpk, rsrc = l2_red_peak()
+        if tcols > 0 and rpk:
+            red_bytes = units * 4  # gathered x_j payload = RED payload (E * F * 4)
+            r_ach = red_bytes / (kern_ms * 1e-3) / 1e9
+            roof = dict(roof, bound="l2_red", achieved=r_ach, peak=rpk, frac=r_ach / rpk, peak_source=rsrc,
+                        l2_red_bytes_per_call=red_bytes, tile_cols=tcols, tiles=-(-F // tcols),
+                        modeled_achieved=achieved, modeled_peak=peak, modeled_frac=achieved / peak,
+                        note="atomic strategy in L2 column tiles: every x_j row slice is gathered from and every "
+                             "message RED-added into L2-resident slices; achieved = E*F*4 / call time against "
+                             "the measured gather + RED rate; modeled_* = the north_star HBM byte model")
 
     result = {
         "metric": "aggregation edges*F/s", "value": value, "unit": "edges*F/s", "n_gpus": world,

@@ -138,6 +138,15 @@ pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, 
  * repay the extra read+write of `out` per pass (host-only; queries the L2 size). */
 pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_cols,
                                         int64_t row_bytes, int64_t* col_block);
+/* Column-tile width of the atomic strategy (plan NULL) for a reduce into n_out rows
+ * of `ncols` floats gathering from n_src rows (n_src = 0: edge-space src, as
+ * pyg_scatter): the tile keeps the accumulation target (fp32 out, or the 64-bit
+ * MAX keys) and the gathered slice inside the L2 budget (PYG_COO_L2_MB /
+ * PYG_COO_L2_MB_MAX), so every red.global hits L2 (P:270-271's atomics, sized
+ * for B200's L2).  *cols = 0: one tile (everything fits,
+ * or even 8 columns do not).  Host-only; never fails for valid sizes. */
+pyg_status_t pyg_atomic_tile_cols(int64_t n_out, int64_t n_src, int64_t ncols, pyg_reduce_t reduce,
+                                  int64_t* cols);
 /* Sub-plan of rows [row_lo, row_hi) sharing the parent's arrays (dst-range
  * partitioning for the multi-GPU layer).  Output row r of a call using the
  * slice is global row row_lo + r; arg outputs stay GLOBAL edge ids. */
@@ -227,7 +236,12 @@ pyg_status_t pyg_peer_wait(uint32_t* const* flags, int n, uint32_t value, void* 
  *   edges over slots of <= 2048 entries (one atomic counter per hub hands out
  *   positions) whose fp32 partials are combined in fp64, so no fp32 atomic chain
  *   exceeds 2048 terms (Q12).  The size is the worst case for E edges
- *   (E/2048 + E/2049 slots x F_out floats); a MAX call needs none of it.
+ *   (E/2048 + E/2049 slots x F_out floats).  When the output is split into L2
+ *   column tiles (pyg_atomic_tile_cols > 0) it also holds the compact-tile
+ *   scratch -- the tile's accumulation target (n_out x W floats, or 64-bit keys
+ *   for MAX) and its gathered slice (n_src x W floats, sized with n_src = n_out);
+ *   with less workspace (e.g. bipartite n_src > n_out) the tiles run in place,
+ *   slower but with the same results.
  * For pyg_propagate_backward pass (plan_T, E, n_src, F).  Host-only. */
 pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t E, int64_t n_out, int64_t F_out,
                                 pyg_reduce_t reduce, uint32_t flags, size_t* bytes);

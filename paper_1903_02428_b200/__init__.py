@@ -20,7 +20,7 @@ from ._abi import (FORCE_ATOMIC, FORCE_SEGMENT, MAX, MEAN, NO_TMA, PHI_CONCAT_XI
                    launch_count, lib)
 
 __all__ = [
-    "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
+    "Plan", "pyg_degree", "pyg_plan_build", "pyg_plan_suggest_col_block", "pyg_atomic_tile_cols", "pyg_scatter", "pyg_scatter_backward", "pyg_propagate",
     "pyg_propagate_backward", "pyg_gcn_norm", "pyg_collate", "pyg_global_pool", "pyg_workspace_size",
     "pyg_halo_build", "pyg_gather_rows", "pyg_ipc_handle", "pyg_ipc_open", "pyg_ipc_close", "pyg_halo_push", "pyg_segment_softmax", "pyg_segment_softmax_backward",
     "pyg_gat_propagate", "pyg_gat_backward", "pyg_gat_backward_workspace_size", "pyg_gat_propagate_workspace_size", "pyg_peer_signal", "pyg_peer_wait", "pyg_appnp", "pyg_dense_transform", "pyg_gcn_layer", "pyg_gat_transform", "launch_count", "PygError", "SUM", "MEAN", "MAX", "PHI_CONCAT_XI", "VALIDATE", "FORCE_ATOMIC",
@@ -155,6 +155,13 @@ def pyg_plan_suggest_col_block(E: int, n_rows: int, n_cols: int, row_bytes: int)
     check(lib.pyg_plan_suggest_col_block(E, n_rows, n_cols, row_bytes, ctypes.byref(cb)),
           "pyg_plan_suggest_col_block")
     return cb.value
+
+
+def pyg_atomic_tile_cols(n_out: int, n_src: int, ncols: int, reduce="sum") -> int:
+    """Column-tile width of the atomic strategy (0: one tile); see pyg_gs.h."""
+    c = ctypes.c_int64()
+    check(lib.pyg_atomic_tile_cols(n_out, n_src, ncols, _red(reduce), ctypes.byref(c)), "pyg_atomic_tile_cols")
+    return c.value
 
 
 def pyg_plan_build(row_index: torch.Tensor, col_index: Optional[torch.Tensor], n_rows: int,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "pyg_plan_workspace_size": ([I64, I64, I64, I64, ctypes.POINTER(SZ)], C),
     "pyg_plan_build": ([P, P, I64, I64, I64, I64, U32, P, SZ, PP, P], C),
     "pyg_plan_suggest_col_block": ([I64, I64, I64, I64, ctypes.POINTER(I64)], C),
+    "pyg_atomic_tile_cols": ([I64, I64, I64, ctypes.c_int, ctypes.POINTER(I64)], C),
     "pyg_plan_slice": ([P, I64, I64, PP], C),
     "pyg_plan_passes": ([P, I64, I64, PP], C),
     "pyg_plan_view": ([P, ctypes.POINTER(PlanView)], C),

@@ -55,6 +55,7 @@ static Knobs read_knobs() {
     k.gat_warps = get("PYG_GAT_WARPS", 8);
     k.coo_l2_mb = get("PYG_COO_L2_MB", 72);
     k.coo_tile = get("PYG_COO_TILE", 1);
+    k.coo_compact = get("PYG_COO_COMPACT", 1);
     k.coo_chunk = get("PYG_COO_CHUNK", 128);
     k.coo_l2_mb_max = get("PYG_COO_L2_MB_MAX", 96);
     k.gat_fwd_warp_kb = get("PYG_GAT_FWD_WARP_KB", 5);
@@ -179,6 +180,14 @@ pyg_status_t pyg_plan_workspace_size(int64_t E, int64_t n_rows, int64_t n_cols, 
             "plan_workspace_size: bad args");
     REQUIRE(E <= kMaxI32 && n_rows <= kMaxI32 && n_cols <= kMaxI32, PYG_ERR_UNSUPPORTED, "plan: sizes must be < 2^31");
     return plan_workspace(E, n_rows, n_cols, col_block, bytes);
+}
+
+pyg_status_t pyg_atomic_tile_cols(int64_t n_out, int64_t n_src, int64_t ncols, pyg_reduce_t reduce, int64_t* cols) {
+    REQUIRE(cols && n_out >= 0 && n_src >= 0 && ncols >= 0 && ncols <= kMaxI32, PYG_ERR_INVALID_ARGUMENT,
+            "atomic_tile_cols: bad args");
+    REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "atomic_tile_cols: bad reduce");
+    *cols = coo_tile_cols(n_out, n_src, ncols, reduce);
+    return PYG_OK;
 }
 
 pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_cols, int64_t row_bytes,
@@ -343,7 +352,7 @@ pyg_status_t pyg_workspace_size(const pyg_plan_t* plan, int64_t E, int64_t n_out
     REQUIRE(reduce >= PYG_SUM && reduce <= PYG_MAX, PYG_ERR_INVALID_ARGUMENT, "workspace_size: bad reduce");
     size_t b;
     if (use_plan(plan, flags)) b = std::max(coo_deg_bytes(n_out), segment_ws_bytes(plan, F_out, (int)reduce));
-    else b = coo_deg_bytes(n_out) + coo_ws_bytes(E, n_out, F_out, (int)reduce);
+    else b = coo_deg_bytes(n_out) + coo_ws_bytes(E, n_out, F_out, (int)reduce, n_out);  // n_src = n_out
     *bytes = b + 256;
     return PYG_OK;
 }

@@ -66,6 +66,7 @@ struct Knobs {
     int gat_fwd_warp_kb = 5;   // PYG_GAT_FWD_WARP_KB: ring bytes per warp of the one-pass GAT forward
     int gat_fwd_sm_kb = 160;   // PYG_GAT_FWD_SM_KB
     int coo_tile = 1;     // PYG_COO_TILE: 0 keeps every atomic launch on the generic coo_kernel
+    int coo_compact = 1;  // PYG_COO_COMPACT: L2 column tiles through packed scratch -- 1 auto (large spans), 2 always, 0 never
     int coo_chunk = 128;  // PYG_COO_CHUNK: edges per warp of the tile kernel
     int coo_l2_mb = 72;   // PYG_COO_L2_MB: L2 budget of the atomic path's column tiles (0: no tiling)
     int coo_l2_mb_max = 96;  // PYG_COO_L2_MB_MAX: the same for MAX (keys mostly read, not written)

@@ -122,13 +122,18 @@ struct CooArgs {
     const int32_t* hub_base = nullptr;  // [n_out] first slot of a hub row (read for hubs only)
     const uint32_t* hub_bits = nullptr; // [n_out / 32] 1 bit per row: is a hub
     int32_t* hub_cursor = nullptr;      // [slots x column tiles] entry counters (by first slot)
+    const int32_t* hub_count = nullptr; // device: number of hub rows (hub_assign_kernel)
+    int tile_y = 0, n_tiles = 0;        // compact column tiles launched one by one (0: grid.y tiles)
     float* part = nullptr;              // [slots x ldp] slot partials = virtual rows n_out + slot
     int64_t ldp = 0;
 };
 // Whole atomic reduce of one column block: zero the target, degrees and hub slots (SUM / MEAN),
 // the COO kernel, then the epilogue (mean divide + fp64 hub combine, or the MAX key decode).
 pyg_status_t coo_reduce(const CooArgs& a, int reduce, void* ws, size_t ws_bytes, cudaStream_t s);
-size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce);
+// n_src: rows the call gathers from (0: edge-space rows), sizes the compact-tile scratch
+size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce, int64_t n_src);
+// L2 column-tile width of the atomic path (0: one tile)
+int64_t coo_tile_cols(int64_t n_out, int64_t n_src, int64_t ncols, int reduce);
 // counts (and first edge id) per target for the COO path
 pyg_status_t coo_degree(const int64_t* sidx, int64_t E, int64_t n, int32_t* deg, int32_t* first,
                         cudaStream_t s);

@@ -7,6 +7,8 @@
 //                traffic); payload = W * 4 bytes per row;
 //   gather_red : the COO kernel's per-edge pattern -- load a random W-float row of table A
 //                (LDG.128 per lane) and red.global.add it into a random row of table B;
+//   gather_red_ld608 : gather_red on 32-float slices of 608-float rows (a column tile of Reddit's
+//                X / out: the same bytes over 19x the address range -- TLB reach);
 //   bulk_red   : one lane per warp issues cp.reduce.async.bulk.global.shared::cta.add.f32 of a
 //                W-float smem row into a random row (the TMA bulk-reduce engine instead of REDs).
 // Tables: 233k rows (Reddit's N) x W floats.  Best over 1..8 CTAs of 256 threads per SM.
@@ -56,6 +58,22 @@ __global__ void gather_red_kernel(const float* __restrict__ A, float* B, uint32_
         const uint32_t r = hash32((uint32_t)k * 2654435761u + 777u) % rows;
         const float4 x = __ldg(reinterpret_cast<const float4*>(A + (int64_t)s * W) + l);
         red4(B + (int64_t)r * W + 4 * l, x.x, x.y, x.z, x.w);
+    }
+}
+
+// the same pattern on W-float slices of rows `ld` floats apart (the atomic kernel's column tile of a
+// wide row-major X / out: same bytes, spread over ld / W times the address range)
+template <int W>
+__global__ void gather_red_strided_kernel(const float* __restrict__ A, float* B, uint32_t rows, int64_t ld, int64_t n) {
+    constexpr int L = W / 4;
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / L;
+    const int l = threadIdx.x % L;
+    for (int64_t k = g; k < n; k += ng) {
+        const uint32_t s = hash32((uint32_t)k * 2246822519u + 99u) % rows;
+        const uint32_t r = hash32((uint32_t)k * 2654435761u + 777u) % rows;
+        const float4 x = __ldg(reinterpret_cast<const float4*>(A + (int64_t)s * ld) + l);
+        red4(B + (int64_t)r * ld + 4 * l, x.x, x.y, x.z, x.w);
     }
 }
 
@@ -133,6 +151,19 @@ int main() {
     printf(", \"red_w64_gbs\": %.1f, \"red_w64_ctas\": %d", r, bb);
     r = best_rate(sms, [&](int g) { gather_red_kernel<32><<<g, 256>>>(A, B, rows, n); }, (double)n * 128, &bb);
     printf(", \"gather_red_w32_gbs\": %.1f, \"gather_red_w32_ctas\": %d", r, bb);
+    {
+        const int64_t ld = 608;  // Reddit's padded row: 19 column tiles of 32 floats
+        float *SA = nullptr, *SB = nullptr;
+        CK(cudaMalloc(&SA, (size_t)rows * ld * 4));
+        CK(cudaMalloc(&SB, (size_t)rows * ld * 4));
+        CK(cudaMemset(SA, 0, (size_t)rows * ld * 4));
+        CK(cudaMemset(SB, 0, (size_t)rows * ld * 4));
+        r = best_rate(sms, [&](int g) { gather_red_strided_kernel<32><<<g, 256>>>(SA, SB, rows, ld, n); },
+                      (double)n * 128, &bb);
+        printf(", \"gather_red_w32_ld608_gbs\": %.1f, \"gather_red_w32_ld608_ctas\": %d", r, bb);
+        CK(cudaFree(SA));
+        CK(cudaFree(SB));
+    }
     r = best_rate(sms, [&](int g) { bulk_red_kernel<32><<<g, 256>>>(B, rows, n); }, (double)n * 128, &bb);
     printf(", \"bulk_red_w32_gbs\": %.1f, \"bulk_red_w32_ctas\": %d", r, bb);
     r = best_rate(sms, [&](int g) { bulk_red_kernel<64><<<g, 256>>>(B, rows, n); }, (double)n * 256, &bb);

@@ -13,7 +13,7 @@ import paper_1903_02428_b200 as pg  # noqa: E402
 import synth  # noqa: E402
 from tests.tolerance import check_close, check_exact  # noqa: E402
 
-assert os.environ.get("PYG_COO_L2_MB") == "1"
+assert os.environ.get("PYG_COO_L2_MB") == "1" and os.environ.get("PYG_COO_L2_MB_MAX") == "1"
 DEV = "cuda:0"
 
 

@@ -89,3 +89,26 @@ def test_product_does_not_use_the_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r'#\s*include\s*[<"][^>"]*pyg_gs', txt)
             assert not re.search(r"\bPYG_(OK|ERR_[A-Z_]+|SUM|MEAN|MAX|PHI_[A-Z_]+|VALIDATE|FORCE_[A-Z_]+)\b", re.sub(r"/\*.*?\*/", "", txt, flags=re.S))
+
+
+def test_atomic_tile_cols_host_query():
+    """The atomic strategy's L2 column tiles (coo.cu l2_tile_cols) at the default budgets (72 MB,
+    96 MB for MAX): Reddit-shaped out + X slices -> 32-column tiles (sum: 466k rows x 4 B x 32 = 60 MB;
+    max: 8-byte keys, 89 MB); PubMed-shaped sum (79 MB untiled) -> 64; R-MAT (80 MB per column) and
+    Cora (fits) -> one tile; bad arguments are refused on the host."""
+    if any(k in os.environ for k in ("PYG_COO_L2_MB", "PYG_COO_L2_MB_MAX")):
+        pytest.skip("budget overridden in the environment")
+    import paper_1903_02428_b200 as pg
+
+    assert pg.pyg_atomic_tile_cols(232965, 232965, 602, "mean") == 32
+    assert pg.pyg_atomic_tile_cols(232965, 232965, 602, "max") == 32
+    assert pg.pyg_atomic_tile_cols(19717, 19717, 500, "sum") == 64
+    assert pg.pyg_atomic_tile_cols(10_000_000, 10_000_000, 128, "sum") == 0
+    assert pg.pyg_atomic_tile_cols(2708, 2708, 16, "max") == 0
+    # edge-space src (scatter): only the output slice counts
+    assert pg.pyg_atomic_tile_cols(232965, 0, 602, "sum") == 64
+    from paper_1903_02428_b200 import _abi
+
+    c = ctypes.c_int64()
+    assert _abi.lib.pyg_atomic_tile_cols(-1, 0, 4, 0, ctypes.byref(c)) == 1
+    assert _abi.lib.pyg_atomic_tile_cols(10, 0, 4, 7, ctypes.byref(c)) == 1
