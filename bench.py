@@ -1001,7 +1001,8 @@ def main():
     # Which roof binds: when the matrix one pass gathers from fits in L2 (a source block of a blocked plan,
     # or the whole X / transformed H) the x_j rows come from L2, so the physical roof is the L2 -> SM
     # gather bandwidth, measured by scripts/l2peak.cu (profiles/l2_peak.json); the HBM-model number stays
-    # as modeled_frac.  The atomic strategy is bound by the DRAM read-modify-write of `out` (HBM).
+    # as modeled_frac.  The atomic strategy is bound by the DRAM read-modify-write of `out` (HBM) unless
+    # its column tiles fit L2 (below).
     l2pk, l2src = l2_gather_peak()
     l2_size = torch.cuda.get_device_properties(dev).L2_cache_size
     Fg = a.hidden if gcn is not None else (gatl["H"] * gatl["C"] if gatl else F)

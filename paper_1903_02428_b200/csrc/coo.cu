@@ -721,7 +721,7 @@ CooGeom coo_geometry(const CooArgs& a, int reduce) {
     const int64_t nvec = cdiv(a.ncols, g.V);
     const int W = l2_tile_cols(a, reduce);
     if (g.V == 4 && knobs().coo_tile && a.E < (1LL << 31) && a.n_out + slot_cap(a.E) < (1LL << 31) &&
-        (W >= 16 || (W == 0 && a.ncols <= 64))) {
+        (W >= 16 || (W == 0 && a.ncols <= (knobs().coo_tile == 2 ? 128 : 64)))) {
         int lpr = 4;
         while (4 * lpr < (W ? W : a.ncols)) lpr <<= 1;
         g.tile_lpr = lpr;
@@ -762,6 +762,7 @@ pyg_status_t launch_tile(const CooArgs& a, const CooGeom& g, cudaStream_t s) {
         case 4: coo_tile_kernel<4, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
         case 8: coo_tile_kernel<8, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
         case 16: coo_tile_kernel<16, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
+        case 32: coo_tile_kernel<32, RED><<<grid, 256, 0, s>>>(a, chunk, g.ovk); break;
         default: return fail(PYG_ERR_INVALID_ARGUMENT, "internal: bad tile lanes %d", g.tile_lpr);
     }
     PYG_LAUNCHED();
