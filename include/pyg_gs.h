@@ -134,8 +134,10 @@ pyg_status_t pyg_plan_build(const int64_t* row_index, const int64_t* col_index, 
                             int64_t n_rows, int64_t n_cols, int64_t col_block, uint32_t flags,
                             void* workspace, size_t bytes, pyg_plan_t** plan, void* stream);
 /* Suggest col_block for gathering rows of `row_bytes` bytes (ldx * 4) on the
- * current device: 0 when X fits in L2 or when the reuse (E / n_cols) does not
- * repay the extra read+write of `out` per pass (host-only; queries the L2 size). */
+ * current device: blocks of ~0.4 x L2; 0 when X fits one block or when the
+ * reuse (E / n_cols) does not repay the extra read+write of `out` per pass, with
+ * half of L2 counted as the reuse capacity of an unblocked random gather
+ * (host-only; queries the L2 size). */
 pyg_status_t pyg_plan_suggest_col_block(int64_t E, int64_t n_rows, int64_t n_cols,
                                         int64_t row_bytes, int64_t* col_block);
 /* Column-tile width of the atomic strategy (plan NULL) for a reduce into n_out rows

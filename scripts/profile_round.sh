@@ -32,13 +32,20 @@ done
 # atomic COO strategy: atomic throughput evidence (north_star: "atomic throughput")
 timeout 900 $FULL -k regex:coo_kernel -s 3 -c 1 -o $O/full_rmat_sum_atomic python bench.py --config rmat --reduce sum --strategy atomic $Q > /dev/null 2>&1
 export_rep $O/full_rmat_sum_atomic
-timeout 900 $FULL -k regex:coo_kernel -s 3 -c 1 -o $O/full_reddit_mean_atomic python bench.py --strategy atomic $Q > /dev/null 2>&1
+timeout 900 $FULL -k regex:coo_tile -s 19 -c 1 -o $O/full_reddit_mean_atomic python bench.py --strategy atomic $Q > /dev/null 2>&1
 export_rep $O/full_reddit_mean_atomic
+timeout 600 ncu --metrics $M --clock-control none --csv --log-file $O/launches_reddit_mean_atomic.csv python bench.py --strategy atomic $Q > /dev/null 2>&1
 for red in sum max; do
   timeout 600 python bench.py --config rmat --reduce $red --steps 10 --no-e2e --no-cpu --no-variants > $O/bench_rmat_$red.json 2> $O/bench_rmat_$red.err
   timeout 600 python bench.py --config rmat --reduce $red --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_rmat_${red}_atomic.json 2> $O/bench_rmat_${red}_atomic.err
 done
-timeout 600 python bench.py --strategy atomic --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_reddit_mean_atomic.json 2> $O/bench_reddit_mean_atomic.err
+timeout 600 python bench.py --strategy atomic --steps 5 --no-cpu --no-variants > $O/bench_reddit_mean_atomic.json 2> $O/bench_reddit_mean_atomic.err
+timeout 600 python bench.py --strategy atomic --reduce max --steps 5 --no-e2e --no-cpu --no-variants > $O/bench_reddit_max_atomic.json 2> $O/bench_reddit_max_atomic.err
+for cfg in pubmed clouds cora; do
+  timeout 300 python bench.py --config $cfg --strategy atomic --steps 50 --no-e2e --no-variants --no-cpu > $O/bench_${cfg}_atomic.json 2> $O/bench_${cfg}_atomic.err
+done
+nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/l2red scripts/l2red.cu && timeout 300 /tmp/l2red > $O/l2red.json 2> $O/l2red.err
+nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/l2peak scripts/l2peak.cu && timeout 300 /tmp/l2peak > $O/l2peak.json 2> $O/l2peak.err
 for cfg in pubmed clouds cora; do  # pubmed = GCN fwd+bwd
   timeout 300 python bench.py --config $cfg --steps 50 --no-e2e --no-variants > $O/bench_$cfg.json 2> $O/bench_$cfg.err
 done
@@ -74,4 +81,7 @@ timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pyt
 timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_transform.py -q -x \
   -k "(tma_pipeline and 128) or split_hub or rmat_h4c16 or (transform and 1000) or far_logits or one_pass or (bulk and 602)" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
 
+# the atomic path's L2 column tiles (packed and in place) under memcheck, in the test's child process
+PYG_COO_L2_MB=1 PYG_COO_L2_MB_MAX=1 PYG_COO_COMPACT=2 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 python tests/_coo_tiles_child.py > $O/sanitizer_memcheck_coo_tiles.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck_coo_tiles.txt
+PYG_COO_L2_MB=1 PYG_COO_L2_MB_MAX=1 PYG_COO_COMPACT=2 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 99 python tests/_coo_tiles_child.py > $O/sanitizer_racecheck_coo_tiles.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck_coo_tiles.txt
 gzip -f $O/launches_*.csv

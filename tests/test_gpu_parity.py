@@ -532,8 +532,8 @@ def test_batching_equivalence_on_gpu(pg):
 
 
 def test_suggest_col_block_decisions(pg):
-    """pyg_plan_suggest_col_block (host logic + the device's L2 size): X that fits L2 -> 0 (one
-    pass); Reddit-shaped reuse (E / n = 492, |X| = 566 MB) -> blocks of about 0.4 x L2; R-MAT-shaped
+    """pyg_plan_suggest_col_block (host logic + the device's L2 size): X that fits one 0.4 x L2
+    block -> 0 (one pass); Reddit-shaped reuse (E / n = 492, |X| = 566 MB) -> blocks of about 0.4 x L2; R-MAT-shaped
     low reuse (average degree 20, |X| = 5.1 GB) -> 0, since the extra read+write of out per pass
     costs more than the DRAM it saves."""
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
@@ -542,6 +542,10 @@ def test_suggest_col_block_decisions(pg):
     assert cb > 0
     assert 0.2 * l2 <= cb * 608 * 4 <= 0.45 * l2
     assert pg.pyg_plan_suggest_col_block(200_000_000, 10_000_000, 10_000_000, 128 * 4) == 0
+    # a matrix just under L2 (Reddit's GCN-transformed H, 232,965 x 128) is still blocked: a random
+    # gather keeps only about half of L2 as reuse capacity
+    cb = pg.pyg_plan_suggest_col_block(114_615_892 + 232_965, 232_965, 232_965, 128 * 4)
+    assert 0 < cb and cb * 128 * 4 <= 0.45 * l2
 
 
 @pytest.mark.parametrize("sizes,F", [([1024] * 64, 64), ([0, 100_003, 7, 0, 2048], 19), ([3, 1, 0, 9], 300)])
