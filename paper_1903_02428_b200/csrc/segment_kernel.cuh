@@ -19,6 +19,8 @@
 //   * accum/finalize let source-blocked plans add pass after pass into `out`.
 #pragma once
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace pyg {
@@ -88,6 +90,9 @@ __device__ __forceinline__ unsigned group_mask() {
 #ifndef PYG_MAX_U
 #define PYG_MAX_U 1
 #endif
+#ifndef PYG_MAX_FRONT
+#define PYG_MAX_FRONT 1
+#endif
 
 // MAX of a wide segment (17-20 floats per lane, e.g. Reddit's 602 columns) with the argmax kept as a
 // 16-bit position inside the segment, two per register (segments are <= 2048 positions: light rows
@@ -140,6 +145,12 @@ __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t 
                 }
             }
     };
+    // all chunks but the last are full for every lane when the tile reaches that far (Reddit: 4 of 5):
+    // a compile-time-true load predicate for them, so the loop does not rematerialise per-chunk column
+    // checks under the 80-register cap
+    const bool front_full = PYG_MAX_FRONT && (a.ncols >= c0 + (NCH - 1) * LPR * V);
+    auto run = [&](auto front) {
+    constexpr bool FRONT = decltype(front)::value;
     for (int64_t base = beg; base < end; base += LPR) {
         const int n = (int)min((int64_t)LPR, end - base);
         int mg = 0;
@@ -160,7 +171,7 @@ __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t 
                 const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch)
-                    if (cv[ch]) ld<V>(v[u][ch], row + ch * LPR * V);
+                    if ((FRONT && ch < NCH - 1) || cv[ch]) ld<V>(v[u][ch], row + ch * LPR * V);
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) take(v[u], sv[u], pos0 + (uint32_t)(t + u));
@@ -171,10 +182,13 @@ __device__ __forceinline__ void accumulate_max_packed(const SegArgs& a, int64_t 
             const float* row = reinterpret_cast<const float*>(Xl + (uint64_t)(uint32_t)g * row_bytes);
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch)
-                if (cv[ch]) ld<V>(v[0][ch], row + ch * LPR * V);
+                if ((FRONT && ch < NCH - 1) || cv[ch]) ld<V>(v[0][ch], row + ch * LPR * V);
             take(v[0], sc, pos0 + (uint32_t)t);
         }
     }
+    };
+    if (front_full) run(std::true_type{});
+    else run(std::false_type{});
     // positions -> edge ids (0xffff: no edge yet)
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch)
