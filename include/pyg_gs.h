@@ -450,8 +450,9 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
  *   h [n x F] stride ldh; out [n x F] stride ldo (overwritten); scratch [n x F]
  *   stride ldo, required for K > 1 (ping-pong buffer); K >= 0 (K = 0 copies h);
  *   0 <= alpha <= 1.  plan: forward plan over n targets / n sources.  Per-call
- *   fp32 rounding of every z_k.  workspace: pyg_workspace_size(plan, n, F, SUM).
- *   Asynchronous. */
+ *   fp32 rounding of every z_k.  workspace: pyg_workspace_size(plan, n, F, SUM);
+ *   with E * 4 + 256 more bytes the weights are gathered into plan order once and
+ *   every step streams them (same results).  Asynchronous. */
 pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const float* edge_weight,
                        int64_t K, float alpha, const pyg_plan_t* plan, float* out, int64_t ldo,
                        float* scratch, void* workspace, size_t workspace_bytes, void* stream);

@@ -469,8 +469,9 @@ def pyg_appnp(h: torch.Tensor, plan: Plan, K: int = 10, alpha: float = 0.1, edge
     _, _, ldo = _rows(out, "out")
     if scratch is None and K > 1:
         scratch = torch.empty((n, ldo), dtype=torch.float32, device=dev)[:, :F]
-    if workspace is None:
-        workspace = _workspace(pyg_workspace_size(plan, n, F, SUM), dev)
+    if workspace is None:  # + E floats: the weights in plan order (streamed by every step)
+        extra = plan.view()["E"] * 4 + 256 if edge_weight is not None else 0
+        workspace = _workspace(pyg_workspace_size(plan, n, F, SUM) + extra, dev)
     check(lib.pyg_appnp(_ptr(h), n, F, ldh, _ptr(edge_weight), K, alpha, plan.handle, _ptr(out), ldo, _ptr(scratch),
                         _ptr(workspace), workspace.numel(), _stream(dev)), "pyg_appnp")
     return out

@@ -815,6 +815,17 @@ pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const 
         return PYG_OK;
     }
     const int32_t* eid = plan->perm_identity ? nullptr : plan->perm;
+    const float* wk = edge_weight;
+    // the K steps read the same weights in the same plan order: with room in the workspace they are
+    // gathered into position order once (w_pos[p] = w[perm[p]]), so every step streams 4 bytes per
+    // position instead of an edge id plus a random 32-byte sector of w
+    const size_t seg_need = segment_ws_bytes(plan, F, PYG_SUM) + 256;
+    if (edge_weight && eid && plan->E > 0 && ws && ws_bytes >= seg_need + (size_t)plan->E * 4 + 256) {
+        float* w_pos = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(seg_need, 256));
+        PYG_TRY(gather_by_index(edge_weight, eid, plan->E, w_pos, s));
+        wk = w_pos;
+        eid = nullptr;  // SUM reads edge ids only for the weights
+    }
     const float* z = h;
     int64_t ldz = ldh;
     for (int64_t k = 0; k < K; ++k) {
@@ -822,7 +833,7 @@ pyg_status_t pyg_appnp(const float* h, int64_t n, int64_t F, int64_t ldh, const 
         float* dst = ((K - 1 - k) % 2 == 0) ? out : scratch;
         SegArgs a;
         a.X = z; a.ldx = ldz; a.ncols = (int)F;
-        a.rowptr = plan->rowptr; a.gidx = plan->col; a.eid = eid; a.w = edge_weight;
+        a.rowptr = plan->rowptr; a.gidx = plan->col; a.eid = eid; a.w = wk;
         a.out = dst; a.ldo = ldo; a.n_rows = n; a.E_sentinel = plan->E;
         a.heavy_threshold = plan->heavy_threshold; a.allow_pad_read = 1;
         a.blend = alpha != 0.0f ? h : nullptr; a.ldb = ldh;

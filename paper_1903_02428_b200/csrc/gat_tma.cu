@@ -26,6 +26,10 @@
 #include "segment_tma.cuh"
 
 namespace pyg {
+#ifndef PYG_GAT_STCS
+#define PYG_GAT_STCS 1
+#endif
+
 namespace gat {
 
 using tma::bar_expect;
@@ -634,7 +638,11 @@ __global__ void __launch_bounds__(256, 1) gat_fwd_tma_kernel(const __grid_consta
         const float cs = cpre > 0.0f ? cpre : slope * cpre;  // the row's shift c_i (>= every logit)
         const float p = mine ? expf(l - cs) : 0.0f;
         const int e = my_i == 0 ? eids.x : my_i == 1 ? eids.y : my_i == 2 ? eids.z : eids.w;
+#if PYG_GAT_STCS
+        if (mine) __stcs(a.alpha + (int64_t)e * H + my_h, p);  // streamed past L2 (z rows of hubs stay)
+#else
         if (mine) a.alpha[(int64_t)e * H + my_h] = p;
+#endif
         sts32f(scr + 4u * (uint32_t)lane, p);
         __syncwarp();
         // (3) aggregation in position order (unrolled: a rolled loop with one flush path measured slower,
@@ -1184,7 +1192,11 @@ __global__ void __launch_bounds__(256) gat_fwd_block_kernel(BlockArgs a) {
                     const float pre = __ldg(a.s_src + (int64_t)jm * H + my_h) + sd;
                     const float l = pre > 0.0f ? pre : a.slope * pre;
                     p = expf(l - cs);
+#if PYG_GAT_STCS
+                    __stcs(a.alpha + (int64_t)em * H + my_h, p);  // streamed: keeps the L2-resident z block
+#else
                     a.alpha[(int64_t)em * H + my_h] = p;
+#endif
                 }
                 ps += p;
 #pragma unroll

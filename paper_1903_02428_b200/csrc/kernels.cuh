@@ -98,6 +98,8 @@ struct SegArgs {
 pyg_status_t segment_reduce(const SegArgs& a, int reduce, const pyg_plan* plan, void* ws,
                             size_t ws_bytes, cudaStream_t s);
 size_t segment_ws_bytes(const pyg_plan* plan, int64_t ncols, int reduce);
+// out[p] = v[idx[p]] (per-edge values into plan position order)
+pyg_status_t gather_by_index(const float* v, const int32_t* idx, int64_t n, float* out, cudaStream_t s);
 
 // ---- atomic COO --------------------------------------------------------------------
 struct CooArgs {

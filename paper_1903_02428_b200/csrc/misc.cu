@@ -274,6 +274,20 @@ pyg_status_t xdst_grad(const float* g, int64_t ldg, int F, int64_t n, const int3
     return PYG_OK;
 }
 
+__global__ void gather_by_index_kernel(const float* __restrict__ v, const int32_t* __restrict__ idx, int64_t n,
+                                       float* __restrict__ out) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        out[p] = __ldg(v + __ldg(idx + p));
+}
+
+pyg_status_t gather_by_index(const float* v, const int32_t* idx, int64_t n, float* out, cudaStream_t s) {
+    if (n <= 0) return PYG_OK;
+    gather_by_index_kernel<<<grid_for(n), 256, 0, s>>>(v, idx, n, out);
+    PYG_LAUNCHED();
+    PYG_CUDA(cudaGetLastError());
+    return PYG_OK;
+}
+
 pyg_status_t max_route_grad(const float* g, int64_t ldg, const int64_t* arg, int64_t lda, int F, int64_t n_dst,
                             const int64_t* src, const float* w, int64_t E, float* gx, int64_t ldgx, cudaStream_t s) {
     if (n_dst <= 0 || F <= 0) return PYG_OK;

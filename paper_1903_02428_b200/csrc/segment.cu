@@ -117,7 +117,13 @@ Geometry choose(const SegArgs& a) {
         // 256-bit loads only when they fill clearly more lanes: at equal utilisation V = 4 won
         // (GCN aggregation at F = 512 on 9 L2-resident passes: 13.0 ms with V = 4, NCH = 4 vs 20.8 ms
         // with V = 8, NCH = 2, whose SASS keeps the loaded rows in local memory; gpurun_out/r2h)
-        if (V == 8 ? g.util > best.util * 1.05 : (g.util >= best.util - 1e-9 || (V <= 4 && g.util >= 0.75))) best = g;
+        // Rows of <= 64 floats are the exception: 8 lanes x 256 bits per row keep twice the rows per warp
+        // in flight (point clouds F = 64: 0.072 -> 0.048 ms per step; F = 128 / 500 measured slower with
+        // V = 8, 3.72 -> 4.77 / 0.064 -> 0.074 ms; gpurun_out/r3r)
+        const bool narrow8 = V == 8 && a.ncols <= 64 && g.util >= best.util - 1e-9;
+        if (V == 8 ? (g.util > best.util * 1.05 || narrow8)
+                   : (g.util >= best.util - 1e-9 || (V <= 4 && g.util >= 0.75)))
+            best = g;
     }
     // Few rows with narrow features (e.g. 10,000 rows x 16 columns): one group of LPR lanes per row
     // leaves most of the GPU idle (4 lanes per row at V = 4 -> 40k threads).  Narrow the vector

@@ -74,14 +74,7 @@ timeout 600 ncu --metrics $M --clock-control none -k regex:"tf32|seg_|combine|de
 timeout 900 $FULL -k regex:tf32 -s 1 -c 1 -o $O/full_tf32_reddit python bench.py --config reddit --op gcn $Q > /dev/null 2>&1
 export_rep $O/full_tf32_reddit
 timeout 600 python scripts/fig3.py --out $O/fig3.json > $O/fig3.log 2>&1
-# memory-safety evidence: compute-sanitizer memcheck / racecheck on representative small tests
-timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_appnp.py tests/test_gpu_transform.py tests/test_gpu_dist.py -q -x \
-  -k "scatter_printed or split_hub or (tma_pipeline and 128) or (source_blocked and 37) or collate or concat_and_edge_attr or backward or cora or rmat_h4c16 or softmax or power_law or pubmed_shaped or (transform and 300) or gcn_layer or halo_plan or far_logits or one_pass or (bulk and 602)" \
-  > $O/sanitizer_memcheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck.txt
-timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 99 python -m pytest tests/test_gpu_parity.py tests/test_gpu_attention.py tests/test_gpu_transform.py -q -x \
-  -k "(tma_pipeline and 128) or split_hub or rmat_h4c16 or (transform and 1000) or far_logits or one_pass or (bulk and 602)" > $O/sanitizer_racecheck.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck.txt
-
-# the atomic path's L2 column tiles (packed and in place) under memcheck, in the test's child process
-PYG_COO_L2_MB=1 PYG_COO_L2_MB_MAX=1 PYG_COO_COMPACT=2 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 python tests/_coo_tiles_child.py > $O/sanitizer_memcheck_coo_tiles.txt 2>&1; echo "exit=$?" >> $O/sanitizer_memcheck_coo_tiles.txt
-PYG_COO_L2_MB=1 PYG_COO_L2_MB_MAX=1 PYG_COO_COMPACT=2 timeout 900 compute-sanitizer --tool racecheck --error-exitcode 99 python tests/_coo_tiles_child.py > $O/sanitizer_racecheck_coo_tiles.txt 2>&1; echo "exit=$?" >> $O/sanitizer_racecheck_coo_tiles.txt
+# (compute-sanitizer is closed on this pool since round 2's last session: runs under it left GPUs
+# needing a reset.  The round-2 memcheck / racecheck logs are profiles/r2a_sanitizer_* and
+# r2ab_sanitizer_*; memory safety of later kernels rests on bounds-checked parity tests.)
 gzip -f $O/launches_*.csv
