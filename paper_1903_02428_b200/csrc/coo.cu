@@ -381,6 +381,50 @@ __global__ void __launch_bounds__(256, 3) coo_tile_kernel(CooArgs a, int64_t chu
             }
             continue;
         }
+        if (RED != PYG_MAX && LPR < 32 && n == 32 && dup && off32 && __all_sync(full, m == full)) {
+            // 32 edges into ONE target (target-sorted input, high in-degree: Fig. 3's coalesced case):
+            // each group sums its positions, a butterfly over the groups adds them up, one RED
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int k0 = 0; k0 < PER; k0 += U) {
+                float v[U][4];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int gg = __shfl_sync(full, g, grp * PER + k0 + u);
+                    const float* row = reinterpret_cast<const float*>(reinterpret_cast<const char*>(Xc) +
+                                                                     (uint64_t)(uint32_t)gg * xrb);
+                    if (full_ld) {
+                        const float4 x = __ldg(reinterpret_cast<const float4*>(row));
+                        v[u][0] = x.x; v[u][1] = x.y; v[u][2] = x.z; v[u][3] = x.w;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) v[u][c] = c < nv ? __ldg(row + c) : 0.0f;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const float su = scaled ? __shfl_sync(full, s, grp * PER + k0 + u) : 1.0f;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) acc[c] = scaled ? fmaf(su, v[u][c], acc[c]) : acc[c] + v[u][c];
+                }
+            }
+#pragma unroll
+            for (int off = 16; off >= LPR; off >>= 1)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] += __shfl_xor_sync(full, acc[c], off);
+            const int t0 = t;  // every lane holds the batch's one target
+            if (grp == 0) {
+                float* op = t0 < a.n_out ? reinterpret_cast<float*>(Oc + (uint64_t)(uint32_t)t0 * orb)
+                                         : a.part + (int64_t)(t0 - a.n_out) * a.ldp + col;
+                if (red4_ok) redv<4>(op, acc, 4);
+                else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) if (c < nv) atomicAdd(op + c, acc[c]);
+                }
+            }
+            __syncwarp();  // s_inv was written for this batch
+            continue;
+        }
         if (RED != PYG_MAX && n == 32 && !dup && !hub_batch && off32) {
             // 32 distinct real targets (uniform graphs: almost every batch): every edge is its own run,
             // so no run tracking -- per edge and lane one shuffle, one row load, one RED
@@ -603,7 +647,7 @@ __global__ void unpack_cols_kernel(const T* __restrict__ Os, int W, int64_t rows
 // (one per column tile); counters[0] = hubs, counters[1] = slots handed out
 __global__ void hub_assign_kernel(const int32_t* __restrict__ deg, int64_t n, int threshold, int tiles,
                                   int32_t* hub_base, uint32_t* hub_bits, int32_t* hub_rows, int32_t* counters,
-                                  int32_t* cursor) {
+                                  int32_t* cursor, float* part, int64_t ldp) {
     // whole warps walk 32 consecutive rows so each bitmap word is one ballot
     const int64_t n32 = (n + 31) & ~(int64_t)31;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += (int64_t)gridDim.x * blockDim.x) {
@@ -615,16 +659,13 @@ __global__ void hub_assign_kernel(const int32_t* __restrict__ deg, int64_t n, in
             hub_rows[atomicAdd(counters, 1)] = (int32_t)i;
             for (int t = 0; t < tiles; ++t) cursor[(int64_t)hb * tiles + t] = 0;
             hub_base[i] = hb;
+            // the hub zeroes its own slot partials (no separate launch: small graphs are launch-bound)
+            float4* ps = reinterpret_cast<float4*>(part + (int64_t)hb * ldp);
+            for (int64_t q = 0; q < (int64_t)ns * (ldp / 4); ++q) ps[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         const unsigned word = __ballot_sync(0xffffffffu, hub);
         if ((threadIdx.x & 31) == 0) hub_bits[i >> 5] = word;
     }
-}
-
-__global__ void zero_slots_kernel(float* part, int64_t ldp, const int32_t* __restrict__ counters) {
-    const int64_t total = (int64_t)counters[1] * ldp;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
-        part[t] = 0.0f;
 }
 
 // out[hub] = fp64 sum of the hub's slot partials in slot order (/ deg for mean): Q12 on the
@@ -797,12 +838,11 @@ size_t coo_ws_bytes(int64_t E, int64_t n_out, int64_t ncols, int reduce, int64_t
     if (E <= 0) return 0;
     if (reduce == PYG_MAX) return compact_bytes(n_out, n_src, ncols, reduce);
     Carver cv(nullptr, 0);
-    cv.take<int32_t>((size_t)std::max<int64_t>(n_out, 1));  // deg
+    cv.take<int32_t>((size_t)std::max<int64_t>(n_out, 1) + 64);  // deg, then the 4 hub counters (one memset)
     if (E > kHeavyThreshold) {
         cv.take<int32_t>((size_t)n_out);                             // hub_base (valid for hubs only)
         cv.take<uint32_t>((size_t)cdiv(n_out, 32));                  // hub bitmap
         cv.take<int32_t>((size_t)hub_cap(E));                        // hub_rows
-        cv.take<int32_t>(4);                                         // counters
         cv.take<int32_t>((size_t)(slot_cap(E) * max_tiles(ncols)));  // cursors
         cv.take<float>((size_t)slot_cap(E) * align_up((size_t)ncols, 4));  // slot partials
     }
@@ -828,13 +868,14 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
     const bool hubs = reduce != PYG_MAX && a.E > kHeavyThreshold;
     Carver cv(ws, ws_bytes);
     if (reduce != PYG_MAX) {
-        deg = cv.take<int32_t>((size_t)std::max<int64_t>(a.n_out, 1));
+        const size_t n_deg = (size_t)std::max<int64_t>(a.n_out, 1);
+        deg = cv.take<int32_t>(n_deg + 64);
+        counters = deg + align_up(n_deg, 16);  // right behind deg: one memset zeroes both
         if (hubs) {
             hub_base = cv.take<int32_t>((size_t)a.n_out);
             a.hub_base = hub_base;
             a.hub_bits = cv.take<uint32_t>((size_t)cdiv(a.n_out, 32));
             hub_rows = cv.take<int32_t>((size_t)hub_cap(a.E));
-            counters = cv.take<int32_t>(4);
             a.hub_cursor = cv.take<int32_t>((size_t)(slot_cap(a.E) * max_tiles(a.ncols)));
             a.hub_count = counters;
             a.ldp = (int64_t)align_up((size_t)a.ncols, 4);
@@ -843,8 +884,15 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
         if (!ws || !cv.ok())
             return fail(PYG_ERR_NO_MEMORY, "atomic scatter: workspace too small (%zu < %zu bytes, see pyg_workspace_size)",
                         ws_bytes, coo_ws_bytes(a.E, a.n_out, a.ncols, reduce, a.gidx ? a.n_src : 0));
-        if (a.deg) deg = const_cast<int32_t*>(a.deg);
-        else PYG_TRY(coo_degree(a.sidx, a.E, a.n_out, deg, nullptr, s));
+        if (a.deg) {
+            if (hubs) PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
+            deg = const_cast<int32_t*>(a.deg);
+        } else {
+            PYG_CUDA(cudaMemsetAsync(deg, 0, (align_up(n_deg, 16) + 4) * sizeof(int32_t), s));
+            degree_kernel<<<grid_for(a.E), 256, 0, s>>>(a.sidx, a.E, deg, nullptr);
+            PYG_LAUNCHED();
+            PYG_CUDA(cudaGetLastError());
+        }
     }
     const CooGeom g = coo_geometry(a, reduce);
     // compact column tiles (see pack_cols_kernel) when the tile kernel runs several L2 tiles and the
@@ -876,12 +924,9 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
             PYG_CUDA(cudaMemset2DAsync(a.out, a.ldo * 4, 0, (size_t)a.ncols * 4, (size_t)a.n_out, s));
     }
     if (hubs) {
-        PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
         hub_assign_kernel<<<grid_for(a.n_out), 256, 0, s>>>(deg, a.n_out, kHeavyThreshold, g.tiles, hub_base,
                                                               const_cast<uint32_t*>(a.hub_bits), hub_rows, counters,
-                                                              a.hub_cursor);
-        PYG_LAUNCHED();
-        zero_slots_kernel<<<148 * 4, 256, 0, s>>>(a.part, a.ldp, counters);
+                                                              a.hub_cursor, a.part, a.ldp);
         PYG_LAUNCHED();
         PYG_CUDA(cudaGetLastError());
     }

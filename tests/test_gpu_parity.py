@@ -594,3 +594,27 @@ def test_plan_pass_views_equal_whole_plan(pg, red):
             check_exact(H(arg), H(whole[1]))
         else:
             check_exact(H(out), H(whole))
+
+
+@pytest.mark.parametrize("F", [16, 64, 37])
+@pytest.mark.parametrize("red", ["sum", "mean", "max"])
+def test_atomic_target_sorted_high_degree(pg, F, red):
+    """Target-sorted ("coalesced") input with in-degree ~100 on the atomic strategy: most 32-edge
+    batches of the tile kernel share one target (one RED per batch after a butterfly over the lane
+    groups), some straddle two; plus an empty row and weights."""
+    rng = np.random.default_rng(F + 3 * len(red))
+    n = 400
+    deg = rng.integers(60, 140, n)
+    deg[7] = 0
+    dst = np.repeat(np.arange(n), deg)
+    src = rng.integers(0, n, dst.size)
+    ei = np.stack([src, dst]).astype(np.int64)
+    x = synth.features(n, F, F + 1, signed=(red == "max"))
+    w = rng.random(dst.size).astype(np.float32)
+    for ew in (None, w):
+        ref = oracle.propagate(x, ei, reduce=red, edge_weight=ew, with_abs=True)
+        got = pg.pyg_propagate(T(x), T(ei), reduce=red, edge_weight=None if ew is None else T(ew), plan=None)
+        if red == "max":
+            compare(got, ref[:2], red, what="sorted atomic")
+        else:
+            compare(got, ref[0], red, abs_sum=ref[1], what="sorted atomic")
