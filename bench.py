@@ -507,7 +507,7 @@ def run_reference(a):
     rng = np.random.default_rng(110)
     if a.op in ("gat", "gatlayer"):
         H = a.heads or 8
-        C = a.gat_c or (8 if cfg in ("cora", "pubmed", "clouds") else max(1, F // H))
+        C = a.gat_c or (8 if cfg in ("cora", "pubmed", "clouds") else max(4, F // H // 4 * 4))
         zc = rng.standard_normal((N, H * C)).astype(np.float32)
         ss = rng.standard_normal((N, H)).astype(np.float32)
         sd = rng.standard_normal((N, H)).astype(np.float32)
@@ -762,7 +762,9 @@ def main():
         # z = x W: the GAT paper's 8 heads x 8 channels on the citation graphs, 8 x F/8 on
         # the large graphs; z is a seeded input (the transform is the tcgen05 path, --op gcn)
         H = a.heads or 8
-        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, F // H))
+        # (channels per head a multiple of 4: a float4 chunk stays inside one head on the one-pass
+        # kernels; Reddit's 602 columns -> 8 x 72)
+        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(4, F // H // 4 * 4))
         t1 = time.perf_counter()
         if plan_full.view()["n_col_blocks"] > 1:
             plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)

@@ -992,7 +992,9 @@ bool gat_fwd_tma_eligible(const pyg_plan* plan, int H, int C, int F, const float
         !plan->task_pos || !plan->pos_row)
         return false;
     if (plan->n_empty > 0 && !plan->row_order) return false;
-    if (!(H == 4 || H == 8) || F % 4 || F > 1024 || F < 16 || C <= 0) return false;
+    // C % 4: a float4 chunk of z must stay inside one head (its weight is the head's alpha); C = 75
+    // (Reddit's 600 = 8 x 75) straddles heads and takes the two-pass kernels
+    if (!(H == 4 || H == 8) || F % 4 || F > 1024 || F < 16 || C <= 0 || C % 4) return false;
     if (mode != 1 && plan->n_light_tasks < 1024) return false;
     if (!al16(z) || ldz % 4 || !al16(out) || ldo % 4) return false;
     if (!al16(alpha) || !al16(s_src) || !al16(s_dst)) return false;
@@ -1323,9 +1325,10 @@ pyg_status_t gat_fwd_blocked(const pyg_plan* plan, int H, int C, int F, const fl
     const int64_t n = plan->n_rows;
     const size_t np = plan->parts.size();
     if (np > (size_t)kMaxParts) return fail(PYG_ERR_UNSUPPORTED, "gat_propagate: at most %d source blocks", kMaxParts);
-    if (F % 4 || F > 1024 || (reinterpret_cast<uintptr_t>(z) & 15) || ldz % 4 || (reinterpret_cast<uintptr_t>(out) & 15) ||
+    if (C % 4 || F > 1024 || (reinterpret_cast<uintptr_t>(z) & 15) || ldz % 4 || (reinterpret_cast<uintptr_t>(out) & 15) ||
         ldo % 4 || !plan->deg)
-        return fail(PYG_ERR_UNSUPPORTED, "gat_propagate on a source-blocked plan: H*C %% 4 == 0, <= 1024, 16-byte rows");
+        return fail(PYG_ERR_UNSUPPORTED, "gat_propagate on a source-blocked plan: C %% 4 == 0 (a float4 chunk inside one "
+                                         "head), H*C <= 1024, 16-byte rows");
     Carver cv(ws, ws_bytes);
     cv.take<unsigned long long>(1);
     unsigned* smax = cv.take<unsigned>(8);

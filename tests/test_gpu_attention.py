@@ -37,13 +37,19 @@ def _case(name):
         return synth.rmat_edges_np(scale=12, E=300000, N=n, seed=9), n, n, 4, 16
     if name == "bipartite_h2c36":  # n_src != n_dst, many empty targets, F = 72 (3 float4 chunks/lane)
         return np.stack([rng.integers(0, 700, 3000), rng.integers(0, 900, 3000)]).astype(np.int64), 700, 900, 2, 36
+    if name == "h8c5":  # 8 heads of 5 channels: float4 chunks straddle heads -> two-pass kernels even with TMA forced
+        n = 600
+        return np.stack([rng.integers(0, n, 9000), rng.integers(0, n, 9000)]).astype(np.int64), n, n, 8, 5
+    if name == "h4c6":  # F = 24, C % 4 = 2
+        n = 500
+        return np.stack([rng.integers(0, n, 6000), rng.integers(0, n, 6000)]).astype(np.int64), n, n, 4, 6
     if name == "wide_h8c64":  # H*C = 512
         n = 1200
         return np.stack([rng.integers(0, n, 20000), rng.integers(0, n, 20000)]).astype(np.int64), n, n, 8, 64
     raise KeyError(name)
 
 
-CASES = ["cora_h8c8", "ragged_h3c5", "rmat_h4c16", "bipartite_h2c36", "wide_h8c64"]
+CASES = ["cora_h8c8", "ragged_h3c5", "rmat_h4c16", "bipartite_h2c36", "wide_h8c64", "h8c5", "h4c6"]
 
 
 def _inputs(name):
@@ -182,6 +188,22 @@ def test_gat_forward_source_blocked(factored, outlier):
     check_close(a.cpu().numpy(), ralpha, what="alpha")
     check_close(out.cpu().numpy(), ref, abs_sum=ab, what="out")
     assert torch.equal(out[n - 100:], torch.zeros_like(out[n - 100:]))
+
+
+def test_gat_source_blocked_needs_whole_float4_heads():
+    """The blocked GAT forward weighs each float4 chunk of z with one head's alpha: C % 4 != 0 (a chunk
+    straddling two heads) is refused instead of computed wrong."""
+    import paper_1903_02428_b200 as pg
+
+    rng = np.random.default_rng(5)
+    n, H, C, E = 600, 4, 6, 5000
+    ei = _t(np.stack([rng.integers(0, n, E), rng.integers(0, n, E)]).astype(np.int64))
+    plan = pg.pyg_plan_build(ei[1], ei[0], n, n, col_block=200)
+    z = torch.randn((n, H * C), device=DEV)
+    s = torch.randn((n, H), device=DEV)
+    with pytest.raises(pg.PygError) as e:
+        pg.pyg_gat_propagate(z, s, s, H, plan)
+    assert e.value.status == "PYG_ERR_UNSUPPORTED"
 
 
 def test_gat_zero_attention_equals_mean():
