@@ -1150,7 +1150,7 @@ def main():
         result["cpu_baseline"] = {"value": rate, "unit": "edges*F/s", "cores": 1, "kind": "oracle",
                                   "sample": sample, "parity_on_sample": ok, "host": host_info(),
                                   "full_pass": full_pass_record(a.config, red) if a.op == "propagate" else None}
-        if not ok:
+        if ok is False:  # None: no element-wise check for this op (see parity_on_sample)
             result["parity_error"] = "GPU output disagrees with the oracle on the sampled rows"
 
     # ---- e2e at N > 1: every step the edge list and this rank's X rows come from pinned host memory,
