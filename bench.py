@@ -301,6 +301,13 @@ def l2_gather_peak():
         return None, None
 
 
+def gat_fwd_blocked_ok(C, F):
+    """The blocked GAT forward weighs float4 chunks with one head's alpha (C % 4 == 0); it keeps 4 rows
+    of up to 2 float4 chunks per lane in flight, so it is taken for rows of <= 256 floats (Reddit 8 x 72:
+    275 ms blocked against 257 ms on the unblocked one-pass kernel, gpurun_out/r3ac)."""
+    return C % 4 == 0 and F <= 256
+
+
 def l2_red_peak():
     """Measured gather + red.global.add.v4 throughput into L2-resident rows (scripts/l2red.cu,
     profiles/l2_red.json): the roof of the atomic strategy once its column tiles fit L2."""
@@ -787,11 +794,17 @@ def main():
         gat["row_sums"] = torch.empty((N, H), device=dev) if E >= (1 << 22) else None
         gws = torch.empty(max(pg.pyg_gat_backward_workspace_size(plan, planT, H, C, gat["row_sums"] is not None), 1),
                           dtype=torch.uint8, device=dev)
-        gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan, H, C), 1), dtype=torch.uint8, device=dev)
+        # the forward gathers z rows: when z exceeds L2 (Reddit 8 x 72: 537 MB) it runs on a source-blocked
+        # plan, one L2-resident pass per block; alpha (by edge id) and row_sums carry over to the backward,
+        # which runs on the unblocked plan and its transpose
+        cb_f = pg.pyg_plan_suggest_col_block(E, N, N, F * 4) if a.col_block == "auto" else 0
+        plan_f = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb_f) if cb_f > 0 and gat_fwd_blocked_ok(C, F) else plan
+        gat["fwd_col_blocks"] = plan_f.view()["n_col_blocks"]
+        gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan_f, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 2, "gat"
 
         def compute():
-            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan, out=gat["out"], alpha=gat["alpha"], workspace=gfw,
+            o, al = pg.pyg_gat_propagate(zc, s_src, s_dst, H, plan_f, out=gat["out"], alpha=gat["alpha"], workspace=gfw,
                                          row_sums=gat["row_sums"])
             gat["grads"] = pg.pyg_gat_backward(zc, s_src, s_dst, H, al, gout, plan, planT, out=o, workspace=gws,
                                                row_sums=gat["row_sums"])
@@ -1085,6 +1098,8 @@ def main():
     if gat is not None:
         result["config"]["op"] = "gat"
         result["config"]["heads"] = gat["H"]
+        result["config"]["channels"] = F // gat["H"]
+        result["config"]["forward_col_blocks"] = gat["fwd_col_blocks"]
         result["config"]["step"] = ("GAT aggregation forward (segment softmax + alpha-weighted sum) + backward "
                                     "(grad z, s_src, s_dst)")
         result["plans_ms"] = prep_ms

@@ -132,6 +132,36 @@ def test_gat_backward(name, tma, mode, monkeypatch):
     check_close(got["s_dst"].cpu().numpy(), ref["s_dst"], abs_sum=ref["abs_s_dst"], what="grad_s_dst")
 
 
+@pytest.mark.parametrize("factored", [False, True])
+def test_gat_blocked_forward_then_backward(factored, monkeypatch):
+    """Training step with the forward on a source-blocked plan (z above L2 in the bench) and the one-pass
+    backward on the unblocked plan + its transpose: alpha (by edge id) and row_sums mean the same
+    thing on both plans, so the gradients equal the oracle's."""
+    import paper_1903_02428_b200 as pg
+
+    monkeypatch.setenv("PYG_SEG_TMA", "1")
+    rng = np.random.default_rng(31)
+    n, H, C, E = 1500, 8, 16, 24000
+    ei = np.stack([rng.integers(0, n, E), rng.integers(0, n - 50, E)]).astype(np.int64)
+    z = rng.standard_normal((n, H * C)).astype(np.float32)
+    ss = rng.standard_normal((n, H)).astype(np.float32)
+    sd = rng.standard_normal((n, H)).astype(np.float32)
+    g = rng.standard_normal((n, H * C)).astype(np.float32)
+    eit = _t(ei)
+    plan_b = pg.pyg_plan_build(eit[1], eit[0], n, n, col_block=400)
+    assert plan_b.view()["n_col_blocks"] == 4
+    plan = pg.pyg_plan_build(eit[1], eit[0], n, n)
+    planT = pg.pyg_plan_build(eit[0], eit[1], n, n)
+    zt, sst, sdt = _t(z), _t(ss), _t(sd)
+    rs = torch.empty((n, H), device=DEV) if factored else None
+    out, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan_b, row_sums=rs)
+    got = pg.pyg_gat_backward(zt, sst, sdt, H, alpha, _t(g), plan, planT, out=out, row_sums=rs)
+    ref = oracle.gat_backward(z, ss, sd, ei, H, g, n_dst=n, with_abs=True)
+    check_close(got["z"].cpu().numpy(), ref["z"], abs_sum=ref["abs_z"], what="grad_z")
+    check_close(got["s_src"].cpu().numpy(), ref["s_src"], abs_sum=ref["abs_s_src"], what="grad_s_src")
+    check_close(got["s_dst"].cpu().numpy(), ref["s_dst"], abs_sum=ref["abs_s_dst"], what="grad_s_dst")
+
+
 @pytest.mark.parametrize("fused", ["0", "1"])
 def test_gat_forward_far_logits_fall_back_exactly(fused, monkeypatch):
     """The one-pass forward shifts each row's logits by the bound leaky_relu(max_j s_src[j] + s_dst[i])
