@@ -302,10 +302,11 @@ def l2_gather_peak():
 
 
 def gat_fwd_blocked_ok(C, F):
-    """The blocked GAT forward weighs float4 chunks with one head's alpha (C % 4 == 0); it keeps 4 rows
-    of up to 2 float4 chunks per lane in flight, so it is taken for rows of <= 256 floats (Reddit 8 x 72:
-    275 ms blocked against 257 ms on the unblocked one-pass kernel, gpurun_out/r3ac)."""
-    return C % 4 == 0 and F <= 256
+    """The blocked GAT forward weighs float4 chunks with one head's alpha (C % 4 == 0).  Taken for rows
+    of <= 256 floats (PYG_BENCH_GAT_BLOCKED_MAX_F): for Reddit's 8 x 72 it measured 275 ms per training
+    step against 257 ms unblocked at first (gpurun_out/r3ac), 251.6 vs 255.5 ms once wide rows kept fewer
+    z rows in flight (gpurun_out/r3ad) -- within noise, so the wide case stays on the one-pass kernel."""
+    return C % 4 == 0 and F <= int(os.environ.get("PYG_BENCH_GAT_BLOCKED_MAX_F", "256"))
 
 
 def l2_red_peak():

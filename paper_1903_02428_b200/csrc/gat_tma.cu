@@ -1141,7 +1141,7 @@ struct BlockArgs {
 // weight of position i, head h (one s_src load and one exp per lane per group), the column lanes
 // gather the 4 z_j rows (loads in flight together) and take each weight by a shuffle.
 template <int NCH>
-__global__ void __launch_bounds__(256) gat_fwd_block_kernel(BlockArgs a) {
+__global__ void __launch_bounds__(256, NCH >= 3 ? 2 : 3) gat_fwd_block_kernel(BlockArgs a) {
     const int lane = threadIdx.x & 31;
     const int my_i = lane >> 3, my_h = lane & 7;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1178,14 +1178,22 @@ __global__ void __launch_bounds__(256) gat_fwd_block_kernel(BlockArgs a) {
                 int js[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) js[u] = __shfl_sync(0xffffffffu, jl, (t0 + u) & 31);
-                float4 zv[4][NCH];
+                // z rows in flight per lane: all 4 positions for rows of <= 2 chunks, 2 or 1 at a time for wider
+                // rows (a wide row's 4 x NCH float4 capped the kernel at 1-2 CTAs per SM: NCH = 6 took 182
+                // registers)
+                constexpr int UH = NCH <= 2 ? 4 : (NCH <= 4 ? 2 : 1);
+                float4 zv[UH][NCH];
+                auto load_z = [&](int u0) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < UH; ++u)
 #pragma unroll
-                    for (int ch = 0; ch < NCH; ++ch)
-                        zv[u][ch] = (cval[ch] && t0 + u < cnt)
-                                        ? __ldg(reinterpret_cast<const float4*>(a.z + (int64_t)js[u] * a.ldz) + lane + 32 * ch)
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int ch = 0; ch < NCH; ++ch)
+                            zv[u][ch] = (cval[ch] && t0 + u0 + u < cnt)
+                                            ? __ldg(reinterpret_cast<const float4*>(a.z + (int64_t)js[u0 + u] * a.ldz) +
+                                                    lane + 32 * ch)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                };
+                load_z(0);
                 // weight of (position t0 + my_i, head my_h)
                 const int jm = __shfl_sync(0xffffffffu, jl, (t0 + my_i) & 31);
                 const int em = __shfl_sync(0xffffffffu, el, (t0 + my_i) & 31);
@@ -1202,15 +1210,19 @@ __global__ void __launch_bounds__(256) gat_fwd_block_kernel(BlockArgs a) {
                 }
                 ps += p;
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+                for (int u0 = 0; u0 < 4; u0 += UH) {
+                    if (u0 > 0) load_z(u0);
 #pragma unroll
-                    for (int ch = 0; ch < NCH; ++ch) {
-                        const float w = __shfl_sync(0xffffffffu, p, u * 8 + hch[ch]);
-                        acc[ch][0] = fmaf(w, zv[u][ch].x, acc[ch][0]);
-                        acc[ch][1] = fmaf(w, zv[u][ch].y, acc[ch][1]);
-                        acc[ch][2] = fmaf(w, zv[u][ch].z, acc[ch][2]);
-                        acc[ch][3] = fmaf(w, zv[u][ch].w, acc[ch][3]);
-                    }
+                    for (int u = 0; u < UH; ++u)
+#pragma unroll
+                        for (int ch = 0; ch < NCH; ++ch) {
+                            const float w = __shfl_sync(0xffffffffu, p, (u0 + u) * 8 + hch[ch]);
+                            acc[ch][0] = fmaf(w, zv[u][ch].x, acc[ch][0]);
+                            acc[ch][1] = fmaf(w, zv[u][ch].y, acc[ch][1]);
+                            acc[ch][2] = fmaf(w, zv[u][ch].z, acc[ch][2]);
+                            acc[ch][3] = fmaf(w, zv[u][ch].w, acc[ch][3]);
+                        }
+                }
             }
         }
         // the row's per-head sum over its position groups (lanes h, h + 8, h + 16, h + 24)
