@@ -590,11 +590,20 @@ bool aligned(const void* p, int bytes) { return (reinterpret_cast<uintptr_t>(p) 
 
 constexpr int kNch[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16};
 
-__global__ void degree_kernel(const int64_t* __restrict__ sidx, int64_t E, int32_t* deg, int32_t* first) {
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < E; k += (int64_t)gridDim.x * blockDim.x) {
+__global__ void degree_kernel(const int64_t* __restrict__ sidx, int64_t E, int32_t* deg, int32_t* first,
+                              float* zero_out = nullptr, int64_t ldo = 0, int ncols = 0, int64_t n_rows = 0) {
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = t0; k < E; k += nt) {
         const int64_t i = sidx[k];
         if (deg) atomicAdd(deg + i, 1);
         if (first) atomicMin(first + i, (int32_t)k);
+    }
+    if (zero_out) {
+        const int64_t total = n_rows * ncols;
+        for (int64_t t = t0; t < total; t += nt) {
+            const int64_t r = t / ncols;
+            zero_out[r * ldo + (t - r * ncols)] = 0.0f;
+        }
     }
 }
 
@@ -884,15 +893,6 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
         if (!ws || !cv.ok())
             return fail(PYG_ERR_NO_MEMORY, "atomic scatter: workspace too small (%zu < %zu bytes, see pyg_workspace_size)",
                         ws_bytes, coo_ws_bytes(a.E, a.n_out, a.ncols, reduce, a.gidx ? a.n_src : 0));
-        if (a.deg) {
-            if (hubs) PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
-            deg = const_cast<int32_t*>(a.deg);
-        } else {
-            PYG_CUDA(cudaMemsetAsync(deg, 0, (align_up(n_deg, 16) + 4) * sizeof(int32_t), s));
-            degree_kernel<<<grid_for(a.E), 256, 0, s>>>(a.sidx, a.E, deg, nullptr);
-            PYG_LAUNCHED();
-            PYG_CUDA(cudaGetLastError());
-        }
     }
     const CooGeom g = coo_geometry(a, reduce);
     // compact column tiles (see pack_cols_kernel) when the tile kernel runs several L2 tiles and the
@@ -917,7 +917,26 @@ pyg_status_t coo_reduce(const CooArgs& a0, int reduce, void* ws, size_t ws_bytes
         if (!ws || !c2.ok()) Os = nullptr, Ks = nullptr, Xs = nullptr;
     }
     const bool compact = Os || Ks;
-    if (!compact) {  // zero the accumulation target (outputs are overwritten, Q14)
+    bool out_zeroed = false;
+    if (reduce != PYG_MAX) {
+        if (a.deg) {
+            if (hubs) PYG_CUDA(cudaMemsetAsync(counters, 0, 4 * sizeof(int32_t), s));
+            deg = const_cast<int32_t*>(a.deg);
+        } else {
+            const size_t n_deg = (size_t)std::max<int64_t>(a.n_out, 1);
+            PYG_CUDA(cudaMemsetAsync(deg, 0, (align_up(n_deg, 16) + 4) * sizeof(int32_t), s));
+            // the degree pass also zeroes a small in-place target (one launch fewer: tiny graphs are launch-
+            // bound; Fig. 3 atomic 25-29 -> 24-27 ms per 1,000 calls); large ones keep the memset (R-MAT's
+            // 5 GB: 34.3 ms with it, 35.8 ms zeroed by the degree pass, gpurun_out/r3ah)
+            out_zeroed = !compact && a.n_out * a.ncols <= (int64_t)(16 << 20);
+            const int64_t work = std::max<int64_t>(a.E, out_zeroed ? a.n_out * a.ncols : 0);
+            degree_kernel<<<grid_for(work), 256, 0, s>>>(a.sidx, a.E, deg, nullptr, out_zeroed ? a.out : nullptr,
+                                                         a.ldo, a.ncols, a.n_out);
+            PYG_LAUNCHED();
+            PYG_CUDA(cudaGetLastError());
+        }
+    }
+    if (!compact && !out_zeroed) {  // zero the accumulation target (outputs are overwritten, Q14)
         if (reduce == PYG_MAX)
             PYG_CUDA(cudaMemset2DAsync(a.keys, a.ldk * 8, 0, (size_t)a.ncols * 8, (size_t)a.n_out, s));
         else
