@@ -820,7 +820,10 @@ def main():
         C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(1, min(F, 256) // H))
         # the gathered matrix is z [N x H*C]: source blocks sized for ITS rows (an L2-resident pass per
         # block when z exceeds L2, e.g. Reddit 232,965 x 256 floats = 238 MB)
-        cb_z = pg.pyg_plan_suggest_col_block(E, N, N, H * C * 4) if a.col_block == "auto" else int(a.col_block)
+        # (sized for twice the z row: blocks of ~0.2 x L2 -- the per-edge alpha stores and s_src reads
+        # share L2 with the block; Reddit 8 x 32: 8 passes 11.3-11.6 ms against 5 passes 12.1-12.3 ms,
+        # gpurun_out/r3s)
+        cb_z = pg.pyg_plan_suggest_col_block(E, N, N, 2 * H * C * 4) if a.col_block == "auto" else int(a.col_block)
         if plan_full.view()["col_block"] != cb_z:
             plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb_z)
             col_block = cb_z
