@@ -302,11 +302,12 @@ def l2_gather_peak():
 
 
 def gat_fwd_blocked_ok(C, F):
-    """The blocked GAT forward weighs float4 chunks with one head's alpha (C % 4 == 0).  Taken for rows
-    of <= 256 floats (PYG_BENCH_GAT_BLOCKED_MAX_F): for Reddit's 8 x 72 it measured 275 ms per training
-    step against 257 ms unblocked at first (gpurun_out/r3ac), 251.6 vs 255.5 ms once wide rows kept fewer
-    z rows in flight (gpurun_out/r3ad) -- within noise, so the wide case stays on the one-pass kernel."""
-    return C % 4 == 0 and F <= int(os.environ.get("PYG_BENCH_GAT_BLOCKED_MAX_F", "256"))
+    """The blocked GAT forward weighs float4 chunks with one head's alpha (C % 4 == 0); rows up to
+    PYG_BENCH_GAT_BLOCKED_MAX_F floats (default: the kernel's 1024).  Reddit training step at 8 x 64 with
+    the blocked transposed plan: 113.1 ms with the blocked forward, 126.1 ms with the unblocked one-pass
+    forward (gpurun_out/r3ao); at 8 x 72 the blocked forward first measured slower (275 vs 257 ms,
+    gpurun_out/r3ac) until wide rows kept fewer z rows in flight (251.6 vs 255.5 ms, gpurun_out/r3ad)."""
+    return C % 4 == 0 and F <= int(os.environ.get("PYG_BENCH_GAT_BLOCKED_MAX_F", "1024"))
 
 
 def l2_red_peak():
@@ -515,7 +516,7 @@ def run_reference(a):
     rng = np.random.default_rng(110)
     if a.op in ("gat", "gatlayer"):
         H = a.heads or 8
-        C = a.gat_c or (8 if cfg in ("cora", "pubmed", "clouds") else max(4, F // H // 4 * 4))
+        C = a.gat_c or (8 if cfg in ("cora", "pubmed", "clouds") else max(4, 1 << ((F // H).bit_length() - 1)))
         zc = rng.standard_normal((N, H * C)).astype(np.float32)
         ss = rng.standard_normal((N, H)).astype(np.float32)
         sd = rng.standard_normal((N, H)).astype(np.float32)
@@ -770,14 +771,17 @@ def main():
         # z = x W: the GAT paper's 8 heads x 8 channels on the citation graphs, 8 x F/8 on
         # the large graphs; z is a seeded input (the transform is the tcgen05 path, --op gcn)
         H = a.heads or 8
-        # (channels per head a multiple of 4: a float4 chunk stays inside one head on the one-pass
-        # kernels; Reddit's 602 columns -> 8 x 72)
-        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(4, F // H // 4 * 4))
+        # (channels per head: the largest power of two <= F / H -- the one-pass TMA forward needs C % 4 == 0
+        # and the one-pass backward a power of two; Reddit's 602 columns -> 8 x 64, R-MAT's 128 -> 8 x 16.
+        # With 8 x 72 the backward took the two-pass softmax kernel: 167 of a 243 ms step, gpurun_out/r3an)
+        C = a.gat_c or (8 if a.config in ("cora", "pubmed", "clouds") else max(4, 1 << ((F // H).bit_length() - 1)))
         t1 = time.perf_counter()
         if plan_full.view()["n_col_blocks"] > 1:
             plan = plan_full = pg.pyg_plan_build(ei[1], ei[0], N, N)
             col_block = 0
-        planT = pg.pyg_plan_build(ei[0], ei[1], N, N)
+        # the transposed plan gathers grad_out rows (n x H*C): source-blocked when they exceed L2
+        cb_t = pg.pyg_plan_suggest_col_block(E, N, N, H * C * 4) if a.col_block == "auto" else 0
+        planT = pg.pyg_plan_build(ei[0], ei[1], N, N, col_block=cb_t)
         torch.cuda.synchronize()
         prep_ms = (time.perf_counter() - t1) * 1e3
         gg = torch.Generator(device=dev)
@@ -801,6 +805,7 @@ def main():
         cb_f = pg.pyg_plan_suggest_col_block(E, N, N, F * 4) if a.col_block == "auto" else 0
         plan_f = pg.pyg_plan_build(ei[1], ei[0], N, N, col_block=cb_f) if cb_f > 0 and gat_fwd_blocked_ok(C, F) else plan
         gat["fwd_col_blocks"] = plan_f.view()["n_col_blocks"]
+        gat["T_col_blocks"] = planT.view()["n_col_blocks"]
         gfw = torch.empty(max(pg.pyg_gat_propagate_workspace_size(plan_f, H, C), 1), dtype=torch.uint8, device=dev)
         passes, red = 2, "gat"
 
@@ -1104,10 +1109,13 @@ def main():
         result["config"]["heads"] = gat["H"]
         result["config"]["channels"] = F // gat["H"]
         result["config"]["forward_col_blocks"] = gat["fwd_col_blocks"]
+        result["config"]["transposed_col_blocks"] = gat["T_col_blocks"]
         result["config"]["step"] = ("GAT aggregation forward (segment softmax + alpha-weighted sum) + backward "
                                     "(grad z, s_src, s_dst)")
         result["plans_ms"] = prep_ms
-        result["roofline"]["note"] = "achieved = algorithmic bytes of the whole step (5 kernels, gat_step_bytes) / step time"
+        result["roofline"]["note"] = ("achieved = algorithmic bytes of the whole step (5 kernels, gat_step_bytes) / step time; "
+                                      "with source-blocked forward / transposed plans those passes gather from L2, so "
+                                      "the HBM-modeled frac can exceed 1")
     elif passes == 2:
         result["config"]["step"] = "GCN forward (w = D^-1/2 (A+I) D^-1/2) + backward w.r.t. X"
         result["config"]["E_with_self_loops"] = E

@@ -748,9 +748,13 @@ pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t 
             kAttnMaxHeads);
     REQUIRE(plan && plan->n_rows == n_dst && (plan->col || plan->E == 0) && plan->parts.empty() && plan->E == E,
             PYG_ERR_DIMENSION, "gat_backward: `plan` must be the forward plan");
-    REQUIRE(plan_T && plan_T->n_rows == n_src && (plan_T->col || plan_T->E == 0) && plan_T->parts.empty() &&
-                plan_T->n_cols <= n_dst && plan_T->E == E,
-            PYG_ERR_DIMENSION, "gat_backward: plan_T must be built with row_index = sources, col_index = targets");
+    // plan_T may be source-blocked (blocks of grad_out rows): grad_z and grad_s_src are segment sums over it,
+    // one L2-resident pass per block when grad_out exceeds L2
+    REQUIRE(plan_T && plan_T->n_rows == n_src && (plan_T->col || plan_T->E == 0) && plan_T->n_cols <= n_dst &&
+                plan_T->E == E && (plan_T->parts.empty() || plan_T->n_passes == 0 ||
+                                   plan_T->n_passes == (int64_t)plan_T->parts.size()),
+            PYG_ERR_DIMENSION, "gat_backward: plan_T must be built with row_index = sources, col_index = targets "
+                               "(whole plan, not a pass view)");
     REQUIRE(E == 0 || (z && s_src && s_dst && alpha && grad_out && grad_logit), PYG_ERR_INVALID_ARGUMENT,
             "gat_backward: null input (grad_logit [E x H] is required)");
     REQUIRE(n_dst * H == 0 || grad_s_dst, PYG_ERR_INVALID_ARGUMENT, "gat_backward: null grad_s_dst");

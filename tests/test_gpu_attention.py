@@ -132,8 +132,9 @@ def test_gat_backward(name, tma, mode, monkeypatch):
     check_close(got["s_dst"].cpu().numpy(), ref["s_dst"], abs_sum=ref["abs_s_dst"], what="grad_s_dst")
 
 
+@pytest.mark.parametrize("blocked_T", [False, True])
 @pytest.mark.parametrize("factored", [False, True])
-def test_gat_blocked_forward_then_backward(factored, monkeypatch):
+def test_gat_blocked_forward_then_backward(factored, blocked_T, monkeypatch):
     """Training step with the forward on a source-blocked plan (z above L2 in the bench) and the one-pass
     backward on the unblocked plan + its transpose: alpha (by edge id) and row_sums mean the same
     thing on both plans, so the gradients equal the oracle's."""
@@ -151,7 +152,10 @@ def test_gat_blocked_forward_then_backward(factored, monkeypatch):
     plan_b = pg.pyg_plan_build(eit[1], eit[0], n, n, col_block=400)
     assert plan_b.view()["n_col_blocks"] == 4
     plan = pg.pyg_plan_build(eit[1], eit[0], n, n)
-    planT = pg.pyg_plan_build(eit[0], eit[1], n, n)
+    # blocked_T: grad_z / grad_s_src as passes over blocks of grad_out rows (the transposed plan's sources)
+    planT = pg.pyg_plan_build(eit[0], eit[1], n, n, col_block=350 if blocked_T else 0)
+    if blocked_T:
+        assert planT.view()["n_col_blocks"] == 5
     zt, sst, sdt = _t(z), _t(ss), _t(sd)
     rs = torch.empty((n, H), device=DEV) if factored else None
     out, alpha = pg.pyg_gat_propagate(zt, sst, sdt, H, plan_b, row_sums=rs)
