@@ -426,7 +426,10 @@ pyg_status_t pyg_gat_backward_workspace_size(const pyg_plan_t* plan, const pyg_p
  *   gather4 pipeline; H in {4, 8}, C a power of two <= 128 or a multiple of 128, 16-byte
  *   aligned rows); without it (or outside those shapes) two passes per row recompute the sum.
  * row_sums: NULL (alpha normalised) or the forward's row_sums (alpha in factored form).
- * plan: the forward plan; plan_T: row_index = sources, col_index = targets.
+ * plan: the forward plan (unblocked); plan_T: row_index = sources, col_index = targets -- it may be
+ *   source-blocked (blocks of grad_out rows, pyg_plan_suggest_col_block with row_bytes = 4*H*C):
+ *   grad_z and grad_s_src then run as one L2-resident pass per block.  The forward may have run
+ *   on a blocked plan of the same edges: alpha (by edge id) and row_sums mean the same.
  * H*C <= 4096.  workspace: pyg_gat_backward_workspace_size(plan, plan_T, H, C, row_sums != NULL).
  * Asynchronous. */
 pyg_status_t pyg_gat_backward(const float* z, int64_t n_src, int64_t H, int64_t C, int64_t ldz,
